@@ -1,0 +1,171 @@
+/*
+ * dawn.h — C ABI of libdawn.so, the B200 (sm_100a) hot path of DAWN (arXiv 2208.04514):
+ * unweighted single-source / multi-source / all-pairs shortest paths by repeated
+ * boolean vector x CSR products (SOVM, Algorithm 2, Eq. 9) and
+ * their pull form (BOVM, Algorithm 1, Eq. 4).
+ *
+ * Conventions:
+ *  - Every function returns dawn_status; no C++ exception crosses this boundary.  On a
+ *    non-DAWN_OK return dawn_last_error() (thread-local) describes the failure.
+ *  - Argument validation happens on the host BEFORE anything is enqueued; on error nothing
+ *    has been enqueued and no output has been written.
+ *  - The library never allocates device memory.  Graph arrays, workspace and outputs are
+ *    caller-owned device buffers (PyTorch tensors in the Python binding) that must outlive
+ *    the dawn_graph handle.  Only the small host-side handle is heap-allocated.
+ *  - Compute calls are asynchronous on `stream` (a cudaStream_t passed as void*).  Device
+ *    faults surface at the caller's next synchronisation (DAWN_ERR_CUDA from a later call).
+ *  - One in-flight call per graph handle (the handle's workspace holds the frontier state).
+ *    The graph arrays themselves are immutable and may be shared by several handles.
+ *  - Distances are uint32: d(s) = 0, d(v) = hop count of a shortest directed path s ~> v
+ *    along out-edges (Theorem 1), DAWN_UNREACHED if none (reading Q4 of
+ *    the paper's 0 sentinel collides with d(s) = 0).
+ */
+#ifndef DAWN_H
+#define DAWN_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DAWN_UNREACHED 0xFFFFFFFFu
+
+typedef enum {
+  DAWN_OK = 0,
+  DAWN_ERR_INVALID_ARGUMENT = 1, /* null pointer, n < 1, m < 0, unknown flag / variant       */
+  DAWN_ERR_BOUNDS = 2,           /* a source id outside [0, n)    */
+  DAWN_ERR_CONFIG = 3,           /* PULL requested on a directed graph loaded without CSC     */
+  DAWN_ERR_CAPACITY = 4,         /* output capacity too small; m >= 2^32; n >= 2^31           */
+  DAWN_ERR_WORKSPACE = 5,        /* workspace smaller than dawn_workspace_bytes()             */
+  DAWN_ERR_INVALID_GRAPH = 6,    /* CSR invariant violated (only with DAWN_GRAPH_VALIDATE)    */
+  DAWN_ERR_CUDA = 7              /* a CUDA runtime error (launch failure, earlier fault)      */
+} dawn_status;
+
+/* Graph flags. */
+enum {
+  DAWN_GRAPH_SYMMETRIC = 1, /* arcs come in both directions: CSC == CSR, in_* may be NULL   */
+  DAWN_GRAPH_VALIDATE = 2   /* check row_ptr monotone, row_ptr[0]=0, row_ptr[n]=m, cols in
+                               range; synchronises `stream` once                           */
+};
+
+/* Direction variants of one level step. */
+enum {
+  DAWN_AUTO = 0, /* direction-optimising: push while the frontier is small, pull while it is
+                    wide (switch on measured frontier density, device-side)                 */
+  DAWN_PUSH = 1, /* SOVM only (Algorithm 2): expand the frontier's out-rows (CSR)            */
+  DAWN_PULL = 2  /* BOVM only (Algorithm 1): unreached vertices scan in-rows (CSC) until the
+                    first frontier in-neighbour                                              */
+};
+
+/* Per-source statistics of dawn_sssp (device memory, 32 bytes). */
+typedef struct {
+  uint32_t levels;         /* eccentricity eps(s): rounds that found >= 1 vertex    */
+  uint32_t reached;        /* #{v != s : d(v) finite}       */
+  uint64_t edges_reach;    /* E10: sum of out-degrees over reached v incl. s
+                              = the GTEPS numerator                                          */
+  uint64_t edges_examined; /* adjacency entries actually read by the executed schedule       */
+  uint32_t push_levels;    /* levels run as push (SOVM)                                      */
+  uint32_t pull_levels;    /* levels run as pull (BOVM)                                      */
+} dawn_sssp_stats;
+
+/* Per-source record for msssp / apsp (32 bytes; SURVEY §8(c) "derived outputs").
+ * ecc = max finite d (0 if nothing reached); reached = #{v != s : d finite};
+ * sum_dist = sum of finite d; hash = sum over finite v of splitmix64((v << 32) | d(v))
+ * mod 2^64 (order independent).                                                             */
+typedef struct {
+  uint32_t source, ecc, reached, pad;
+  uint64_t sum_dist, hash;
+} dawn_record;
+
+typedef struct dawn_graph_s *dawn_graph;
+
+/* Bytes of device workspace a graph handle needs (graph-resident arrays + the frontier state
+ * of one SSSP + one 64-source batch).  flags as for dawn_graph_load_csr. Returns 0 if the
+ * sizes are unsupported (n < 1, n >= 2^31, m < 0, m >= 2^32).                               */
+size_t dawn_workspace_bytes(int64_t n, int64_t m, uint32_t flags);
+
+/*
+ * Make a graph resident (untimed per SPEC S:L357).
+ *   n, m         vertex and arc counts (directed arcs; a symmetric graph stores both).
+ *   row_ptr      device int64[n+1], CSR offsets (PAPER Table 1 "CSR", L103; D1).
+ *   col          device int32[m], CSR column ids, rows need not be sorted; no self-loops are
+ *                required for correctness (they never change a distance).
+ *   in_row_ptr, in_col   device CSC (in-edges), or NULL.  Ignored when
+ *                DAWN_GRAPH_SYMMETRIC is set (CSC == CSR).  Without them a directed graph
+ *                supports only DAWN_PUSH / DAWN_AUTO (which then never pulls).
+ *   flags        DAWN_GRAPH_SYMMETRIC | DAWN_GRAPH_VALIDATE.
+ *   workspace    device buffer of >= dawn_workspace_bytes(n, m, flags) bytes, 256-B aligned.
+ *   stream       cudaStream_t; the one-time conversion kernels are enqueued on it.
+ *   out          receives the handle.  Arrays are referenced, not copied (except a 32-bit
+ *                offset copy held in the workspace).
+ * Errors: INVALID_ARGUMENT, CAPACITY (m >= 2^32, n >= 2^31), WORKSPACE, INVALID_GRAPH, CUDA.
+ */
+dawn_status dawn_graph_load_csr(int64_t n, int64_t m, const int64_t *row_ptr, const int32_t *col,
+                                const int64_t *in_row_ptr, const int32_t *in_col, uint32_t flags,
+                                void *workspace, size_t ws_bytes, void *stream, dawn_graph *out);
+
+/* Free the host-side handle only (device memory belongs to the caller). NULL is a no-op. */
+dawn_status dawn_graph_destroy(dawn_graph g);
+
+/* Direction-switch thresholds for DAWN_AUTO (Beamer-style, cited by the paper at L123):
+ * push -> pull when alpha * m_f > m_u ; pull -> push when beta * n_f < n and shrinking.
+ * Defaults alpha = 14, beta = 24. ms_alpha: 64-source kernel pulls when
+ * ms_alpha * m_active > m (default 8).  Values <= 0 keep the current setting.               */
+dawn_status dawn_graph_set_tuning(dawn_graph g, double alpha, double beta, double ms_alpha);
+
+/*
+ * Single-source shortest paths (SSSP), one enqueue: initialisation, every level (push or
+ * pull, chosen on the device) and the per-source statistics run in ONE persistent kernel;
+ * the frontier-empty test is on the device (no host round trip per level; PAPER L174-179
+ * conditions 1-2, Algorithm 2 lines 15-17).
+ *   source   vertex id in [0, n)                               -> else DAWN_ERR_BOUNDS
+ *   variant  DAWN_AUTO / DAWN_PUSH / DAWN_PULL                   -> else INVALID_ARGUMENT
+ *   dist     device uint32[n] output (fully overwritten)
+ *   stats    device dawn_sssp_stats* or NULL
+ */
+dawn_status dawn_sssp(dawn_graph g, int64_t source, uint32_t variant, uint32_t *dist,
+                      dawn_sssp_stats *stats, void *stream);
+
+/*
+ * Multi-source: k sources (HOST array; all validated before any work),
+ * processed 64 at a time by the bit-parallel kernel (bit j of a vertex word = source 64b+j
+ * of the batch; one adjacency pass serves 64 BFS trees).
+ *   dist   device uint32[k][n] (source-major) or NULL.  k*n must be < 2^40 else CAPACITY.
+ *   rec    device dawn_record[k] or NULL (record i belongs to sources[i]).
+ * Repeated sources give identical rows and records.
+ */
+dawn_status dawn_msssp(dawn_graph g, const int64_t *sources, int64_t k, uint32_t *dist,
+                       dawn_record *rec, void *stream);
+
+/*
+ * The host-side shard rule of dawn_apsp: the sources are cut into 64-source batches in the
+ * given order; batch b belongs to rank (b mod world).  Writes the indices (into sources[])
+ * owned by `rank`, ascending, into idx (capacity cap) and their count into *count.  Pure host
+ * function, no device work.
+ */
+dawn_status dawn_apsp_shard(int64_t k, int32_t rank, int32_t world, int64_t *idx, int64_t cap,
+                            int64_t *count);
+
+/*
+ * APSP records for this rank's shard (PAPER E11-E12 L303-308: APSP = one SOVM per source; the
+ * caller passes e.g. the vertices of the largest WCC).  Computes the records of the sources
+ * dawn_apsp_shard() assigns to `rank`, in that order, into rec[0 .. *n_written).  The caller
+ * gathers the shards across ranks (torch.distributed / NCCL all-gather).
+ *   sources  HOST int64[k], all in [0, n)       rec  device dawn_record[cap]
+ *   n_written HOST, receives the shard size (known before any work; CAPACITY if > cap).
+ */
+dawn_status dawn_apsp(dawn_graph g, const int64_t *sources, int64_t k, int32_t rank, int32_t world,
+                      dawn_record *rec, int64_t cap, int64_t *n_written, void *stream);
+
+/* Thread-local description of the last error of this thread ("" if none). */
+const char *dawn_last_error(void);
+
+/* Library version string, e.g. "dawn-b200 0.1 sm_100a". */
+const char *dawn_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DAWN_H */

@@ -1,0 +1,258 @@
+"""dawn-b200: DAWN (arXiv 2208.04514) unweighted shortest paths on B200 (sm_100a).
+
+Thin ctypes binding over ``libdawn.so`` (C ABI in ``include/dawn.h``).  This module only
+marshals arguments: every step of the path (init, push/pull levels, direction choice,
+frontier-empty test, records) runs in the CUDA kernels of ``csrc/``.  PyTorch provides device
+memory (tensors), the current stream and ``torch.distributed`` for the APSP gather.
+
+There is no CPU fallback: if ``libdawn.so`` is missing or fails to load, importing the
+compute entry points raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+import torch
+
+__all__ = ["build", "Graph", "sssp", "msssp", "apsp", "apsp_shard", "DawnError", "UNREACHED",
+           "AUTO", "PUSH", "PULL", "REC_DTYPE", "records_to_numpy", "stats_to_dict",
+           "gather_records"]
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_CSRC = os.path.join(_HERE, "csrc")
+_LIB = os.path.join(_HERE, "libdawn.so")
+_INCLUDE = os.path.join(os.path.dirname(_HERE), "include")
+
+UNREACHED = 0xFFFFFFFF
+AUTO, PUSH, PULL = 0, 1, 2
+_VARIANTS = {"auto": AUTO, "push": PUSH, "pull": PULL, AUTO: AUTO, PUSH: PUSH, PULL: PULL}
+REC_DTYPE = np.dtype([("source", "<u4"), ("ecc", "<u4"), ("reached", "<u4"), ("pad", "<u4"),
+                      ("sum_dist", "<u8"), ("hash", "<u8")])
+NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
+              "-shared", "-Xcompiler", "-fPIC", "-Xcompiler", "-O3"]
+
+_STATUS = {0: "DAWN_OK", 1: "DAWN_ERR_INVALID_ARGUMENT", 2: "DAWN_ERR_BOUNDS",
+           3: "DAWN_ERR_CONFIG", 4: "DAWN_ERR_CAPACITY", 5: "DAWN_ERR_WORKSPACE",
+           6: "DAWN_ERR_INVALID_GRAPH", 7: "DAWN_ERR_CUDA"}
+
+
+class DawnError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{_STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+def _sources():
+    return [os.path.join(_CSRC, f) for f in sorted(os.listdir(_CSRC))
+            if f.endswith((".cu", ".cuh", ".h"))] + [os.path.join(_INCLUDE, "dawn.h")]
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    """Compile libdawn.so in-tree for sm_100a (nvcc; cross-compiles without a GPU)."""
+    srcs = _sources()
+    newest = max(os.path.getmtime(s) for s in srcs)
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < newest:
+        cmd = ["nvcc", *NVCC_FLAGS, os.path.join(_CSRC, "dawn.cu"), "-o", _LIB + ".tmp"]
+        if verbose:
+            cmd.insert(1, "-Xptxas=-v")
+        subprocess.check_call(cmd)
+        os.replace(_LIB + ".tmp", _LIB)
+    return _LIB
+
+
+_lib = None
+
+
+class _SsspStats(ctypes.Structure):
+    _fields_ = [("levels", ctypes.c_uint32), ("reached", ctypes.c_uint32),
+                ("edges_reach", ctypes.c_uint64), ("edges_examined", ctypes.c_uint64),
+                ("push_levels", ctypes.c_uint32), ("pull_levels", ctypes.c_uint32)]
+
+
+def lib():
+    """The loaded libdawn.so (raises if it cannot be loaded: no fallback path exists)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(_LIB):
+            raise ImportError(f"libdawn.so not built ({_LIB}); run paper_2208_04514_b200.build()")
+        L = ctypes.CDLL(_LIB)
+        vp, i64, u32, i32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_uint32, ctypes.c_int32
+        st = ctypes.c_int
+        L.dawn_workspace_bytes.restype = ctypes.c_size_t
+        L.dawn_workspace_bytes.argtypes = [i64, i64, u32]
+        L.dawn_graph_load_csr.restype = st
+        L.dawn_graph_load_csr.argtypes = [i64, i64, vp, vp, vp, vp, u32, vp, ctypes.c_size_t, vp,
+                                          ctypes.POINTER(vp)]
+        L.dawn_graph_destroy.restype = st
+        L.dawn_graph_destroy.argtypes = [vp]
+        L.dawn_graph_set_tuning.restype = st
+        L.dawn_graph_set_tuning.argtypes = [vp, ctypes.c_double, ctypes.c_double, ctypes.c_double]
+        L.dawn_sssp.restype = st
+        L.dawn_sssp.argtypes = [vp, i64, u32, vp, vp, vp]
+        L.dawn_msssp.restype = st
+        L.dawn_msssp.argtypes = [vp, vp, i64, vp, vp, vp]
+        L.dawn_apsp_shard.restype = st
+        L.dawn_apsp_shard.argtypes = [i64, i32, i32, vp, i64, ctypes.POINTER(ctypes.c_int64)]
+        L.dawn_apsp.restype = st
+        L.dawn_apsp.argtypes = [vp, vp, i64, i32, i32, vp, i64, ctypes.POINTER(ctypes.c_int64), vp]
+        L.dawn_last_error.restype = ctypes.c_char_p
+        L.dawn_last_error.argtypes = []
+        L.dawn_version.restype = ctypes.c_char_p
+        L.dawn_version.argtypes = []
+        _lib = L
+    return _lib
+
+
+def _check(status: int):
+    if status != 0:
+        raise DawnError(status, lib().dawn_last_error().decode())
+
+
+def _stream(stream=None) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def _dptr(t: torch.Tensor | None) -> int | None:
+    if t is None:
+        return None
+    assert t.is_cuda and t.is_contiguous(), "expected a contiguous CUDA tensor"
+    return t.data_ptr()
+
+
+class Graph:
+    """A device-resident graph handle (dawn_graph_load_csr).
+
+    row_ptr int64[n+1], col int32[m] (CUDA tensors, or numpy arrays that are uploaded).
+    For directed graphs pass the CSC (in_row_ptr, in_col) to enable pull / auto switching.
+    The handle keeps references to every tensor it uses (graph arrays + workspace).
+    """
+
+    def __init__(self, row_ptr, col, symmetric: bool, in_row_ptr=None, in_col=None,
+                 validate: bool = False, device=None, stream=None):
+        dev = torch.device(device) if device is not None else torch.device("cuda",
+                                                                            torch.cuda.current_device())
+        to = lambda a, dt: (a if isinstance(a, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(a))
+                            ).to(device=dev, dtype=dt).contiguous()
+        self.row_ptr = to(row_ptr, torch.int64)
+        self.col = to(col, torch.int32)
+        self.n = int(self.row_ptr.numel() - 1)
+        self.m = int(self.col.numel())
+        self.symmetric = bool(symmetric)
+        self.in_row_ptr = to(in_row_ptr, torch.int64) if in_row_ptr is not None else None
+        self.in_col = to(in_col, torch.int32) if in_col is not None else None
+        flags = (1 if symmetric else 0) | (2 if validate else 0)
+        nbytes = lib().dawn_workspace_bytes(self.n, self.m, flags)
+        if nbytes == 0:
+            raise DawnError(4, "unsupported graph size")
+        self.workspace = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+        self.device = dev
+        h = ctypes.c_void_p()
+        with torch.cuda.device(dev):
+            _check(lib().dawn_graph_load_csr(
+                self.n, self.m, _dptr(self.row_ptr), _dptr(self.col) if self.m else None,
+                _dptr(self.in_row_ptr), _dptr(self.in_col), flags, _dptr(self.workspace),
+                nbytes, _stream(stream), ctypes.byref(h)))
+        self._h = h
+
+    @property
+    def handle(self):
+        return self._h
+
+    def set_tuning(self, alpha: float = 0, beta: float = 0, ms_alpha: float = 0):
+        _check(lib().dawn_graph_set_tuning(self._h, alpha, beta, ms_alpha))
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h and _lib is not None:
+            _lib.dawn_graph_destroy(h)
+            self._h = None
+
+
+def sssp(g: Graph, source: int, variant="auto", stats: bool = False, out: torch.Tensor | None = None,
+         stream=None):
+    """dawn_sssp: distances as an int32 CUDA tensor (uint32 bits; UNREACHED reads as -1).
+
+    With stats=True also returns a 32-byte CUDA tensor holding dawn_sssp_stats
+    (see stats_to_dict)."""
+    dist = out if out is not None else torch.empty(g.n, dtype=torch.int32, device=g.device)
+    assert dist.numel() == g.n and dist.dtype == torch.int32
+    st = torch.zeros(4, dtype=torch.int64, device=g.device) if stats else None
+    _check(lib().dawn_sssp(g.handle, int(source), _VARIANTS[variant], _dptr(dist), _dptr(st),
+                           _stream(stream)))
+    return (dist, st) if stats else dist
+
+
+def stats_to_dict(st: torch.Tensor) -> dict:
+    raw = st.cpu().numpy().tobytes()
+    s = _SsspStats.from_buffer_copy(raw)
+    return {f: getattr(s, f) for f, _ in _SsspStats._fields_}
+
+
+def records_to_numpy(rec: torch.Tensor) -> np.ndarray:
+    return np.frombuffer(rec.cpu().numpy().tobytes(), dtype=REC_DTYPE)
+
+
+def msssp(g: Graph, sources, dist: bool = True, records: bool = True, stream=None):
+    """dawn_msssp (64-source bit-parallel kernel).  Returns (dist int32[k, n] | None,
+    records int64[k, 4] CUDA tensor (32-byte dawn_record rows) | None)."""
+    src = np.ascontiguousarray(np.asarray(sources, dtype=np.int64).reshape(-1))
+    k = len(src)
+    d = torch.empty((k, g.n), dtype=torch.int32, device=g.device) if dist else None
+    r = torch.empty((k, 4), dtype=torch.int64, device=g.device) if records else None
+    _check(lib().dawn_msssp(g.handle, src.ctypes.data_as(ctypes.c_void_p), k, _dptr(d), _dptr(r),
+                            _stream(stream)))
+    return d, r
+
+
+def apsp_shard(k: int, rank: int, world: int) -> np.ndarray:
+    """Indices into the source list owned by `rank` (dawn_apsp_shard: 64-batches, b mod world)."""
+    cnt = ctypes.c_int64(0)
+    _check(lib().dawn_apsp_shard(k, rank, world, None, 0, ctypes.byref(cnt)))
+    idx = np.empty(cnt.value, np.int64)
+    _check(lib().dawn_apsp_shard(k, rank, world, idx.ctypes.data_as(ctypes.c_void_p), len(idx),
+                                 ctypes.byref(cnt)))
+    return idx
+
+
+def apsp(g: Graph, sources, rank: int = 0, world: int = 1, group=None, gather: bool = True,
+         stream=None):
+    """dawn_apsp for this rank's shard, then (world > 1, gather=True) one NCCL all-gather of the
+    32-byte records.  Returns int64[k, 4] records in source order (gathered) or this rank's
+    shard records (gather=False)."""
+    src = np.ascontiguousarray(np.asarray(sources, dtype=np.int64).reshape(-1))
+    k = len(src)
+    mine = apsp_shard(k, rank, world)
+    cap = max(1, len(mine))
+    rec = torch.zeros((cap, 4), dtype=torch.int64, device=g.device)
+    nw = ctypes.c_int64(0)
+    _check(lib().dawn_apsp(g.handle, src.ctypes.data_as(ctypes.c_void_p), k, rank, world,
+                           _dptr(rec), cap, ctypes.byref(nw), _stream(stream)))
+    if world == 1 or not gather:
+        return rec[: nw.value]
+    return gather_records(rec[: nw.value], k, world, group)
+
+
+def gather_records(local: torch.Tensor, k: int, world: int, group=None) -> torch.Tensor:
+    """Reassemble per-rank APSP shards (int64[*, 4] record rows) into source order with one
+    all-gather (NCCL over NVLink on GPU tensors; gloo on CPU tensors).  The only collective of
+    the APSP path."""
+    import torch.distributed as dist
+    maxcap = len(apsp_shard(k, 0, world))  # rank 0 always owns the largest shard
+    buf = torch.zeros((maxcap, 4), dtype=torch.int64, device=local.device)
+    buf[: local.shape[0]] = local
+    parts = [torch.empty_like(buf) for _ in range(world)]
+    dist.all_gather(parts, buf, group=group)
+    full = torch.empty((k, 4), dtype=torch.int64, device=local.device)
+    for r in range(world):
+        idx = apsp_shard(k, r, world)
+        if len(idx):
+            full[torch.from_numpy(idx).to(local.device)] = parts[r][: len(idx)]
+    return full
+
+
+def version() -> str:
+    return lib().dawn_version().decode()

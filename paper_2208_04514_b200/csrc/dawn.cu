@@ -1,0 +1,374 @@
+// dawn.cu — libdawn.so: the C ABI of include/dawn.h over the sm_100a kernels.
+// Host side validates, lays out the caller's workspace and enqueues ONE cooperative persistent
+// kernel per call (no per-level host work).  No torch types cross this boundary.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/dawn.h"
+#include "layout.h"
+#include "ms64_kernel.cuh"
+#include "sssp_kernel.cuh"
+
+using namespace dawn;
+
+namespace {
+
+thread_local std::string g_err;
+
+dawn_status fail(dawn_status s, const std::string &msg) {
+  g_err = msg;
+  return s;
+}
+dawn_status cuda_fail(cudaError_t e, const char *where) {
+  return fail(DAWN_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+constexpr int kNT = 512;  // threads per CTA of the persistent kernels
+
+int env_int(const char *name, int dflt) {
+  const char *e = getenv(name);
+  return (e && *e) ? atoi(e) : dflt;
+}
+
+// ---------------------------------------------------------------- graph residency kernels
+__global__ void k_offsets32(const int64_t *__restrict__ in, uint32_t *__restrict__ out, int64_t n1) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n1;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = (uint32_t)in[i];
+}
+
+// noin bit v = (in-degree(v) == 0); counts vertices with in-degree > 0.
+__global__ void k_noin(const uint32_t *__restrict__ irp, uint32_t n, uint32_t nwords,
+                       uint32_t *__restrict__ noin, uint32_t *n_hasin) {
+  uint32_t local = 0;
+  for (uint32_t w = blockIdx.x * blockDim.x + threadIdx.x; w < nwords;
+       w += gridDim.x * blockDim.x) {
+    uint32_t bits = 0;
+    for (uint32_t b = 0; b < 32; ++b) {
+      const uint32_t v = w * 32 + b;
+      if (v < n && irp[v + 1] == irp[v]) bits |= 1u << b;
+      if (v < n && irp[v + 1] != irp[v]) local++;
+    }
+    noin[w] = bits;
+  }
+  local = warp_sum(local);
+  if ((threadIdx.x & 31) == 0 && local) atomicAdd(n_hasin, local);
+}
+
+// CSR invariants: row_ptr[0] = 0, monotone, row_ptr[n] = m, cols in [0, n).
+__global__ void k_validate(const int64_t *__restrict__ rp, const int32_t *__restrict__ col,
+                           int64_t n, int64_t m, uint32_t *err) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t t0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t0 == 0 && (rp[0] != 0 || rp[n] != m)) atomicOr(err, 1u);
+  for (int64_t i = t0; i < n; i += stride)
+    if (rp[i + 1] < rp[i]) atomicOr(err, 2u);
+  for (int64_t j = t0; j < m; j += stride)
+    if (col[j] < 0 || col[j] >= n) atomicOr(err, 4u);
+}
+
+}  // namespace
+
+struct dawn_graph_s {
+  int64_t n, m;
+  uint32_t flags;
+  int device;
+  int nsm;
+  char *ws;
+  Layout L;
+  const int32_t *col, *icol;
+  bool has_csc;
+  float alpha = 14.f, beta = 24.f, ms_alpha = 8.f;
+  int sssp_grid, ms_grid;
+};
+
+namespace {
+
+template <class T>
+T *at(dawn_graph g, size_t off) {
+  return reinterpret_cast<T *>(g->ws + off);
+}
+
+int grid_for(const void *fn, int nsm, const char *env_bps) {
+  int bps = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, fn, kNT, 0);
+  bps = std::max(1, std::min(bps, env_int(env_bps, 2)));
+  return std::min<int>(nsm * bps, (int)kMaxBlocks);
+}
+
+dawn_status set_device(dawn_graph g) {
+  cudaError_t e = cudaSetDevice(g->device);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+  return DAWN_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *dawn_last_error(void) { return g_err.c_str(); }
+const char *dawn_version(void) { return "dawn-b200 0.1 sm_100a"; }
+
+size_t dawn_workspace_bytes(int64_t n, int64_t m, uint32_t flags) {
+  if (n < 1 || n >= (int64_t(1) << 31) || m < 0 || m >= (int64_t(1) << 32)) return 0;
+  return make_layout(n, m, flags).total;
+}
+
+dawn_status dawn_graph_load_csr(int64_t n, int64_t m, const int64_t *row_ptr, const int32_t *col,
+                                const int64_t *in_row_ptr, const int32_t *in_col, uint32_t flags,
+                                void *workspace, size_t ws_bytes, void *stream, dawn_graph *out) {
+  g_err.clear();
+  if (!out) return fail(DAWN_ERR_INVALID_ARGUMENT, "out is NULL");
+  *out = nullptr;
+  if (n < 1 || m < 0) return fail(DAWN_ERR_INVALID_ARGUMENT, "n must be >= 1 and m >= 0");
+  if (n >= (int64_t(1) << 31) || m >= (int64_t(1) << 32))
+    return fail(DAWN_ERR_CAPACITY, "n must be < 2^31 and m < 2^32 (32-bit offsets)");
+  if (flags & ~uint32_t(DAWN_GRAPH_SYMMETRIC | DAWN_GRAPH_VALIDATE))
+    return fail(DAWN_ERR_INVALID_ARGUMENT, "unknown graph flag");
+  if (!row_ptr || (!col && m > 0) || !workspace)
+    return fail(DAWN_ERR_INVALID_ARGUMENT, "row_ptr/col/workspace is NULL");
+  const bool sym = flags & DAWN_GRAPH_SYMMETRIC;
+  const bool has_csc = sym || (in_row_ptr && (in_col || m == 0));
+  if (!sym && ((in_row_ptr == nullptr) != (in_col == nullptr) && m > 0))
+    return fail(DAWN_ERR_INVALID_ARGUMENT, "in_row_ptr and in_col must both be given or NULL");
+  if (reinterpret_cast<uintptr_t>(workspace) & 255)
+    return fail(DAWN_ERR_INVALID_ARGUMENT, "workspace must be 256-byte aligned");
+  Layout L = make_layout(n, m, flags);
+  if (ws_bytes < L.total)
+    return fail(DAWN_ERR_WORKSPACE, "workspace too small: need " + std::to_string(L.total) +
+                                        " bytes, got " + std::to_string(ws_bytes));
+  cudaPointerAttributes pa{};
+  cudaError_t e = cudaPointerGetAttributes(&pa, workspace);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaPointerGetAttributes(workspace)");
+  if (pa.type != cudaMemoryTypeDevice)
+    return fail(DAWN_ERR_INVALID_ARGUMENT, "workspace is not device memory");
+  auto *g = new dawn_graph_s;
+  g->n = n;
+  g->m = m;
+  g->flags = flags;
+  g->device = pa.device;
+  g->ws = static_cast<char *>(workspace);
+  g->L = L;
+  g->col = col;
+  g->has_csc = has_csc;
+  g->icol = sym ? col : in_col;
+  if ((e = cudaSetDevice(g->device)) != cudaSuccess) { delete g; return cuda_fail(e, "cudaSetDevice"); }
+  cudaDeviceGetAttribute(&g->nsm, cudaDevAttrMultiProcessorCount, g->device);
+  g->alpha = (float)env_int("DAWN_ALPHA", 14);
+  g->beta = (float)env_int("DAWN_BETA", 24);
+  g->ms_alpha = (float)env_int("DAWN_MS_ALPHA", 8);
+  g->sssp_grid = grid_for((const void *)k_sssp<kNT>, g->nsm, "DAWN_SSSP_BPS");
+  g->ms_grid = grid_for((const void *)k_ms64<kNT>, g->nsm, "DAWN_MS_BPS");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const uint32_t nwords = (uint32_t)((n + 31) / 32);
+  const int blocks = std::max(1, std::min<int>(g->nsm * 4, (int)((n + 255) / 256)));
+  cudaMemsetAsync(g->ws + L.ctrl, 0, sizeof(Ctrl), st);
+  cudaMemsetAsync(g->ws + L.msctrl, 0, sizeof(MsCtrl), st);
+  if (flags & DAWN_GRAPH_VALIDATE) {
+    k_validate<<<blocks, 256, 0, st>>>(row_ptr, col, n, m, &at<Ctrl>(g, L.ctrl)->err);
+    if (!sym && has_csc && m > 0)
+      k_validate<<<blocks, 256, 0, st>>>(in_row_ptr, in_col, n, m, &at<Ctrl>(g, L.ctrl)->err);
+    uint32_t err = 0;
+    cudaMemcpyAsync(&err, &at<Ctrl>(g, L.ctrl)->err, 4, cudaMemcpyDeviceToHost, st);
+    if ((e = cudaStreamSynchronize(st)) != cudaSuccess) { delete g; return cuda_fail(e, "validate"); }
+    if (err) {
+      delete g;
+      return fail(DAWN_ERR_INVALID_GRAPH, std::string("CSR invariant violated:") +
+                                              ((err & 1) ? " row_ptr[0]!=0 or row_ptr[n]!=m" : "") +
+                                              ((err & 2) ? " row_ptr not monotone" : "") +
+                                              ((err & 4) ? " column id out of range" : ""));
+    }
+  }
+  k_offsets32<<<blocks, 256, 0, st>>>(row_ptr, at<uint32_t>(g, L.rp), n + 1);
+  const uint32_t *irp = at<uint32_t>(g, L.rp);
+  if (!sym) {
+    if (has_csc) {
+      k_offsets32<<<blocks, 256, 0, st>>>(in_row_ptr, at<uint32_t>(g, L.irp), n + 1);
+      irp = at<uint32_t>(g, L.irp);
+    } else {
+      // no CSC: treat every vertex as possibly reachable (noin = 0) — push only
+      cudaMemsetAsync(g->ws + L.irp, 0, 4 * (size_t)(n + 1), st);
+    }
+  }
+  if (sym || has_csc) {
+    k_noin<<<blocks, 256, 0, st>>>(irp, (uint32_t)n, nwords, at<uint32_t>(g, L.noin),
+                                   &at<Ctrl>(g, L.ctrl)->n_hasin);
+  } else {
+    cudaMemsetAsync(g->ws + L.noin, 0, 4 * (size_t)nwords, st);
+    uint32_t nh = (uint32_t)n;
+    cudaMemcpyAsync(&at<Ctrl>(g, L.ctrl)->n_hasin, &nh, 4, cudaMemcpyHostToDevice, st);
+    cudaStreamSynchronize(st);
+  }
+  if ((e = cudaGetLastError()) != cudaSuccess) { delete g; return cuda_fail(e, "graph load"); }
+  *out = g;
+  return DAWN_OK;
+}
+
+dawn_status dawn_graph_destroy(dawn_graph g) {
+  delete g;
+  return DAWN_OK;
+}
+
+dawn_status dawn_graph_set_tuning(dawn_graph g, double alpha, double beta, double ms_alpha) {
+  if (!g) return fail(DAWN_ERR_INVALID_ARGUMENT, "graph is NULL");
+  if (alpha > 0) g->alpha = (float)alpha;
+  if (beta > 0) g->beta = (float)beta;
+  if (ms_alpha > 0) g->ms_alpha = (float)ms_alpha;
+  return DAWN_OK;
+}
+
+dawn_status dawn_sssp(dawn_graph g, int64_t source, uint32_t variant, uint32_t *dist,
+                      dawn_sssp_stats *stats, void *stream) {
+  g_err.clear();
+  if (!g || !dist) return fail(DAWN_ERR_INVALID_ARGUMENT, "graph or dist is NULL");
+  if (variant > DAWN_PULL) return fail(DAWN_ERR_INVALID_ARGUMENT, "unknown variant");
+  if (source < 0 || source >= g->n)
+    return fail(DAWN_ERR_BOUNDS, "source " + std::to_string(source) + " not in [0, n)");
+  if (variant == DAWN_PULL && !g->has_csc)
+    return fail(DAWN_ERR_CONFIG, "PULL needs CSC (in-edges) on a directed graph");
+  dawn_status s = set_device(g);
+  if (s != DAWN_OK) return s;
+  const Layout &L = g->L;
+  SsspParams p{};
+  p.n = (uint32_t)g->n;
+  p.nwords = (uint32_t)((g->n + 31) / 32);
+  p.m = (unsigned long long)g->m;
+  p.rp = at<uint32_t>(g, L.rp);
+  p.irp = at<uint32_t>(g, L.irp);
+  p.col = g->col;
+  p.icol = g->icol;
+  p.noin = at<uint32_t>(g, L.noin);
+  p.vis = at<uint32_t>(g, L.vis);
+  p.fb[0] = at<uint32_t>(g, L.fb0);
+  p.fb[1] = at<uint32_t>(g, L.fb1);
+  for (int i = 0; i < 2; ++i) {
+    p.Lv[i] = at<uint32_t>(g, L.Lv[i]);
+    p.Lsd[i] = at<uint2>(g, L.Lsd[i]);
+    p.Hv[i] = at<uint32_t>(g, L.Hv[i]);
+    p.Hsd[i] = at<uint2>(g, L.Hsd[i]);
+    p.Hp[i] = at<uint32_t>(g, L.Hp[i]);
+    p.Pm[i] = at<uint32_t>(g, L.Pm[i]);
+  }
+  p.ctrl = at<Ctrl>(g, L.ctrl);
+  p.dist = dist;
+  p.stats = stats;
+  p.source = (uint32_t)source;
+  p.variant = variant;
+  p.can_pull = g->has_csc ? 1u : 0u;
+  p.sym = (g->flags & DAWN_GRAPH_SYMMETRIC) ? 1u : 0u;
+  p.alpha = g->alpha;
+  p.beta = g->beta;
+  int grid = g->sssp_grid;
+  const int small_m = env_int("DAWN_SMALL_M", 1 << 15);
+  if (g->m + g->n <= small_m) grid = 1;  // tiny graphs: one CTA, barriers are __syncthreads
+  void *args[] = {&p};
+  cudaError_t e = cudaLaunchCooperativeKernel((const void *)k_sssp<kNT>, dim3(grid), dim3(kNT),
+                                              args, 0, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "k_sssp launch");
+  return DAWN_OK;
+}
+
+static dawn_status launch_ms(dawn_graph g, const std::vector<uint32_t> &src, uint32_t *dist,
+                             dawn_record *rec, cudaStream_t st) {
+  const Layout &L = g->L;
+  for (size_t off = 0; off < src.size(); off += (L.srccap / 64) * 64) {
+    const size_t cnt = std::min(src.size() - off, (size_t)((L.srccap / 64) * 64));
+    cudaError_t e = cudaMemcpyAsync(g->ws + L.srcbuf, src.data() + off, 4 * cnt,
+                                    cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) return cuda_fail(e, "source upload");
+    MsParams p{};
+    p.n = (uint32_t)g->n;
+    p.nwords = (uint32_t)((g->n + 31) / 32);
+    p.m = (unsigned long long)g->m;
+    p.rp = at<uint32_t>(g, L.rp);
+    p.irp = at<uint32_t>(g, L.irp);
+    p.col = g->col;
+    p.icol = g->icol;
+    p.seen = at<unsigned long long>(g, L.seen);
+    p.F[0] = at<unsigned long long>(g, L.F0);
+    p.F[1] = at<unsigned long long>(g, L.F1);
+    p.nxt = at<unsigned long long>(g, L.nxt);
+    p.ctrl = at<MsCtrl>(g, L.msctrl);
+    p.sources = at<uint32_t>(g, L.srcbuf);
+    p.count = (uint32_t)cnt;
+    p.rec = rec ? rec + off : nullptr;
+    p.dist = dist ? dist + off * (size_t)g->n : nullptr;
+    p.can_pull = g->has_csc ? 1u : 0u;
+    p.sym = (g->flags & DAWN_GRAPH_SYMMETRIC) ? 1u : 0u;
+    p.ms_alpha = g->ms_alpha;
+    p.part = at<uint4>(g, L.part);
+    int grid = g->ms_grid;
+    const int small_m = env_int("DAWN_SMALL_M", 1 << 15);
+    if (g->m + g->n <= small_m) grid = 1;
+    void *args[] = {&p};
+    e = cudaLaunchCooperativeKernel((const void *)k_ms64<kNT>, dim3(grid), dim3(kNT), args, 0, st);
+    if (e != cudaSuccess) return cuda_fail(e, "k_ms64 launch");
+  }
+  return DAWN_OK;
+}
+
+dawn_status dawn_msssp(dawn_graph g, const int64_t *sources, int64_t k, uint32_t *dist,
+                       dawn_record *rec, void *stream) {
+  g_err.clear();
+  if (!g || (!sources && k > 0) || k < 0) return fail(DAWN_ERR_INVALID_ARGUMENT, "bad arguments");
+  for (int64_t i = 0; i < k; ++i)
+    if (sources[i] < 0 || sources[i] >= g->n)
+      return fail(DAWN_ERR_BOUNDS, "sources[" + std::to_string(i) + "] = " +
+                                       std::to_string(sources[i]) + " not in [0, n)");
+  if (dist && (double)k * (double)g->n >= 1099511627776.0)
+    return fail(DAWN_ERR_CAPACITY, "k*n too large for a dense output");
+  if (k == 0) return DAWN_OK;
+  dawn_status s = set_device(g);
+  if (s != DAWN_OK) return s;
+  std::vector<uint32_t> src(sources, sources + k);
+  return launch_ms(g, src, dist, rec, static_cast<cudaStream_t>(stream));
+}
+
+dawn_status dawn_apsp_shard(int64_t k, int32_t rank, int32_t world, int64_t *idx, int64_t cap,
+                            int64_t *count) {
+  g_err.clear();
+  if (k < 0 || world < 1 || rank < 0 || rank >= world || !count)
+    return fail(DAWN_ERR_INVALID_ARGUMENT, "need k >= 0, 0 <= rank < world");
+  int64_t c = 0;
+  const int64_t nb = (k + 63) / 64;
+  for (int64_t b = rank; b < nb; b += world) {
+    const int64_t e = std::min(k, (b + 1) * 64);
+    for (int64_t i = b * 64; i < e; ++i) {
+      if (idx && c < cap) idx[c] = i;
+      ++c;
+    }
+  }
+  *count = c;
+  if (idx && c > cap) return fail(DAWN_ERR_CAPACITY, "idx capacity too small");
+  return DAWN_OK;
+}
+
+dawn_status dawn_apsp(dawn_graph g, const int64_t *sources, int64_t k, int32_t rank, int32_t world,
+                      dawn_record *rec, int64_t cap, int64_t *n_written, void *stream) {
+  g_err.clear();
+  if (!g || !rec || !n_written || (!sources && k > 0) || k < 0)
+    return fail(DAWN_ERR_INVALID_ARGUMENT, "bad arguments");
+  if (world < 1 || rank < 0 || rank >= world)
+    return fail(DAWN_ERR_INVALID_ARGUMENT, "need 0 <= rank < world");
+  for (int64_t i = 0; i < k; ++i)
+    if (sources[i] < 0 || sources[i] >= g->n)
+      return fail(DAWN_ERR_BOUNDS, "sources[" + std::to_string(i) + "] not in [0, n)");
+  std::vector<uint32_t> mine;
+  const int64_t nb = (k + 63) / 64;
+  for (int64_t b = rank; b < nb; b += world)
+    for (int64_t i = b * 64; i < std::min(k, (b + 1) * 64); ++i) mine.push_back((uint32_t)sources[i]);
+  *n_written = (int64_t)mine.size();
+  if ((int64_t)mine.size() > cap) return fail(DAWN_ERR_CAPACITY, "rec capacity too small");
+  if (mine.empty()) return DAWN_OK;
+  dawn_status s = set_device(g);
+  if (s != DAWN_OK) return s;
+  return launch_ms(g, mine, nullptr, rec, static_cast<cudaStream_t>(stream));
+}
+
+}  // extern "C"

@@ -1,0 +1,229 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, element by element.
+
+Bar (BASELINE.json north_star): bit-exact distances, tolerance 0; records bit-exact.
+Every test here runs on a B200 via gpurun (marker `gpu`).
+"""
+import numpy as np
+import pytest
+import torch
+
+import graphgen
+import oracle
+import paper_2208_04514_b200 as dawn
+
+pytestmark = pytest.mark.gpu
+UNR = oracle.UNREACHED
+VARIANTS = ("auto", "push", "pull")
+
+
+def dev_graph(g: graphgen.Graph, csc: bool = True):
+    if g.symmetric:
+        return dawn.Graph(g.row_ptr, g.col, True, validate=True)
+    if csc:
+        p, i = g.transpose()
+        return dawn.Graph(g.row_ptr, g.col, False, p, i, validate=True)
+    return dawn.Graph(g.row_ptr, g.col, False, validate=True)
+
+
+def gpu_dist(G, s, variant="auto", stats=False):
+    r = dawn.sssp(G, s, variant, stats=stats)
+    if stats:
+        d, st = r
+        return d.cpu().numpy().view(np.uint32), dawn.stats_to_dict(st)
+    return r.cpu().numpy().view(np.uint32)
+
+
+def check_sssp(g, G, sources, variants=VARIANTS, oracle_fn="bfs_fifo"):
+    for s in sources:
+        s = int(s)
+        exp, ost = getattr(oracle, oracle_fn)(g.n, g.row_ptr, g.col, s)
+        rec, er = oracle.record(g.n, g.row_ptr, s, exp)
+        for v in variants:
+            d, st = gpu_dist(G, s, v, stats=True)
+            bad = np.nonzero(d != exp)[0]
+            assert len(bad) == 0, (g.name, s, v, bad[:5], d[bad[:5]], exp[bad[:5]])
+            assert st["levels"] == int(rec["ecc"]), (g.name, s, v, st)
+            assert st["reached"] == int(rec["reached"]), (g.name, s, v, st)
+            assert st["edges_reach"] == er, (g.name, s, v, st, er)
+            assert st["push_levels"] + st["pull_levels"] >= st["levels"]
+
+
+# ------------------------------------------------------------------ hand fixtures / corpus
+def test_golden_fixtures_all_variants():
+    import json, os
+    gold = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "records.json")))
+    for fx in gold["fixtures"]:
+        g = graphgen.from_edges(fx["n"], fx["edges"])
+        G = dev_graph(g)
+        for c in fx["cases"]:
+            for v in VARIANTS:
+                assert gpu_dist(G, c["src"], v).tolist() == c["dist"], (fx["name"], v)
+        srcs = [c["src"] for c in fx["cases"]]
+        d, r = dawn.msssp(G, srcs)
+        recs = dawn.records_to_numpy(r)
+        for i, c in enumerate(fx["cases"]):
+            assert d[i].cpu().numpy().view(np.uint32).tolist() == c["dist"]
+            assert int(recs[i]["ecc"]) == c["ecc"] and int(recs[i]["reached"]) == c["reached"]
+            assert int(recs[i]["sum_dist"]) == c["sum_dist"]
+            assert int(recs[i]["hash"]) == int(c["hash"], 16)
+
+
+def test_er_corpus_all_sources_all_variants():
+    for n in (8, 33, 100, 256):
+        for p in (0.01, 0.05, 0.1, 0.3):
+            g = graphgen.er_prob(n, p, 77 + n)
+            G = dev_graph(g)
+            check_sssp(g, G, range(0, n, max(1, n // 16)))
+
+
+def test_directed_without_csc_is_push_only():
+    g = graphgen.er_prob(64, 0.05, 5)
+    G = dev_graph(g, csc=False)
+    check_sssp(g, G, range(0, 64, 9), variants=("auto", "push"))
+    with pytest.raises(dawn.DawnError) as e:
+        dawn.sssp(G, 0, "pull")
+    assert e.value.status == 3
+
+
+def test_closed_forms_grid_hypercube_cycle_path():
+    W, H = 300, 170
+    g = graphgen.grid(W, H)
+    G = dev_graph(g)
+    r, c = np.divmod(np.arange(W * H), W)
+    for s in (0, W * H - 1, (H // 2) * W + W // 2):
+        r0, c0 = divmod(s, W)
+        exp = (np.abs(r - r0) + np.abs(c - c0)).astype(np.uint32)
+        for v in VARIANTS:
+            assert np.array_equal(gpu_dist(G, s, v), exp), (s, v)
+    k = 12
+    n = 1 << k
+    hc = graphgen.from_edges(n, [[u, u ^ (1 << b)] for u in range(n) for b in range(k)])
+    Gh = dev_graph(hc)
+    for s in (0, 1234, n - 1):
+        exp = np.array([bin(v ^ s).count("1") for v in range(n)], np.uint32)
+        for v in VARIANTS:
+            assert np.array_equal(gpu_dist(Gh, s, v), exp)
+    n = 5000
+    cyc = graphgen.from_edges(n, [[v, (v + 1) % n] for v in range(n)])
+    Gc = dev_graph(cyc)
+    for v in VARIANTS:
+        d = gpu_dist(Gc, 17, v)
+        assert np.array_equal(d, ((np.arange(n) - 17) % n).astype(np.uint32))
+    # path: eps = n - 1 hits the loop cap exactly (reading Q8)
+    pth = graphgen.from_edges(n, [[v, v + 1] for v in range(n - 1)])
+    Gp = dev_graph(pth)
+    for v in VARIANTS:
+        assert np.array_equal(gpu_dist(Gp, 0, v), np.arange(n, dtype=np.uint32))
+
+
+def test_edge_cases():
+    g1 = graphgen.from_edges(1, np.zeros((0, 2)))
+    G1 = dev_graph(g1)
+    for v in VARIANTS:
+        assert gpu_dist(G1, 0, v).tolist() == [0]
+    g2 = graphgen.from_edges(2, np.zeros((0, 2)))
+    G2 = dev_graph(g2)
+    assert gpu_dist(G2, 1).tolist() == [UNR, 0]          # s = n-1 valid
+    with pytest.raises(dawn.DawnError) as e:
+        dawn.sssp(G2, 2)                                   # s = n -> BOUNDS
+    assert e.value.status == 2
+    with pytest.raises(dawn.DawnError) as e:
+        dawn.msssp(G2, [0, 5])
+    assert e.value.status == 2
+    # star: leaf source (degree 0) and hub source
+    star = graphgen.from_edges(300, [[0, k] for k in range(1, 300)])
+    Gs = dev_graph(star)
+    check_sssp(star, Gs, [0, 1, 299])
+
+
+def test_hub_rows_and_repeated_sources():
+    # a hub with 70K out-arcs (> 64K, SURVEY §8(c) edge cases) inside a sparse graph
+    n = 80000
+    edges = [[0, v] for v in range(1, 70001)] + [[v, v + 1] for v in range(70000, n - 1)]
+    g = graphgen.from_edges(n, edges, symmetric=True)
+    G = dev_graph(g)
+    check_sssp(g, G, [0, 5, 79999])
+    d, r = dawn.msssp(G, [5, 5, 0, 5])
+    recs = dawn.records_to_numpy(r)
+    assert recs[0].tobytes() == recs[1].tobytes() == recs[3].tobytes()
+    assert torch.equal(d[0], d[1]) and torch.equal(d[0], d[3])
+
+
+@pytest.mark.parametrize("scale", [10, 14, 16])
+def test_kron_sampled_sources(scale):
+    g = graphgen.kron(scale, 16)
+    G = dev_graph(g)
+    srcs = list(g.sample_sources(6, seed=scale)) + [int(np.argmax(g.degrees()))]
+    check_sssp(g, G, srcs)
+    # isolated source
+    iso = np.nonzero(g.degrees() == 0)[0]
+    if len(iso):
+        check_sssp(g, G, [int(iso[0])])
+
+
+def test_config_c1_er_1000_8000():
+    g = graphgen.config_graph("C1")
+    G = dev_graph(g)
+    check_sssp(g, G, [0], oracle_fn="sovm")
+    check_sssp(g, G, range(1, 1000, 37))
+
+
+# ------------------------------------------------------------------ multi-source / APSP
+def _check_records(g, srcs, recs):
+    exp = oracle.records(g.n, g.row_ptr, g.col, srcs)
+    for i in range(len(srcs)):
+        assert recs[i].tobytes() == exp[i].tobytes(), (i, srcs[i], recs[i], exp[i])
+
+
+@pytest.mark.parametrize("k", [1, 63, 64, 70, 130])
+def test_msssp_dist_and_records(k):
+    g = graphgen.kron(13, 16)
+    G = dev_graph(g)
+    srcs = np.concatenate([g.sample_sources(k - 1, seed=k), [int(np.argmin(g.degrees()))]])
+    d, r = dawn.msssp(G, srcs)
+    D = d.cpu().numpy().view(np.uint32)
+    for i in range(0, k, max(1, k // 9)):
+        exp = oracle.bfs_fifo(g.n, g.row_ptr, g.col, int(srcs[i]))[0]
+        assert np.array_equal(D[i], exp), i
+    _check_records(g, srcs, dawn.records_to_numpy(r))
+
+
+def test_msssp_directed_er():
+    g = graphgen.config_graph("C1")
+    G = dev_graph(g)
+    srcs = np.arange(0, 1000, 7)
+    d, r = dawn.msssp(G, srcs)
+    D = d.cpu().numpy().view(np.uint32)
+    for i, s in enumerate(srcs):
+        assert np.array_equal(D[i], oracle.bfs_fifo(g.n, g.row_ptr, g.col, int(s))[0])
+    _check_records(g, srcs, dawn.records_to_numpy(r))
+
+
+def test_apsp_shards_cover_and_match():
+    g = graphgen.kron(12, 16)
+    G = dev_graph(g)
+    verts, e_wcc = g.largest_wcc()
+    full = dawn.records_to_numpy(dawn.apsp(G, verts))
+    _check_records(g, verts, full)
+    # E10/E11 property on every source of the largest WCC of a symmetric graph
+    assert np.all(full["reached"] == len(verts) - 1)
+    for world in (2, 3, 8):
+        parts = [dawn.records_to_numpy(dawn.apsp(G, verts, rank=r, world=world, gather=False))
+                 for r in range(world)]
+        re = np.empty(len(verts), full.dtype)
+        for r in range(world):
+            re[dawn.apsp_shard(len(verts), r, world)] = parts[r]
+        assert re.tobytes() == full.tobytes()
+
+
+def test_determinism():
+    g = graphgen.kron(15, 16)
+    G = dev_graph(g)
+    s = int(g.sample_sources(1, 3)[0])
+    a = [gpu_dist(G, s, v) for v in VARIANTS]
+    for _ in range(3):
+        for i, v in enumerate(VARIANTS):
+            assert np.array_equal(gpu_dist(G, s, v), a[i])
+    d1, r1 = dawn.msssp(G, g.sample_sources(100, 4))
+    d2, r2 = dawn.msssp(G, g.sample_sources(100, 4))
+    assert torch.equal(d1, d2) and torch.equal(r1, r2)
