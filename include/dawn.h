@@ -46,8 +46,10 @@ typedef enum {
 /* Graph flags. */
 enum {
   DAWN_GRAPH_SYMMETRIC = 1, /* arcs come in both directions: CSC == CSR, in_* may be NULL   */
-  DAWN_GRAPH_VALIDATE = 2   /* check row_ptr monotone, row_ptr[0]=0, row_ptr[n]=m, cols in
+  DAWN_GRAPH_VALIDATE = 2,  /* check row_ptr monotone, row_ptr[0]=0, row_ptr[n]=m, cols in
                                range; synchronises `stream` once                           */
+  DAWN_GRAPH_TRACE = 4      /* dawn_sssp records one dawn_trace_rec per level (device
+                               %globaltimer), readable with dawn_graph_trace               */
 };
 
 /* Direction variants of one level step. */
@@ -78,6 +80,18 @@ typedef struct {
   uint32_t source, ecc, reached, pad;
   uint64_t sum_dist, hash;
 } dawn_record;
+
+/* Per-level trace of the last dawn_sssp call on a graph loaded with DAWN_GRAPH_TRACE. */
+typedef struct {
+  uint64_t t_ns;     /* device %globaltimer when level `level` started (after its barrier)   */
+  uint32_t level;    /* L: the frontier holds the vertices at distance L                     */
+  uint32_t dir;      /* 0 push, 1 pull, 2 = stop (frontier empty / all reachable found)      */
+  uint32_t nf;       /* |frontier L|                                                          */
+  uint32_t rep;      /* frontier representation before the level: 0 queue, 1 bitmap          */
+  uint64_t mf;       /* sum of out-degrees of frontier L                                      */
+  uint64_t t_first;  /* %globaltimer when the first CTA finished level L's work               */
+  uint64_t t_last;   /* %globaltimer when the last CTA finished level L's work (pre-barrier)  */
+} dawn_trace_rec;
 
 typedef struct dawn_graph_s *dawn_graph;
 
@@ -110,9 +124,10 @@ dawn_status dawn_graph_load_csr(int64_t n, int64_t m, const int64_t *row_ptr, co
 dawn_status dawn_graph_destroy(dawn_graph g);
 
 /* Direction-switch thresholds for DAWN_AUTO (Beamer-style, cited by the paper at L123):
- * push -> pull when alpha * m_f > m_u ; pull -> push when beta * n_f < n and shrinking.
- * Defaults alpha = 14, beta = 24. ms_alpha: 64-source kernel pulls when
- * ms_alpha * m_active > m (default 8).  Values <= 0 keep the current setting.               */
+ * push -> pull when alpha * m_f > m_u and the frontier grows; pull -> push when
+ * beta * n_f < n and it shrinks.  Defaults alpha = 4 (measured on Kronecker-20, B200),
+ * beta = 24.  ms_alpha: the 64-source kernel pulls when ms_alpha * m_active > m_unsettled
+ * (default 2).  Values <= 0 keep the current setting.                                         */
 dawn_status dawn_graph_set_tuning(dawn_graph g, double alpha, double beta, double ms_alpha);
 
 /*
@@ -158,6 +173,12 @@ dawn_status dawn_apsp_shard(int64_t k, int32_t rank, int32_t world, int64_t *idx
  */
 dawn_status dawn_apsp(dawn_graph g, const int64_t *sources, int64_t k, int32_t rank, int32_t world,
                       dawn_record *rec, int64_t cap, int64_t *n_written, void *stream);
+
+/* Copy the per-level trace of the last dawn_sssp call (graph loaded with DAWN_GRAPH_TRACE)
+ * into host_out[0 .. min(cap, levels+1)); *count receives the number of records.  Synchronises
+ * `stream`.  CONFIG if the graph was loaded without DAWN_GRAPH_TRACE.                        */
+dawn_status dawn_graph_trace(dawn_graph g, dawn_trace_rec *host_out, int64_t cap, int64_t *count,
+                             void *stream);
 
 /* Thread-local description of the last error of this thread ("" if none). */
 const char *dawn_last_error(void);

@@ -100,6 +100,8 @@ def lib():
         L.dawn_apsp.argtypes = [vp, vp, i64, i32, i32, vp, i64, ctypes.POINTER(ctypes.c_int64), vp]
         L.dawn_last_error.restype = ctypes.c_char_p
         L.dawn_last_error.argtypes = []
+        L.dawn_graph_trace.restype = st
+        L.dawn_graph_trace.argtypes = [vp, vp, i64, ctypes.POINTER(ctypes.c_int64), vp]
         L.dawn_version.restype = ctypes.c_char_p
         L.dawn_version.argtypes = []
         _lib = L
@@ -132,7 +134,7 @@ class Graph:
     """
 
     def __init__(self, row_ptr, col, symmetric: bool, in_row_ptr=None, in_col=None,
-                 validate: bool = False, device=None, stream=None):
+                 validate: bool = False, device=None, stream=None, trace: bool = False):
         dev = torch.device(device) if device is not None else torch.device("cuda",
                                                                             torch.cuda.current_device())
         to = lambda a, dt: (a if isinstance(a, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(a))
@@ -144,7 +146,7 @@ class Graph:
         self.symmetric = bool(symmetric)
         self.in_row_ptr = to(in_row_ptr, torch.int64) if in_row_ptr is not None else None
         self.in_col = to(in_col, torch.int32) if in_col is not None else None
-        flags = (1 if symmetric else 0) | (2 if validate else 0)
+        flags = (1 if symmetric else 0) | (2 if validate else 0) | (4 if trace else 0)
         nbytes = lib().dawn_workspace_bytes(self.n, self.m, flags)
         if nbytes == 0:
             raise DawnError(4, "unsupported graph size")
@@ -161,6 +163,16 @@ class Graph:
     @property
     def handle(self):
         return self._h
+
+    def trace(self, stream=None) -> np.ndarray:
+        """Per-level trace of the last sssp call (graph built with trace=True)."""
+        dt = np.dtype([("t_ns", "<u8"), ("level", "<u4"), ("dir", "<u4"), ("nf", "<u4"),
+                       ("rep", "<u4"), ("mf", "<u8"), ("t_first", "<u8"), ("t_last", "<u8")])
+        buf = np.zeros(1 << 16, dt)
+        cnt = ctypes.c_int64(0)
+        _check(lib().dawn_graph_trace(self._h, buf.ctypes.data_as(ctypes.c_void_p), len(buf),
+                                      ctypes.byref(cnt), _stream(stream)))
+        return buf[: min(cnt.value, len(buf))].copy()
 
     def set_tuning(self, alpha: float = 0, beta: float = 0, ms_alpha: float = 0):
         _check(lib().dawn_graph_set_tuning(self._h, alpha, beta, ms_alpha))

@@ -64,31 +64,51 @@ __device__ __forceinline__ void red_or64(unsigned long long *p, unsigned long lo
   asm volatile("red.relaxed.gpu.global.or.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
-// Sense-free generation barrier across all CTAs of a cooperative launch.
-// count/gen live in the workspace control block; gen only grows.
+__device__ __forceinline__ unsigned long long ld_acquire64(const unsigned long long *p) {
+  unsigned long long r;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(r) : "l"(p) : "memory");
+  return r;
+}
+__device__ __forceinline__ void red_add_release64(unsigned long long *p, unsigned long long v) {
+  asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void fence_acq_rel_gpu() {
+  asm volatile("fence.acq_rel.gpu;" ::: "memory");
+}
+
+// Grid barrier over all CTAs of a cooperative launch: a monotonic 64-bit arrival counter.
+// Barrier k of a launch waits for mono >= k * nblocks (measured 1.4 us at 148 CTAs on B200,
+// vs 2.6 us for a generation/reset barrier: scripts/barrier_bench.cu).  The last CTA to leave
+// the kernel resets the counter (grid_exit), so every launch starts from 0.
 struct GridBarrier {
-  uint32_t count;
-  uint32_t gen;
+  unsigned long long mono;
+  uint32_t exit_count;
+  uint32_t pad;
 };
 
-__device__ __forceinline__ void grid_sync(GridBarrier *b, uint32_t nblocks) {
+__device__ __forceinline__ void grid_sync(GridBarrier *b, uint32_t nblocks,
+                                          unsigned long long &target) {
   __syncthreads();
   if (threadIdx.x == 0) {
+    target += nblocks;
     if (nblocks > 1) {
-      uint32_t gen = ld_acquire(&b->gen);
-      __threadfence();
-      uint32_t arrived = atomicAdd(&b->count, 1u);
-      if (arrived == nblocks - 1) {
-        b->count = 0;
-        st_release(&b->gen, gen + 1);
-      } else {
-        while (ld_acquire(&b->gen) == gen) {
-        }
+      red_add_release64(&b->mono, 1ull);
+      while (ld_acquire64(&b->mono) < target) {
       }
     }
-    __threadfence();  // invalidates this SM's L1 (CCTL.IVALL): later weak loads see peers' data
+    fence_acq_rel_gpu();  // also invalidates this SM's L1: later weak loads see peers' data
   }
   __syncthreads();
+}
+
+// Call once per CTA after its last grid_sync.
+__device__ __forceinline__ void grid_exit(GridBarrier *b, uint32_t nblocks) {
+  if (threadIdx.x == 0 && nblocks > 1) {
+    if (atomicAdd(&b->exit_count, 1u) == nblocks - 1) {
+      b->mono = 0;
+      b->exit_count = 0;
+    }
+  }
 }
 
 __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t x) {

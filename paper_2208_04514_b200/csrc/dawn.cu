@@ -73,6 +73,89 @@ __global__ void k_validate(const int64_t *__restrict__ rp, const int32_t *__rest
     if (col[j] < 0 || col[j] >= n) atomicOr(err, 4u);
 }
 
+// ---- static heavy-row pieces (rows with degree > kHeavy, cut into kHPiece-edge pieces)
+__device__ __forceinline__ uint32_t hpieces(const uint32_t *rp, uint32_t v) {
+  const uint32_t d = rp[v + 1] - rp[v];
+  return d > kHeavy ? (d + kHPiece - 1) / kHPiece : 0u;
+}
+
+// pass 1: per 2048-vertex block, the piece count (-> tmp[block]) and the heavy bitmap words
+__global__ void k_hcount(const uint32_t *__restrict__ rp, uint32_t n, uint32_t *__restrict__ bits,
+                         uint32_t *__restrict__ tmp) {
+  __shared__ uint32_t sm[32];
+  const uint32_t base = blockIdx.x * kScanBlock;
+  uint32_t local = 0;
+  for (uint32_t w = threadIdx.x; w < kScanBlock / 32; w += blockDim.x) {
+    uint32_t b = 0;
+    for (uint32_t i = 0; i < 32; ++i) {
+      const uint32_t v = base + w * 32 + i;
+      if (v < n) {
+        const uint32_t c = hpieces(rp, v);
+        if (c) b |= 1u << i;
+        local += c;
+      }
+    }
+    if (base / 32 + w < (n + 31) / 32) bits[base / 32 + w] = b;
+  }
+  local = warp_sum(local);
+  if ((threadIdx.x & 31) == 0) sm[threadIdx.x / 32] = local;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t t = 0;
+    for (uint32_t i = 0; i < blockDim.x / 32; ++i) t += sm[i];
+    tmp[blockIdx.x] = t;
+  }
+}
+
+// pass 2: one CTA: exclusive scan of the block counts; total -> *total
+__global__ void k_hscan(uint32_t *tmp, uint32_t nblk, uint32_t *total) {
+  if (threadIdx.x == 0) {
+    uint32_t run = 0;
+    for (uint32_t i = 0; i < nblk; ++i) {
+      const uint32_t c = tmp[i];
+      tmp[i] = run;
+      run += c;
+    }
+    *total = run;
+  }
+}
+
+// pass 3: write pieces (vertex, start, end) in vertex order
+__global__ void k_hfill(const uint32_t *__restrict__ rp, uint32_t n, const uint32_t *__restrict__ tmp,
+                        uint32_t *__restrict__ hv, uint32_t *__restrict__ hs,
+                        uint32_t *__restrict__ he) {
+  __shared__ uint32_t sm[1024];
+  constexpr uint32_t kPer = kScanBlock / 256;  // blockDim.x == 256
+  const uint32_t v0 = blockIdx.x * kScanBlock + threadIdx.x * kPer;
+  uint32_t c = 0;
+  for (uint32_t i = 0; i < kPer; ++i)
+    if (v0 + i < n) c += hpieces(rp, v0 + i);
+  sm[threadIdx.x] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t run = tmp[blockIdx.x];
+    for (uint32_t i = 0; i < blockDim.x; ++i) {
+      const uint32_t x = sm[i];
+      sm[i] = run;
+      run += x;
+    }
+  }
+  __syncthreads();
+  uint32_t o = sm[threadIdx.x];
+  for (uint32_t i = 0; i < kPer; ++i) {
+    const uint32_t v = v0 + i;
+    if (v >= n) break;
+    const uint32_t s = rp[v], e = rp[v + 1];
+    if (e - s <= kHeavy) continue;
+    for (uint32_t a = s; a < e; a += kHPiece) {
+      hv[o] = v;
+      hs[o] = a;
+      he[o] = min(e, a + kHPiece);
+      ++o;
+    }
+  }
+}
+
 }  // namespace
 
 struct dawn_graph_s {
@@ -84,8 +167,9 @@ struct dawn_graph_s {
   Layout L;
   const int32_t *col, *icol;
   bool has_csc;
-  float alpha = 14.f, beta = 24.f, ms_alpha = 8.f;
+  float alpha = 4.f, beta = 24.f, ms_alpha = 2.f;
   int sssp_grid, ms_grid;
+  bool trace;
 };
 
 namespace {
@@ -129,7 +213,7 @@ dawn_status dawn_graph_load_csr(int64_t n, int64_t m, const int64_t *row_ptr, co
   if (n < 1 || m < 0) return fail(DAWN_ERR_INVALID_ARGUMENT, "n must be >= 1 and m >= 0");
   if (n >= (int64_t(1) << 31) || m >= (int64_t(1) << 32))
     return fail(DAWN_ERR_CAPACITY, "n must be < 2^31 and m < 2^32 (32-bit offsets)");
-  if (flags & ~uint32_t(DAWN_GRAPH_SYMMETRIC | DAWN_GRAPH_VALIDATE))
+  if (flags & ~uint32_t(DAWN_GRAPH_SYMMETRIC | DAWN_GRAPH_VALIDATE | DAWN_GRAPH_TRACE))
     return fail(DAWN_ERR_INVALID_ARGUMENT, "unknown graph flag");
   if (!row_ptr || (!col && m > 0) || !workspace)
     return fail(DAWN_ERR_INVALID_ARGUMENT, "row_ptr/col/workspace is NULL");
@@ -158,11 +242,12 @@ dawn_status dawn_graph_load_csr(int64_t n, int64_t m, const int64_t *row_ptr, co
   g->col = col;
   g->has_csc = has_csc;
   g->icol = sym ? col : in_col;
+  g->trace = flags & DAWN_GRAPH_TRACE;
   if ((e = cudaSetDevice(g->device)) != cudaSuccess) { delete g; return cuda_fail(e, "cudaSetDevice"); }
   cudaDeviceGetAttribute(&g->nsm, cudaDevAttrMultiProcessorCount, g->device);
-  g->alpha = (float)env_int("DAWN_ALPHA", 14);
+  g->alpha = (float)env_int("DAWN_ALPHA", 4);
   g->beta = (float)env_int("DAWN_BETA", 24);
-  g->ms_alpha = (float)env_int("DAWN_MS_ALPHA", 8);
+  g->ms_alpha = (float)env_int("DAWN_MS_ALPHA", 2);
   g->sssp_grid = grid_for((const void *)k_sssp<kNT>, g->nsm, "DAWN_SSSP_BPS");
   g->ms_grid = grid_for((const void *)k_ms64<kNT>, g->nsm, "DAWN_MS_BPS");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -205,6 +290,30 @@ dawn_status dawn_graph_load_csr(int64_t n, int64_t m, const int64_t *row_ptr, co
     cudaMemcpyAsync(&at<Ctrl>(g, L.ctrl)->n_hasin, &nh, 4, cudaMemcpyHostToDevice, st);
     cudaStreamSynchronize(st);
   }
+  // static heavy-row pieces: out-rows (push side of the 64-source kernel) and in-rows (pull)
+  {
+    const uint32_t nblk = (uint32_t)((n + kScanBlock - 1) / kScanBlock);
+    Ctrl *C = at<Ctrl>(g, L.ctrl);
+    auto build_list = [&](const uint32_t *rows, const HeavyList &h, uint32_t *count) {
+      k_hcount<<<nblk, 256, 0, st>>>(rows, (uint32_t)n, at<uint32_t>(g, h.bits),
+                                     at<uint32_t>(g, L.scan_tmp));
+      k_hscan<<<1, 32, 0, st>>>(at<uint32_t>(g, L.scan_tmp), nblk, count);
+      k_hfill<<<nblk, 256, 0, st>>>(rows, (uint32_t)n, at<uint32_t>(g, L.scan_tmp),
+                                    at<uint32_t>(g, h.v), at<uint32_t>(g, h.s),
+                                    at<uint32_t>(g, h.e));
+    };
+    build_list(at<uint32_t>(g, L.rp), L.hout, &C->n_hp_out);
+    if (L.own_irp) {
+      if (has_csc) {
+        build_list(at<uint32_t>(g, L.irp), L.hin, &C->n_hp_in);
+      } else {
+        cudaMemsetAsync(g->ws + L.hin.bits, 0, 4 * (size_t)nwords, st);
+        cudaMemsetAsync(&C->n_hp_in, 0, 4, st);
+      }
+    } else {
+      cudaMemcpyAsync(&C->n_hp_in, &C->n_hp_out, 4, cudaMemcpyDeviceToDevice, st);
+    }
+  }
   if ((e = cudaGetLastError()) != cudaSuccess) { delete g; return cuda_fail(e, "graph load"); }
   *out = g;
   return DAWN_OK;
@@ -244,16 +353,17 @@ dawn_status dawn_sssp(dawn_graph g, int64_t source, uint32_t variant, uint32_t *
   p.col = g->col;
   p.icol = g->icol;
   p.noin = at<uint32_t>(g, L.noin);
+  p.hin_v = at<uint32_t>(g, L.hin.v);
+  p.hin_s = at<uint32_t>(g, L.hin.s);
+  p.hin_e = at<uint32_t>(g, L.hin.e);
+  p.hin_bits = at<uint32_t>(g, L.hin.bits);
   p.vis = at<uint32_t>(g, L.vis);
-  p.fb[0] = at<uint32_t>(g, L.fb0);
-  p.fb[1] = at<uint32_t>(g, L.fb1);
+  for (int i = 0; i < 3; ++i) p.fb[i] = at<uint32_t>(g, L.fb[i]);
+  p.trace = g->trace ? at<TraceRec>(g, L.trace) : nullptr;
   for (int i = 0; i < 2; ++i) {
     p.Lv[i] = at<uint32_t>(g, L.Lv[i]);
     p.Lsd[i] = at<uint2>(g, L.Lsd[i]);
-    p.Hv[i] = at<uint32_t>(g, L.Hv[i]);
-    p.Hsd[i] = at<uint2>(g, L.Hsd[i]);
-    p.Hp[i] = at<uint32_t>(g, L.Hp[i]);
-    p.Pm[i] = at<uint32_t>(g, L.Pm[i]);
+    p.Cf[i] = at<uint32_t>(g, L.Cf[i]);
   }
   p.ctrl = at<Ctrl>(g, L.ctrl);
   p.dist = dist;
@@ -290,6 +400,15 @@ static dawn_status launch_ms(dawn_graph g, const std::vector<uint32_t> &src, uin
     p.irp = at<uint32_t>(g, L.irp);
     p.col = g->col;
     p.icol = g->icol;
+    p.hout_v = at<uint32_t>(g, L.hout.v);
+    p.hout_s = at<uint32_t>(g, L.hout.s);
+    p.hout_e = at<uint32_t>(g, L.hout.e);
+    p.hout_bits = at<uint32_t>(g, L.hout.bits);
+    p.hin_v = at<uint32_t>(g, L.hin.v);
+    p.hin_s = at<uint32_t>(g, L.hin.s);
+    p.hin_e = at<uint32_t>(g, L.hin.e);
+    p.hin_bits = at<uint32_t>(g, L.hin.bits);
+    p.sctrl = at<Ctrl>(g, L.ctrl);
     p.seen = at<unsigned long long>(g, L.seen);
     p.F[0] = at<unsigned long long>(g, L.F0);
     p.F[1] = at<unsigned long long>(g, L.F1);
@@ -328,6 +447,28 @@ dawn_status dawn_msssp(dawn_graph g, const int64_t *sources, int64_t k, uint32_t
   if (s != DAWN_OK) return s;
   std::vector<uint32_t> src(sources, sources + k);
   return launch_ms(g, src, dist, rec, static_cast<cudaStream_t>(stream));
+}
+
+dawn_status dawn_graph_trace(dawn_graph g, dawn_trace_rec *host_out, int64_t cap, int64_t *count,
+                             void *stream) {
+  g_err.clear();
+  if (!g || !count || (cap > 0 && !host_out)) return fail(DAWN_ERR_INVALID_ARGUMENT, "bad arguments");
+  if (!g->trace) return fail(DAWN_ERR_CONFIG, "graph loaded without DAWN_GRAPH_TRACE");
+  dawn_status s = set_device(g);
+  if (s != DAWN_OK) return s;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  uint32_t nrec = 0;
+  cudaMemcpyAsync(&nrec, &at<Ctrl>(g, g->L.ctrl)->trace_n, 4, cudaMemcpyDeviceToHost, st);
+  cudaError_t e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return cuda_fail(e, "trace");
+  const int64_t k = std::min<int64_t>(cap, nrec);
+  static_assert(sizeof(dawn_trace_rec) == sizeof(TraceRec), "trace record layout");
+  if (k > 0) {
+    e = cudaMemcpy(host_out, g->ws + g->L.trace, sizeof(TraceRec) * k, cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return cuda_fail(e, "trace copy");
+  }
+  *count = nrec;
+  return DAWN_OK;
 }
 
 dawn_status dawn_apsp_shard(int64_t k, int32_t rank, int32_t world, int64_t *idx, int64_t cap,

@@ -9,47 +9,74 @@
 
 namespace dawn {
 
-// Light/heavy split of push-mode frontier entries (SURVEY §2.5 k_push load balancing):
-// rows with deg <= kLight go to 32-entry warp groups; longer rows are cut into kPiece-edge
-// pieces that warps take independently (hub rows: max degree 64K at scale 20, 406K at 24).
-constexpr uint32_t kLight = 128;
-constexpr uint32_t kPiece = 512;
+// Push-mode frontier queue (SURVEY §2.5 k_push load balancing): every entry carries its row
+// start and its exclusive edge offset within the frontier (allocated together with its slot
+// by one 64-bit atomic per 32 entries), so the frontier's edges split into kChunk-edge chunks
+// of equal size; Cf[c] names the entry holding chunk c's first edge.  Hub rows (64K arcs at
+// scale 20) therefore spread over many warps with no separate heavy path.
+constexpr uint32_t kChunk = 32;   // Cf granularity = one warp round
+constexpr uint32_t kIlp = 4;      // chunks per warp item when the frontier is wide
+// Solo levels: a push level whose frontier has <= kSoloE edges runs on CTA 0 alone with
+// __syncthreads instead of the grid barrier (the other CTAs wait for the stretch to end).
+constexpr uint32_t kSoloE = 512;
+// Static heavy rows (built once at load): rows with degree > kHeavy are scanned in kHPiece-edge
+// pieces by whole warps in the pull step and in the 64-source kernel; lighter rows are scanned
+// by one lane each (early exit, 4 probes per round trip).
+constexpr uint32_t kHeavy = 32;
+constexpr uint32_t kHPiece = 256;
+constexpr uint32_t kScanBlock = 2048;  // elements per CTA in the load-time piece scan
+constexpr uint32_t kMaxBlocks = 2048;  // cap on persistent grid size (partials buffer)
+constexpr uint32_t kTraceCap = 1 << 16;
 
 enum : uint32_t { kPush = 0, kPull = 1, kRepQueue = 0, kRepBitmap = 1 };
 
 struct Slot {                 // counters of one frontier (3 rotate: written, read, reset)
   uint32_t n_new;             // vertices discovered into this frontier
-  uint32_t n_light;           // queue entries (push-mode representation)
-  uint32_t n_heavy;
-  uint32_t n_pieces;
+  uint32_t pad0;
+  unsigned long long qpack;   // queue: (entries << 32) | edges  (push-mode representation)
   unsigned long long m_new;   // sum of out-degrees of the frontier (m_f)
-  unsigned long long pad;
+  unsigned long long pad1;
 };
 
 struct Ctrl {
   GridBarrier bar;
-  uint32_t pad0[14];
+  uint32_t pad0[12];
   Slot slot[3];
   unsigned long long examined;  // per-source accumulator (reduced per CTA)
   uint32_t n_hasin;             // #vertices with in-degree > 0 (written at load)
   uint32_t err;                 // graph validation result (written at load)
-  uint32_t pad1[12];
+  uint32_t n_hp_out, n_hp_in;   // static heavy-piece counts (written at load)
+  uint32_t trace_n;
+  uint32_t solo_epoch;          // CTA 0 -> others: a solo stretch ended (see k_sssp)
+  uint32_t pad1[8];
+  alignas(16) unsigned char solo_state[256];  // LevelState snapshot published with solo_epoch
 };
-
-constexpr uint32_t kMaxBlocks = 2048;  // cap on persistent grid size (partials buffer)
 
 struct MsCtrl {
   GridBarrier bar;
-  uint32_t pad0[14];
-  unsigned long long cnt[3][4];   // per level slot: [0] n_active words, [1] m_active, [2] any new
+  uint32_t pad0[12];
+  unsigned long long cnt[3][4];   // per level slot: [0] n_active, [1] m_active, [2] m_full
   uint32_t pad1[8];
 };
 
+// One trace record per level of the last traced dawn_sssp call (DAWN_TRACE=1).
+struct TraceRec {
+  unsigned long long t_ns;  // %globaltimer at the level start (after the barrier)
+  uint32_t level, dir, nf, pad;
+  unsigned long long mf;
+  unsigned long long t_first, t_last;  // first / last CTA done with the level's work
+};
+
+struct HeavyList {  // static pieces of rows with degree > kHeavy
+  size_t v, s, e, bits;
+};
+
 struct Layout {
-  size_t rp, irp, noin, vis, fb0, fb1, Lv[2], Lsd[2], Hv[2], Hsd[2], Hp[2], Pm[2], ctrl;
+  size_t rp, irp, noin, vis, fb[3], Lv[2], Lsd[2], Cf[2], ctrl, trace;
+  HeavyList hout, hin;
+  size_t scan_tmp;
   size_t seen, F0, F1, nxt, msctrl, part, srcbuf, total;
-  uint64_t srccap;
-  uint64_t capH, capP;
+  uint64_t srccap, capCf, capHP;
   bool own_irp;
 };
 
@@ -64,24 +91,30 @@ inline Layout make_layout(int64_t n, int64_t m, uint32_t flags) {
     return at;
   };
   const uint64_t W = (uint64_t)(n + 31) / 32;
-  L.capH = (uint64_t)m / kLight + 1;
-  L.capP = (uint64_t)m / kPiece + L.capH + 1;
+  L.capCf = (uint64_t)m / kChunk + 2;
+  L.capHP = (uint64_t)m / kHPiece + (uint64_t)m / kHeavy + 1;
   L.own_irp = !(flags & DAWN_GRAPH_SYMMETRIC);
   L.rp = take(4 * (size_t)(n + 1));
   L.irp = L.own_irp ? take(4 * (size_t)(n + 1)) : L.rp;
   L.noin = take(4 * W);
   L.vis = take(4 * W);
-  L.fb0 = take(4 * W);
-  L.fb1 = take(4 * W);
+  for (int i = 0; i < 3; ++i) L.fb[i] = take(4 * W);
   for (int i = 0; i < 2; ++i) {
     L.Lv[i] = take(4 * (size_t)n);
     L.Lsd[i] = take(8 * (size_t)n);
-    L.Hv[i] = take(4 * L.capH);
-    L.Hsd[i] = take(8 * L.capH);
-    L.Hp[i] = take(4 * L.capH);
-    L.Pm[i] = take(4 * L.capP);
+    L.Cf[i] = take(4 * L.capCf);
   }
   L.ctrl = take(sizeof(Ctrl));
+  L.trace = take(sizeof(TraceRec) * kTraceCap);
+  auto heavy = [&](HeavyList &h) {
+    h.v = take(4 * L.capHP);
+    h.s = take(4 * L.capHP);
+    h.e = take(4 * L.capHP);
+    h.bits = take(4 * W);
+  };
+  heavy(L.hout);
+  if (L.own_irp) heavy(L.hin); else L.hin = L.hout;
+  L.scan_tmp = take(4 * ((size_t)n / kScanBlock + 2));
   L.seen = take(8 * (size_t)n);
   L.F0 = take(8 * (size_t)n);
   L.F1 = take(8 * (size_t)n);

@@ -4,11 +4,14 @@
 //   PUSH (SOVM, Algorithm 2; Eq. 9): the frontier queue's CSR rows
 //        are expanded; a target u is claimed by an atomic test-and-set on the `vis` bitmap
 //        (the "distance[col[j]] = 0" filter of line 6, reading Q1), dist[u] = L+1, and u is
-//        appended to the next queue with a warp-aggregated atomic (ballot + popc);
+//        appended to the next queue through a per-warp shared-memory stage (ballot + popc),
+//        flushed 32 entries per global atomic;
 //   PULL (BOVM, Algorithm 1; Eq. 4): every unreached vertex scans
-//        its CSC row until the first in-neighbour in the level-L frontier bitmap (early exit),
-//        a warp owns 32 vertices = one bitmap word, so the next bitmap is written without
-//        atomics and the frontier read is a level-start snapshot (reading Q2).
+//        its CSC row until the first in-neighbour in the level-L frontier bitmap (early exit).
+//        Rows of in-degree <= kHeavy: one lane each, 4 probes per round trip; longer rows: a
+//        static list of kHPiece-edge pieces scanned by whole warps (32 probes per round trip,
+//        early exit across pieces through the `vis` bit).  The frontier bitmap read is a
+//        level-start snapshot; the next one is a separate buffer (reading Q2).
 // The direction is chosen on the device from the frontier's measured size (n_f, m_f) against
 // the unexplored edges (Beamer's rule, cited by the paper at L123), and the frontier-empty
 // test (PAPER.md L174-179 conditions 1-2) is evaluated after each grid barrier: no host
@@ -24,76 +27,122 @@ struct SsspParams {
   const uint32_t *rp, *irp;
   const int32_t *col, *icol;
   const uint32_t *noin;
-  uint32_t *vis, *fb[2];
-  uint32_t *Lv[2];
-  uint2 *Lsd[2];
-  uint32_t *Hv[2];
-  uint2 *Hsd[2];
-  uint32_t *Hp[2], *Pm[2];
+  const uint32_t *hin_v, *hin_s, *hin_e, *hin_bits;  // static heavy in-row pieces
+  uint32_t *vis, *fb[3];
+  uint32_t *Lv[2];   // frontier queue: vertex
+  uint2 *Lsd[2];     //                 (row start, edge offset within the frontier)
+  uint32_t *Cf[2];   //                 chunk c -> entry holding edge c*kChunk
   Ctrl *ctrl;
+  TraceRec *trace;
   uint32_t *dist;
   dawn_sssp_stats *stats;
   uint32_t source, variant, can_pull, sym;
   float alpha, beta;
 };
 
-
-struct LevelState {
-  uint32_t L, nf, prev_nf, dir, rep, q, b, stop, ecc;
+struct __align__(16) LevelState {
+  uint32_t L, nf, prev_nf, dir, rep, q, b, stop, ecc, solo;
   uint32_t push_levels, pull_levels, reached;
-  uint32_t n_light, n_heavy, n_pieces;
-  unsigned long long mf, explored, push_edges;
+  uint32_t qn, n_hp;            // queue entries of frontier L; static heavy pieces
+  uint32_t qe;                  // queue edges of frontier L
+  unsigned long long mf, explored, push_edges, pad;
+};
+static_assert(sizeof(LevelState) % 16 == 0, "LevelState is copied as uint4");
+
+struct WarpStage {
+  uint32_t u[64], rs[64], d[64];
 };
 
-// Warp-collective append of discovered vertices to queue `q` (light rows / heavy pieces).
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Flush the first k (<= 32) staged entries to queue q: one 64-bit atomic reserves k slots AND
+// their edge range; entry i gets (row start, exclusive edge offset) and the chunk map Cf gets
+// the entry for every chunk boundary inside its row.  Warp-collective.
+__device__ __forceinline__ void stage_emit(const SsspParams &p, Slot *s, int q, WarpStage &stg,
+                                           uint32_t k) {
+  const uint32_t lane = lane_id();
+  const uint32_t d = lane < k ? stg.d[lane] : 0u;
+  const uint32_t incl = warp_incl_scan(d);
+  const uint32_t D = __shfl_sync(DAWN_FULL, incl, 31);
+  unsigned long long old = 0;
+  if (lane == 0) old = atomicAdd(&s->qpack, ((unsigned long long)k << 32) | D);
+  old = __shfl_sync(DAWN_FULL, old, 0);
+  const uint32_t i = (uint32_t)(old >> 32) + lane;
+  const uint32_t o = (uint32_t)old + incl - d;
+  if (lane < k) {
+    p.Lv[q][i] = stg.u[lane];
+    p.Lsd[q][i] = make_uint2(stg.rs[lane], o);
+  }
+  // chunk map: entry i owns chunks [ceil(o/C), ceil((o+d)/C)); written warp-cooperatively so
+  // a hub row (1000 chunks) costs 32 lanes' stores, not one lane's loop
+  const uint32_t c0 = (o + kChunk - 1) / kChunk;
+  const uint32_t nc = (lane < k) ? (o + d + kChunk - 1) / kChunk - c0 : 0u;
+  const uint32_t inc2 = warp_incl_scan(nc);
+  const uint32_t T = __shfl_sync(DAWN_FULL, inc2, 31);
+  const uint32_t ex2 = inc2 - nc;
+  for (uint32_t xb = 0; xb < T; xb += 32) {
+    const uint32_t x = xb + lane;
+    uint32_t kk = 0;
+#pragma unroll
+    for (uint32_t step = 16; step; step >>= 1) {
+      const uint32_t e = __shfl_sync(DAWN_FULL, ex2, kk + step);
+      if (e <= x) kk += step;
+    }
+    const uint32_t cb = __shfl_sync(DAWN_FULL, c0, kk) + x - __shfl_sync(DAWN_FULL, ex2, kk);
+    const uint32_t ik = __shfl_sync(DAWN_FULL, i, kk);
+    if (x < T) p.Cf[q][cb] = ik;
+  }
+  __syncwarp();
+}
+
+// Warp-collective append of discovered vertices (has: lane discovered u, row start rs,
+// out-degree d) through the warp's shared-memory stage; 32 entries per global atomic.
 // Vertices with out-degree 0 are not enqueued ("skipping ... reachable nodes
 // with an out-degree of 0").
 __device__ __forceinline__ void enqueue_frontier(const SsspParams &p, Slot *s, int q, bool has,
-                                                 uint32_t u, uint32_t rs, uint32_t d) {
+                                                 uint32_t u, uint32_t rs, uint32_t d,
+                                                 WarpStage &stg, uint32_t &cnt) {
   const uint32_t lane = lane_id();
-  const bool isL = has && d > 0 && d <= kLight;
-  const bool isH = has && d > kLight;
-  const uint32_t mL = __ballot_sync(DAWN_FULL, isL);
-  if (mL) {
-    const uint32_t leader = __ffs(mL) - 1;
-    uint32_t base = 0;
-    if (lane == leader) base = atomicAdd(&s->n_light, __popc(mL));
-    base = __shfl_sync(DAWN_FULL, base, leader);
-    if (isL) {
-      const uint32_t pos = base + __popc(mL & lanemask_lt());
-      p.Lv[q][pos] = u;
-      p.Lsd[q][pos] = make_uint2(rs, d);
-    }
+  const bool put = has && d > 0;
+  const uint32_t mk = __ballot_sync(DAWN_FULL, put);
+  if (!mk) return;
+  if (put) {
+    const uint32_t pos = cnt + __popc(mk & lanemask_lt());
+    stg.u[pos] = u;
+    stg.rs[pos] = rs;
+    stg.d[pos] = d;
   }
-  const uint32_t mH = __ballot_sync(DAWN_FULL, isH);
-  if (mH) {
-    const uint32_t np = isH ? (d + kPiece - 1) / kPiece : 0;
-    const uint32_t incl = warp_incl_scan(np);
-    const uint32_t tot = __shfl_sync(DAWN_FULL, incl, 31);
-    const uint32_t leader = __ffs(mH) - 1;
-    uint32_t hb = 0, pb = 0;
-    if (lane == leader) {
-      hb = atomicAdd(&s->n_heavy, __popc(mH));
-      pb = atomicAdd(&s->n_pieces, tot);
+  cnt += __popc(mk);
+  __syncwarp();
+  if (cnt >= 32) {
+    stage_emit(p, s, q, stg, 32);
+    const uint32_t rem = cnt - 32;
+    if (lane < rem) {
+      stg.u[lane] = stg.u[32 + lane];
+      stg.rs[lane] = stg.rs[32 + lane];
+      stg.d[lane] = stg.d[32 + lane];
     }
-    hb = __shfl_sync(DAWN_FULL, hb, leader);
-    pb = __shfl_sync(DAWN_FULL, pb, leader);
-    if (isH) {
-      const uint32_t pos = hb + __popc(mH & lanemask_lt());
-      const uint32_t first = pb + incl - np;
-      p.Hv[q][pos] = u;
-      p.Hsd[q][pos] = make_uint2(rs, d);
-      p.Hp[q][pos] = first;
-      for (uint32_t i = 0; i < np; ++i) p.Pm[q][first + i] = pos;
-    }
+    __syncwarp();
+    cnt = rem;
   }
+}
+
+__device__ __forceinline__ void stage_flush(const SsspParams &p, Slot *s, int q, WarpStage &stg,
+                                            uint32_t &cnt) {
+  if (cnt) stage_emit(p, s, q, stg, cnt);
+  cnt = 0;
 }
 
 // Push-mode visit of arc (frontier vertex) -> u, warp-collective (all lanes call; `act`
 // false for idle lanes).
 __device__ __forceinline__ void push_visit(const SsspParams &p, Slot *ns, int qn, uint32_t L1,
                                            bool act, uint32_t u, uint32_t &n_new,
-                                           unsigned long long &m_new) {
+                                           unsigned long long &m_new, WarpStage &stg,
+                                           uint32_t &cnt) {
   bool disc = false;
   uint32_t rs = 0, d = 0;
   if (act) {
@@ -108,58 +157,99 @@ __device__ __forceinline__ void push_visit(const SsspParams &p, Slot *ns, int qn
     n_new += 1;
     m_new += d;
   }
-  enqueue_frontier(p, ns, qn, disc, u, rs, d);
+  enqueue_frontier(p, ns, qn, disc, u, rs, d, stg, cnt);
 }
 
-__device__ void push_level(const SsspParams &p, const LevelState &st, Slot *ns, uint32_t gwarp,
-                           uint32_t nwarps, uint32_t &n_new, unsigned long long &m_new) {
+// One push level over the queue.  Chunk c = edges [32c, 32c+32) of the frontier; a warp item
+// is J consecutive chunks (J = kIlp when the frontier has enough edges to keep every warp busy,
+// else 1), processed with all J chains' loads in flight together (memory-level parallelism):
+// Cf[c] -> 32-entry window of (row start, edge offset) -> owner by 5-step shfl search -> col ->
+// vis test-and-set -> rp of the discovered vertex.
+template <int J>
+__device__ __forceinline__ void push_item(const SsspParams &p, const LevelState &st, Slot *ns,
+                                          uint32_t item, uint32_t &n_new,
+                                          unsigned long long &m_new, WarpStage &stg,
+                                          uint32_t &cnt) {
   const int q = st.q, qn = q ^ 1;
   const uint32_t lane = lane_id();
   const uint32_t L1 = st.L + 1;
-  const uint32_t G = (st.n_light + 31) / 32;
-  const uint32_t items = G + st.n_pieces;
-  for (uint32_t it = gwarp; it < items; it += nwarps) {
-    if (it < G) {
-      // 32 light rows; edges of the group dealt to lanes round-robin (owner by shfl search)
-      const uint32_t idx = it * 32 + lane;
-      uint32_t s = 0, d = 0;
-      if (idx < st.n_light) {
-        const uint2 sd = ld_cg2(p.Lsd[q] + idx);
-        s = sd.x;
-        d = sd.y;
-      }
-      const uint32_t incl = warp_incl_scan(d);
-      const uint32_t total = __shfl_sync(DAWN_FULL, incl, 31);
-      const uint32_t excl = incl - d;
-      for (uint32_t base = 0; base < total; base += 32) {
-        const uint32_t t = base + lane;
-        uint32_t k = 0;
+  const uint32_t E = st.qe, cntq = st.qn;
+  uint32_t w0[J], u[J], rsd[J], dd[J];
+  bool act[J], disc[J];
+  uint2 sd[J];
 #pragma unroll
-        for (uint32_t step = 16; step; step >>= 1) {
-          const uint32_t e = __shfl_sync(DAWN_FULL, excl, k + step);
-          if (e <= t) k += step;
-        }
-        const uint32_t ek = __shfl_sync(DAWN_FULL, excl, k);
-        const uint32_t sk = __shfl_sync(DAWN_FULL, s, k);
-        const bool act = t < total;
-        const uint32_t u = act ? (uint32_t)ld_nc(p.col + sk + (t - ek)) : 0u;
-        push_visit(p, ns, qn, L1, act, u, n_new, m_new);
-      }
-    } else {
-      const uint32_t pc = it - G;
-      const uint32_t h = ld_cg(p.Pm[q] + pc);
-      const uint2 sd = ld_cg2(p.Hsd[q] + h);
-      const uint32_t p0 = ld_cg(p.Hp[q] + h);
-      const uint32_t off = (pc - p0) * kPiece;
-      const uint32_t len = min(kPiece, sd.y - off);
-      const int32_t *row = p.col + sd.x + off;
-      for (uint32_t i = 0; i < len; i += 32) {
-        const bool act = i + lane < len;
-        const uint32_t u = act ? (uint32_t)ld_nc(row + i + lane) : 0u;
-        push_visit(p, ns, qn, L1, act, u, n_new, m_new);
-      }
+  for (int j = 0; j < J; ++j) {
+    const uint32_t c = item * J + j;
+    w0[j] = (c * kChunk < E) ? ld_cg(p.Cf[q] + c) : 0u;
+  }
+#pragma unroll
+  for (int j = 0; j < J; ++j) {
+    const uint32_t idx = w0[j] + lane;
+    sd[j] = (idx < cntq) ? ld_cg2(p.Lsd[q] + idx) : make_uint2(0u, 0xffffffffu);
+  }
+#pragma unroll
+  for (int j = 0; j < J; ++j) {
+    const uint32_t t = (item * J + j) * kChunk + lane;
+    uint32_t k = 0;
+#pragma unroll
+    for (uint32_t step = 16; step; step >>= 1) {
+      const uint32_t e = __shfl_sync(DAWN_FULL, sd[j].y, k + step);
+      if (e <= t) k += step;
+    }
+    const uint32_t ok = __shfl_sync(DAWN_FULL, sd[j].y, k);
+    const uint32_t sk = __shfl_sync(DAWN_FULL, sd[j].x, k);
+    act[j] = t < E;
+    u[j] = act[j] ? (uint32_t)ld_nc(p.col + sk + (t - ok)) : 0u;
+  }
+  uint32_t cur[J];
+#pragma unroll
+  for (int j = 0; j < J; ++j) cur[j] = act[j] ? p.vis[u[j] >> 5] : ~0u;  // weak: stale 0 = atomic
+#pragma unroll
+  for (int j = 0; j < J; ++j) {
+    const uint32_t bit = 1u << (u[j] & 31);
+    disc[j] = false;
+    if (!(cur[j] & bit)) disc[j] = !(atomicOr(p.vis + (u[j] >> 5), bit) & bit);
+  }
+#pragma unroll
+  for (int j = 0; j < J; ++j) {
+    rsd[j] = 0;
+    dd[j] = 0;
+    if (disc[j]) {
+      rsd[j] = ld_nc(p.rp + u[j]);
+      dd[j] = ld_nc(p.rp + u[j] + 1);
     }
   }
+#pragma unroll
+  for (int j = 0; j < J; ++j) {
+    if (disc[j]) {
+      dd[j] -= rsd[j];
+      p.dist[u[j]] = L1;
+      n_new += 1;
+      m_new += dd[j];
+    }
+    enqueue_frontier(p, ns, qn, disc[j], u[j], rsd[j], dd[j], stg, cnt);
+  }
+}
+
+__device__ void push_level(const SsspParams &p, const LevelState &st, Slot *ns, uint32_t gwarp,
+                           uint32_t nwarps, uint32_t &n_new, unsigned long long &m_new,
+                           WarpStage &stg) {
+  const uint32_t E = st.qe;
+  const uint32_t nchunks = (E + kChunk - 1) / kChunk;
+  uint32_t cnt = 0;
+  if (nchunks >= nwarps * kIlp) {
+    const uint32_t items = (nchunks + kIlp - 1) / kIlp;
+    for (uint32_t it = gwarp; it < items; it += nwarps)
+      push_item<kIlp>(p, st, ns, it, n_new, m_new, stg, cnt);
+  } else {
+    for (uint32_t it = gwarp; it < nchunks; it += nwarps)
+      push_item<1>(p, st, ns, it, n_new, m_new, stg, cnt);
+  }
+  stage_flush(p, ns, st.q ^ 1, stg, cnt);
+}
+
+__device__ __forceinline__ bool fb_test(const uint32_t *fb, uint32_t v) {
+  return (fb[v >> 5] >> (v & 31)) & 1u;
 }
 
 __device__ void pull_level(const SsspParams &p, const LevelState &st, uint32_t gwarp,
@@ -168,38 +258,123 @@ __device__ void pull_level(const SsspParams &p, const LevelState &st, uint32_t g
   const uint32_t lane = lane_id();
   const uint32_t L1 = st.L + 1;
   const uint32_t *fcur = p.fb[st.b];
-  uint32_t *fnext = p.fb[st.b ^ 1];
+  uint32_t *fnext = p.fb[(st.b + 1) % 3];
+  uint32_t *fclr = p.fb[(st.b + 2) % 3];  // held frontier L-1: cleared for level L+1
   const uint32_t tail_bits = p.n & 31;
-  for (uint32_t w = gwarp; w < p.nwords; w += nwarps) {
-    const uint32_t vw = ld_cg(p.vis + w);
-    uint32_t todo = ~vw;
-    if (w == p.nwords - 1 && tail_bits) todo &= (1u << tail_bits) - 1;
-    bool found = false;
-    uint32_t s = 0, e = 0;
-    const uint32_t u = w * 32 + lane;
-    if ((todo >> lane) & 1u) {
-      s = ld_nc(p.irp + u);
-      e = ld_nc(p.irp + u + 1);
-      uint32_t j = s;
-      for (; j < e; ++j) {
-        const uint32_t v = (uint32_t)ld_nc(p.icol + j);
-        if ((fcur[v >> 5] >> (v & 31)) & 1u) {
-          found = true;
-          ++j;
-          break;
+  // (1) light rows: lane per vertex, a warp owns vis words w and w + nwarps (two independent
+  //     scans in flight per lane), 4 in-neighbours probed per round trip
+  constexpr int J = 2;
+  for (uint32_t wb = gwarp; wb < p.nwords; wb += nwarps * J) {
+    uint32_t w[J], vw[J], todo[J], s[J], e[J], j0[J];
+    bool need[J], found[J];
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+      w[j] = wb + j * nwarps;
+      vw[j] = 0;
+      todo[j] = 0;
+      if (w[j] < p.nwords) {
+        vw[j] = ld_cg(p.vis + w[j]);
+        todo[j] = ~vw[j] & ~ld_nc(p.hin_bits + w[j]);
+        if (w[j] == p.nwords - 1 && tail_bits) todo[j] &= (1u << tail_bits) - 1;
+        if (lane == 0) fclr[w[j]] = 0;
+      }
+      need[j] = (todo[j] >> lane) & 1u;
+      found[j] = false;
+      s[j] = e[j] = 0;
+    }
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+      if (need[j]) {
+        const uint32_t u = w[j] * 32 + lane;
+        s[j] = ld_nc(p.irp + u);
+        e[j] = ld_nc(p.irp + u + 1);
+      }
+      j0[j] = s[j];
+    }
+    for (;;) {
+      bool any = false;
+      uint32_t v[J][4];
+#pragma unroll
+      for (int j = 0; j < J; ++j) {
+        const bool go = need[j] && !found[j] && j0[j] < e[j];
+        any |= go;
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          v[j][i] = (go && j0[j] + i < e[j]) ? (uint32_t)ld_nc(p.icol + j0[j] + i) : 0xffffffffu;
+      }
+      if (!any) break;
+#pragma unroll
+      for (int j = 0; j < J; ++j) {
+        if (v[j][0] == 0xffffffffu) continue;
+        uint32_t hit = 4;
+#pragma unroll
+        for (int i = 3; i >= 0; --i)
+          if (v[j][i] != 0xffffffffu && fb_test(fcur, v[j][i])) hit = i;
+        if (hit < 4) {
+          found[j] = true;
+          j0[j] += hit + 1;
+        } else {
+          j0[j] += 4;
         }
       }
-      examined += j - s;
     }
-    const uint32_t nb = __ballot_sync(DAWN_FULL, found);
-    if (lane == 0) {
-      fnext[w] = nb;
-      if (nb) p.vis[w] = vw | nb;
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+      if (need[j]) examined += min(j0[j], e[j]) - s[j];
+      const uint32_t nb = __ballot_sync(DAWN_FULL, found[j]);
+      if (lane == 0 && nb) {
+        red_or(fnext + w[j], nb);
+        red_or(p.vis + w[j], nb);
+      }
+      if (found[j]) {
+        const uint32_t u = w[j] * 32 + lane;
+        p.dist[u] = L1;
+        n_new += 1;
+        m_new += p.sym ? (e[j] - s[j]) : (ld_nc(p.rp + u + 1) - ld_nc(p.rp + u));
+      }
     }
-    if (found) {
-      p.dist[u] = L1;
-      n_new += 1;
-      m_new += p.sym ? (e - s) : (ld_nc(p.rp + u + 1) - ld_nc(p.rp + u));
+  }
+  // (2) heavy rows: static pieces; 32 pieces tested per warp (vis), then a warp scans each
+  //     live piece 32 in-edges per round trip
+  for (uint32_t pb = gwarp * 32; pb < st.n_hp; pb += nwarps * 32) {
+    const uint32_t pc = pb + lane;
+    uint32_t u = 0, s = 0, e = 0;
+    bool need = false;
+    if (pc < st.n_hp) {
+      u = ld_nc(p.hin_v + pc);
+      s = ld_nc(p.hin_s + pc);
+      e = ld_nc(p.hin_e + pc);
+      need = !((ld_cg(p.vis + (u >> 5)) >> (u & 31)) & 1u);
+    }
+    uint32_t nm = __ballot_sync(DAWN_FULL, need);
+    while (nm) {
+      const uint32_t k = __ffs(nm) - 1;
+      nm &= nm - 1;
+      const uint32_t uk = __shfl_sync(DAWN_FULL, u, k);
+      const uint32_t sk = __shfl_sync(DAWN_FULL, s, k);
+      const uint32_t ek = __shfl_sync(DAWN_FULL, e, k);
+      const uint32_t w = uk >> 5, bit = 1u << (uk & 31);
+      for (uint32_t j = sk; j < ek; j += 32) {
+        const bool act = j + lane < ek;
+        const bool hit = act && fb_test(fcur, (uint32_t)ld_nc(p.icol + j + lane));
+        const uint32_t hm = __ballot_sync(DAWN_FULL, hit);
+        if (hm) {
+          if (lane == 0) {
+            examined += __ffs(hm);
+            const uint32_t old = atomicOr(p.vis + w, bit);
+            if (!(old & bit)) {
+              red_or(fnext + w, bit);
+              p.dist[uk] = L1;
+              n_new += 1;
+              m_new += p.sym ? (ld_nc(p.irp + uk + 1) - ld_nc(p.irp + uk))
+                             : (ld_nc(p.rp + uk + 1) - ld_nc(p.rp + uk));
+            }
+          }
+          break;
+        }
+        if (lane == 0) examined += min(32u, ek - j);
+        if ((((j - sk) >> 5) & 3) == 3 && (ld_cg(p.vis + w) & bit)) break;
+      }
     }
   }
 }
@@ -222,17 +397,96 @@ __device__ __forceinline__ void block_flush(uint32_t a, unsigned long long b, ui
   }
 }
 
+// Level header (thread 0 of every CTA; identical inputs -> identical decisions everywhere):
+// read frontier L's counters, apply the stop tests (a5) and choose the direction (a4).
+__device__ __forceinline__ void level_header(const SsspParams &p, Ctrl *C, LevelState &st,
+                                             uint32_t max_reach, uint32_t nblocks) {
+  const Slot *cs = &C->slot[st.L % 3];
+  st.nf = ld_cg(&cs->n_new);
+  st.mf = ld_cg(&cs->m_new);
+  const unsigned long long qp = ld_cg(&cs->qpack);
+  st.qn = (uint32_t)(qp >> 32);
+  st.qe = (uint32_t)qp;
+  if (blockIdx.x == 0) C->slot[(st.L + 2) % 3] = Slot{0, 0, 0, 0, 0};
+  if (st.L > 0) st.reached += st.nf;
+  st.explored += st.mf;
+  st.stop = 0;
+  st.solo = 0;
+  if (st.nf == 0) {
+    st.stop = 1;
+    st.ecc = st.L - 1;
+  } else if (st.reached + 1 >= max_reach || st.L + 1 >= p.n) {
+    st.stop = 1;  // condition 1: nothing left to discover
+    st.ecc = st.L;
+  } else {
+    if (p.variant == DAWN_PUSH || !p.can_pull) {
+      st.dir = kPush;
+    } else if (p.variant == DAWN_PULL) {
+      st.dir = kPull;
+    } else {
+      const double mu = (double)(p.m - st.explored);
+      if (st.dir == kPush) {
+        if ((double)st.mf * p.alpha > mu && st.nf > st.prev_nf) st.dir = kPull;
+      } else {
+        if ((double)st.nf * p.beta < (double)p.n && st.nf < st.prev_nf) st.dir = kPush;
+      }
+    }
+    st.prev_nf = st.nf;
+    st.solo = (nblocks > 1 && st.dir == kPush && st.rep == kRepQueue && st.qe <= kSoloE) ? 1u : 0u;
+  }
+  if (p.trace && blockIdx.x == 0 && st.L < kTraceCap) {
+    TraceRec r;
+    r.t_ns = globaltimer();
+    r.level = st.L;
+    r.dir = st.stop ? 2u : st.dir;
+    r.nf = st.nf;
+    r.pad = st.rep | (st.solo << 1);
+    r.mf = st.mf;
+    r.t_first = p.trace[st.L].t_first;
+    r.t_last = p.trace[st.L].t_last;
+    p.trace[st.L] = r;
+    C->trace_n = st.L + 1;
+  }
+}
+
+__device__ __forceinline__ void trace_done(const SsspParams &p, uint32_t L) {
+  if (p.trace && threadIdx.x == 0 && L < kTraceCap) {
+    const unsigned long long t = globaltimer();
+    atomicMin(&p.trace[L].t_first, t);
+    atomicMax(&p.trace[L].t_last, t);
+  }
+}
+
+__device__ __forceinline__ void level_advance(LevelState &st) {
+  if (st.dir == kPush) {
+    st.push_levels++;
+    st.push_edges += st.mf;
+    st.q ^= 1;
+    st.rep = kRepQueue;
+  } else {
+    st.pull_levels++;
+    st.b = (st.b + 1) % 3;
+    st.rep = kRepBitmap;
+  }
+  st.L++;
+}
+
 template <int NT>
 __global__ void __launch_bounds__(NT) k_sssp(SsspParams p) {
   __shared__ LevelState st;
   __shared__ unsigned long long red[2];
+  __shared__ WarpStage stage[NT / 32];
+  static_assert(sizeof(LevelState) <= sizeof(((Ctrl *)0)->solo_state), "solo_state too small");
   const uint32_t nblocks = gridDim.x;
   const uint32_t gwarp = blockIdx.x * (NT / 32) + threadIdx.x / 32;
   const uint32_t nwarps = nblocks * (NT / 32);
   const uint32_t gtid = blockIdx.x * NT + threadIdx.x;
   const uint32_t nthreads = nblocks * NT;
+  WarpStage &stg = stage[threadIdx.x / 32];
   Ctrl *C = p.ctrl;
   const uint32_t src = p.source;
+  unsigned long long bar_target = 0;
+  uint32_t solo_epoch = 0;
   // condition 1 bound: only vertices with an in-edge (plus s itself) can ever be reached
   const uint32_t max_reach = ld_cg(&C->n_hasin) + ((p.noin[src >> 5] >> (src & 31)) & 1u);
 
@@ -241,91 +495,107 @@ __global__ void __launch_bounds__(NT) k_sssp(SsspParams p) {
   for (uint32_t w = gtid; w < p.nwords; w += nthreads)
     p.vis[w] = p.noin[w] | ((w == (src >> 5)) ? (1u << (src & 31)) : 0u);
   if (blockIdx.x == 0 && threadIdx.x == 0) {
-    for (int i = 0; i < 3; ++i) C->slot[i] = Slot{0, 0, 0, 0, 0, 0};
+    for (int i = 0; i < 3; ++i) C->slot[i] = Slot{0, 0, 0, 0, 0};
     C->examined = 0;
+    C->solo_epoch = 0;
     const uint32_t rs = p.rp[src], d = p.rp[src + 1] - rs;
     Slot &s0 = C->slot[0];
     s0.n_new = 1;
     s0.m_new = d;
-    if (d > 0 && d <= kLight) {
+    if (d > 0) {
       p.Lv[0][0] = src;
-      p.Lsd[0][0] = make_uint2(rs, d);
-      s0.n_light = 1;
-    } else if (d > kLight) {
-      const uint32_t np = (d + kPiece - 1) / kPiece;
-      p.Hv[0][0] = src;
-      p.Hsd[0][0] = make_uint2(rs, d);
-      p.Hp[0][0] = 0;
-      for (uint32_t i = 0; i < np; ++i) p.Pm[0][i] = 0;
-      s0.n_heavy = 1;
-      s0.n_pieces = np;
+      p.Lsd[0][0] = make_uint2(rs, 0u);
+      for (uint32_t c = 0; c * kChunk < d; ++c) p.Cf[0][c] = 0;
+      s0.qpack = (1ull << 32) | d;
+    }
+  }
+  if (p.trace) {
+    const uint32_t ntr = min(p.n + 1, kTraceCap);
+    for (uint32_t i = gtid; i < ntr; i += nthreads) {
+      p.trace[i].t_first = ~0ull;
+      p.trace[i].t_last = 0;
     }
   }
   if (threadIdx.x == 0) {
     st = LevelState{};
     st.dir = (p.variant == DAWN_PULL) ? kPull : kPush;
+    st.n_hp = ld_cg(&C->n_hp_in);
   }
-  grid_sync(&C->bar, nblocks);
+  grid_sync(&C->bar, nblocks, bar_target);
 
   unsigned long long examined = 0;
+  bool have_header = false;
   for (;;) {
-    if (threadIdx.x == 0) {
-      const Slot *cs = &C->slot[st.L % 3];
-      st.nf = ld_cg(&cs->n_new);
-      st.mf = ld_cg(&cs->m_new);
-      st.n_light = ld_cg(&cs->n_light);
-      st.n_heavy = ld_cg(&cs->n_heavy);
-      st.n_pieces = ld_cg(&cs->n_pieces);
-      if (blockIdx.x == 0) C->slot[(st.L + 2) % 3] = Slot{0, 0, 0, 0, 0, 0};
-      if (st.L > 0) st.reached += st.nf;
-      st.explored += st.mf;
-      st.stop = 0;
-      if (st.nf == 0) {
-        st.stop = 1;
-        st.ecc = st.L - 1;
-      } else if (st.reached + 1 >= max_reach || st.L + 1 >= p.n) {
-        st.stop = 1;  // condition 1: nothing left to discover
-        st.ecc = st.L;
-      } else {
-        // a4 direction choice (identical in every CTA: same inputs)
-        if (p.variant == DAWN_PUSH || !p.can_pull) {
-          st.dir = kPush;
-        } else if (p.variant == DAWN_PULL) {
-          st.dir = kPull;
-        } else {
-          const double mu = (double)(p.m - st.explored);
-          if (st.dir == kPush) {
-            if ((double)st.mf * p.alpha > mu && st.nf > st.prev_nf) st.dir = kPull;
-          } else {
-            if ((double)st.nf * p.beta < (double)p.n && st.nf < st.prev_nf) st.dir = kPush;
-          }
-        }
-        st.prev_nf = st.nf;
-      }
+    if (!have_header) {
+      if (threadIdx.x == 0) level_header(p, C, st, max_reach, nblocks);
+      __syncthreads();
     }
-    __syncthreads();
+    have_header = false;
     if (st.stop) break;
 
+    if (st.solo) {
+      // ---- solo stretch: narrow push levels on CTA 0 with __syncthreads only
+      if (blockIdx.x != 0) {
+        if (threadIdx.x == 0) {
+          ++solo_epoch;
+          while (ld_acquire(&C->solo_epoch) < solo_epoch) {
+          }
+          fence_acq_rel_gpu();
+          const uint4 *src4 = reinterpret_cast<const uint4 *>(C->solo_state);
+          uint4 *dst4 = reinterpret_cast<uint4 *>(&st);
+#pragma unroll
+          for (int i = 0; i < (int)(sizeof(LevelState) / 16); ++i) dst4[i] = __ldcg(src4 + i);
+        }
+        __syncthreads();
+        have_header = true;  // CTA 0 published the post-header state of this level
+        continue;
+      }
+      const uint32_t lw = threadIdx.x / 32;
+      for (;;) {
+        Slot *ns = &C->slot[(st.L + 1) % 3];
+        uint32_t n_new = 0;
+        unsigned long long m_new = 0;
+        push_level(p, st, ns, lw, NT / 32, n_new, m_new, stg);
+        block_flush(n_new, m_new, &ns->n_new, &ns->m_new, red);
+        trace_done(p, st.L);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          level_advance(st);
+          level_header(p, C, st, max_reach, nblocks);
+        }
+        __syncthreads();
+        if (st.stop || !st.solo) break;
+      }
+      if (threadIdx.x == 0) {
+        const uint4 *src4 = reinterpret_cast<const uint4 *>(&st);
+        uint4 *dst4 = reinterpret_cast<uint4 *>(C->solo_state);
+#pragma unroll
+        for (int i = 0; i < (int)(sizeof(LevelState) / 16); ++i) dst4[i] = src4[i];
+        ++solo_epoch;
+        st_release(&C->solo_epoch, solo_epoch);
+      }
+      have_header = true;
+      continue;
+    }
+
     if (st.dir == kPull && st.rep == kRepQueue) {
-      // queue -> frontier bitmap fb[b]: clear, barrier, scatter, barrier
+      // queue -> frontier bitmap fb[b] (and a clean fb[b+1] for the pull to write)
       uint32_t *fb = p.fb[st.b];
-      for (uint32_t w = gtid; w < p.nwords; w += nthreads) fb[w] = 0;
-      grid_sync(&C->bar, nblocks);
-      for (uint32_t i = gtid; i < st.n_light; i += nthreads) {
+      uint32_t *fn = p.fb[(st.b + 1) % 3];
+      for (uint32_t w = gtid; w < p.nwords; w += nthreads) { fb[w] = 0; fn[w] = 0; }
+      grid_sync(&C->bar, nblocks, bar_target);
+      for (uint32_t i = gtid; i < st.qn; i += nthreads) {
         const uint32_t v = ld_cg(p.Lv[st.q] + i);
         red_or(fb + (v >> 5), 1u << (v & 31));
       }
-      for (uint32_t i = gtid; i < st.n_heavy; i += nthreads) {
-        const uint32_t v = ld_cg(p.Hv[st.q] + i);
-        red_or(fb + (v >> 5), 1u << (v & 31));
-      }
-      grid_sync(&C->bar, nblocks);
+      grid_sync(&C->bar, nblocks, bar_target);
       if (threadIdx.x == 0) st.rep = kRepBitmap;
     } else if (st.dir == kPush && st.rep == kRepBitmap) {
       // frontier bitmap fb[b] -> queue q (ballot/popc compaction), barrier
       Slot *cs = &C->slot[st.L % 3];
       const uint32_t *fb = p.fb[st.b];
       const uint32_t lane = lane_id();
+      uint32_t cnt = 0;
       for (uint32_t base = gwarp * 32; base < p.nwords; base += nwarps * 32) {
         const uint32_t w = base + lane;
         uint32_t bits = (w < p.nwords) ? ld_cg(fb + w) : 0u;
@@ -338,14 +608,15 @@ __global__ void __launch_bounds__(NT) k_sssp(SsspParams p) {
             rs = ld_nc(p.rp + u);
             d = ld_nc(p.rp + u + 1) - rs;
           }
-          enqueue_frontier(p, cs, st.q, has, u, rs, d);
+          enqueue_frontier(p, cs, st.q, has, u, rs, d, stg, cnt);
         }
       }
-      grid_sync(&C->bar, nblocks);
+      stage_flush(p, cs, st.q, stg, cnt);
+      grid_sync(&C->bar, nblocks, bar_target);
       if (threadIdx.x == 0) {
-        st.n_light = ld_cg(&cs->n_light);
-        st.n_heavy = ld_cg(&cs->n_heavy);
-        st.n_pieces = ld_cg(&cs->n_pieces);
+        const unsigned long long qp = ld_cg(&cs->qpack);
+        st.qn = (uint32_t)(qp >> 32);
+        st.qe = (uint32_t)qp;
         st.rep = kRepQueue;
       }
       __syncthreads();
@@ -355,32 +626,21 @@ __global__ void __launch_bounds__(NT) k_sssp(SsspParams p) {
     uint32_t n_new = 0;
     unsigned long long m_new = 0;
     if (st.dir == kPush) {
-      push_level(p, st, ns, gwarp, nwarps, n_new, m_new);
+      push_level(p, st, ns, gwarp, nwarps, n_new, m_new, stg);
     } else {
       pull_level(p, st, gwarp, nwarps, n_new, m_new, examined);
     }
     block_flush(n_new, m_new, &ns->n_new, &ns->m_new, red);
-    grid_sync(&C->bar, nblocks);
-    if (threadIdx.x == 0) {
-      if (st.dir == kPush) {
-        st.push_levels++;
-        st.push_edges += st.mf;
-        st.q ^= 1;
-        st.rep = kRepQueue;
-      } else {
-        st.pull_levels++;
-        st.b ^= 1;
-        st.rep = kRepBitmap;
-      }
-      st.L++;
-    }
+    trace_done(p, st.L);
+    grid_sync(&C->bar, nblocks, bar_target);
+    if (threadIdx.x == 0) level_advance(st);
     __syncthreads();
   }
 
   // ---- a7 statistics
   if (p.stats) {
     block_flush(0u, examined, nullptr, &C->examined, red);
-    grid_sync(&C->bar, nblocks);
+    grid_sync(&C->bar, nblocks, bar_target);
     if (blockIdx.x == 0 && threadIdx.x == 0) {
       dawn_sssp_stats s;
       s.levels = st.ecc;
@@ -392,6 +652,7 @@ __global__ void __launch_bounds__(NT) k_sssp(SsspParams p) {
       *p.stats = s;
     }
   }
+  grid_exit(&C->bar, nblocks);
 }
 
 }  // namespace dawn

@@ -227,3 +227,18 @@ def test_determinism():
     d1, r1 = dawn.msssp(G, g.sample_sources(100, 4))
     d2, r2 = dawn.msssp(G, g.sample_sources(100, 4))
     assert torch.equal(d1, d2) and torch.equal(r1, r2)
+
+
+def test_trace_levels_consistent():
+    g = graphgen.kron(14, 16)
+    G = dawn.Graph(g.row_ptr, g.col, True, trace=True)
+    s = int(g.sample_sources(1, 9)[0])
+    for v in VARIANTS:
+        d, st = gpu_dist(G, s, v, stats=True)
+        tr = G.trace()
+        assert len(tr) == st["levels"] + 2 or len(tr) == st["levels"] + 1
+        assert tr["nf"][0] == 1 and np.all(np.diff(tr["t_ns"].astype(np.int64)) >= 0)
+        fin = d != UNR
+        counts = np.bincount(d[fin], minlength=len(tr))
+        assert np.array_equal(tr["nf"][: st["levels"] + 1], counts[: st["levels"] + 1])
+        assert tr["dir"][-1] == 2
