@@ -332,7 +332,7 @@ def run_apsp(args, rank, world, dev, steps=None, warmup=None):
                          "frac": achieved / peak, "peak_kind": peak_kind,
                          "kernel": "k_ms64 (one persistent launch per rank)",
                          "bytes_model": "per source B_SOVM = 4*E_wcc + 8*S_wcc + 32",
-                         "traffic": None},
+                         "traffic": json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json"))).get("apsp-C5") if os.path.exists(os.path.join(ROOT, "profiles", "ncu_traffic.json")) else None},
             "check": {"all_reached_S_wcc_minus_1": bool(np.all(recs["reached"] == k - 1))},
             "clocks": clk.summary()}, g, verts
 

@@ -91,6 +91,8 @@ typedef struct {
   uint64_t mf;       /* sum of out-degrees of frontier L                                      */
   uint64_t t_first;  /* %globaltimer when the first CTA finished level L's work               */
   uint64_t t_last;   /* %globaltimer when the last CTA finished level L's work (pre-barrier)  */
+  uint64_t cyc[4];   /* SM cycles summed over all warps: [0] push items / pull light rows,
+                        [1] pull heavy-row pieces, [2] queue flush + counters, [3] conversions */
 } dawn_trace_rec;
 
 typedef struct dawn_graph_s *dawn_graph;
@@ -123,11 +125,15 @@ dawn_status dawn_graph_load_csr(int64_t n, int64_t m, const int64_t *row_ptr, co
 /* Free the host-side handle only (device memory belongs to the caller). NULL is a no-op. */
 dawn_status dawn_graph_destroy(dawn_graph g);
 
-/* Direction-switch thresholds for DAWN_AUTO (Beamer-style, cited by the paper at L123):
- * push -> pull when alpha * m_f > m_u and the frontier grows; pull -> push when
- * beta * n_f < n and it shrinks.  Defaults alpha = 4 (measured on Kronecker-20, B200),
- * beta = 24.  ms_alpha: the 64-source kernel pulls when ms_alpha * m_active > m_unsettled
- * (default 2).  Values <= 0 keep the current setting.                                         */
+/* Direction-switch thresholds for DAWN_AUTO (the paper's two operators, A1/A2, chosen per level
+ * on the device; switch idea after Beamer, cited by the paper at L123):
+ *   push -> pull when alpha * m_f^2 > n_u * m_u and the frontier grows (m_f: out-degree sum of
+ *            the frontier, n_u / m_u: vertices / arcs not yet reached) — the cost of a pull
+ *            sweep is ~ n_u early-exit scans of length ~ m_u / m_f;
+ *   pull -> push when beta * n_f < n and the frontier shrinks.
+ * Defaults alpha = 2, beta = 24 (measured on Kronecker-20/24, B200).  ms_alpha: the 64-source
+ * kernel pulls when ms_alpha * m_active > m_unsettled (default 2).  Values <= 0 keep the
+ * current setting.                                                                           */
 dawn_status dawn_graph_set_tuning(dawn_graph g, double alpha, double beta, double ms_alpha);
 
 /*

@@ -23,7 +23,7 @@ __all__ = ["build", "Graph", "sssp", "msssp", "apsp", "apsp_shard", "DawnError",
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _CSRC = os.path.join(_HERE, "csrc")
-_LIB = os.path.join(_HERE, "libdawn.so")
+_LIB = os.environ.get("DAWN_LIB") or os.path.join(_HERE, "libdawn.so")  # DAWN_LIB: A/B builds
 _INCLUDE = os.path.join(os.path.dirname(_HERE), "include")
 
 UNREACHED = 0xFFFFFFFF
@@ -50,17 +50,21 @@ def _sources():
             if f.endswith((".cu", ".cuh", ".h"))] + [os.path.join(_INCLUDE, "dawn.h")]
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    """Compile libdawn.so in-tree for sm_100a (nvcc; cross-compiles without a GPU)."""
+def build(force: bool = False, verbose: bool = False, out: str | None = None,
+          defines: tuple = ()) -> str:
+    """Compile libdawn.so in-tree for sm_100a (nvcc; cross-compiles without a GPU).
+    `out`/`defines` build an experimental variant (e.g. defines=("DAWN_PULL_J=4",))."""
+    target = out or _LIB
     srcs = _sources()
     newest = max(os.path.getmtime(s) for s in srcs)
-    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < newest:
-        cmd = ["nvcc", *NVCC_FLAGS, os.path.join(_CSRC, "dawn.cu"), "-o", _LIB + ".tmp"]
+    if force or out or not os.path.exists(target) or os.path.getmtime(target) < newest:
+        cmd = ["nvcc", *NVCC_FLAGS, *[f"-D{d}" for d in defines],
+               os.path.join(_CSRC, "dawn.cu"), "-o", target + ".tmp"]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
         subprocess.check_call(cmd)
-        os.replace(_LIB + ".tmp", _LIB)
-    return _LIB
+        os.replace(target + ".tmp", target)
+    return target
 
 
 _lib = None
@@ -167,7 +171,8 @@ class Graph:
     def trace(self, stream=None) -> np.ndarray:
         """Per-level trace of the last sssp call (graph built with trace=True)."""
         dt = np.dtype([("t_ns", "<u8"), ("level", "<u4"), ("dir", "<u4"), ("nf", "<u4"),
-                       ("rep", "<u4"), ("mf", "<u8"), ("t_first", "<u8"), ("t_last", "<u8")])
+                       ("rep", "<u4"), ("mf", "<u8"), ("t_first", "<u8"), ("t_last", "<u8"),
+                       ("cyc", "<u8", (4,))])
         buf = np.zeros(1 << 16, dt)
         cnt = ctypes.c_int64(0)
         _check(lib().dawn_graph_trace(self._h, buf.ctypes.data_as(ctypes.c_void_p), len(buf),

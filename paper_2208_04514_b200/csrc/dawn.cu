@@ -13,6 +13,7 @@
 #include "../../include/dawn.h"
 #include "layout.h"
 #include "ms64_kernel.cuh"
+#include "small_kernel.cuh"
 #include "sssp_kernel.cuh"
 
 using namespace dawn;
@@ -120,38 +121,53 @@ __global__ void k_hscan(uint32_t *tmp, uint32_t nblk, uint32_t *total) {
   }
 }
 
-// pass 3: write pieces (vertex, start, end) in vertex order
-__global__ void k_hfill(const uint32_t *__restrict__ rp, uint32_t n, const uint32_t *__restrict__ tmp,
-                        uint32_t *__restrict__ hv, uint32_t *__restrict__ hs,
-                        uint32_t *__restrict__ he) {
-  __shared__ uint32_t sm[1024];
-  constexpr uint32_t kPer = kScanBlock / 256;  // blockDim.x == 256
-  const uint32_t v0 = blockIdx.x * kScanBlock + threadIdx.x * kPer;
-  uint32_t c = 0;
-  for (uint32_t i = 0; i < kPer; ++i)
-    if (v0 + i < n) c += hpieces(rp, v0 + i);
-  sm[threadIdx.x] = c;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    uint32_t run = tmp[blockIdx.x];
-    for (uint32_t i = 0; i < blockDim.x; ++i) {
-      const uint32_t x = sm[i];
-      sm[i] = run;
-      run += x;
+// pass 3 (piece-major order): hc[c] = #heavy rows with exactly c pieces; maxc
+__global__ void k_hhist(const uint32_t *__restrict__ rp, uint32_t n, uint32_t *hc, uint32_t *maxc) {
+  uint32_t mx = 0;
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+    const uint32_t c = hpieces(rp, v);
+    if (c) {
+      atomicAdd(hc + c, 1u);
+      mx = max(mx, c);
     }
   }
-  __syncthreads();
-  uint32_t o = sm[threadIdx.x];
-  for (uint32_t i = 0; i < kPer; ++i) {
-    const uint32_t v = v0 + i;
-    if (v >= n) break;
+  for (int o = 16; o; o >>= 1) mx = max(mx, __shfl_xor_sync(DAWN_FULL, mx, o));
+  if ((threadIdx.x & 31) == 0 && mx) atomicMax(maxc, mx);
+}
+
+// pass 4 (one thread): base[k] = #pieces with piece index < k  (rows with > k pieces: suffix
+// sums of hc); cursor[k] = 0
+__global__ void k_hbase(uint32_t *hc, uint32_t *base, uint32_t *cursor, const uint32_t *maxc) {
+  if (threadIdx.x != 0) return;
+  const uint32_t mx = *maxc;
+  uint32_t rows = 0;  // rows with > k pieces, built from the top
+  for (uint32_t c = mx; c >= 1; --c) {
+    rows += hc[c];
+    hc[c] = rows;      // now hc[c] = #rows with >= c pieces = #pieces of index c-1
+  }
+  uint32_t run = 0;
+  for (uint32_t k = 0; k < mx; ++k) {
+    base[k] = run;
+    cursor[k] = 0;
+    run += hc[k + 1];
+  }
+}
+
+// pass 5: write every piece at base[k] + (arrival order within index k): all first pieces,
+// then all second pieces, ...  A later piece of a row usually finds the row already settled
+// by an earlier one (pull early exit survives the split).
+__global__ void k_hfill(const uint32_t *__restrict__ rp, uint32_t n, const uint32_t *__restrict__ base,
+                        uint32_t *cursor, uint32_t *__restrict__ hv, uint32_t *__restrict__ hs,
+                        uint32_t *__restrict__ he) {
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
     const uint32_t s = rp[v], e = rp[v + 1];
     if (e - s <= kHeavy) continue;
-    for (uint32_t a = s; a < e; a += kHPiece) {
+    uint32_t k = 0;
+    for (uint32_t a = s; a < e; a += kHPiece, ++k) {
+      const uint32_t o = base[k] + atomicAdd(cursor + k, 1u);
       hv[o] = v;
       hs[o] = a;
       he[o] = min(e, a + kHPiece);
-      ++o;
     }
   }
 }
@@ -167,9 +183,10 @@ struct dawn_graph_s {
   Layout L;
   const int32_t *col, *icol;
   bool has_csc;
-  float alpha = 4.f, beta = 24.f, ms_alpha = 2.f;
+  float alpha = 2.f, beta = 24.f, ms_alpha = 2.f;
   int sssp_grid, ms_grid;
   bool trace;
+  size_t small_cap;  // max dynamic smem for k_small (0 = disabled)
 };
 
 namespace {
@@ -245,10 +262,21 @@ dawn_status dawn_graph_load_csr(int64_t n, int64_t m, const int64_t *row_ptr, co
   g->trace = flags & DAWN_GRAPH_TRACE;
   if ((e = cudaSetDevice(g->device)) != cudaSuccess) { delete g; return cuda_fail(e, "cudaSetDevice"); }
   cudaDeviceGetAttribute(&g->nsm, cudaDevAttrMultiProcessorCount, g->device);
-  g->alpha = (float)env_int("DAWN_ALPHA", 4);
+  g->alpha = (float)env_int("DAWN_ALPHA", 2);
   g->beta = (float)env_int("DAWN_BETA", 24);
   g->ms_alpha = (float)env_int("DAWN_MS_ALPHA", 2);
   g->sssp_grid = grid_for((const void *)k_sssp<kNT>, g->nsm, "DAWN_SSSP_BPS");
+  {
+    int optin = 0;
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, g->device);
+    const size_t cap = (size_t)std::max(0, optin - 1024);
+    g->small_cap = 0;
+    if (env_int("DAWN_SMALL", 1) &&
+        cudaFuncSetAttribute((const void *)k_small<1024>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cap) == cudaSuccess)
+      g->small_cap = cap;
+    cudaGetLastError();
+  }
   g->ms_grid = grid_for((const void *)k_ms64<kNT>, g->nsm, "DAWN_MS_BPS");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const uint32_t nwords = (uint32_t)((n + 31) / 32);
@@ -298,9 +326,15 @@ dawn_status dawn_graph_load_csr(int64_t n, int64_t m, const int64_t *row_ptr, co
       k_hcount<<<nblk, 256, 0, st>>>(rows, (uint32_t)n, at<uint32_t>(g, h.bits),
                                      at<uint32_t>(g, L.scan_tmp));
       k_hscan<<<1, 32, 0, st>>>(at<uint32_t>(g, L.scan_tmp), nblk, count);
-      k_hfill<<<nblk, 256, 0, st>>>(rows, (uint32_t)n, at<uint32_t>(g, L.scan_tmp),
-                                    at<uint32_t>(g, h.v), at<uint32_t>(g, h.s),
-                                    at<uint32_t>(g, h.e));
+      const size_t cap = (size_t)m / kHPiece + 3;
+      uint32_t *hc = at<uint32_t>(g, L.piece_tmp), *base = hc + cap, *cursor = base + cap,
+               *maxc = cursor + cap;
+      cudaMemsetAsync(hc, 0, 4 * cap, st);
+      cudaMemsetAsync(maxc, 0, 4, st);
+      k_hhist<<<blocks, 256, 0, st>>>(rows, (uint32_t)n, hc, maxc);
+      k_hbase<<<1, 32, 0, st>>>(hc, base, cursor, maxc);
+      k_hfill<<<blocks, 256, 0, st>>>(rows, (uint32_t)n, base, cursor, at<uint32_t>(g, h.v),
+                                      at<uint32_t>(g, h.s), at<uint32_t>(g, h.e));
     };
     build_list(at<uint32_t>(g, L.rp), L.hout, &C->n_hp_out);
     if (L.own_irp) {
@@ -344,6 +378,16 @@ dawn_status dawn_sssp(dawn_graph g, int64_t source, uint32_t variant, uint32_t *
   dawn_status s = set_device(g);
   if (s != DAWN_OK) return s;
   const Layout &L = g->L;
+  const size_t small_bytes = small_smem_bytes(g->n, g->m);
+  if (variant != DAWN_PULL && !g->trace && small_bytes <= g->small_cap) {
+    // whole SSSP in one CTA's shared memory (tiny graphs, e.g. configs[0])
+    SmallParams sp{(uint32_t)g->n, (uint32_t)g->m, at<uint32_t>(g, L.rp), g->col, dist, stats,
+                   (uint32_t)source};
+    k_small<1024><<<1, 1024, small_bytes, static_cast<cudaStream_t>(stream)>>>(sp);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "k_small launch");
+    return DAWN_OK;
+  }
   SsspParams p{};
   p.n = (uint32_t)g->n;
   p.nwords = (uint32_t)((g->n + 31) / 32);

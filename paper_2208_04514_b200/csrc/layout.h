@@ -24,9 +24,14 @@ constexpr uint32_t kSoloE = 512;
 // by one lane each (early exit, 4 probes per round trip).
 constexpr uint32_t kHeavy = 32;
 constexpr uint32_t kHPiece = 256;
+constexpr uint32_t kHeavyProbe = 16;  // in-edges a heavy row probes lane-parallel in the sweep
 constexpr uint32_t kScanBlock = 2048;  // elements per CTA in the load-time piece scan
 constexpr uint32_t kMaxBlocks = 2048;  // cap on persistent grid size (partials buffer)
 constexpr uint32_t kTraceCap = 1 << 16;
+
+#ifndef DAWN_PULL_J
+#define DAWN_PULL_J 2  // vis words per warp iteration of the pull sweep (independent scans)
+#endif
 
 enum : uint32_t { kPush = 0, kPull = 1, kRepQueue = 0, kRepBitmap = 1 };
 
@@ -65,6 +70,8 @@ struct TraceRec {
   uint32_t level, dir, nf, pad;
   unsigned long long mf;
   unsigned long long t_first, t_last;  // first / last CTA done with the level's work
+  unsigned long long cyc[4];           // sum over warps of clock64 cycles: [0] light/push work,
+                                       // [1] heavy pull pieces, [2] flush, [3] conversions
 };
 
 struct HeavyList {  // static pieces of rows with degree > kHeavy
@@ -74,7 +81,7 @@ struct HeavyList {  // static pieces of rows with degree > kHeavy
 struct Layout {
   size_t rp, irp, noin, vis, fb[3], Lv[2], Lsd[2], Cf[2], ctrl, trace;
   HeavyList hout, hin;
-  size_t scan_tmp;
+  size_t scan_tmp, piece_tmp;
   size_t seen, F0, F1, nxt, msctrl, part, srcbuf, total;
   uint64_t srccap, capCf, capHP;
   bool own_irp;
@@ -115,6 +122,7 @@ inline Layout make_layout(int64_t n, int64_t m, uint32_t flags) {
   heavy(L.hout);
   if (L.own_irp) heavy(L.hin); else L.hin = L.hout;
   L.scan_tmp = take(4 * ((size_t)n / kScanBlock + 2));
+  L.piece_tmp = take(4 * (3 * ((size_t)m / kHPiece + 3) + 1));
   L.seen = take(8 * (size_t)n);
   L.F0 = take(8 * (size_t)n);
   L.F1 = take(8 * (size_t)n);

@@ -263,7 +263,9 @@ __global__ void __launch_bounds__(NT) k_ms64(MsParams p) {
         // pass 1b: heavy in-rows by static pieces; partial ORs meet in nxt[u]
         for (uint32_t pc = gwarp; pc < st.n_hp_in; pc += nwarps) {
           const uint32_t u = ld_nc(p.hin_v + pc);
-          const unsigned long long U = ~p.seen[u] & active;
+          // bits already found by earlier pieces of this row (pieces are stored piece-major:
+          // all first pieces, then all second pieces, ...) need not be looked for again
+          const unsigned long long U = ~p.seen[u] & active & ~ld_cg(p.nxt + u);
           if (!U) continue;
           const uint32_t s = ld_nc(p.hin_s + pc), e = ld_nc(p.hin_e + pc);
           unsigned long long acc = 0;

@@ -59,44 +59,82 @@ __device__ __forceinline__ unsigned long long globaltimer() {
   return t;
 }
 
+// Per-warp phase cycle accounting (trace builds only): lane 0 adds its warp's cycles.
+__device__ __forceinline__ void phase_add(const SsspParams &p, uint32_t L, int ph,
+                                          long long &t0) {
+  if (p.trace) {
+    const long long t = clock64();
+    if (lane_id() == 0 && L < kTraceCap)
+      atomicAdd(&p.trace[L].cyc[ph], (unsigned long long)(t - t0));
+    t0 = t;
+  }
+}
+
 // Flush the first k (<= 32) staged entries to queue q: one 64-bit atomic reserves k slots AND
 // their edge range; entry i gets (row start, exclusive edge offset) and the chunk map Cf gets
 // the entry for every chunk boundary inside its row.  Warp-collective.
-__device__ __forceinline__ void stage_emit(const SsspParams &p, Slot *s, int q, WarpStage &stg,
-                                           uint32_t k) {
+// Write the first k staged entries at the packed queue position `old` = (slot << 32) | edge
+// offset, reserved by the caller.  Warp-collective.
+__device__ __forceinline__ void stage_write(const SsspParams &p, int q, WarpStage &stg,
+                                            uint32_t k, unsigned long long old) {
   const uint32_t lane = lane_id();
   const uint32_t d = lane < k ? stg.d[lane] : 0u;
   const uint32_t incl = warp_incl_scan(d);
-  const uint32_t D = __shfl_sync(DAWN_FULL, incl, 31);
-  unsigned long long old = 0;
-  if (lane == 0) old = atomicAdd(&s->qpack, ((unsigned long long)k << 32) | D);
-  old = __shfl_sync(DAWN_FULL, old, 0);
   const uint32_t i = (uint32_t)(old >> 32) + lane;
   const uint32_t o = (uint32_t)old + incl - d;
   if (lane < k) {
     p.Lv[q][i] = stg.u[lane];
     p.Lsd[q][i] = make_uint2(stg.rs[lane], o);
   }
-  // chunk map: entry i owns chunks [ceil(o/C), ceil((o+d)/C)); written warp-cooperatively so
-  // a hub row (1000 chunks) costs 32 lanes' stores, not one lane's loop
+  // chunk map: entry i owns chunks [ceil(o/C), ceil((o+d)/C)).  Rows with many chunks (hubs:
+  // 12K chunks for a 400K-arc row) are filled by the whole warp with coalesced stores, one row
+  // at a time; short rows lane-serially in parallel.
   const uint32_t c0 = (o + kChunk - 1) / kChunk;
   const uint32_t nc = (lane < k) ? (o + d + kChunk - 1) / kChunk - c0 : 0u;
-  const uint32_t inc2 = warp_incl_scan(nc);
-  const uint32_t T = __shfl_sync(DAWN_FULL, inc2, 31);
-  const uint32_t ex2 = inc2 - nc;
-  for (uint32_t xb = 0; xb < T; xb += 32) {
-    const uint32_t x = xb + lane;
-    uint32_t kk = 0;
-#pragma unroll
-    for (uint32_t step = 16; step; step >>= 1) {
-      const uint32_t e = __shfl_sync(DAWN_FULL, ex2, kk + step);
-      if (e <= x) kk += step;
-    }
-    const uint32_t cb = __shfl_sync(DAWN_FULL, c0, kk) + x - __shfl_sync(DAWN_FULL, ex2, kk);
+  const bool big = nc > 8;
+  if (!big)
+    for (uint32_t x = 0; x < nc; ++x) p.Cf[q][c0 + x] = i;
+  uint32_t bm = __ballot_sync(DAWN_FULL, big);
+  while (bm) {
+    const uint32_t kk = __ffs(bm) - 1;
+    bm &= bm - 1;
+    const uint32_t cb = __shfl_sync(DAWN_FULL, c0, kk), nb = __shfl_sync(DAWN_FULL, nc, kk);
     const uint32_t ik = __shfl_sync(DAWN_FULL, i, kk);
-    if (x < T) p.Cf[q][cb] = ik;
+    for (uint32_t x = lane; x < nb; x += 32) p.Cf[q][cb + x] = ik;
   }
   __syncwarp();
+}
+
+__device__ __forceinline__ void stage_emit(const SsspParams &p, Slot *s, int q, WarpStage &stg,
+                                           uint32_t k) {
+  const uint32_t lane = lane_id();
+  const uint32_t D = warp_sum(lane < k ? stg.d[lane] : 0u);
+  unsigned long long old = 0;
+  if (lane == 0) old = atomicAdd(&s->qpack, ((unsigned long long)k << 32) | D);
+  stage_write(p, q, stg, k, __shfl_sync(DAWN_FULL, old, 0));
+}
+
+// End-of-level flush of every warp's leftover stage (< 32 entries) with ONE atomic per CTA
+// (a per-warp atomic here serialised ~4.7K same-address atomics: 7.6 us per level).
+// CTA-collective: every thread of the CTA must call it.
+__device__ __forceinline__ void cta_flush(const SsspParams &p, Slot *s, int q, WarpStage &stg,
+                                          uint32_t cnt, unsigned long long *sm) {
+  const uint32_t lane = lane_id(), w = threadIdx.x / 32, nw = blockDim.x / 32;
+  const uint32_t D = warp_sum(lane < cnt ? stg.d[lane] : 0u);
+  if (lane == 0) sm[w] = ((unsigned long long)cnt << 32) | D;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long run = 0;
+    for (uint32_t i = 0; i < nw; ++i) {
+      const unsigned long long x = sm[i];
+      sm[i] = run;
+      run += x;
+    }
+    sm[nw] = run ? atomicAdd(&s->qpack, run) : 0ull;
+  }
+  __syncthreads();
+  if (cnt) stage_write(p, q, stg, cnt, sm[nw] + sm[w]);
+  __syncthreads();
 }
 
 // Warp-collective append of discovered vertices (has: lane discovered u, row start rs,
@@ -131,11 +169,6 @@ __device__ __forceinline__ void enqueue_frontier(const SsspParams &p, Slot *s, i
   }
 }
 
-__device__ __forceinline__ void stage_flush(const SsspParams &p, Slot *s, int q, WarpStage &stg,
-                                            uint32_t &cnt) {
-  if (cnt) stage_emit(p, s, q, stg, cnt);
-  cnt = 0;
-}
 
 // Push-mode visit of arc (frontier vertex) -> u, warp-collective (all lanes call; `act`
 // false for idle lanes).
@@ -233,7 +266,7 @@ __device__ __forceinline__ void push_item(const SsspParams &p, const LevelState 
 
 __device__ void push_level(const SsspParams &p, const LevelState &st, Slot *ns, uint32_t gwarp,
                            uint32_t nwarps, uint32_t &n_new, unsigned long long &m_new,
-                           WarpStage &stg) {
+                           WarpStage &stg, long long &t0, unsigned long long *fsm) {
   const uint32_t E = st.qe;
   const uint32_t nchunks = (E + kChunk - 1) / kChunk;
   uint32_t cnt = 0;
@@ -245,7 +278,9 @@ __device__ void push_level(const SsspParams &p, const LevelState &st, Slot *ns, 
     for (uint32_t it = gwarp; it < nchunks; it += nwarps)
       push_item<1>(p, st, ns, it, n_new, m_new, stg, cnt);
   }
-  stage_flush(p, ns, st.q ^ 1, stg, cnt);
+  phase_add(p, st.L, 0, t0);
+  cta_flush(p, ns, st.q ^ 1, stg, cnt, fsm);
+  phase_add(p, st.L, 2, t0);
 }
 
 __device__ __forceinline__ bool fb_test(const uint32_t *fb, uint32_t v) {
@@ -254,7 +289,7 @@ __device__ __forceinline__ bool fb_test(const uint32_t *fb, uint32_t v) {
 
 __device__ void pull_level(const SsspParams &p, const LevelState &st, uint32_t gwarp,
                            uint32_t nwarps, uint32_t &n_new, unsigned long long &m_new,
-                           unsigned long long &examined) {
+                           unsigned long long &examined, long long &t0) {
   const uint32_t lane = lane_id();
   const uint32_t L1 = st.L + 1;
   const uint32_t *fcur = p.fb[st.b];
@@ -263,18 +298,20 @@ __device__ void pull_level(const SsspParams &p, const LevelState &st, uint32_t g
   const uint32_t tail_bits = p.n & 31;
   // (1) light rows: lane per vertex, a warp owns vis words w and w + nwarps (two independent
   //     scans in flight per lane), 4 in-neighbours probed per round trip
-  constexpr int J = 2;
+  constexpr int J = DAWN_PULL_J;
   for (uint32_t wb = gwarp; wb < p.nwords; wb += nwarps * J) {
-    uint32_t w[J], vw[J], todo[J], s[J], e[J], j0[J];
+    uint32_t w[J], vw[J], todo[J], s[J], e[J], j0[J], hv[J], ef[J];
     bool need[J], found[J];
 #pragma unroll
     for (int j = 0; j < J; ++j) {
       w[j] = wb + j * nwarps;
       vw[j] = 0;
       todo[j] = 0;
+      hv[j] = 0;
       if (w[j] < p.nwords) {
         vw[j] = ld_cg(p.vis + w[j]);
-        todo[j] = ~vw[j] & ~ld_nc(p.hin_bits + w[j]);
+        todo[j] = ~vw[j];
+        hv[j] = ld_nc(p.hin_bits + w[j]);
         if (w[j] == p.nwords - 1 && tail_bits) todo[j] &= (1u << tail_bits) - 1;
         if (lane == 0) fclr[w[j]] = 0;
       }
@@ -290,17 +327,20 @@ __device__ void pull_level(const SsspParams &p, const LevelState &st, uint32_t g
         e[j] = ld_nc(p.irp + u + 1);
       }
       j0[j] = s[j];
+      // heavy rows (in-degree > kHeavy): only the first kHeavyProbe in-edges here, lane-parallel
+      // with everything else; the static pieces finish the rows still unsettled
+      ef[j] = ((hv[j] >> lane) & 1u) ? min(e[j], s[j] + kHeavyProbe) : e[j];
     }
     for (;;) {
       bool any = false;
       uint32_t v[J][4];
 #pragma unroll
       for (int j = 0; j < J; ++j) {
-        const bool go = need[j] && !found[j] && j0[j] < e[j];
+        const bool go = need[j] && !found[j] && j0[j] < ef[j];
         any |= go;
 #pragma unroll
         for (int i = 0; i < 4; ++i)
-          v[j][i] = (go && j0[j] + i < e[j]) ? (uint32_t)ld_nc(p.icol + j0[j] + i) : 0xffffffffu;
+          v[j][i] = (go && j0[j] + i < ef[j]) ? (uint32_t)ld_nc(p.icol + j0[j] + i) : 0xffffffffu;
       }
       if (!any) break;
 #pragma unroll
@@ -320,7 +360,7 @@ __device__ void pull_level(const SsspParams &p, const LevelState &st, uint32_t g
     }
 #pragma unroll
     for (int j = 0; j < J; ++j) {
-      if (need[j]) examined += min(j0[j], e[j]) - s[j];
+      if (need[j]) examined += min(j0[j], ef[j]) - s[j];
       const uint32_t nb = __ballot_sync(DAWN_FULL, found[j]);
       if (lane == 0 && nb) {
         red_or(fnext + w[j], nb);
@@ -334,6 +374,7 @@ __device__ void pull_level(const SsspParams &p, const LevelState &st, uint32_t g
       }
     }
   }
+  phase_add(p, st.L, 0, t0);
   // (2) heavy rows: static pieces; 32 pieces tested per warp (vis), then a warp scans each
   //     live piece 32 in-edges per round trip
   for (uint32_t pb = gwarp * 32; pb < st.n_hp; pb += nwarps * 32) {
@@ -377,6 +418,7 @@ __device__ void pull_level(const SsspParams &p, const LevelState &st, uint32_t g
       }
     }
   }
+  phase_add(p, st.L, 1, t0);
 }
 
 // Block-wide sum of two counters, then one global atomic per CTA.
@@ -424,9 +466,14 @@ __device__ __forceinline__ void level_header(const SsspParams &p, Ctrl *C, Level
     } else if (p.variant == DAWN_PULL) {
       st.dir = kPull;
     } else {
+      // push costs ~ m_f edge visits; a pull sweep costs ~ n_u scans of expected length
+      // min(deg, m_u / m_f) (early exit once a frontier in-neighbour is met), so pull wins once
+      // alpha * m_f^2 > n_u * m_u.  (Beamer's linear m_f > m_u / alpha, cited by the paper at
+      // L123, picked the slower direction at Kronecker-20 L2 or Kronecker-24 L2 for any alpha.)
       const double mu = (double)(p.m - st.explored);
+      const double nu = (double)(max_reach - 1 - min(st.reached, max_reach - 1));
       if (st.dir == kPush) {
-        if ((double)st.mf * p.alpha > mu && st.nf > st.prev_nf) st.dir = kPull;
+        if ((double)st.mf * (double)st.mf * p.alpha > nu * mu && st.nf > st.prev_nf) st.dir = kPull;
       } else {
         if ((double)st.nf * p.beta < (double)p.n && st.nf < st.prev_nf) st.dir = kPush;
       }
@@ -444,6 +491,7 @@ __device__ __forceinline__ void level_header(const SsspParams &p, Ctrl *C, Level
     r.mf = st.mf;
     r.t_first = p.trace[st.L].t_first;
     r.t_last = p.trace[st.L].t_last;
+    for (int k = 0; k < 4; ++k) r.cyc[k] = p.trace[st.L].cyc[k];
     p.trace[st.L] = r;
     C->trace_n = st.L + 1;
   }
@@ -476,6 +524,7 @@ __global__ void __launch_bounds__(NT) k_sssp(SsspParams p) {
   __shared__ LevelState st;
   __shared__ unsigned long long red[2];
   __shared__ WarpStage stage[NT / 32];
+  __shared__ unsigned long long fsm[NT / 32 + 1];
   static_assert(sizeof(LevelState) <= sizeof(((Ctrl *)0)->solo_state), "solo_state too small");
   const uint32_t nblocks = gridDim.x;
   const uint32_t gwarp = blockIdx.x * (NT / 32) + threadIdx.x / 32;
@@ -514,6 +563,7 @@ __global__ void __launch_bounds__(NT) k_sssp(SsspParams p) {
     for (uint32_t i = gtid; i < ntr; i += nthreads) {
       p.trace[i].t_first = ~0ull;
       p.trace[i].t_last = 0;
+      for (int k = 0; k < 4; ++k) p.trace[i].cyc[k] = 0;
     }
   }
   if (threadIdx.x == 0) {
@@ -555,7 +605,8 @@ __global__ void __launch_bounds__(NT) k_sssp(SsspParams p) {
         Slot *ns = &C->slot[(st.L + 1) % 3];
         uint32_t n_new = 0;
         unsigned long long m_new = 0;
-        push_level(p, st, ns, lw, NT / 32, n_new, m_new, stg);
+        long long t0 = clock64();
+        push_level(p, st, ns, lw, NT / 32, n_new, m_new, stg, t0, fsm);
         block_flush(n_new, m_new, &ns->n_new, &ns->m_new, red);
         trace_done(p, st.L);
         __syncthreads();
@@ -578,6 +629,7 @@ __global__ void __launch_bounds__(NT) k_sssp(SsspParams p) {
       continue;
     }
 
+    long long tconv = clock64();
     if (st.dir == kPull && st.rep == kRepQueue) {
       // queue -> frontier bitmap fb[b] (and a clean fb[b+1] for the pull to write)
       uint32_t *fb = p.fb[st.b];
@@ -611,7 +663,7 @@ __global__ void __launch_bounds__(NT) k_sssp(SsspParams p) {
           enqueue_frontier(p, cs, st.q, has, u, rs, d, stg, cnt);
         }
       }
-      stage_flush(p, cs, st.q, stg, cnt);
+      cta_flush(p, cs, st.q, stg, cnt, fsm);
       grid_sync(&C->bar, nblocks, bar_target);
       if (threadIdx.x == 0) {
         const unsigned long long qp = ld_cg(&cs->qpack);
@@ -625,12 +677,14 @@ __global__ void __launch_bounds__(NT) k_sssp(SsspParams p) {
     Slot *ns = &C->slot[(st.L + 1) % 3];
     uint32_t n_new = 0;
     unsigned long long m_new = 0;
+    phase_add(p, st.L, 3, tconv);
     if (st.dir == kPush) {
-      push_level(p, st, ns, gwarp, nwarps, n_new, m_new, stg);
+      push_level(p, st, ns, gwarp, nwarps, n_new, m_new, stg, tconv, fsm);
     } else {
-      pull_level(p, st, gwarp, nwarps, n_new, m_new, examined);
+      pull_level(p, st, gwarp, nwarps, n_new, m_new, examined, tconv);
     }
     block_flush(n_new, m_new, &ns->n_new, &ns->m_new, red);
+    phase_add(p, st.L, 2, tconv);
     trace_done(p, st.L);
     grid_sync(&C->bar, nblocks, bar_target);
     if (threadIdx.x == 0) level_advance(st);
