@@ -31,6 +31,9 @@ extern "C" {
 #endif
 
 #define DAWN_UNREACHED 0xFFFFFFFFu
+/* Sources per pass of the bit-parallel multi-source kernel (4 x 64-bit words per vertex) and the
+ * unit of the APSP shard rule. */
+#define DAWN_MS_BATCH 256
 
 typedef enum {
   DAWN_OK = 0,
@@ -125,16 +128,30 @@ dawn_status dawn_graph_load_csr(int64_t n, int64_t m, const int64_t *row_ptr, co
 /* Free the host-side handle only (device memory belongs to the caller). NULL is a no-op. */
 dawn_status dawn_graph_destroy(dawn_graph g);
 
-/* Direction-switch thresholds for DAWN_AUTO (the paper's two operators, A1/A2, chosen per level
- * on the device; switch idea after Beamer, cited by the paper at L123):
- *   push -> pull when alpha * m_f^2 > n_u * m_u and the frontier grows (m_f: out-degree sum of
- *            the frontier, n_u / m_u: vertices / arcs not yet reached) — the cost of a pull
- *            sweep is ~ n_u early-exit scans of length ~ m_u / m_f;
- *   pull -> push when beta * n_f < n and the frontier shrinks.
- * Defaults alpha = 2, beta = 24 (measured on Kronecker-20/24, B200).  ms_alpha: the 64-source
- * kernel pulls when ms_alpha * m_active > m_unsettled (default 2).  Values <= 0 keep the
- * current setting.                                                                           */
-dawn_status dawn_graph_set_tuning(dawn_graph g, double alpha, double beta, double ms_alpha);
+/* Tunables of a graph handle (dawn_graph_set_param).  Defaults were measured on B200 with the
+ * Kronecker-20/24 configs; they change speed only, never results.
+ *   DAWN_PARAM_ALPHA  push -> pull when alpha * m_f^2 > n_u * m_u and the frontier grows
+ *                     (m_f: out-degree sum of the frontier; n_u / m_u: vertices / arcs not yet
+ *                     reached).  A pull sweep costs ~ n_u early-exit scans of length ~ m_u/m_f.
+ *                     The switch idea is Beamer's, cited by the paper at L123.  Default 2.
+ *   DAWN_PARAM_BETA   pull -> push when beta * n_f < n and the frontier shrinks.  Default 24.
+ *   DAWN_PARAM_MS_ALPHA  the multi-source kernel pulls when ms_alpha * m_active > m_unsettled.
+ *                     Default 2.
+ *   DAWN_PARAM_BITMAP_PUSH_EDGES  push levels whose frontier has >= this many arcs mark
+ *                     candidates in a bitmap (fire-and-forget) and settle them in a second pass
+ *                     instead of one returning atomic per arc.  Default 262144.
+ *   DAWN_PARAM_SOLO_EDGES  push levels with <= this many arcs run on one CTA with block-level
+ *                     barriers only.  Default 512.                                              */
+typedef enum {
+  DAWN_PARAM_ALPHA = 0,
+  DAWN_PARAM_BETA = 1,
+  DAWN_PARAM_MS_ALPHA = 2,
+  DAWN_PARAM_BITMAP_PUSH_EDGES = 3,
+  DAWN_PARAM_SOLO_EDGES = 4
+} dawn_param;
+
+/* Set one tunable (INVALID_ARGUMENT for an unknown key or a negative value). */
+dawn_status dawn_graph_set_param(dawn_graph g, dawn_param key, double value);
 
 /*
  * Single-source shortest paths (SSSP), one enqueue: initialisation, every level (push or
@@ -151,8 +168,9 @@ dawn_status dawn_sssp(dawn_graph g, int64_t source, uint32_t variant, uint32_t *
 
 /*
  * Multi-source: k sources (HOST array; all validated before any work),
- * processed 64 at a time by the bit-parallel kernel (bit j of a vertex word = source 64b+j
- * of the batch; one adjacency pass serves 64 BFS trees).
+ * processed DAWN_MS_BATCH (256) at a time by the bit-parallel kernel: each vertex holds four
+ * 64-bit words, bit j of the batch's word w = source DAWN_MS_BATCH*b + 64w + j, so one adjacency
+ * pass serves 256 BFS trees (a 32-byte word = one L2 sector).
  *   dist   device uint32[k][n] (source-major) or NULL.  k*n must be < 2^40 else CAPACITY.
  *   rec    device dawn_record[k] or NULL (record i belongs to sources[i]).
  * Repeated sources give identical rows and records.
@@ -161,8 +179,8 @@ dawn_status dawn_msssp(dawn_graph g, const int64_t *sources, int64_t k, uint32_t
                        dawn_record *rec, void *stream);
 
 /*
- * The host-side shard rule of dawn_apsp: the sources are cut into 64-source batches in the
- * given order; batch b belongs to rank (b mod world).  Writes the indices (into sources[])
+ * The host-side shard rule of dawn_apsp: the sources are cut into DAWN_MS_BATCH-source batches
+ * in the given order; batch b belongs to rank (b mod world).  Writes the indices (into sources[])
  * owned by `rank`, ascending, into idx (capacity cap) and their count into *count.  Pure host
  * function, no device work.
  */

@@ -18,7 +18,7 @@ import numpy as np
 import torch
 
 __all__ = ["build", "Graph", "sssp", "msssp", "apsp", "apsp_shard", "DawnError", "UNREACHED",
-           "AUTO", "PUSH", "PULL", "REC_DTYPE", "records_to_numpy", "stats_to_dict",
+           "AUTO", "PUSH", "PULL", "MS_BATCH", "REC_DTYPE", "records_to_numpy", "stats_to_dict",
            "gather_records"]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -27,6 +27,7 @@ _LIB = os.environ.get("DAWN_LIB") or os.path.join(_HERE, "libdawn.so")  # DAWN_L
 _INCLUDE = os.path.join(os.path.dirname(_HERE), "include")
 
 UNREACHED = 0xFFFFFFFF
+MS_BATCH = 256  # DAWN_MS_BATCH: sources per bit-parallel pass / APSP shard unit
 AUTO, PUSH, PULL = 0, 1, 2
 _VARIANTS = {"auto": AUTO, "push": PUSH, "pull": PULL, AUTO: AUTO, PUSH: PUSH, PULL: PULL}
 REC_DTYPE = np.dtype([("source", "<u4"), ("ecc", "<u4"), ("reached", "<u4"), ("pad", "<u4"),
@@ -92,8 +93,8 @@ def lib():
                                           ctypes.POINTER(vp)]
         L.dawn_graph_destroy.restype = st
         L.dawn_graph_destroy.argtypes = [vp]
-        L.dawn_graph_set_tuning.restype = st
-        L.dawn_graph_set_tuning.argtypes = [vp, ctypes.c_double, ctypes.c_double, ctypes.c_double]
+        L.dawn_graph_set_param.restype = st
+        L.dawn_graph_set_param.argtypes = [vp, ctypes.c_int, ctypes.c_double]
         L.dawn_sssp.restype = st
         L.dawn_sssp.argtypes = [vp, i64, u32, vp, vp, vp]
         L.dawn_msssp.restype = st
@@ -179,8 +180,13 @@ class Graph:
                                       ctypes.byref(cnt), _stream(stream)))
         return buf[: min(cnt.value, len(buf))].copy()
 
-    def set_tuning(self, alpha: float = 0, beta: float = 0, ms_alpha: float = 0):
-        _check(lib().dawn_graph_set_tuning(self._h, alpha, beta, ms_alpha))
+    _PARAMS = {"alpha": 0, "beta": 1, "ms_alpha": 2, "bitmap_push_edges": 3, "solo_edges": 4}
+
+    def set_tuning(self, **kw):
+        """dawn_graph_set_param for each keyword (alpha, beta, ms_alpha, bitmap_push_edges,
+        solo_edges).  Speed only; results never change."""
+        for k, v in kw.items():
+            _check(lib().dawn_graph_set_param(self._h, self._PARAMS[k], float(v)))
 
     def __del__(self):
         h = getattr(self, "_h", None)
@@ -226,7 +232,8 @@ def msssp(g: Graph, sources, dist: bool = True, records: bool = True, stream=Non
 
 
 def apsp_shard(k: int, rank: int, world: int) -> np.ndarray:
-    """Indices into the source list owned by `rank` (dawn_apsp_shard: 64-batches, b mod world)."""
+    """Indices into the source list owned by `rank` (dawn_apsp_shard: MS_BATCH-source batches,
+    batch b on rank b mod world)."""
     cnt = ctypes.c_int64(0)
     _check(lib().dawn_apsp_shard(k, rank, world, None, 0, ctypes.byref(cnt)))
     idx = np.empty(cnt.value, np.int64)

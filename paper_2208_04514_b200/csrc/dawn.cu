@@ -187,6 +187,7 @@ struct dawn_graph_s {
   int sssp_grid, ms_grid;
   bool trace;
   size_t small_cap;  // max dynamic smem for k_small (0 = disabled)
+  uint32_t bmpush_e = 1u << 18, solo_e = 512;
 };
 
 namespace {
@@ -214,7 +215,7 @@ dawn_status set_device(dawn_graph g) {
 extern "C" {
 
 const char *dawn_last_error(void) { return g_err.c_str(); }
-const char *dawn_version(void) { return "dawn-b200 0.1 sm_100a"; }
+const char *dawn_version(void) { return "dawn-b200 0.2 sm_100a"; }
 
 size_t dawn_workspace_bytes(int64_t n, int64_t m, uint32_t flags) {
   if (n < 1 || n >= (int64_t(1) << 31) || m < 0 || m >= (int64_t(1) << 32)) return 0;
@@ -282,6 +283,7 @@ dawn_status dawn_graph_load_csr(int64_t n, int64_t m, const int64_t *row_ptr, co
   const uint32_t nwords = (uint32_t)((n + 31) / 32);
   const int blocks = std::max(1, std::min<int>(g->nsm * 4, (int)((n + 255) / 256)));
   cudaMemsetAsync(g->ws + L.ctrl, 0, sizeof(Ctrl), st);
+  cudaMemsetAsync(g->ws + L.cand, 0, 4 * (size_t)nwords, st);  // invariant: zero between uses
   cudaMemsetAsync(g->ws + L.msctrl, 0, sizeof(MsCtrl), st);
   if (flags & DAWN_GRAPH_VALIDATE) {
     k_validate<<<blocks, 256, 0, st>>>(row_ptr, col, n, m, &at<Ctrl>(g, L.ctrl)->err);
@@ -358,11 +360,18 @@ dawn_status dawn_graph_destroy(dawn_graph g) {
   return DAWN_OK;
 }
 
-dawn_status dawn_graph_set_tuning(dawn_graph g, double alpha, double beta, double ms_alpha) {
+dawn_status dawn_graph_set_param(dawn_graph g, dawn_param key, double value) {
+  g_err.clear();
   if (!g) return fail(DAWN_ERR_INVALID_ARGUMENT, "graph is NULL");
-  if (alpha > 0) g->alpha = (float)alpha;
-  if (beta > 0) g->beta = (float)beta;
-  if (ms_alpha > 0) g->ms_alpha = (float)ms_alpha;
+  if (!(value >= 0)) return fail(DAWN_ERR_INVALID_ARGUMENT, "value must be >= 0");
+  switch (key) {
+    case DAWN_PARAM_ALPHA: g->alpha = (float)value; break;
+    case DAWN_PARAM_BETA: g->beta = (float)value; break;
+    case DAWN_PARAM_MS_ALPHA: g->ms_alpha = (float)value; break;
+    case DAWN_PARAM_BITMAP_PUSH_EDGES: g->bmpush_e = (uint32_t)std::min(value, 4294967295.0); break;
+    case DAWN_PARAM_SOLO_EDGES: g->solo_e = (uint32_t)std::min(value, 4294967295.0); break;
+    default: return fail(DAWN_ERR_INVALID_ARGUMENT, "unknown parameter");
+  }
   return DAWN_OK;
 }
 
@@ -402,6 +411,7 @@ dawn_status dawn_sssp(dawn_graph g, int64_t source, uint32_t variant, uint32_t *
   p.hin_e = at<uint32_t>(g, L.hin.e);
   p.hin_bits = at<uint32_t>(g, L.hin.bits);
   p.vis = at<uint32_t>(g, L.vis);
+  p.cand = at<uint32_t>(g, L.cand);
   for (int i = 0; i < 3; ++i) p.fb[i] = at<uint32_t>(g, L.fb[i]);
   p.trace = g->trace ? at<TraceRec>(g, L.trace) : nullptr;
   for (int i = 0; i < 2; ++i) {
@@ -418,6 +428,8 @@ dawn_status dawn_sssp(dawn_graph g, int64_t source, uint32_t variant, uint32_t *
   p.sym = (g->flags & DAWN_GRAPH_SYMMETRIC) ? 1u : 0u;
   p.alpha = g->alpha;
   p.beta = g->beta;
+  p.bmpush_e = g->bmpush_e;
+  p.solo_e = g->solo_e;
   int grid = g->sssp_grid;
   const int small_m = env_int("DAWN_SMALL_M", 1 << 15);
   if (g->m + g->n <= small_m) grid = 1;  // tiny graphs: one CTA, barriers are __syncthreads
@@ -431,8 +443,9 @@ dawn_status dawn_sssp(dawn_graph g, int64_t source, uint32_t variant, uint32_t *
 static dawn_status launch_ms(dawn_graph g, const std::vector<uint32_t> &src, uint32_t *dist,
                              dawn_record *rec, cudaStream_t st) {
   const Layout &L = g->L;
-  for (size_t off = 0; off < src.size(); off += (L.srccap / 64) * 64) {
-    const size_t cnt = std::min(src.size() - off, (size_t)((L.srccap / 64) * 64));
+  const size_t chunk = (L.srccap / kMsBatch) * kMsBatch;
+  for (size_t off = 0; off < src.size(); off += chunk) {
+    const size_t cnt = std::min(src.size() - off, chunk);
     cudaError_t e = cudaMemcpyAsync(g->ws + L.srcbuf, src.data() + off, 4 * cnt,
                                     cudaMemcpyHostToDevice, st);
     if (e != cudaSuccess) return cuda_fail(e, "source upload");
@@ -521,10 +534,11 @@ dawn_status dawn_apsp_shard(int64_t k, int32_t rank, int32_t world, int64_t *idx
   if (k < 0 || world < 1 || rank < 0 || rank >= world || !count)
     return fail(DAWN_ERR_INVALID_ARGUMENT, "need k >= 0, 0 <= rank < world");
   int64_t c = 0;
-  const int64_t nb = (k + 63) / 64;
+  const int64_t B = kMsBatch;
+  const int64_t nb = (k + B - 1) / B;
   for (int64_t b = rank; b < nb; b += world) {
-    const int64_t e = std::min(k, (b + 1) * 64);
-    for (int64_t i = b * 64; i < e; ++i) {
+    const int64_t e = std::min(k, (b + 1) * B);
+    for (int64_t i = b * B; i < e; ++i) {
       if (idx && c < cap) idx[c] = i;
       ++c;
     }
@@ -545,9 +559,10 @@ dawn_status dawn_apsp(dawn_graph g, const int64_t *sources, int64_t k, int32_t r
     if (sources[i] < 0 || sources[i] >= g->n)
       return fail(DAWN_ERR_BOUNDS, "sources[" + std::to_string(i) + "] not in [0, n)");
   std::vector<uint32_t> mine;
-  const int64_t nb = (k + 63) / 64;
+  const int64_t B = kMsBatch;
+  const int64_t nb = (k + B - 1) / B;
   for (int64_t b = rank; b < nb; b += world)
-    for (int64_t i = b * 64; i < std::min(k, (b + 1) * 64); ++i) mine.push_back((uint32_t)sources[i]);
+    for (int64_t i = b * B; i < std::min(k, (b + 1) * B); ++i) mine.push_back((uint32_t)sources[i]);
   *n_written = (int64_t)mine.size();
   if ((int64_t)mine.size() > cap) return fail(DAWN_ERR_CAPACITY, "rec capacity too small");
   if (mine.empty()) return DAWN_OK;

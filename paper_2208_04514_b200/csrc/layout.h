@@ -16,9 +16,10 @@ namespace dawn {
 // scale 20) therefore spread over many warps with no separate heavy path.
 constexpr uint32_t kChunk = 32;   // Cf granularity = one warp round
 constexpr uint32_t kIlp = 4;      // chunks per warp item when the frontier is wide
-// Solo levels: a push level whose frontier has <= kSoloE edges runs on CTA 0 alone with
+// Solo levels (DAWN_PARAM_SOLO_EDGES): a narrow push level runs on CTA 0 alone with
 // __syncthreads instead of the grid barrier (the other CTAs wait for the stretch to end).
-constexpr uint32_t kSoloE = 512;
+// Bitmap push (DAWN_PARAM_BITMAP_PUSH_EDGES): a wide push level marks candidates with
+// fire-and-forget red.or into a bitmap and settles them in a word-owner filter pass.
 // Static heavy rows (built once at load): rows with degree > kHeavy are scanned in kHPiece-edge
 // pieces by whole warps in the pull step and in the 64-source kernel; lighter rows are scanned
 // by one lane each (early exit, 4 probes per round trip).
@@ -28,6 +29,10 @@ constexpr uint32_t kHeavyProbe = 16;  // in-edges a heavy row probes lane-parall
 constexpr uint32_t kScanBlock = 2048;  // elements per CTA in the load-time piece scan
 constexpr uint32_t kMaxBlocks = 2048;  // cap on persistent grid size (partials buffer)
 constexpr uint32_t kTraceCap = 1 << 16;
+// Multi-source kernel: kMsW 64-bit words per vertex = kMsBatch sources per adjacency pass.
+constexpr int kMsW = 4;
+constexpr uint32_t kMsBatch = 64 * kMsW;
+static_assert(kMsBatch == DAWN_MS_BATCH, "dawn.h DAWN_MS_BATCH must match kMsW");
 
 #ifndef DAWN_PULL_J
 #define DAWN_PULL_J 2  // vis words per warp iteration of the pull sweep (independent scans)
@@ -79,7 +84,7 @@ struct HeavyList {  // static pieces of rows with degree > kHeavy
 };
 
 struct Layout {
-  size_t rp, irp, noin, vis, fb[3], Lv[2], Lsd[2], Cf[2], ctrl, trace;
+  size_t rp, irp, noin, vis, cand, fb[3], Lv[2], Lsd[2], Cf[2], ctrl, trace;
   HeavyList hout, hin;
   size_t scan_tmp, piece_tmp;
   size_t seen, F0, F1, nxt, msctrl, part, srcbuf, total;
@@ -105,6 +110,7 @@ inline Layout make_layout(int64_t n, int64_t m, uint32_t flags) {
   L.irp = L.own_irp ? take(4 * (size_t)(n + 1)) : L.rp;
   L.noin = take(4 * W);
   L.vis = take(4 * W);
+  L.cand = take(4 * W);
   for (int i = 0; i < 3; ++i) L.fb[i] = take(4 * W);
   for (int i = 0; i < 2; ++i) {
     L.Lv[i] = take(4 * (size_t)n);
@@ -123,12 +129,12 @@ inline Layout make_layout(int64_t n, int64_t m, uint32_t flags) {
   if (L.own_irp) heavy(L.hin); else L.hin = L.hout;
   L.scan_tmp = take(4 * ((size_t)n / kScanBlock + 2));
   L.piece_tmp = take(4 * (3 * ((size_t)m / kHPiece + 3) + 1));
-  L.seen = take(8 * (size_t)n);
-  L.F0 = take(8 * (size_t)n);
-  L.F1 = take(8 * (size_t)n);
-  L.nxt = take(8 * (size_t)n);
+  L.seen = take(8 * kMsW * (size_t)n);
+  L.F0 = take(8 * kMsW * (size_t)n);
+  L.F1 = take(8 * kMsW * (size_t)n);
+  L.nxt = take(8 * kMsW * (size_t)n);
   L.msctrl = take(sizeof(MsCtrl));
-  L.part = take(sizeof(uint32_t) * 4 * 64 * 2 * kMaxBlocks);
+  L.part = take(sizeof(uint32_t) * 4 * kMsBatch * 2 * kMaxBlocks);
   L.srccap = (uint64_t)(n > 65536 ? n : 65536);
   L.srcbuf = take(4 * L.srccap);
   L.total = o;

@@ -28,7 +28,7 @@ struct SsspParams {
   const int32_t *col, *icol;
   const uint32_t *noin;
   const uint32_t *hin_v, *hin_s, *hin_e, *hin_bits;  // static heavy in-row pieces
-  uint32_t *vis, *fb[3];
+  uint32_t *vis, *cand, *fb[3];  // cand: candidate bitmap of bitmap-push levels (zero between uses)
   uint32_t *Lv[2];   // frontier queue: vertex
   uint2 *Lsd[2];     //                 (row start, edge offset within the frontier)
   uint32_t *Cf[2];   //                 chunk c -> entry holding edge c*kChunk
@@ -38,10 +38,11 @@ struct SsspParams {
   dawn_sssp_stats *stats;
   uint32_t source, variant, can_pull, sym;
   float alpha, beta;
+  uint32_t bmpush_e, solo_e;  // DAWN_PARAM_BITMAP_PUSH_EDGES / DAWN_PARAM_SOLO_EDGES
 };
 
 struct __align__(16) LevelState {
-  uint32_t L, nf, prev_nf, dir, rep, q, b, stop, ecc, solo;
+  uint32_t L, nf, prev_nf, dir, rep, q, b, stop, ecc, solo, bm;
   uint32_t push_levels, pull_levels, reached;
   uint32_t qn, n_hp;            // queue entries of frontier L; static heavy pieces
   uint32_t qe;                  // queue edges of frontier L
@@ -59,13 +60,17 @@ __device__ __forceinline__ unsigned long long globaltimer() {
   return t;
 }
 
-// Per-warp phase cycle accounting (trace builds only): lane 0 adds its warp's cycles.
+// Per-warp phase cycle accounting (trace builds only): lane 0 adds its warp's cycles to a
+// per-CTA shared accumulator; trace_done folds it into the level's record (4 atomics per CTA).
+__device__ unsigned long long *phase_smem() {
+  __shared__ unsigned long long acc[4];
+  return acc;
+}
 __device__ __forceinline__ void phase_add(const SsspParams &p, uint32_t L, int ph,
                                           long long &t0) {
   if (p.trace) {
     const long long t = clock64();
-    if (lane_id() == 0 && L < kTraceCap)
-      atomicAdd(&p.trace[L].cyc[ph], (unsigned long long)(t - t0));
+    if (lane_id() == 0 && L < kTraceCap) atomicAdd(phase_smem() + ph, (unsigned long long)(t - t0));
     t0 = t;
   }
 }
@@ -198,7 +203,7 @@ __device__ __forceinline__ void push_visit(const SsspParams &p, Slot *ns, int qn
 // else 1), processed with all J chains' loads in flight together (memory-level parallelism):
 // Cf[c] -> 32-entry window of (row start, edge offset) -> owner by 5-step shfl search -> col ->
 // vis test-and-set -> rp of the discovered vertex.
-template <int J>
+template <int J, bool CAND>
 __device__ __forceinline__ void push_item(const SsspParams &p, const LevelState &st, Slot *ns,
                                           uint32_t item, uint32_t &n_new,
                                           unsigned long long &m_new, WarpStage &stg,
@@ -237,6 +242,15 @@ __device__ __forceinline__ void push_item(const SsspParams &p, const LevelState 
   uint32_t cur[J];
 #pragma unroll
   for (int j = 0; j < J; ++j) cur[j] = act[j] ? p.vis[u[j] >> 5] : ~0u;  // weak: stale 0 = atomic
+  if (CAND) {
+    // bitmap push: mark the candidate, settle later in cand_filter (no returning atomic)
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+      const uint32_t bit = 1u << (u[j] & 31);
+      if (!(cur[j] & bit)) red_or(p.cand + (u[j] >> 5), bit);
+    }
+    return;
+  }
 #pragma unroll
   for (int j = 0; j < J; ++j) {
     const uint32_t bit = 1u << (u[j] & 31);
@@ -270,13 +284,21 @@ __device__ void push_level(const SsspParams &p, const LevelState &st, Slot *ns, 
   const uint32_t E = st.qe;
   const uint32_t nchunks = (E + kChunk - 1) / kChunk;
   uint32_t cnt = 0;
+  if (st.bm) {
+    constexpr int JB = 2 * kIlp;  // candidate mode keeps less state per chain: deeper ILP
+    const uint32_t items = (nchunks + JB - 1) / JB;
+    for (uint32_t it = gwarp; it < items; it += nwarps)
+      push_item<JB, true>(p, st, ns, it, n_new, m_new, stg, cnt);
+    phase_add(p, st.L, 0, t0);
+    return;
+  }
   if (nchunks >= nwarps * kIlp) {
     const uint32_t items = (nchunks + kIlp - 1) / kIlp;
     for (uint32_t it = gwarp; it < items; it += nwarps)
-      push_item<kIlp>(p, st, ns, it, n_new, m_new, stg, cnt);
+      push_item<kIlp, false>(p, st, ns, it, n_new, m_new, stg, cnt);
   } else {
     for (uint32_t it = gwarp; it < nchunks; it += nwarps)
-      push_item<1>(p, st, ns, it, n_new, m_new, stg, cnt);
+      push_item<1, false>(p, st, ns, it, n_new, m_new, stg, cnt);
   }
   phase_add(p, st.L, 0, t0);
   cta_flush(p, ns, st.q ^ 1, stg, cnt, fsm);
@@ -315,17 +337,21 @@ __device__ void pull_level(const SsspParams &p, const LevelState &st, uint32_t g
         if (w[j] == p.nwords - 1 && tail_bits) todo[j] &= (1u << tail_bits) - 1;
         if (lane == 0) fclr[w[j]] = 0;
       }
-      need[j] = (todo[j] >> lane) & 1u;
       found[j] = false;
       s[j] = e[j] = 0;
+      // row bounds loaded speculatively with the vis word (coalesced; saves a round trip)
+      if (w[j] < p.nwords) {
+        const uint32_t u = w[j] * 32 + lane;
+        if (u < p.n) {
+          s[j] = ld_nc(p.irp + u);
+          e[j] = ld_nc(p.irp + u + 1);
+        }
+      }
     }
 #pragma unroll
     for (int j = 0; j < J; ++j) {
-      if (need[j]) {
-        const uint32_t u = w[j] * 32 + lane;
-        s[j] = ld_nc(p.irp + u);
-        e[j] = ld_nc(p.irp + u + 1);
-      }
+      need[j] = (todo[j] >> lane) & 1u;
+      if (!need[j]) e[j] = s[j];
       j0[j] = s[j];
       // heavy rows (in-degree > kHeavy): only the first kHeavyProbe in-edges here, lane-parallel
       // with everything else; the static pieces finish the rows still unsettled
@@ -362,7 +388,15 @@ __device__ void pull_level(const SsspParams &p, const LevelState &st, uint32_t g
     for (int j = 0; j < J; ++j) {
       if (need[j]) examined += min(j0[j], ef[j]) - s[j];
       const uint32_t nb = __ballot_sync(DAWN_FULL, found[j]);
-      if (lane == 0 && nb) {
+      if (nb & hv[j]) {
+        // a heavy row may be settled concurrently by one of its static pieces: claim with a
+        // returning atomic so each vertex is counted (and enqueued) exactly once
+        uint32_t old = 0;
+        if (lane == 0) old = atomicOr(p.vis + w[j], nb);
+        old = __shfl_sync(DAWN_FULL, old, 0);
+        if ((old >> lane) & 1u) found[j] = false;
+        if (lane == 0 && (nb & ~old)) red_or(fnext + w[j], nb & ~old);
+      } else if (lane == 0 && nb) {
         red_or(fnext + w[j], nb);
         red_or(p.vis + w[j], nb);
       }
@@ -419,6 +453,44 @@ __device__ void pull_level(const SsspParams &p, const LevelState &st, uint32_t g
     }
   }
   phase_add(p, st.L, 1, t0);
+}
+
+// Second half of a bitmap-push level: word owners settle the candidates (new = cand & ~vis),
+// write the frontier bitmap fb[b+1] (every word), clear fb[b+2] and cand, set dist = L+1.
+// 32 words per warp iteration (one lane each), then lane-per-vertex for words with news.
+__device__ void cand_filter(const SsspParams &p, const LevelState &st, uint32_t gwarp,
+                            uint32_t nwarps, uint32_t &n_new, unsigned long long &m_new) {
+  const uint32_t lane = lane_id();
+  const uint32_t L1 = st.L + 1;
+  uint32_t *fnext = p.fb[(st.b + 1) % 3];
+  uint32_t *fclr = p.fb[(st.b + 2) % 3];
+  for (uint32_t base = gwarp * 32; base < p.nwords; base += nwarps * 32) {
+    const uint32_t w = base + lane;
+    uint32_t nw = 0;
+    if (w < p.nwords) {
+      const uint32_t c = ld_cg(p.cand + w);
+      if (c) {
+        const uint32_t vw = ld_cg(p.vis + w);
+        nw = c & ~vw;
+        p.cand[w] = 0;
+        if (nw) p.vis[w] = vw | nw;
+      }
+      fnext[w] = nw;
+      fclr[w] = 0;
+    }
+    uint32_t mk = __ballot_sync(DAWN_FULL, nw != 0);
+    while (mk) {
+      const uint32_t k = __ffs(mk) - 1;
+      mk &= mk - 1;
+      const uint32_t wk = __shfl_sync(DAWN_FULL, w, k), bits = __shfl_sync(DAWN_FULL, nw, k);
+      if ((bits >> lane) & 1u) {
+        const uint32_t u = wk * 32 + lane;
+        p.dist[u] = L1;
+        n_new += 1;
+        m_new += ld_nc(p.rp + u + 1) - ld_nc(p.rp + u);
+      }
+    }
+  }
 }
 
 // Block-wide sum of two counters, then one global atomic per CTA.
@@ -479,7 +551,8 @@ __device__ __forceinline__ void level_header(const SsspParams &p, Ctrl *C, Level
       }
     }
     st.prev_nf = st.nf;
-    st.solo = (nblocks > 1 && st.dir == kPush && st.rep == kRepQueue && st.qe <= kSoloE) ? 1u : 0u;
+    st.solo = (nblocks > 1 && st.dir == kPush && st.rep == kRepQueue && st.qe <= p.solo_e) ? 1u : 0u;
+    st.bm = (st.dir == kPush && !st.solo && st.mf >= p.bmpush_e) ? 1u : 0u;
   }
   if (p.trace && blockIdx.x == 0 && st.L < kTraceCap) {
     TraceRec r;
@@ -487,7 +560,7 @@ __device__ __forceinline__ void level_header(const SsspParams &p, Ctrl *C, Level
     r.level = st.L;
     r.dir = st.stop ? 2u : st.dir;
     r.nf = st.nf;
-    r.pad = st.rep | (st.solo << 1);
+    r.pad = st.rep | (st.solo << 1) | (st.bm << 2);
     r.mf = st.mf;
     r.t_first = p.trace[st.L].t_first;
     r.t_last = p.trace[st.L].t_last;
@@ -497,16 +570,29 @@ __device__ __forceinline__ void level_header(const SsspParams &p, Ctrl *C, Level
   }
 }
 
+// CTA-collective (every thread calls it after the level's work)
 __device__ __forceinline__ void trace_done(const SsspParams &p, uint32_t L) {
-  if (p.trace && threadIdx.x == 0 && L < kTraceCap) {
+  if (!p.trace) return;
+  __syncthreads();
+  if (threadIdx.x == 0 && L < kTraceCap) {
     const unsigned long long t = globaltimer();
     atomicMin(&p.trace[L].t_first, t);
     atomicMax(&p.trace[L].t_last, t);
+    unsigned long long *a = phase_smem();
+    for (int k = 0; k < 4; ++k) {
+      if (a[k]) atomicAdd(&p.trace[L].cyc[k], a[k]);
+      a[k] = 0;
+    }
   }
 }
 
 __device__ __forceinline__ void level_advance(LevelState &st) {
-  if (st.dir == kPush) {
+  if (st.dir == kPush && st.bm) {  // bitmap push: the next frontier is fb[b+1]
+    st.push_levels++;
+    st.push_edges += st.mf;
+    st.b = (st.b + 1) % 3;
+    st.rep = kRepBitmap;
+  } else if (st.dir == kPush) {
     st.push_levels++;
     st.push_edges += st.mf;
     st.q ^= 1;
@@ -566,6 +652,7 @@ __global__ void __launch_bounds__(NT) k_sssp(SsspParams p) {
       for (int k = 0; k < 4; ++k) p.trace[i].cyc[k] = 0;
     }
   }
+  if (threadIdx.x < 4) phase_smem()[threadIdx.x] = 0;
   if (threadIdx.x == 0) {
     st = LevelState{};
     st.dir = (p.variant == DAWN_PULL) ? kPull : kPush;
@@ -680,6 +767,11 @@ __global__ void __launch_bounds__(NT) k_sssp(SsspParams p) {
     phase_add(p, st.L, 3, tconv);
     if (st.dir == kPush) {
       push_level(p, st, ns, gwarp, nwarps, n_new, m_new, stg, tconv, fsm);
+      if (st.bm) {
+        grid_sync(&C->bar, nblocks, bar_target);
+        cand_filter(p, st, gwarp, nwarps, n_new, m_new);
+        phase_add(p, st.L, 1, tconv);
+      }
     } else {
       pull_level(p, st, gwarp, nwarps, n_new, m_new, examined, tconv);
     }

@@ -26,6 +26,8 @@ def test_builds_and_exports_every_declared_symbol():
     for n in names:
         assert hasattr(L, n), n
     assert dawn.version().endswith("sm_100a")
+    hdr = open(os.path.join(ROOT, "include", "dawn.h")).read()
+    assert f"#define DAWN_MS_BATCH {dawn.MS_BATCH}" in hdr
 
 
 def test_sass_is_sm100a():
@@ -68,9 +70,9 @@ def test_apsp_shard_rule_partitions(k, world):
     assert np.array_equal(allidx, np.arange(k))
     for r, p in enumerate(parts):
         assert np.all(np.diff(p) > 0)
-        assert np.all((p // 64) % world == r)
+        assert np.all((p // dawn.MS_BATCH) % world == r)
     sizes = [len(p) for p in parts]
     assert sizes[0] == max(sizes)
-    assert max(sizes) - min(sizes) <= 64
+    assert max(sizes) - min(sizes) <= dawn.MS_BATCH
     with pytest.raises(dawn.DawnError):
         dawn.apsp_shard(k, world, world)

@@ -242,3 +242,15 @@ def test_trace_levels_consistent():
         counts = np.bincount(d[fin], minlength=len(tr))
         assert np.array_equal(tr["nf"][: st["levels"] + 1], counts[: st["levels"] + 1])
         assert tr["dir"][-1] == 2
+
+
+@pytest.mark.parametrize("knobs", [dict(bitmap_push_edges=64), dict(bitmap_push_edges=0, solo_edges=0),
+                                   dict(solo_edges=100000, alpha=1000), dict(alpha=0, beta=1e9)])
+def test_tunables_never_change_results(knobs):
+    # every schedule knob (bitmap push on every level, no solo levels, long solo stretches,
+    # never/always pull) must give the oracle's distances (tolerance 0)
+    for g in (graphgen.kron(13, 16), graphgen.er_prob(3000, 0.002, 4), graphgen.grid(200, 150)):
+        G = dev_graph(g)
+        G.set_tuning(**knobs)
+        srcs = [0, g.n - 1] + list(g.sample_sources(3, seed=2))
+        check_sssp(g, G, srcs, variants=("auto", "push"))
