@@ -151,22 +151,29 @@ def cpu_oracle_apsp(g, verts, budget_s: float):
 
 
 # ------------------------------------------------------------------------------- GPU arms
-def run_sssp(args, rank, world, dev):
+def run_sssp(args, rank, world, dev, cfg=None, steps=None, warmup=None, e2e=True, reps=1):
+    """One SSSP config.  A step = every bench source once (64 for C2/C4; the single source
+    repeated `reps` times for C1/C3)."""
     import torch
     import torch.distributed as tdist
     import paper_2208_04514_b200 as dawn
 
-    cfg = args.config
+    cfg = cfg or args.config
+    steps = args.steps if steps is None else steps
+    warmup = args.warmup if warmup is None else warmup
     g = build_graph(cfg)
     G = dawn.Graph(g.row_ptr, g.col, g.symmetric,
                    *(g.transpose() if not g.symmetric else (None, None)))
     srcs = sources_for(g, cfg, rank)
+    if reps > 1:
+        srcs = np.repeat(srcs, reps)
     k = len(srcs)
-    out = torch.empty((k, g.n), dtype=torch.int32, device=dev)
+    out = torch.empty((min(k, 64), g.n), dtype=torch.int32, device=dev)
+    orow = lambda i: out[i % out.shape[0]]
     # E_reach per source (the E10 numerator) from the kernel's own statistics, untimed
     er, reached, examined, pushl, pulll = [], [], [], [], []
     for i, s in enumerate(srcs):
-        _, st = dawn.sssp(G, int(s), args.variant, stats=True, out=out[i])
+        _, st = dawn.sssp(G, int(s), args.variant, stats=True, out=orow(i))
         d = dawn.stats_to_dict(st)
         er.append(d["edges_reach"]); reached.append(d["reached"]); examined.append(d["edges_examined"])
         pushl.append(d["push_levels"]); pulll.append(d["pull_levels"])
@@ -178,13 +185,13 @@ def run_sssp(args, rank, world, dev):
             if times is not None:
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record(stream)
-                dawn.sssp(G, int(s), args.variant, out=out[i])
+                dawn.sssp(G, int(s), args.variant, out=orow(i))
                 e1.record(stream)
                 times.append((e0, e1))
             else:
-                dawn.sssp(G, int(s), args.variant, out=out[i])
+                dawn.sssp(G, int(s), args.variant, out=orow(i))
 
-    for _ in range(args.warmup):
+    for _ in range(warmup):
         step()
         flush.zero_()
     torch.cuda.synchronize()
@@ -193,7 +200,7 @@ def run_sssp(args, rank, world, dev):
     torch.cuda.synchronize()
     step_ms, launch_pairs = [], []
     with ClockSampler(dev.index if dev.index is not None else 0) as clk:
-        for _ in range(args.steps):
+        for _ in range(steps):
             flush.zero_()  # L2 flush between timed steps (write 2.2x L2)
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(stream)
@@ -211,7 +218,7 @@ def run_sssp(args, rank, world, dev):
         tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
         tot_ms = float(t.item())
     edges_step = float(sum(er))
-    value = edges_step * args.steps * world / (tot_ms * 1e-3) / 1e9
+    value = edges_step * steps * world / (tot_ms * 1e-3) / 1e9
 
     # roofline: dominant (only) kernel k_sssp; algorithmic bytes B_SOVM(s) = 4E + 8S + 4n
     peak, peak_kind = peaks()
@@ -226,12 +233,23 @@ def run_sssp(args, rank, world, dev):
     if os.path.exists(tp):
         traffic = json.load(open(tp)).get(f"sssp-{cfg}-{args.variant}")
 
+    if not e2e:
+        peak, _ = peaks()
+        return {"value": value, "unit": "GTEPS", "ms_per_step": tot_ms / steps, "steps": steps,
+                "sources_per_step": k, "n": g.n, "m": g.m, "workload": f"{cfg}: {CONFIG_TEXT[cfg]}",
+                "avg_launch_us": avg_launch_ms * 1e3, "edges_reach_mean": float(np.mean(er)),
+                "levels": {"push_mean": float(np.mean(pushl)), "pull_mean": float(np.mean(pulll))},
+                "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                             "frac": achieved / peak, "achieved_exec": achieved_exec,
+                             "frac_exec": achieved_exec / peak,
+                             "bytes_model": "B_SOVM = 4*E_reach + 8*S_reach + 4*n"},
+                "clocks": clk.summary()}, g, srcs, er
     # e2e through the public API with HOST buffers: sources H2D (pinned) + 64 dist rows D2H
     host_src = torch.from_numpy(srcs.copy()).pin_memory()
     dev_src = torch.empty_like(host_src, device=dev)
     host_out = torch.empty((k, g.n), dtype=torch.int32).pin_memory()
     e2e_ms = []
-    for it in range(max(1, args.steps)):
+    for it in range(max(1, steps)):
         flush.zero_()
         torch.cuda.synchronize()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -251,8 +269,8 @@ def run_sssp(args, rank, world, dev):
 
     res = {
         "metric": "SSSP GTEPS (1 B200) and APSP sources/sec at 1/2/4/8 B200 vs HBM roofline",
-        "value": value, "unit": "GTEPS", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": tot_ms / args.steps, "higher_is_better": True,
+        "value": value, "unit": "GTEPS", "n_gpus": world, "steps": steps,
+        "warmup": warmup, "ms_per_step": tot_ms / steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
         "config": {"workload": f"{cfg}: {CONFIG_TEXT[cfg]}", "n": g.n, "m": g.m,
                    "sources_per_rank": k, "variant": args.variant,
@@ -260,7 +278,7 @@ def run_sssp(args, rank, world, dev):
                    "teps_numerator": "E_reach = sum of out-degrees of reached vertices incl. s "
                                      "(directed arcs, PAPER E10)",
                    "parallelism": f"dp{world} (independent sources per rank)"},
-        "gpu_launches": k * args.steps,
+        "gpu_launches": k * steps,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
                      "kernel": "k_sssp (one persistent launch per SSSP)",
@@ -362,6 +380,15 @@ def run_dawn(args):
                                              f"over the first {cnt} largest-WCC sources, {dt:.1f} s"}
     else:
         res, g, srcs, er = run_sssp(args, rank, world, dev)
+        if args.extra and world == 1:
+            ex = {}
+            for cfg, reps, st in (("C1", 64, max(3, args.steps)), ("C3", 1, 2), ("C4", 1, 2)):
+                if cfg == args.config:
+                    continue
+                r, _, _, _ = run_sssp(args, rank, world, dev, cfg=cfg, steps=st, warmup=3,
+                                      e2e=False, reps=reps)
+                ex[cfg] = r
+            res["extra_configs"] = ex
         if args.secondary:
             sec, _, _ = run_apsp(args, rank, world, dev, steps=max(1, min(args.steps, 3)),
                                  warmup=1)
@@ -441,6 +468,8 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=15.0, help="seconds of oracle CPU work")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-secondary", dest="secondary", action="store_false")
+    ap.add_argument("--no-extra", dest="extra", action="store_false",
+                    help="skip the C1/C3/C4 lines (reported under extra_configs)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "dawn":
         print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)

@@ -34,6 +34,12 @@ constexpr int kMsW = 4;
 constexpr uint32_t kMsBatch = 64 * kMsW;
 static_assert(kMsBatch == DAWN_MS_BATCH, "dawn.h DAWN_MS_BATCH must match kMsW");
 
+#ifndef DAWN_PULL_DEEP
+#define DAWN_PULL_DEEP 1  // 8-probe pull rounds on sparse frontiers
+#endif
+#ifndef DAWN_SSSP_MINB
+#define DAWN_SSSP_MINB 2  // __launch_bounds__ min blocks of k_sssp: 2 x 16 warps per SM (64 regs)
+#endif
 #ifndef DAWN_PULL_J
 #define DAWN_PULL_J 2  // vis words per warp iteration of the pull sweep (independent scans)
 #endif

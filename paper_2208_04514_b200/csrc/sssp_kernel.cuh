@@ -42,7 +42,7 @@ struct SsspParams {
 };
 
 struct __align__(16) LevelState {
-  uint32_t L, nf, prev_nf, dir, rep, q, b, stop, ecc, solo, bm;
+  uint32_t L, nf, prev_nf, dir, rep, q, b, stop, ecc, solo, bm, deep;
   uint32_t push_levels, pull_levels, reached;
   uint32_t qn, n_hp;            // queue entries of frontier L; static heavy pieces
   uint32_t qe;                  // queue edges of frontier L
@@ -309,6 +309,7 @@ __device__ __forceinline__ bool fb_test(const uint32_t *fb, uint32_t v) {
   return (fb[v >> 5] >> (v & 31)) & 1u;
 }
 
+template <int PR>  // in-edges probed per lane per round trip (8 when the frontier is sparse)
 __device__ void pull_level(const SsspParams &p, const LevelState &st, uint32_t gwarp,
                            uint32_t nwarps, uint32_t &n_new, unsigned long long &m_new,
                            unsigned long long &examined, long long &t0) {
@@ -359,28 +360,28 @@ __device__ void pull_level(const SsspParams &p, const LevelState &st, uint32_t g
     }
     for (;;) {
       bool any = false;
-      uint32_t v[J][4];
+      uint32_t v[J][PR];
 #pragma unroll
       for (int j = 0; j < J; ++j) {
         const bool go = need[j] && !found[j] && j0[j] < ef[j];
         any |= go;
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
+        for (int i = 0; i < PR; ++i)
           v[j][i] = (go && j0[j] + i < ef[j]) ? (uint32_t)ld_nc(p.icol + j0[j] + i) : 0xffffffffu;
       }
       if (!any) break;
 #pragma unroll
       for (int j = 0; j < J; ++j) {
         if (v[j][0] == 0xffffffffu) continue;
-        uint32_t hit = 4;
+        uint32_t hit = PR;
 #pragma unroll
-        for (int i = 3; i >= 0; --i)
+        for (int i = PR - 1; i >= 0; --i)
           if (v[j][i] != 0xffffffffu && fb_test(fcur, v[j][i])) hit = i;
-        if (hit < 4) {
+        if (hit < PR) {
           found[j] = true;
           j0[j] += hit + 1;
         } else {
-          j0[j] += 4;
+          j0[j] += PR;
         }
       }
     }
@@ -478,17 +479,31 @@ __device__ void cand_filter(const SsspParams &p, const LevelState &st, uint32_t 
       fnext[w] = nw;
       fclr[w] = 0;
     }
-    uint32_t mk = __ballot_sync(DAWN_FULL, nw != 0);
-    while (mk) {
-      const uint32_t k = __ffs(mk) - 1;
-      mk &= mk - 1;
-      const uint32_t wk = __shfl_sync(DAWN_FULL, w, k), bits = __shfl_sync(DAWN_FULL, nw, k);
-      if ((bits >> lane) & 1u) {
-        const uint32_t u = wk * 32 + lane;
-        p.dist[u] = L1;
-        n_new += 1;
-        m_new += ld_nc(p.rp + u + 1) - ld_nc(p.rp + u);
+    // lane-parallel over this lane's word: up to 4 new vertices per round trip
+    uint32_t bits = nw;
+    while (bits) {
+      uint32_t u[4], a[4], b[4];
+      int k = 0;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        u[i] = 0xffffffffu;
+        if (bits) {
+          u[i] = w * 32 + (__ffs(bits) - 1);
+          bits &= bits - 1;
+          k = i + 1;
+        }
       }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if (i < k) {
+          a[i] = ld_nc(p.rp + u[i]);
+          b[i] = ld_nc(p.rp + u[i] + 1);
+          p.dist[u[i]] = L1;
+        }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if (i < k) m_new += b[i] - a[i];
+      n_new += k;
     }
   }
 }
@@ -553,6 +568,10 @@ __device__ __forceinline__ void level_header(const SsspParams &p, Ctrl *C, Level
     st.prev_nf = st.nf;
     st.solo = (nblocks > 1 && st.dir == kPush && st.rep == kRepQueue && st.qe <= p.solo_e) ? 1u : 0u;
     st.bm = (st.dir == kPush && !st.solo && st.mf >= p.bmpush_e) ? 1u : 0u;
+    // sparse frontier (a probe hits with probability ~ m_f / (m_f + m_u) < 1/6): probe 8
+    // in-edges per round trip instead of 4
+    st.deep = (st.dir == kPull && 6.0 * (double)st.mf < (double)(p.m - st.explored) + (double)st.mf)
+                  ? 1u : 0u;
   }
   if (p.trace && blockIdx.x == 0 && st.L < kTraceCap) {
     TraceRec r;
@@ -606,7 +625,7 @@ __device__ __forceinline__ void level_advance(LevelState &st) {
 }
 
 template <int NT>
-__global__ void __launch_bounds__(NT) k_sssp(SsspParams p) {
+__global__ void __launch_bounds__(NT, DAWN_SSSP_MINB) k_sssp(SsspParams p) {
   __shared__ LevelState st;
   __shared__ unsigned long long red[2];
   __shared__ WarpStage stage[NT / 32];
@@ -773,7 +792,12 @@ __global__ void __launch_bounds__(NT) k_sssp(SsspParams p) {
         phase_add(p, st.L, 1, tconv);
       }
     } else {
-      pull_level(p, st, gwarp, nwarps, n_new, m_new, examined, tconv);
+#if DAWN_PULL_DEEP
+      if (st.deep)
+        pull_level<8>(p, st, gwarp, nwarps, n_new, m_new, examined, tconv);
+      else
+#endif
+        pull_level<4>(p, st, gwarp, nwarps, n_new, m_new, examined, tconv);
     }
     block_flush(n_new, m_new, &ns->n_new, &ns->m_new, red);
     phase_add(p, st.L, 2, tconv);
