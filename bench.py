@@ -344,7 +344,7 @@ def run_apsp(args, rank, world, dev, steps=None, warmup=None):
     return {"value": value, "unit": "sources/s", "n_gpus": world, "steps": steps,
             "ms_per_step": t / steps, "scaling": "strong",
             "config": {"workload": f"C5: {CONFIG_TEXT['C5']}", "n": g.n, "m": g.m,
-                       "S_wcc": k, "E_wcc": e_wcc, "batch": 64,
+                       "S_wcc": k, "E_wcc": e_wcc, "batch": dawn.MS_BATCH,
                        "l2": "flushed between timed steps"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "peak_kind": peak_kind,

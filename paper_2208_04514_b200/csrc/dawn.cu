@@ -121,6 +121,51 @@ __global__ void k_hscan(uint32_t *tmp, uint32_t nblk, uint32_t *total) {
   }
 }
 
+// ---- static ascending list of vertices with an in-edge (the first pull level's unreached list)
+__global__ void k_lcount(const uint32_t *__restrict__ irp, uint32_t n, uint32_t *__restrict__ tmp) {
+  __shared__ uint32_t sm[32];
+  const uint32_t base = blockIdx.x * kScanBlock;
+  uint32_t c = 0;
+  for (uint32_t i = threadIdx.x; i < kScanBlock; i += blockDim.x) {
+    const uint32_t v = base + i;
+    if (v < n && irp[v + 1] > irp[v]) ++c;
+  }
+  c = warp_sum(c);
+  if ((threadIdx.x & 31) == 0) sm[threadIdx.x / 32] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t t = 0;
+    for (uint32_t i = 0; i < blockDim.x / 32; ++i) t += sm[i];
+    tmp[blockIdx.x] = t;
+  }
+}
+
+__global__ void k_lfill(const uint32_t *__restrict__ irp, uint32_t n, const uint32_t *__restrict__ tmp,
+                        uint32_t *__restrict__ out) {
+  __shared__ uint32_t sm[256];
+  constexpr uint32_t kPer = kScanBlock / 256;  // blockDim.x == 256
+  const uint32_t v0 = blockIdx.x * kScanBlock + threadIdx.x * kPer;
+  uint32_t c = 0;
+  for (uint32_t i = 0; i < kPer; ++i)
+    if (v0 + i < n && irp[v0 + i + 1] > irp[v0 + i]) ++c;
+  sm[threadIdx.x] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t run = tmp[blockIdx.x];
+    for (uint32_t i = 0; i < blockDim.x; ++i) {
+      const uint32_t x = sm[i];
+      sm[i] = run;
+      run += x;
+    }
+  }
+  __syncthreads();
+  uint32_t o = sm[threadIdx.x];
+  for (uint32_t i = 0; i < kPer; ++i) {
+    const uint32_t v = v0 + i;
+    if (v < n && irp[v + 1] > irp[v]) out[o++] = v;
+  }
+}
+
 // pass 3 (piece-major order): hc[c] = #heavy rows with exactly c pieces; maxc
 __global__ void k_hhist(const uint32_t *__restrict__ rp, uint32_t n, uint32_t *hc, uint32_t *maxc) {
   uint32_t mx = 0;
@@ -188,6 +233,7 @@ struct dawn_graph_s {
   bool trace;
   size_t small_cap;  // max dynamic smem for k_small (0 = disabled)
   uint32_t bmpush_e = 1u << 18, solo_e = 512;
+  uint32_t n_hasin = 0;
 };
 
 namespace {
@@ -350,6 +396,18 @@ dawn_status dawn_graph_load_csr(int64_t n, int64_t m, const int64_t *row_ptr, co
       cudaMemcpyAsync(&C->n_hp_in, &C->n_hp_out, 4, cudaMemcpyDeviceToDevice, st);
     }
   }
+  if (sym || has_csc) {  // unreached-list seed for the pull sweep
+    const uint32_t nblk = (uint32_t)((n + kScanBlock - 1) / kScanBlock);
+    const uint32_t *irp2 = sym ? at<uint32_t>(g, L.rp) : at<uint32_t>(g, L.irp);
+    k_lcount<<<nblk, 256, 0, st>>>(irp2, (uint32_t)n, at<uint32_t>(g, L.scan_tmp));
+    k_hscan<<<1, 32, 0, st>>>(at<uint32_t>(g, L.scan_tmp), nblk, at<uint32_t>(g, L.useg));  // total -> scratch
+    k_lfill<<<nblk, 256, 0, st>>>(irp2, (uint32_t)n, at<uint32_t>(g, L.scan_tmp),
+                                  at<uint32_t>(g, L.hasin));
+  }
+  uint32_t nh = 0;
+  cudaMemcpyAsync(&nh, &at<Ctrl>(g, L.ctrl)->n_hasin, 4, cudaMemcpyDeviceToHost, st);
+  if ((e = cudaStreamSynchronize(st)) != cudaSuccess) { delete g; return cuda_fail(e, "graph load"); }
+  g->n_hasin = nh;
   if ((e = cudaGetLastError()) != cudaSuccess) { delete g; return cuda_fail(e, "graph load"); }
   *out = g;
   return DAWN_OK;
@@ -412,6 +470,10 @@ dawn_status dawn_sssp(dawn_graph g, int64_t source, uint32_t variant, uint32_t *
   p.hin_bits = at<uint32_t>(g, L.hin.bits);
   p.vis = at<uint32_t>(g, L.vis);
   p.cand = at<uint32_t>(g, L.cand);
+  p.hasin = at<uint32_t>(g, L.hasin);
+  p.ulist = at<uint32_t>(g, L.ulist);
+  p.useg = at<uint32_t>(g, L.useg);
+  p.n_hasin = g->n_hasin;
   for (int i = 0; i < 3; ++i) p.fb[i] = at<uint32_t>(g, L.fb[i]);
   p.trace = g->trace ? at<TraceRec>(g, L.trace) : nullptr;
   for (int i = 0; i < 2; ++i) {

@@ -92,7 +92,7 @@ struct HeavyList {  // static pieces of rows with degree > kHeavy
 struct Layout {
   size_t rp, irp, noin, vis, cand, fb[3], Lv[2], Lsd[2], Cf[2], ctrl, trace;
   HeavyList hout, hin;
-  size_t scan_tmp, piece_tmp;
+  size_t scan_tmp, piece_tmp, hasin, ulist, useg;
   size_t seen, F0, F1, nxt, msctrl, part, srcbuf, total;
   uint64_t srccap, capCf, capHP;
   bool own_irp;
@@ -135,6 +135,9 @@ inline Layout make_layout(int64_t n, int64_t m, uint32_t flags) {
   if (L.own_irp) heavy(L.hin); else L.hin = L.hout;
   L.scan_tmp = take(4 * ((size_t)n / kScanBlock + 2));
   L.piece_tmp = take(4 * (3 * ((size_t)m / kHPiece + 3) + 1));
+  L.hasin = take(4 * (size_t)n);
+  L.ulist = take(4 * (size_t)n);
+  L.useg = take(4 * (size_t)kMaxBlocks * 32);
   L.seen = take(8 * kMsW * (size_t)n);
   L.F0 = take(8 * kMsW * (size_t)n);
   L.F1 = take(8 * kMsW * (size_t)n);

@@ -28,6 +28,9 @@ struct SsspParams {
   const int32_t *col, *icol;
   const uint32_t *noin;
   const uint32_t *hin_v, *hin_s, *hin_e, *hin_bits;  // static heavy in-row pieces
+  const uint32_t *hasin;  // static ascending list of vertices with an in-edge (n_hasin)
+  uint32_t *ulist, *useg;  // unreached list (per-warp segments) and segment counts
+  uint32_t n_hasin;
   uint32_t *vis, *cand, *fb[3];  // cand: candidate bitmap of bitmap-push levels (zero between uses)
   uint32_t *Lv[2];   // frontier queue: vertex
   uint2 *Lsd[2];     //                 (row start, edge offset within the frontier)
@@ -42,7 +45,7 @@ struct SsspParams {
 };
 
 struct __align__(16) LevelState {
-  uint32_t L, nf, prev_nf, dir, rep, q, b, stop, ecc, solo, bm, deep;
+  uint32_t L, nf, prev_nf, dir, rep, q, b, stop, ecc, solo, bm, deep, ul;
   uint32_t push_levels, pull_levels, reached;
   uint32_t qn, n_hp;            // queue entries of frontier L; static heavy pieces
   uint32_t qe;                  // queue edges of frontier L
@@ -242,39 +245,39 @@ __device__ __forceinline__ void push_item(const SsspParams &p, const LevelState 
   uint32_t cur[J];
 #pragma unroll
   for (int j = 0; j < J; ++j) cur[j] = act[j] ? p.vis[u[j] >> 5] : ~0u;  // weak: stale 0 = atomic
-  if (CAND) {
+  if constexpr (CAND) {
     // bitmap push: mark the candidate, settle later in cand_filter (no returning atomic)
 #pragma unroll
     for (int j = 0; j < J; ++j) {
       const uint32_t bit = 1u << (u[j] & 31);
       if (!(cur[j] & bit)) red_or(p.cand + (u[j] >> 5), bit);
     }
-    return;
-  }
+  } else {
 #pragma unroll
-  for (int j = 0; j < J; ++j) {
-    const uint32_t bit = 1u << (u[j] & 31);
-    disc[j] = false;
-    if (!(cur[j] & bit)) disc[j] = !(atomicOr(p.vis + (u[j] >> 5), bit) & bit);
-  }
-#pragma unroll
-  for (int j = 0; j < J; ++j) {
-    rsd[j] = 0;
-    dd[j] = 0;
-    if (disc[j]) {
-      rsd[j] = ld_nc(p.rp + u[j]);
-      dd[j] = ld_nc(p.rp + u[j] + 1);
+    for (int j = 0; j < J; ++j) {
+      const uint32_t bit = 1u << (u[j] & 31);
+      disc[j] = false;
+      if (!(cur[j] & bit)) disc[j] = !(atomicOr(p.vis + (u[j] >> 5), bit) & bit);
     }
-  }
 #pragma unroll
-  for (int j = 0; j < J; ++j) {
-    if (disc[j]) {
-      dd[j] -= rsd[j];
-      p.dist[u[j]] = L1;
-      n_new += 1;
-      m_new += dd[j];
+    for (int j = 0; j < J; ++j) {
+      rsd[j] = 0;
+      dd[j] = 0;
+      if (disc[j]) {
+        rsd[j] = ld_nc(p.rp + u[j]);
+        dd[j] = ld_nc(p.rp + u[j] + 1);
+      }
     }
-    enqueue_frontier(p, ns, qn, disc[j], u[j], rsd[j], dd[j], stg, cnt);
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+      if (disc[j]) {
+        dd[j] -= rsd[j];
+        p.dist[u[j]] = L1;
+        n_new += 1;
+        m_new += dd[j];
+      }
+      enqueue_frontier(p, ns, qn, disc[j], u[j], rsd[j], dd[j], stg, cnt);
+    }
   }
 }
 
@@ -318,45 +321,49 @@ __device__ void pull_level(const SsspParams &p, const LevelState &st, uint32_t g
   const uint32_t *fcur = p.fb[st.b];
   uint32_t *fnext = p.fb[(st.b + 1) % 3];
   uint32_t *fclr = p.fb[(st.b + 2) % 3];  // held frontier L-1: cleared for level L+1
-  const uint32_t tail_bits = p.n & 31;
-  // (1) light rows: lane per vertex, a warp owns vis words w and w + nwarps (two independent
-  //     scans in flight per lane), 4 in-neighbours probed per round trip
+  // (0) clear the bitmap of frontier L-1 (becomes the write target of level L+1)
+  for (uint32_t w = gwarp * 32 + lane; w < p.nwords; w += nwarps * 32) fclr[w] = 0;
+  // (1) unreached vertices, one lane each, from the warp's segment of the unreached list:
+  //     the static ascending list of vertices with an in-edge at the first pull level, the
+  //     warp's in-place compacted survivors afterwards (order kept, so vis / irp / dist
+  //     accesses of a warp stay coalesced).  J entries per lane in flight.
   constexpr int J = DAWN_PULL_J;
-  for (uint32_t wb = gwarp; wb < p.nwords; wb += nwarps * J) {
-    uint32_t w[J], vw[J], todo[J], s[J], e[J], j0[J], hv[J], ef[J];
-    bool need[J], found[J];
+  const uint32_t cap = (p.n_hasin + nwarps - 1) / nwarps;
+  const uint32_t seg0 = gwarp * cap;
+  const uint32_t *src = (st.ul ? p.ulist : p.hasin) + seg0;
+  uint32_t *dst = p.ulist + seg0;
+  const uint32_t cnt = st.ul ? ld_cg(p.useg + gwarp)
+                             : (seg0 < p.n_hasin ? min(cap, p.n_hasin - seg0) : 0u);
+  uint32_t wr = 0;
+  for (uint32_t ib = 0; ib < cnt; ib += 32 * J) {
+    uint32_t u[J], s[J], e[J], j0[J], ef[J];
+    bool need[J], found[J], hvy[J];
 #pragma unroll
     for (int j = 0; j < J; ++j) {
-      w[j] = wb + j * nwarps;
-      vw[j] = 0;
-      todo[j] = 0;
-      hv[j] = 0;
-      if (w[j] < p.nwords) {
-        vw[j] = ld_cg(p.vis + w[j]);
-        todo[j] = ~vw[j];
-        hv[j] = ld_nc(p.hin_bits + w[j]);
-        if (w[j] == p.nwords - 1 && tail_bits) todo[j] &= (1u << tail_bits) - 1;
-        if (lane == 0) fclr[w[j]] = 0;
-      }
+      const uint32_t i = ib + j * 32 + lane;
+      u[j] = i < cnt ? ld_cg(src + i) : 0xffffffffu;
       found[j] = false;
+      need[j] = false;
+      hvy[j] = false;
       s[j] = e[j] = 0;
-      // row bounds loaded speculatively with the vis word (coalesced; saves a round trip)
-      if (w[j] < p.nwords) {
-        const uint32_t u = w[j] * 32 + lane;
-        if (u < p.n) {
-          s[j] = ld_nc(p.irp + u);
-          e[j] = ld_nc(p.irp + u + 1);
-        }
+    }
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+      if (u[j] != 0xffffffffu) {
+        const uint32_t bit = 1u << (u[j] & 31);
+        need[j] = !(ld_cg(p.vis + (u[j] >> 5)) & bit);   // settled by a push level since
+        hvy[j] = ld_nc(p.hin_bits + (u[j] >> 5)) & bit;
+        s[j] = ld_nc(p.irp + u[j]);                       // speculative, same round trip
+        e[j] = ld_nc(p.irp + u[j] + 1);
       }
     }
 #pragma unroll
     for (int j = 0; j < J; ++j) {
-      need[j] = (todo[j] >> lane) & 1u;
       if (!need[j]) e[j] = s[j];
       j0[j] = s[j];
-      // heavy rows (in-degree > kHeavy): only the first kHeavyProbe in-edges here, lane-parallel
-      // with everything else; the static pieces finish the rows still unsettled
-      ef[j] = ((hv[j] >> lane) & 1u) ? min(e[j], s[j] + kHeavyProbe) : e[j];
+      // heavy rows (in-degree > kHeavy): only the first kHeavyProbe in-edges here; the
+      // static pieces finish the rows still unsettled
+      ef[j] = hvy[j] ? min(e[j], s[j] + kHeavyProbe) : e[j];
     }
     for (;;) {
       bool any = false;
@@ -388,27 +395,30 @@ __device__ void pull_level(const SsspParams &p, const LevelState &st, uint32_t g
 #pragma unroll
     for (int j = 0; j < J; ++j) {
       if (need[j]) examined += min(j0[j], ef[j]) - s[j];
-      const uint32_t nb = __ballot_sync(DAWN_FULL, found[j]);
-      if (nb & hv[j]) {
-        // a heavy row may be settled concurrently by one of its static pieces: claim with a
-        // returning atomic so each vertex is counted (and enqueued) exactly once
-        uint32_t old = 0;
-        if (lane == 0) old = atomicOr(p.vis + w[j], nb);
-        old = __shfl_sync(DAWN_FULL, old, 0);
-        if ((old >> lane) & 1u) found[j] = false;
-        if (lane == 0 && (nb & ~old)) red_or(fnext + w[j], nb & ~old);
-      } else if (lane == 0 && nb) {
-        red_or(fnext + w[j], nb);
-        red_or(p.vis + w[j], nb);
+      if (found[j]) {
+        const uint32_t w = u[j] >> 5, bit = 1u << (u[j] & 31);
+        if (hvy[j]) {
+          // a heavy row may be settled concurrently by one of its static pieces: claim with a
+          // returning atomic so each vertex is counted exactly once
+          if (atomicOr(p.vis + w, bit) & bit) found[j] = false;
+        } else {
+          red_or(p.vis + w, bit);
+        }
       }
       if (found[j]) {
-        const uint32_t u = w[j] * 32 + lane;
-        p.dist[u] = L1;
+        red_or(fnext + (u[j] >> 5), 1u << (u[j] & 31));
+        p.dist[u[j]] = L1;
         n_new += 1;
-        m_new += p.sym ? (e[j] - s[j]) : (ld_nc(p.rp + u + 1) - ld_nc(p.rp + u));
+        m_new += p.sym ? (e[j] - s[j]) : (ld_nc(p.rp + u[j] + 1) - ld_nc(p.rp + u[j]));
       }
+      // survivors (still unreached) stay in the warp's segment, order preserved
+      const bool keep = need[j] && !found[j];
+      const uint32_t km = __ballot_sync(DAWN_FULL, keep);
+      if (keep) dst[wr + __popc(km & lanemask_lt())] = u[j];
+      wr += __popc(km);
     }
   }
+  if (lane == 0) p.useg[gwarp] = wr;
   phase_add(p, st.L, 0, t0);
   // (2) heavy rows: static pieces; 32 pieces tested per warp (vis), then a warp scans each
   //     live piece 32 in-edges per round trip
@@ -620,6 +630,7 @@ __device__ __forceinline__ void level_advance(LevelState &st) {
     st.pull_levels++;
     st.b = (st.b + 1) % 3;
     st.rep = kRepBitmap;
+    st.ul = 1;
   }
   st.L++;
 }
