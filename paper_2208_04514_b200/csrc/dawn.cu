@@ -166,6 +166,44 @@ __global__ void k_lfill(const uint32_t *__restrict__ irp, uint32_t n, const uint
   }
 }
 
+// ---- pull-friendly in-rows: copy each CSC row and move its kTopK in-neighbours of largest
+// out-degree to the front, in descending order (ties: earlier position).  Distances do not
+// depend on adjacency order; a pull probe meets a hub of the frontier first.  Warp per row.
+__global__ void k_topk_rows(const uint32_t *__restrict__ irp, const int32_t *__restrict__ icol,
+                            const uint32_t *__restrict__ rp, uint32_t n, int32_t *__restrict__ out) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t u = gw; u < n; u += nw) {
+    const uint32_t s = irp[u], e = irp[u + 1];
+    for (uint32_t j = s + lane; j < e; j += 32) out[j] = icol[j];
+    __syncwarp();
+    if (e - s < 2) continue;
+    const uint32_t K = min(kTopK, e - s - 1);
+    for (uint32_t i = 0; i < K; ++i) {
+      uint32_t bd = 0, bp = 0xffffffffu;
+      for (uint32_t j = s + i + lane; j < e; j += 32) {
+        const uint32_t v = (uint32_t)out[j];
+        const uint32_t d = rp[v + 1] - rp[v];
+        if (bp == 0xffffffffu || d > bd) { bd = d; bp = j; }
+      }
+      for (int o = 16; o; o >>= 1) {
+        const uint32_t od = __shfl_xor_sync(DAWN_FULL, bd, o), op = __shfl_xor_sync(DAWN_FULL, bp, o);
+        if (op != 0xffffffffu && (bp == 0xffffffffu || od > bd || (od == bd && op < bp))) {
+          bd = od;
+          bp = op;
+        }
+      }
+      if (lane == 0 && bp != s + i) {
+        const int32_t t = out[s + i];
+        out[s + i] = out[bp];
+        out[bp] = t;
+      }
+      __syncwarp();
+    }
+  }
+}
+
 // pass 3 (piece-major order): hc[c] = #heavy rows with exactly c pieces; maxc
 __global__ void k_hhist(const uint32_t *__restrict__ rp, uint32_t n, uint32_t *hc, uint32_t *maxc) {
   uint32_t mx = 0;
@@ -395,6 +433,12 @@ dawn_status dawn_graph_load_csr(int64_t n, int64_t m, const int64_t *row_ptr, co
     } else {
       cudaMemcpyAsync(&C->n_hp_in, &C->n_hp_out, 4, cudaMemcpyDeviceToDevice, st);
     }
+  }
+  if ((sym || has_csc) && m > 0) {  // degree-ordered in-rows for the pull probes
+    const uint32_t *irp2 = sym ? at<uint32_t>(g, L.rp) : at<uint32_t>(g, L.irp);
+    k_topk_rows<<<g->nsm * 8, 256, 0, st>>>(irp2, sym ? col : in_col, at<uint32_t>(g, L.rp),
+                                            (uint32_t)n, at<int32_t>(g, L.icol2));
+    g->icol = at<int32_t>(g, L.icol2);
   }
   if (sym || has_csc) {  // unreached-list seed for the pull sweep
     const uint32_t nblk = (uint32_t)((n + kScanBlock - 1) / kScanBlock);

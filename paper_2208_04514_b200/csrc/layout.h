@@ -25,7 +25,8 @@ constexpr uint32_t kIlp = 4;      // chunks per warp item when the frontier is w
 // by one lane each (early exit, 4 probes per round trip).
 constexpr uint32_t kHeavy = 32;
 constexpr uint32_t kHPiece = 256;
-constexpr uint32_t kHeavyProbe = 16;  // in-edges a heavy row probes lane-parallel in the sweep
+constexpr uint32_t kHeavyProbe = 16;
+constexpr uint32_t kTopK = 8;  // in-row prefix ordered by in-neighbour out-degree (pull probes)  // in-edges a heavy row probes lane-parallel in the sweep
 constexpr uint32_t kScanBlock = 2048;  // elements per CTA in the load-time piece scan
 constexpr uint32_t kMaxBlocks = 2048;  // cap on persistent grid size (partials buffer)
 constexpr uint32_t kTraceCap = 1 << 16;
@@ -92,7 +93,7 @@ struct HeavyList {  // static pieces of rows with degree > kHeavy
 struct Layout {
   size_t rp, irp, noin, vis, cand, fb[3], Lv[2], Lsd[2], Cf[2], ctrl, trace;
   HeavyList hout, hin;
-  size_t scan_tmp, piece_tmp, hasin, ulist, useg;
+  size_t scan_tmp, piece_tmp, hasin, ulist, useg, icol2;
   size_t seen, F0, F1, nxt, msctrl, part, srcbuf, total;
   uint64_t srccap, capCf, capHP;
   bool own_irp;
@@ -138,6 +139,7 @@ inline Layout make_layout(int64_t n, int64_t m, uint32_t flags) {
   L.hasin = take(4 * (size_t)n);
   L.ulist = take(4 * (size_t)n);
   L.useg = take(4 * (size_t)kMaxBlocks * 32);
+  L.icol2 = take(4 * (size_t)m);  // in-rows, highest-degree in-neighbours first
   L.seen = take(8 * kMsW * (size_t)n);
   L.F0 = take(8 * kMsW * (size_t)n);
   L.F1 = take(8 * kMsW * (size_t)n);

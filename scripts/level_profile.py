@@ -7,6 +7,7 @@ variants = (sys.argv[2] if len(sys.argv) > 2 else "auto").split(",")
 nsrc = int(os.environ.get("NSRC", "16"))
 t = time.time(); g = graphgen.config_graph(cfg); print(cfg, "n", g.n, "m", g.m, "gen %.1fs" % (time.time() - t))
 G = dawn.Graph(g.row_ptr, g.col, g.symmetric, *(g.transpose() if not g.symmetric else (None, None)), trace=os.environ.get('TRACE', '1') == '1')
+if os.environ.get('ALPHA'): G.set_tuning(alpha=float(os.environ['ALPHA']))
 srcs = [0] if cfg in ("C1", "C3") else list(g.sample_sources(nsrc, 1))
 CLK = 1.965e3  # cycles per us at max clock
 nw = 296 * 16
