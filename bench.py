@@ -249,14 +249,22 @@ def run_sssp(args, rank, world, dev, cfg=None, steps=None, warmup=None, e2e=True
     dev_src = torch.empty_like(host_src, device=dev)
     host_out = torch.empty((k, g.n), dtype=torch.int32).pin_memory()
     e2e_ms = []
+    copy_stream = torch.cuda.Stream(device=dev)
     for it in range(max(1, steps)):
         flush.zero_()
         torch.cuda.synchronize()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(stream)
         dev_src.copy_(host_src, non_blocking=True)
-        step()
-        host_out.copy_(out, non_blocking=True)
+        # each row's D2H (pinned) overlaps the next source's kernel on a copy stream
+        for i, s in enumerate(srcs):
+            dawn.sssp(G, int(s), args.variant, out=orow(i))
+            done = torch.cuda.Event()
+            done.record(stream)
+            copy_stream.wait_event(done)
+            with torch.cuda.stream(copy_stream):
+                host_out[i].copy_(orow(i), non_blocking=True)
+        stream.wait_stream(copy_stream)
         b.record(stream)
         torch.cuda.synchronize()
         e2e_ms.append(a.elapsed_time(b))
@@ -289,6 +297,8 @@ def run_sssp(args, rank, world, dev, cfg=None, steps=None, warmup=None, e2e=True
                      "exec_bytes_per_launch": float(np.mean(b_exec))},
         "e2e": {"value": e2e_val, "unit": "GTEPS", "h2d_bytes_per_step": int(host_src.numel() * 8),
                 "d2h_bytes_per_step": int(host_out.numel() * 4),
+                "how": "dawn.sssp per source; each distance row copied to pinned host memory on a "
+                       "second stream, overlapping the next source's kernel",
                 "ms_per_step": e2e_tot / len(e2e_ms)},
         "levels": {"push_mean": float(np.mean(pushl)), "pull_mean": float(np.mean(pulll)),
                    "edges_examined_mean": float(np.mean(examined)),

@@ -585,6 +585,8 @@ static dawn_status launch_ms(dawn_graph g, const std::vector<uint32_t> &src, uin
     p.sym = (g->flags & DAWN_GRAPH_SYMMETRIC) ? 1u : 0u;
     p.ms_alpha = g->ms_alpha;
     p.part = at<uint4>(g, L.part);
+    p.trace = g->trace ? at<TraceRec>(g, L.trace) : nullptr;
+    p.trace_n = &at<Ctrl>(g, L.ctrl)->trace_n;
     int grid = g->ms_grid;
     const int small_m = env_int("DAWN_SMALL_M", 1 << 15);
     if (g->m + g->n <= small_m) grid = 1;

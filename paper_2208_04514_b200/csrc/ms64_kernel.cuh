@@ -92,6 +92,8 @@ struct MsParams {
   uint32_t can_pull, sym;
   float ms_alpha;
   uint4 *part;               // per-CTA partial records [2][gridDim.x][kMsBatch]
+  TraceRec *trace;           // per-level trace of the first batch (DAWN_GRAPH_TRACE) or null
+  uint32_t *trace_n;
 };
 
 struct MsState {
@@ -236,6 +238,18 @@ __global__ void __launch_bounds__(NT, DAWN_MS_MINB) k_ms64(MsParams p) {
         st.stop = (st.n_active == 0) || (st.L + 1 >= p.n);
         st.dir = (p.can_pull && (double)st.m_active * p.ms_alpha > (double)st.m_uns) ? kPull
                                                                                      : kPush;
+        if (p.trace && bt == 0 && blockIdx.x == 0 && st.L < kTraceCap) {
+          TraceRec r{};
+          unsigned long long t;
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+          r.t_ns = t;
+          r.level = st.L;
+          r.dir = st.stop ? 2u : st.dir;
+          r.nf = (uint32_t)st.n_active;
+          r.mf = st.m_active;
+          p.trace[st.L] = r;
+          *p.trace_n = st.L + 1;
+        }
       }
       __syncthreads();
       if (st.stop) break;
