@@ -141,13 +141,18 @@ dawn_status dawn_graph_destroy(dawn_graph g);
  *                     candidates in a bitmap (fire-and-forget) and settle them in a second pass
  *                     instead of one returning atomic per arc.  Default 262144.
  *   DAWN_PARAM_SOLO_EDGES  push levels with <= this many arcs run on one CTA with block-level
- *                     barriers only.  Default 512.                                              */
+ *                     barriers only.  Default 512.
+ *   DAWN_PARAM_NARROW_AVG_DEGREE  graphs with m <= value * n (high-diameter shapes: grids,
+ *                     road networks) start each dawn_sssp on one CTA with the frontier in
+ *                     shared memory, handing over to the grid-wide kernel if the frontier
+ *                     outgrows it.  0 disables.  Default 6.                                     */
 typedef enum {
   DAWN_PARAM_ALPHA = 0,
   DAWN_PARAM_BETA = 1,
   DAWN_PARAM_MS_ALPHA = 2,
   DAWN_PARAM_BITMAP_PUSH_EDGES = 3,
-  DAWN_PARAM_SOLO_EDGES = 4
+  DAWN_PARAM_SOLO_EDGES = 4,
+  DAWN_PARAM_NARROW_AVG_DEGREE = 5
 } dawn_param;
 
 /* Set one tunable (INVALID_ARGUMENT for an unknown key or a negative value). */

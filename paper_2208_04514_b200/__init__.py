@@ -180,11 +180,12 @@ class Graph:
                                       ctypes.byref(cnt), _stream(stream)))
         return buf[: min(cnt.value, len(buf))].copy()
 
-    _PARAMS = {"alpha": 0, "beta": 1, "ms_alpha": 2, "bitmap_push_edges": 3, "solo_edges": 4}
+    _PARAMS = {"alpha": 0, "beta": 1, "ms_alpha": 2, "bitmap_push_edges": 3, "solo_edges": 4,
+               "narrow_avg_degree": 5}
 
     def set_tuning(self, **kw):
         """dawn_graph_set_param for each keyword (alpha, beta, ms_alpha, bitmap_push_edges,
-        solo_edges).  Speed only; results never change."""
+        solo_edges, narrow_avg_degree).  Speed only; results never change."""
         for k, v in kw.items():
             _check(lib().dawn_graph_set_param(self._h, self._PARAMS[k], float(v)))
 

@@ -14,6 +14,7 @@
 #include "layout.h"
 #include "ms64_kernel.cuh"
 #include "small_kernel.cuh"
+#include "narrow_kernel.cuh"
 #include "sssp_kernel.cuh"
 
 using namespace dawn;
@@ -272,6 +273,9 @@ struct dawn_graph_s {
   size_t small_cap;  // max dynamic smem for k_small (0 = disabled)
   uint32_t bmpush_e = 1u << 18, solo_e = 512;
   uint32_t n_hasin = 0;
+  float narrow_deg = 6.f;  // k_narrow first when m <= narrow_deg * n (high-diameter shapes)
+  bool narrow_ok = false;
+  uint32_t seq = 0;
 };
 
 namespace {
@@ -360,6 +364,11 @@ dawn_status dawn_graph_load_csr(int64_t n, int64_t m, const int64_t *row_ptr, co
         cudaFuncSetAttribute((const void *)k_small<1024>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cap) == cudaSuccess)
       g->small_cap = cap;
+    cudaGetLastError();
+    g->narrow_ok = cudaFuncSetAttribute((const void *)k_narrow<1024>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)narrow_smem_bytes()) == cudaSuccess &&
+                   narrow_smem_bytes() <= cap;
     cudaGetLastError();
   }
   g->ms_grid = grid_for((const void *)k_ms64<kNT>, g->nsm, "DAWN_MS_BPS");
@@ -472,6 +481,7 @@ dawn_status dawn_graph_set_param(dawn_graph g, dawn_param key, double value) {
     case DAWN_PARAM_MS_ALPHA: g->ms_alpha = (float)value; break;
     case DAWN_PARAM_BITMAP_PUSH_EDGES: g->bmpush_e = (uint32_t)std::min(value, 4294967295.0); break;
     case DAWN_PARAM_SOLO_EDGES: g->solo_e = (uint32_t)std::min(value, 4294967295.0); break;
+    case DAWN_PARAM_NARROW_AVG_DEGREE: g->narrow_deg = (float)value; break;
     default: return fail(DAWN_ERR_INVALID_ARGUMENT, "unknown parameter");
   }
   return DAWN_OK;
@@ -536,6 +546,31 @@ dawn_status dawn_sssp(dawn_graph g, int64_t source, uint32_t variant, uint32_t *
   p.beta = g->beta;
   p.bmpush_e = g->bmpush_e;
   p.solo_e = g->solo_e;
+  p.seq = ++g->seq;
+  if (variant != DAWN_PULL && !g->trace && g->narrow_ok && g->m > 0 &&
+      (double)g->m <= (double)g->narrow_deg * (double)g->n) {
+    // high-diameter shape: one-CTA shared-memory search first; k_sssp resumes or exits
+    NarrowParams np{};
+    np.n = p.n;
+    np.nwords = p.nwords;
+    np.m = p.m;
+    np.rp = p.rp;
+    np.col = p.col;
+    np.noin = p.noin;
+    np.vis = p.vis;
+    np.dist = dist;
+    np.Lv0 = p.Lv[0];
+    np.Lsd0 = p.Lsd[0];
+    np.Cf0 = p.Cf[0];
+    np.ctrl = p.ctrl;
+    np.stats = stats;
+    np.source = (uint32_t)source;
+    np.max_reach_base = g->n_hasin;
+    np.seq = p.seq;
+    k_narrow<1024><<<g->nsm, 1024, narrow_smem_bytes(), static_cast<cudaStream_t>(stream)>>>(np);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "k_narrow launch");
+  }
   int grid = g->sssp_grid;
   const int small_m = env_int("DAWN_SMALL_M", 1 << 15);
   if (g->m + g->n <= small_m) grid = 1;  // tiny graphs: one CTA, barriers are __syncthreads

@@ -65,7 +65,10 @@ struct Ctrl {
   uint32_t n_hp_out, n_hp_in;   // static heavy-piece counts (written at load)
   uint32_t trace_n;
   uint32_t solo_epoch;          // CTA 0 -> others: a solo stretch ended (see k_sssp)
-  uint32_t pad1[8];
+  uint32_t narrow_init;         // k_narrow: CTAs done with the init fill
+  uint32_t narrow_status;       // k_narrow -> k_sssp: 1 finished, 2 resume from the queue
+  uint32_t narrow_seq;          // dawn_sssp call number the status belongs to
+  uint32_t pad1[5];
   alignas(16) unsigned char solo_state[256];  // LevelState snapshot published with solo_epoch
 };
 

@@ -42,6 +42,7 @@ struct SsspParams {
   uint32_t source, variant, can_pull, sym;
   float alpha, beta;
   uint32_t bmpush_e, solo_e;  // DAWN_PARAM_BITMAP_PUSH_EDGES / DAWN_PARAM_SOLO_EDGES
+  uint32_t seq;               // call number (k_narrow hand-over)
 };
 
 struct __align__(16) LevelState {
@@ -655,7 +656,22 @@ __global__ void __launch_bounds__(NT, DAWN_SSSP_MINB) k_sssp(SsspParams p) {
   // condition 1 bound: only vertices with an in-edge (plus s itself) can ever be reached
   const uint32_t max_reach = ld_cg(&C->n_hasin) + ((p.noin[src >> 5] >> (src & 31)) & 1u);
 
+  // ---- k_narrow ran first for this call: finished (nothing to do) or hand-over (resume)
+  uint32_t narrow = 0;
+  if (ld_acquire(&C->narrow_seq) == p.seq) narrow = ld_cg(&C->narrow_status);
+  if (narrow == 1) return;
+  if (narrow == 2) {
+    if (threadIdx.x < 4) phase_smem()[threadIdx.x] = 0;
+    if (threadIdx.x == 0) {
+      const uint4 *s4 = reinterpret_cast<const uint4 *>(C->solo_state);
+      uint4 *d4 = reinterpret_cast<uint4 *>(&st);
+      for (int i = 0; i < (int)(sizeof(LevelState) / 16); ++i) d4[i] = __ldcg(s4 + i);
+      st.n_hp = ld_cg(&C->n_hp_in);
+    }
+    __syncthreads();
+  }
   // ---- a1 init: dist <- UNREACHED (d(s) = 0), vis <- no-in-edge vertices | {s}  (Q4, Q7)
+  if (narrow != 2) {
   for (uint32_t i = gtid; i < p.n; i += nthreads) p.dist[i] = (i == src) ? 0u : kUnreached;
   for (uint32_t w = gtid; w < p.nwords; w += nthreads)
     p.vis[w] = p.noin[w] | ((w == (src >> 5)) ? (1u << (src & 31)) : 0u);
@@ -687,6 +703,7 @@ __global__ void __launch_bounds__(NT, DAWN_SSSP_MINB) k_sssp(SsspParams p) {
     st = LevelState{};
     st.dir = (p.variant == DAWN_PULL) ? kPull : kPush;
     st.n_hp = ld_cg(&C->n_hp_in);
+  }
   }
   grid_sync(&C->bar, nblocks, bar_target);
 

@@ -254,3 +254,22 @@ def test_tunables_never_change_results(knobs):
         G.set_tuning(**knobs)
         srcs = [0, g.n - 1] + list(g.sample_sources(3, seed=2))
         check_sssp(g, G, srcs, variants=("auto", "push"))
+
+
+def test_narrow_kernel_and_handover():
+    # low average degree => dawn_sssp starts on one CTA with the frontier in shared memory
+    # (k_narrow); wide frontiers overflow it and the grid-wide kernel resumes from its queue.
+    rng = np.random.default_rng(11)
+    n = 200_000
+    e = rng.integers(0, n, size=(2 * n, 2))
+    rand = graphgen.from_edges(n, e, symmetric=True)              # avg degree ~4, wide waves
+    tree = graphgen.from_edges(2 ** 17 - 1, [[v, 2 * v + 1] for v in range(2 ** 16 - 1)] +
+                               [[v, 2 * v + 2] for v in range(2 ** 16 - 1)])  # directed tree
+    grid = graphgen.grid(700, 500)
+    for g in (rand, tree, grid):
+        assert g.m <= 6 * g.n
+        G = dev_graph(g)
+        srcs = [0, 1, g.n // 2, g.n - 1]
+        check_sssp(g, G, srcs, variants=("auto", "push"))
+        G.set_tuning(narrow_avg_degree=0)                          # grid-wide kernel only
+        check_sssp(g, G, srcs[:2], variants=("auto",))
