@@ -143,9 +143,11 @@ dawn_status dawn_graph_destroy(dawn_graph g);
  *   DAWN_PARAM_SOLO_EDGES  push levels with <= this many arcs run on one CTA with block-level
  *                     barriers only.  Default 512.
  *   DAWN_PARAM_NARROW_AVG_DEGREE  graphs with m <= value * n (high-diameter shapes: grids,
- *                     road networks) start each dawn_sssp on one CTA with the frontier in
- *                     shared memory, handing over to the grid-wide kernel if the frontier
- *                     outgrows it.  0 disables.  Default 6.                                     */
+ *                     road networks; only when m <= 8 n and n <= 20,971,520, the graphs for which
+ *                     the load keeps k_narrow's augmented arc array) start each dawn_sssp on ONE
+ *                     16-CTA thread-block cluster with the visited bitmap and the frontier queues
+ *                     in distributed shared memory, handing over to the grid-wide kernel if a
+ *                     frontier outgrows the shared-memory queues.  0 disables.  Default 6.     */
 typedef enum {
   DAWN_PARAM_ALPHA = 0,
   DAWN_PARAM_BETA = 1,

@@ -256,6 +256,16 @@ __global__ void k_hfill(const uint32_t *__restrict__ rp, uint32_t n, const uint3
   }
 }
 
+// ---- k_narrow's augmented arcs: arc[j] = (col[j], row_ptr[col[j]], row_ptr[col[j] + 1], 0)
+__global__ void k_arcs(const int32_t *__restrict__ col, const uint32_t *__restrict__ rp, int64_t m,
+                       uint4 *__restrict__ arc) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < m;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t v = (uint32_t)col[j];
+    arc[j] = make_uint4(v, rp[v], rp[v + 1], 0u);
+  }
+}
+
 }  // namespace
 
 struct dawn_graph_s {
@@ -274,7 +284,10 @@ struct dawn_graph_s {
   uint32_t bmpush_e = 1u << 18, solo_e = 512;
   uint32_t n_hasin = 0;
   float narrow_deg = 6.f;  // k_narrow first when m <= narrow_deg * n (high-diameter shapes)
-  bool narrow_ok = false;
+  bool narrow_ok = false;  // arc array built and a 16-CTA cluster fits
+  uint32_t narrow_wpc = 0, narrow_qcap = 0, narrow_grid = 0;
+  size_t narrow_smem = 0;
+  unsigned long long narrow_calls = 0;
   uint32_t seq = 0;
 };
 
@@ -365,10 +378,43 @@ dawn_status dawn_graph_load_csr(int64_t n, int64_t m, const int64_t *row_ptr, co
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cap) == cudaSuccess)
       g->small_cap = cap;
     cudaGetLastError();
-    g->narrow_ok = cudaFuncSetAttribute((const void *)k_narrow<1024>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)narrow_smem_bytes()) == cudaSuccess &&
-                   narrow_smem_bytes() <= cap;
+    // k_narrow: visited slice of ceil(nwords / 16) words (multiple of 4) per CTA, the rest of
+    // the shared memory holds the two frontier queues
+    g->narrow_ok = false;
+    if (L.arc && env_int("DAWN_NARROW", 1)) {
+      const uint32_t nw = (uint32_t)((n + 31) / 32);
+      const uint32_t wpc = ((nw + kNarrowCluster - 1) / kNarrowCluster + 3) & ~3u;
+      const size_t fixed = narrow_smem_bytes(wpc, 0);
+      uint32_t qcap = fixed < cap ? (uint32_t)((cap - fixed) / kNarrowEntryBytes) : 0u;
+      qcap = std::min<uint32_t>(qcap, (uint32_t)env_int("DAWN_NARROW_QCAP", 1 << 20));
+      const size_t bytes = narrow_smem_bytes(wpc, qcap);
+      if (qcap >= 32 && bytes <= cap &&
+          cudaFuncSetAttribute((const void *)k_narrow, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)bytes) == cudaSuccess &&
+          cudaFuncSetAttribute((const void *)k_narrow,
+                               cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess) {
+        cudaLaunchConfig_t cfg{};
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = kNarrowCluster;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.gridDim = dim3(kNarrowCluster * 16);
+        cfg.blockDim = dim3(kNarrowThreads);
+        cfg.dynamicSmemBytes = bytes;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        int ncl = 0;
+        if (cudaOccupancyMaxActiveClusters(&ncl, (const void *)k_narrow, &cfg) == cudaSuccess &&
+            ncl >= 1) {
+          g->narrow_ok = true;
+          g->narrow_wpc = wpc;
+          g->narrow_qcap = qcap;
+          g->narrow_smem = bytes;
+          g->narrow_grid = kNarrowCluster * (uint32_t)std::min(ncl, std::max(1, g->nsm / (int)kNarrowCluster));
+        }
+      }
+    }
     cudaGetLastError();
   }
   g->ms_grid = grid_for((const void *)k_ms64<kNT>, g->nsm, "DAWN_MS_BPS");
@@ -457,6 +503,8 @@ dawn_status dawn_graph_load_csr(int64_t n, int64_t m, const int64_t *row_ptr, co
     k_lfill<<<nblk, 256, 0, st>>>(irp2, (uint32_t)n, at<uint32_t>(g, L.scan_tmp),
                                   at<uint32_t>(g, L.hasin));
   }
+  if (L.arc)
+    k_arcs<<<g->nsm * 8, 256, 0, st>>>(col, at<uint32_t>(g, L.rp), m, at<uint4>(g, L.arc));
   uint32_t nh = 0;
   cudaMemcpyAsync(&nh, &at<Ctrl>(g, L.ctrl)->n_hasin, 4, cudaMemcpyDeviceToHost, st);
   if ((e = cudaStreamSynchronize(st)) != cudaSuccess) { delete g; return cuda_fail(e, "graph load"); }
@@ -547,28 +595,42 @@ dawn_status dawn_sssp(dawn_graph g, int64_t source, uint32_t variant, uint32_t *
   p.bmpush_e = g->bmpush_e;
   p.solo_e = g->solo_e;
   p.seq = ++g->seq;
-  if (variant != DAWN_PULL && !g->trace && g->narrow_ok && g->m > 0 &&
+  if (variant != DAWN_PULL && g->narrow_ok &&
       (double)g->m <= (double)g->narrow_deg * (double)g->n) {
-    // high-diameter shape: one-CTA shared-memory search first; k_sssp resumes or exits
+    // high-diameter shape: the search starts on one 16-CTA cluster (state in distributed
+    // shared memory); k_sssp below resumes from its hand-over or exits at once
     NarrowParams np{};
     np.n = p.n;
     np.nwords = p.nwords;
-    np.m = p.m;
+    np.wpc = g->narrow_wpc;
+    np.qcap = g->narrow_qcap;
     np.rp = p.rp;
-    np.col = p.col;
+    np.arc = at<uint4>(g, L.arc);
     np.noin = p.noin;
     np.vis = p.vis;
     np.dist = dist;
-    np.Lv0 = p.Lv[0];
-    np.Lsd0 = p.Lsd[0];
-    np.Cf0 = p.Cf[0];
+    np.fb0 = p.fb[0];
+    np.fb1 = p.fb[1];
     np.ctrl = p.ctrl;
     np.stats = stats;
     np.source = (uint32_t)source;
     np.max_reach_base = g->n_hasin;
     np.seq = p.seq;
-    k_narrow<1024><<<g->nsm, 1024, narrow_smem_bytes(), static_cast<cudaStream_t>(stream)>>>(np);
-    cudaError_t e = cudaGetLastError();
+    np.fill_target = ++g->narrow_calls * (unsigned long long)g->narrow_grid;
+    np.trace = p.trace;
+    cudaLaunchConfig_t cfg{};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = kNarrowCluster;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3(g->narrow_grid);
+    cfg.blockDim = dim3(kNarrowThreads);
+    cfg.dynamicSmemBytes = g->narrow_smem;
+    cfg.stream = static_cast<cudaStream_t>(stream);
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, k_narrow, np);
     if (e != cudaSuccess) return cuda_fail(e, "k_narrow launch");
   }
   int grid = g->sssp_grid;

@@ -30,6 +30,11 @@ constexpr uint32_t kTopK = 8;  // in-row prefix ordered by in-neighbour out-degr
 constexpr uint32_t kScanBlock = 2048;  // elements per CTA in the load-time piece scan
 constexpr uint32_t kMaxBlocks = 2048;  // cap on persistent grid size (partials buffer)
 constexpr uint32_t kTraceCap = 1 << 16;
+// k_narrow (narrow_kernel.cuh): one 16-CTA cluster, visited bitmap in distributed shared memory
+constexpr uint32_t kNarrowCluster = 16;            // CTAs per cluster (non-portable size)
+constexpr uint32_t kNarrowVisBytes = 160 * 1024;   // max visited-slice bytes per CTA
+constexpr uint64_t kNarrowMaxN = (uint64_t)kNarrowCluster * kNarrowVisBytes * 8;  // 20,971,520
+constexpr uint32_t kNarrowMaxAvgDeg = 8;           // arc array kept when m <= 8 n
 // Multi-source kernel: kMsW 64-bit words per vertex = kMsBatch sources per adjacency pass.
 constexpr int kMsW = 4;
 constexpr uint32_t kMsBatch = 64 * kMsW;
@@ -65,10 +70,10 @@ struct Ctrl {
   uint32_t n_hp_out, n_hp_in;   // static heavy-piece counts (written at load)
   uint32_t trace_n;
   uint32_t solo_epoch;          // CTA 0 -> others: a solo stretch ended (see k_sssp)
-  uint32_t narrow_init;         // k_narrow: CTAs done with the init fill
-  uint32_t narrow_status;       // k_narrow -> k_sssp: 1 finished, 2 resume from the queue
+  uint32_t narrow_status;       // k_narrow -> k_sssp: 1 finished, 2 resume from the bitmap
   uint32_t narrow_seq;          // dawn_sssp call number the status belongs to
-  uint32_t pad1[5];
+  unsigned long long narrow_fill;  // k_narrow: CTAs done with the init fill (monotonic)
+  uint32_t pad1[4];
   alignas(16) unsigned char solo_state[256];  // LevelState snapshot published with solo_epoch
 };
 
@@ -96,7 +101,7 @@ struct HeavyList {  // static pieces of rows with degree > kHeavy
 struct Layout {
   size_t rp, irp, noin, vis, cand, fb[3], Lv[2], Lsd[2], Cf[2], ctrl, trace;
   HeavyList hout, hin;
-  size_t scan_tmp, piece_tmp, hasin, ulist, useg, icol2;
+  size_t scan_tmp, piece_tmp, hasin, ulist, useg, icol2, arc;
   size_t seen, F0, F1, nxt, msctrl, part, srcbuf, total;
   uint64_t srccap, capCf, capHP;
   bool own_irp;
@@ -143,6 +148,9 @@ inline Layout make_layout(int64_t n, int64_t m, uint32_t flags) {
   L.ulist = take(4 * (size_t)n);
   L.useg = take(4 * (size_t)kMaxBlocks * 32);
   L.icol2 = take(4 * (size_t)m);  // in-rows, highest-degree in-neighbours first
+  // k_narrow's augmented arcs (target, target row start, target row end, 0): low-degree graphs
+  L.arc = (m > 0 && (uint64_t)n <= kNarrowMaxN && (uint64_t)m <= (uint64_t)kNarrowMaxAvgDeg * (uint64_t)n)
+              ? take(16 * (size_t)m) : 0;
   L.seen = take(8 * kMsW * (size_t)n);
   L.F0 = take(8 * kMsW * (size_t)n);
   L.F1 = take(8 * kMsW * (size_t)n);

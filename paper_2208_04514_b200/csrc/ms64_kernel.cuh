@@ -296,31 +296,19 @@ __global__ void __launch_bounds__(NT, DAWN_MS_MINB) k_ms64(MsParams p) {
             }
           }
         }
-        // phase A2: heavy active rows by static pieces; 32 pieces tested per warp (F != 0),
-        // then the warp expands each live piece 32 arcs at a time
-        for (uint32_t pb = gwarp * 32; pb < st.n_hp_out; pb += nwarps * 32) {
-          const uint32_t pc = pb + lane;
-          uint32_t v = 0;
-          bool live = false;
-          if (pc < st.n_hp_out) {
-            v = ld_nc(p.hout_v + pc);
-            live = wany<W>(wload<W>(Fc, v));
-          }
-          uint32_t lm = __ballot_sync(DAWN_FULL, live);
-          while (lm) {
-            const uint32_t k = __ffs(lm) - 1;
-            lm &= lm - 1;
-            const uint32_t vk = __shfl_sync(DAWN_FULL, v, k), pk = pb + k;
-            const Word<W> fv = wload<W>(Fc, vk);
-            const uint32_t s = ld_nc(p.hout_s + pk), e = ld_nc(p.hout_e + pk);
-            for (uint32_t j = s + lane; j < e; j += 32) {
-              const uint32_t u = (uint32_t)ld_nc(p.col + j);
-              const Word<W> su = wload<W>(p.seen, u);
+        // phase A2: heavy active rows by static pieces
+        for (uint32_t pc = gwarp; pc < st.n_hp_out; pc += nwarps) {
+          const uint32_t v = ld_nc(p.hout_v + pc);
+          const Word<W> fv = wload<W>(Fc, v);
+          if (!wany<W>(fv)) continue;
+          const uint32_t s = ld_nc(p.hout_s + pc), e = ld_nc(p.hout_e + pc);
+          for (uint32_t j = s + lane; j < e; j += 32) {
+            const uint32_t u = (uint32_t)ld_nc(p.col + j);
+            const Word<W> su = wload<W>(p.seen, u);
 #pragma unroll
-              for (int i = 0; i < W; ++i) {
-                const unsigned long long x = fv.w[i] & ~su.w[i];
-                if (x) red_or64(p.nxt + (size_t)u * W + i, x);
-              }
+            for (int i = 0; i < W; ++i) {
+              const unsigned long long x = fv.w[i] & ~su.w[i];
+              if (x) red_or64(p.nxt + (size_t)u * W + i, x);
             }
           }
         }
@@ -369,17 +357,14 @@ __global__ void __launch_bounds__(NT, DAWN_MS_MINB) k_ms64(MsParams p) {
             if (wany<W>(U)) {
               Word<W> a = wzero<W>();
               const uint32_t s = ld_nc(p.irp + u), e = ld_nc(p.irp + u + 1);
-              for (uint32_t j = s; j < e; j += 4) {  // 4 gathers in flight per lane
+              for (uint32_t j = s; j < e; j += 2) {
                 const uint32_t v0 = (uint32_t)ld_nc(p.icol + j);
                 const uint32_t v1 = j + 1 < e ? (uint32_t)ld_nc(p.icol + j + 1) : v0;
-                const uint32_t v2 = j + 2 < e ? (uint32_t)ld_nc(p.icol + j + 2) : v0;
-                const uint32_t v3 = j + 3 < e ? (uint32_t)ld_nc(p.icol + j + 3) : v0;
                 const Word<W> f0 = wload<W>(Fc, v0), f1 = wload<W>(Fc, v1);
-                const Word<W> f2 = wload<W>(Fc, v2), f3 = wload<W>(Fc, v3);
                 bool cov = true;
 #pragma unroll
                 for (int i = 0; i < W; ++i) {
-                  a.w[i] |= f0.w[i] | f1.w[i] | f2.w[i] | f3.w[i];
+                  a.w[i] |= f0.w[i] | f1.w[i];
                   cov = cov && (a.w[i] & U.w[i]) == U.w[i];
                 }
                 if (cov) break;
@@ -405,52 +390,36 @@ __global__ void __launch_bounds__(NT, DAWN_MS_MINB) k_ms64(MsParams p) {
           }
           ms_record_group<W>(p, nw, u, L1, bbase, hs, acc);
         }
-        // pass 1b: heavy in-rows by static pieces; partial ORs meet in nxt[u].  32 pieces are
-        // tested per warp (row still has bits to find), then each live piece is scanned by the
-        // warp 32 in-edges per round trip.  Bits already found by earlier pieces of the row
-        // (pieces are stored piece-major: all first pieces, then all second pieces, ...) are
-        // not looked for again.
-        for (uint32_t pb = gwarp * 32; pb < st.n_hp_in; pb += nwarps * 32) {
-          const uint32_t pc = pb + lane;
-          uint32_t u = 0;
-          bool live = false;
-          if (pc < st.n_hp_in) {
-            u = ld_nc(p.hin_v + pc);
-            const Word<W> sn = wload<W>(p.seen, u), have = wload_cg<W>(p.nxt, u);
+        // pass 1b: heavy in-rows by static pieces; partial ORs meet in nxt[u]
+        for (uint32_t pc = gwarp; pc < st.n_hp_in; pc += nwarps) {
+          const uint32_t u = ld_nc(p.hin_v + pc);
+          // bits already found by earlier pieces of this row (pieces are stored piece-major:
+          // all first pieces, then all second pieces, ...) need not be looked for again
+          const Word<W> sn = wload<W>(p.seen, u), have = wload_cg<W>(p.nxt, u);
+          Word<W> U;
 #pragma unroll
-            for (int i = 0; i < W; ++i) live = live || (~sn.w[i] & active.w[i] & ~have.w[i]) != 0;
-          }
-          uint32_t lm = __ballot_sync(DAWN_FULL, live);
-          while (lm) {
-            const uint32_t k = __ffs(lm) - 1;
-            lm &= lm - 1;
-            const uint32_t uk = __shfl_sync(DAWN_FULL, u, k), pk = pb + k;
-            const Word<W> sn = wload<W>(p.seen, uk), have = wload_cg<W>(p.nxt, uk);
-            Word<W> U;
-#pragma unroll
-            for (int i = 0; i < W; ++i) U.w[i] = ~sn.w[i] & active.w[i] & ~have.w[i];
-            if (!wany<W>(U)) continue;
-            const uint32_t s = ld_nc(p.hin_s + pk), e = ld_nc(p.hin_e + pk);
-            Word<W> a = wzero<W>();
-            for (uint32_t j = s; j < e; j += 32) {
-              Word<W> f = wzero<W>();
-              if (j + lane < e) f = wload<W>(Fc, (uint32_t)ld_nc(p.icol + j + lane));
-              bool cov = true;
-#pragma unroll
-              for (int i = 0; i < W; ++i) {
-                unsigned long long x = f.w[i];
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) x |= __shfl_xor_sync(DAWN_FULL, x, o);
-                a.w[i] |= x;
-                cov = cov && (a.w[i] & U.w[i]) == U.w[i];
-              }
-              if (cov) break;
-            }
+          for (int i = 0; i < W; ++i) U.w[i] = ~sn.w[i] & active.w[i] & ~have.w[i];
+          if (!wany<W>(U)) continue;
+          const uint32_t s = ld_nc(p.hin_s + pc), e = ld_nc(p.hin_e + pc);
+          Word<W> a = wzero<W>();
+          for (uint32_t j = s; j < e; j += 32) {
+            Word<W> f = wzero<W>();
+            if (j + lane < e) f = wload<W>(Fc, (uint32_t)ld_nc(p.icol + j + lane));
+            bool cov = true;
 #pragma unroll
             for (int i = 0; i < W; ++i) {
-              const unsigned long long x = a.w[i] & U.w[i];
-              if (lane == (uint32_t)i && x) red_or64(p.nxt + (size_t)uk * W + i, x);
+              unsigned long long x = f.w[i];
+#pragma unroll
+              for (int o = 16; o > 0; o >>= 1) x |= __shfl_xor_sync(DAWN_FULL, x, o);
+              a.w[i] |= x;
+              cov = cov && (a.w[i] & U.w[i]) == U.w[i];
             }
+            if (cov) break;
+          }
+#pragma unroll
+          for (int i = 0; i < W; ++i) {
+            const unsigned long long x = a.w[i] & U.w[i];
+            if (lane == (uint32_t)i && x) red_or64(p.nxt + (size_t)u * W + i, x);
           }
         }
         grid_sync(&C->bar, nblocks, bar_target);

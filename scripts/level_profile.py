@@ -19,7 +19,11 @@ for v in variants:
         e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
         e0.record(); d, st = dawn.sssp(G, int(s), v, stats=True); e1.record(); torch.cuda.synchronize()
         ts.append(e0.elapsed_time(e1)); sd = dawn.stats_to_dict(st); er += sd["edges_reach"]
-        traces.append((ts[-1], int(s), sd, G.trace() if os.environ.get('TRACE', '1') == '1' else None))
+        trr = G.trace() if os.environ.get('TRACE', '1') == '1' else None
+        if trr is not None and os.environ.get("PROF"):
+            G.trace_raw = trr
+            trr = trr[: sd["levels"] + 1]
+        traces.append((ts[-1], int(s), sd, trr))
     print(f"== {cfg} {v}: median {np.median(ts)*1e3:.1f} us mean {np.mean(ts)*1e3:.1f} max {np.max(ts)*1e3:.1f}  GTEPS(agg) {er/(sum(ts)*1e-3)/1e9:.1f}")
     print("   per-source us:", [round(x * 1e3) for x in ts])
     for label, (tt, s, sd, tr) in (("median", sorted(traces, key=lambda x: x[0])[len(traces)//2]), ("slowest", max(traces, key=lambda x: x[0]))):
@@ -33,6 +37,14 @@ for v in variants:
             rows = tr
         for r in rows:
             f = lambda x: round((int(x) - t0) / 1e3, 1) if 0 < int(x) < 2**63 else None
+            if r["rep"] & 8:  # k_narrow level: CTA-0 work / cluster-barrier wait / max-CTA work, us
+                print("   L%d NARROW nf=%d mf=%d start=%s  [work0 sync0 maxwork] us = [%s]" % (
+                    r["level"], r["nf"], r["mf"], f(r["t_ns"]), " ".join("%.2f" % (c / CLK) for c in r["cyc"][:3])))
+                if os.environ.get("PROF"):
+                    r2 = G.trace_raw[r["level"] + 32768]
+                    raw = np.array([r2["t_first"], r2["t_last"], r2["cyc"][0], r2["cyc"][1], r2["cyc"][2], r2["cyc"][3]], dtype=np.uint64).view(np.uint32)
+                    print("      stamps (cyc from start) entry/arc/claim/append/sums/sync/exch/barrier/next:", list(raw[:9]), "rank", raw[9])
+                continue
             solo = bool(r["rep"] & 2)
             div = 16 if solo else nw
             cyc = " ".join("%.1f" % (c / div / CLK) for c in r["cyc"])

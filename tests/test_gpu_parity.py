@@ -269,7 +269,22 @@ def test_narrow_kernel_and_handover():
     for g in (rand, tree, grid):
         assert g.m <= 6 * g.n
         G = dev_graph(g)
+        G.set_tuning(narrow_avg_degree=6)
         srcs = [0, 1, g.n // 2, g.n - 1]
         check_sssp(g, G, srcs, variants=("auto", "push"))
         G.set_tuning(narrow_avg_degree=0)                          # grid-wide kernel only
         check_sssp(g, G, srcs[:2], variants=("auto",))
+
+
+def test_narrow_forced_handover(monkeypatch):
+    # tiny shared-memory queues (DAWN_NARROW_QCAP, read at load) make every wide-enough level
+    # overflow: hand-over to k_sssp from the frontier bitmap at many different levels
+    monkeypatch.setenv("DAWN_NARROW_QCAP", "40")
+    rng = np.random.default_rng(12)
+    n = 50_000
+    rand = graphgen.from_edges(n, rng.integers(0, n, size=(n, 2)), symmetric=True)
+    dirg = graphgen.from_edges(n, rng.integers(0, n, size=(3 * n, 2)))
+    for g in (graphgen.grid(300, 200), rand, dirg):
+        G = dev_graph(g)
+        srcs = [0, g.n // 3, g.n - 1] + list(g.sample_sources(3, seed=3))
+        check_sssp(g, G, srcs, variants=("auto", "push"))
