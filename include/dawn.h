@@ -142,19 +142,25 @@ dawn_status dawn_graph_destroy(dawn_graph g);
  *                     instead of one returning atomic per arc.  Default 262144.
  *   DAWN_PARAM_SOLO_EDGES  push levels with <= this many arcs run on one CTA with block-level
  *                     barriers only.  Default 512.
- *   DAWN_PARAM_NARROW_AVG_DEGREE  graphs with m <= value * n (high-diameter shapes: grids,
- *                     road networks; only when m <= 8 n and n <= 20,971,520, the graphs for which
- *                     the load keeps k_narrow's augmented arc array) start each dawn_sssp on ONE
- *                     16-CTA thread-block cluster with the visited bitmap and the frontier queues
- *                     in distributed shared memory, handing over to the grid-wide kernel if a
- *                     frontier outgrows the shared-memory queues.  0 disables.  Default 6.     */
+ *   DAWN_PARAM_CLUSTER_START  1: every push/auto dawn_sssp on a graph with n <= 20,971,520
+ *                     starts on ONE 16-CTA thread-block cluster with the visited bitmap and the
+ *                     frontier queues in distributed shared memory (k_narrow), and hands over to
+ *                     the grid-wide kernel when a queue overflows or the next frontier's rows
+ *                     exceed DAWN_PARAM_CLUSTER_HANDOVER_EDGES arcs.  0: grid-wide kernel only.
+ *                     Default (set at load): 1 when at least half of the sampled arcs join
+ *                     vertices whose visited words live in the same CTA (meshes, road networks:
+ *                     ids follow space), else 0.
+ *   DAWN_PARAM_CLUSTER_HANDOVER_EDGES  see above.  Default: unlimited for the local graphs
+ *                     above (the cluster keeps the whole search), else 1024.  Values >= 1.8e19
+ *                     mean unlimited.                                                          */
 typedef enum {
   DAWN_PARAM_ALPHA = 0,
   DAWN_PARAM_BETA = 1,
   DAWN_PARAM_MS_ALPHA = 2,
   DAWN_PARAM_BITMAP_PUSH_EDGES = 3,
   DAWN_PARAM_SOLO_EDGES = 4,
-  DAWN_PARAM_NARROW_AVG_DEGREE = 5
+  DAWN_PARAM_CLUSTER_START = 5,
+  DAWN_PARAM_CLUSTER_HANDOVER_EDGES = 6
 } dawn_param;
 
 /* Set one tunable (INVALID_ARGUMENT for an unknown key or a negative value). */
@@ -206,8 +212,11 @@ dawn_status dawn_apsp(dawn_graph g, const int64_t *sources, int64_t k, int32_t r
                       dawn_record *rec, int64_t cap, int64_t *n_written, void *stream);
 
 /* Copy the per-level trace of the last dawn_sssp call (graph loaded with DAWN_GRAPH_TRACE)
- * into host_out[0 .. min(cap, levels+1)); *count receives the number of records.  Synchronises
- * `stream`.  CONFIG if the graph was loaded without DAWN_GRAPH_TRACE.                        */
+ * into host_out[0 .. min(cap, levels+1)); *count receives the number of records.  With
+ * cap >= DAWN_TRACE_CAP, host_out[DAWN_TRACE_CAP - 1] also receives the grid-wide kernel's
+ * timeline record (t_ns = kernel entry, t_first = initialisation done, t_last = last level
+ * done).  Synchronises `stream`.  CONFIG if the graph was loaded without DAWN_GRAPH_TRACE.   */
+#define DAWN_TRACE_CAP 65536
 dawn_status dawn_graph_trace(dawn_graph g, dawn_trace_rec *host_out, int64_t cap, int64_t *count,
                              void *stream);
 

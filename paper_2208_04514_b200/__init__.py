@@ -178,14 +178,15 @@ class Graph:
         cnt = ctypes.c_int64(0)
         _check(lib().dawn_graph_trace(self._h, buf.ctypes.data_as(ctypes.c_void_p), len(buf),
                                       ctypes.byref(cnt), _stream(stream)))
-        return buf[: min(cnt.value, len(buf))].copy()
+        self.timeline = buf[-1].copy()  # (t_ns: k_sssp entry, t_first: init done, t_last: end)
+        return buf[: min(cnt.value, len(buf) - 1)].copy()
 
     _PARAMS = {"alpha": 0, "beta": 1, "ms_alpha": 2, "bitmap_push_edges": 3, "solo_edges": 4,
-               "narrow_avg_degree": 5}
+               "cluster_start": 5, "cluster_handover_edges": 6}
 
     def set_tuning(self, **kw):
         """dawn_graph_set_param for each keyword (alpha, beta, ms_alpha, bitmap_push_edges,
-        solo_edges, narrow_avg_degree).  Speed only; results never change."""
+        solo_edges, cluster_start, cluster_handover_edges).  Speed only; results never change."""
         for k, v in kw.items():
             _check(lib().dawn_graph_set_param(self._h, self._PARAMS[k], float(v)))
 

@@ -256,6 +256,26 @@ __global__ void k_hfill(const uint32_t *__restrict__ rp, uint32_t n, const uint3
   }
 }
 
+// ---- id locality of the graph: arcs (v, u) whose visited words have the same owner CTA in
+// k_narrow (word mod 16), over the rows of the first 2^20 vertices (untimed, at load)
+__global__ void k_locality(const uint32_t *__restrict__ rp, const int32_t *__restrict__ col,
+                           uint32_t nv, unsigned long long *cnt) {
+  unsigned long long same = 0, tot = 0;
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < nv; v += gridDim.x * blockDim.x) {
+    const uint32_t s = rp[v], e = min(rp[v + 1], rp[v] + 64u);
+    for (uint32_t j = s; j < e; ++j) {
+      same += (((uint32_t)col[j] >> 5) % kNarrowCluster) == ((v >> 5) % kNarrowCluster);
+      ++tot;
+    }
+  }
+  same = warp_sum(same);
+  tot = warp_sum(tot);
+  if ((threadIdx.x & 31) == 0 && tot) {
+    atomicAdd(cnt, same);
+    atomicAdd(cnt + 1, tot);
+  }
+}
+
 // ---- k_narrow's augmented arcs: arc[j] = (col[j], row_ptr[col[j]], row_ptr[col[j] + 1], 0)
 __global__ void k_arcs(const int32_t *__restrict__ col, const uint32_t *__restrict__ rp, int64_t m,
                        uint4 *__restrict__ arc) {
@@ -283,11 +303,12 @@ struct dawn_graph_s {
   size_t small_cap;  // max dynamic smem for k_small (0 = disabled)
   uint32_t bmpush_e = 1u << 18, solo_e = 512;
   uint32_t n_hasin = 0;
-  float narrow_deg = 6.f;  // k_narrow first when m <= narrow_deg * n (high-diameter shapes)
-  bool narrow_ok = false;  // arc array built and a 16-CTA cluster fits
+  bool cluster_start = false;     // DAWN_PARAM_CLUSTER_START (default set at load)
+  unsigned long long handover_m = 0;  // DAWN_PARAM_CLUSTER_HANDOVER_EDGES (set at load)
+  bool narrow_owner = false;     // owner-computes queues (ids local: most arcs stay in a CTA)
+  bool narrow_ok = false;        // the visited bitmap fits 16 CTAs and the cluster launches
   uint32_t narrow_wpc = 0, narrow_qcap = 0, narrow_grid = 0;
   size_t narrow_smem = 0;
-  unsigned long long narrow_calls = 0;
   uint32_t seq = 0;
 };
 
@@ -381,7 +402,7 @@ dawn_status dawn_graph_load_csr(int64_t n, int64_t m, const int64_t *row_ptr, co
     // k_narrow: visited slice of ceil(nwords / 16) words (multiple of 4) per CTA, the rest of
     // the shared memory holds the two frontier queues
     g->narrow_ok = false;
-    if (L.arc && env_int("DAWN_NARROW", 1)) {
+    if ((uint64_t)n <= kNarrowMaxN && m > 0 && env_int("DAWN_NARROW", 1)) {
       const uint32_t nw = (uint32_t)((n + 31) / 32);
       const uint32_t wpc = ((nw + kNarrowCluster - 1) / kNarrowCluster + 3) & ~3u;
       const size_t fixed = narrow_smem_bytes(wpc, 0);
@@ -505,10 +526,27 @@ dawn_status dawn_graph_load_csr(int64_t n, int64_t m, const int64_t *row_ptr, co
   }
   if (L.arc)
     k_arcs<<<g->nsm * 8, 256, 0, st>>>(col, at<uint32_t>(g, L.rp), m, at<uint4>(g, L.arc));
+  unsigned long long loc[2] = {0, 0};
+  if (g->narrow_ok) {
+    unsigned long long *dcnt = at<unsigned long long>(g, L.part);  // scratch (ms64 partials)
+    cudaMemsetAsync(dcnt, 0, 16, st);
+    k_locality<<<g->nsm * 4, 256, 0, st>>>(at<uint32_t>(g, L.rp), col,
+                                             (uint32_t)std::min<int64_t>(n, 1 << 20), dcnt);
+    cudaMemcpyAsync(loc, dcnt, 16, cudaMemcpyDeviceToHost, st);
+  }
   uint32_t nh = 0;
   cudaMemcpyAsync(&nh, &at<Ctrl>(g, L.ctrl)->n_hasin, 4, cudaMemcpyDeviceToHost, st);
   if ((e = cudaStreamSynchronize(st)) != cudaSuccess) { delete g; return cuda_fail(e, "graph load"); }
   g->n_hasin = nh;
+  // owner computes when at least half of the sampled arcs stay within a CTA (meshes, road
+  // networks: ~97% on the 4096^2 grid); then the cluster keeps the whole search unless a queue
+  // overflows.  Otherwise the cluster only runs the narrow first levels (frontier rows totalling
+  // <= 1024 arcs) and hands the wide ones to the grid-wide kernel.
+  g->narrow_owner = loc[1] > 0 && 2 * loc[0] >= loc[1];
+  g->handover_m = g->narrow_owner ? ~0ull : 1024ull;
+  // Other graphs start on the grid-wide kernel by default: their narrow first levels are a
+  // few microseconds, less than the extra kernel boundary (measured on Kronecker-20: +6 us).
+  g->cluster_start = g->narrow_owner;
   if ((e = cudaGetLastError()) != cudaSuccess) { delete g; return cuda_fail(e, "graph load"); }
   *out = g;
   return DAWN_OK;
@@ -529,7 +567,10 @@ dawn_status dawn_graph_set_param(dawn_graph g, dawn_param key, double value) {
     case DAWN_PARAM_MS_ALPHA: g->ms_alpha = (float)value; break;
     case DAWN_PARAM_BITMAP_PUSH_EDGES: g->bmpush_e = (uint32_t)std::min(value, 4294967295.0); break;
     case DAWN_PARAM_SOLO_EDGES: g->solo_e = (uint32_t)std::min(value, 4294967295.0); break;
-    case DAWN_PARAM_NARROW_AVG_DEGREE: g->narrow_deg = (float)value; break;
+    case DAWN_PARAM_CLUSTER_START: g->cluster_start = value != 0; break;
+    case DAWN_PARAM_CLUSTER_HANDOVER_EDGES:
+      g->handover_m = value >= 1.8e19 ? ~0ull : (unsigned long long)value;
+      break;
     default: return fail(DAWN_ERR_INVALID_ARGUMENT, "unknown parameter");
   }
   return DAWN_OK;
@@ -595,17 +636,19 @@ dawn_status dawn_sssp(dawn_graph g, int64_t source, uint32_t variant, uint32_t *
   p.bmpush_e = g->bmpush_e;
   p.solo_e = g->solo_e;
   p.seq = ++g->seq;
-  if (variant != DAWN_PULL && g->narrow_ok &&
-      (double)g->m <= (double)g->narrow_deg * (double)g->n) {
-    // high-diameter shape: the search starts on one 16-CTA cluster (state in distributed
-    // shared memory); k_sssp below resumes from its hand-over or exits at once
+  if (variant != DAWN_PULL && g->narrow_ok && g->cluster_start) {
+    // the search starts on one 16-CTA cluster (state in distributed shared memory); k_sssp
+    // below resumes from its hand-over (wide frontier or full queue) or exits at once
     NarrowParams np{};
     np.n = p.n;
     np.nwords = p.nwords;
     np.wpc = g->narrow_wpc;
     np.qcap = g->narrow_qcap;
     np.rp = p.rp;
-    np.arc = at<uint4>(g, L.arc);
+    np.arc = L.arc ? at<uint4>(g, L.arc) : nullptr;
+    np.col = g->col;
+    np.owner = g->narrow_owner ? 1u : 0u;
+    np.handover_m = g->handover_m;
     np.noin = p.noin;
     np.vis = p.vis;
     np.dist = dist;
@@ -616,7 +659,6 @@ dawn_status dawn_sssp(dawn_graph g, int64_t source, uint32_t variant, uint32_t *
     np.source = (uint32_t)source;
     np.max_reach_base = g->n_hasin;
     np.seq = p.seq;
-    np.fill_target = ++g->narrow_calls * (unsigned long long)g->narrow_grid;
     np.trace = p.trace;
     cudaLaunchConfig_t cfg{};
     cudaLaunchAttribute attr[1];
@@ -727,6 +769,12 @@ dawn_status dawn_graph_trace(dawn_graph g, dawn_trace_rec *host_out, int64_t cap
   static_assert(sizeof(dawn_trace_rec) == sizeof(TraceRec), "trace record layout");
   if (k > 0) {
     e = cudaMemcpy(host_out, g->ws + g->L.trace, sizeof(TraceRec) * k, cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return cuda_fail(e, "trace copy");
+  }
+  static_assert(DAWN_TRACE_CAP == kTraceCap, "dawn.h DAWN_TRACE_CAP");
+  if (cap >= kTraceCap) {
+    e = cudaMemcpy(host_out + (kTraceCap - 1), g->ws + g->L.trace + sizeof(TraceRec) * (kTraceCap - 1),
+                   sizeof(TraceRec), cudaMemcpyDeviceToHost);
     if (e != cudaSuccess) return cuda_fail(e, "trace copy");
   }
   *count = nrec;

@@ -46,6 +46,12 @@ static_assert(kMsBatch == DAWN_MS_BATCH, "dawn.h DAWN_MS_BATCH must match kMsW")
 #ifndef DAWN_SSSP_MINB
 #define DAWN_SSSP_MINB 2  // __launch_bounds__ min blocks of k_sssp: 2 x 16 warps per SM (64 regs)
 #endif
+#ifndef DAWN_PULL_DEEP_PR
+#define DAWN_PULL_DEEP_PR 8  // in-edges probed per lane per round trip on sparse frontiers
+#endif
+#ifndef DAWN_PULL_PR
+#define DAWN_PULL_PR 4       // ... on dense frontiers
+#endif
 #ifndef DAWN_PULL_J
 #define DAWN_PULL_J 2  // vis words per warp iteration of the pull sweep (independent scans)
 #endif

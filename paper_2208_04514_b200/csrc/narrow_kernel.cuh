@@ -64,13 +64,15 @@ struct NarrowParams {
   uint32_t wpc;     // visited words per CTA (word w lives in CTA w % 16 at index w / 16)
   uint32_t qcap;    // queue entries per buffer per CTA
   const uint32_t *rp;
-  const uint4 *arc;  // (target, target row start, target row end, 0) per arc
+  const uint4 *arc;  // (target, target row start, target row end, 0) per arc, or NULL:
+  const int32_t *col;  //   then targets come from col and their rows from rp (two round trips)
+  uint32_t owner;      // 1: owner computes (mesh-like ids); 0: a CTA queues what it discovers
+  unsigned long long handover_m;  // hand over once the next frontier has more arcs than this
   const uint32_t *noin;
   uint32_t *vis, *dist, *fb0, *fb1;
   Ctrl *ctrl;
   dawn_sssp_stats *stats;
   uint32_t source, max_reach_base, seq;  // max_reach_base = #vertices with an in-edge
-  unsigned long long fill_target;  // narrow_fill value once this call's fill is complete
   TraceRec *trace;                 // per-level trace (DAWN_GRAPH_TRACE) or NULL
 };
 
@@ -79,6 +81,7 @@ struct NarrowParams {
 // queue entry = (vertex, row start, row end, discoverer | staged << 31); a "staged" entry's
 // arcs (rows of <= kNarrowStage arcs) were copied into its row-arcs slot by cp.async in the
 // level that discovered it, so expanding it needs no global load.
+constexpr uint32_t kNarrowBig = 64;  // long rows per CTA per level listed for CTA-wide expansion
 struct NarrowCtl {
   unsigned long long rbase[kNarrowCluster];  // generic address of CTA r's shared window
   uint32_t qn[2];                 // entries appended to this CTA's queue b (may exceed qcap)
@@ -88,6 +91,8 @@ struct NarrowCtl {
   // slot [b][r] = (CTA r's discoveries | overflow << 31, their out-degree sum)
   uint2 x[2][kNarrowCluster];
   unsigned long long mbar[2];     // level barrier b = L & 1 (phase parity (L >> 1) & 1)
+  uint32_t nbig;                  // rows of > 16 arcs this level (expanded by the whole CTA)
+  uint4 big[kNarrowBig];          // (vertex, row start, row end, discoverer)
 };
 constexpr size_t kNarrowCtlBytes = (sizeof(NarrowCtl) + 255) & ~size_t(255);
 
@@ -142,9 +147,6 @@ __device__ __forceinline__ void prefetch_row_l2(const uint4 *p, uint32_t n) {
   const uint32_t bytes = 16u * min(n, 256u);
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
-__device__ __forceinline__ void red_add64_gpu(unsigned long long *p, unsigned long long v) {
-  asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
   return (uint32_t)__cvta_generic_to_shared(p);
 }
@@ -169,6 +171,15 @@ __device__ __forceinline__ T *remote(const NarrowCtl &S, uint32_t r, size_t off)
   return reinterpret_cast<T *>(S.rbase[r] + off);
 }
 
+// Arc j as (target, target row start, target row end): one load from the augmented arc array,
+// else col then row_ptr (two dependent loads).
+__device__ __forceinline__ uint4 narrow_arc(const NarrowParams &p, uint32_t j) {
+  if (p.arc) return ld_nc4(p.arc + j);
+  const uint32_t u = (uint32_t)ld_nc(p.col + j);
+  const uint2 r = make_uint2(ld_nc(p.rp + u), ld_nc(p.rp + u + 1));
+  return make_uint4(u, r.x, r.y, 0u);
+}
+
 // One arc per lane, of the row of frontier vertex `parent` (whose own discoverer is `skip`):
 // claim the target (shared-memory atomic OR on its visited word when this CTA owns the word,
 // DSMEM atomic otherwise), write its distance, and append it to its owner's next queue.
@@ -184,7 +195,8 @@ __device__ __forceinline__ void narrow_visit(const NarrowParams &p, NarrowCtl &S
                                              uint32_t &n_new, uint32_t &m_new) {
   act = act && a.x != skip;  // the row owner's discoverer is visited: skip that arc
   const uint32_t w = a.x >> 5, o = w % kNarrowCluster, bit = 1u << (a.x & 31);
-  const bool loc = o == rank;
+  const bool loc = o == rank;           // claim in this CTA's visited slice
+  const bool qloc = loc || !p.owner;    // append to this CTA's queue
   uint32_t old = ~0u;
   if (act) {
     old = loc ? atomicOr(vis_s + w / kNarrowCluster, bit)
@@ -201,14 +213,14 @@ __device__ __forceinline__ void narrow_visit(const NarrowParams &p, NarrowCtl &S
     n_new += 1;
     m_new += d;
   }
-  const uint32_t bl = __ballot_sync(DAWN_FULL, put && loc);
+  const uint32_t bl = __ballot_sync(DAWN_FULL, put && qloc);
   if (bl) {
     uint32_t base = 0;
     if (lane_id() == 0) base = atomicAdd(&S.qn[nxt], (uint32_t)__popc(bl));
     const uint32_t slot = __shfl_sync(DAWN_FULL, base, 0) + __popc(bl & lanemask_lt());
-    if (put && loc) {
+    if (put && qloc) {
       if (slot < p.qcap) {
-        const bool stage = d <= kNarrowStage;
+        const bool stage = p.arc && d <= kNarrowStage;
         qn_buf[slot] = make_uint4(a.x, a.y, a.z, parent | (stage ? 0x80000000u : 0u));
         if (stage) {
           const uint32_t dst =
@@ -218,7 +230,7 @@ __device__ __forceinline__ void narrow_visit(const NarrowParams &p, NarrowCtl &S
             if (i < d)
               asm volatile("cp.async.cg.shared.global [%0], [%1], 16;"
                            ::"r"(dst + 16 * i), "l"(p.arc + a.y + i) : "memory");
-        } else {
+        } else if (p.arc) {
           prefetch_row_l2(p.arc + a.y, d);
         }
       } else {
@@ -227,14 +239,14 @@ __device__ __forceinline__ void narrow_visit(const NarrowParams &p, NarrowCtl &S
       }
     }
   }
-  if (put && !loc) {
+  if (put && !qloc) {
     const uint32_t s2 = atomicAdd(remote<uint32_t>(S, o, offsetof(NarrowCtl, qn) + 4 * nxt), 1u);
     if (s2 < p.qcap) {
       uint32_t *e = remote<uint32_t>(S, o, qnxt_off + 16 * (size_t)s2);
       const uint32_t r0 = atomicExch(e, a.x), r1 = atomicExch(e + 1, a.y);
       const uint32_t r2 = atomicExch(e + 2, a.z), r3 = atomicExch(e + 3, parent);
       if ((r0 ^ r1 ^ r2 ^ r3) == 0x9e3779b9u) S.pad = 1;  // consume the results
-      prefetch_row_l2(p.arc + a.y, d);
+      if (p.arc) prefetch_row_l2(p.arc + a.y, d);
     } else {
       red_or(p.fb0 + (a.x >> 5), bit);
       S.ovf = 1;
@@ -259,8 +271,8 @@ __global__ void __launch_bounds__(kNarrowThreads, 1) k_narrow(NarrowParams p) {
     p.fb0[w] = 0;
     p.fb1[w] = 0;
   }
-  if (p.trace) {
-    const uint32_t ntr = min(p.n + 1, kTraceCap);
+  if (p.trace) {  // every record k_narrow may use (it runs at most n levels)
+    const uint32_t ntr = min(p.n + 1, kTraceCap - 1);
     for (uint32_t i = gtid; i < ntr; i += nthreads) {
       p.trace[i].t_first = ~0ull;
       p.trace[i].t_last = 0;
@@ -268,7 +280,15 @@ __global__ void __launch_bounds__(kNarrowThreads, 1) k_narrow(NarrowParams p) {
     }
   }
   __syncthreads();
-  if (tid == 0) red_add64_gpu(&C->narrow_fill, 1ull);
+  // fill ticket: every launch of this graph handle adds exactly gridDim.x, so the launch owning
+  // ticket t is complete once the counter reaches (t / gridDim.x + 1) * gridDim.x (no host-side
+  // epoch: the launch stays correct when replayed from a CUDA graph)
+  unsigned long long fill_target = 0;
+  if (tid == 0) {
+    __threadfence();
+    const unsigned long long t = atomicAdd(&C->narrow_fill, 1ull);
+    fill_target = (t / gridDim.x + 1) * (unsigned long long)gridDim.x;
+  }
   if (cluster_id_x() != 0) return;
 
   // ---- cluster 0: visited slice <- no-in-edge | {s}; the source entry in CTA 0's queue 0
@@ -292,11 +312,12 @@ __global__ void __launch_bounds__(kNarrowThreads, 1) k_narrow(NarrowParams p) {
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     S.qn[0] = S.qn[1] = 0;
     S.n_new = S.m_new = S.ovf = 0;
+    S.nbig = 0;
     if (((src >> 5) % kNarrowCluster) == rank && re0 > rs0) {  // the source's owner queues it
       qbuf0[0] = make_uint4(src, rs0, re0, 0x7fffffffu);
       S.qn[0] = 1;
     }
-    while (ld_acquire64(&C->narrow_fill) < p.fill_target) {
+    while (ld_acquire64(&C->narrow_fill) < fill_target) {
     }
     fence_acq_rel_gpu();
   }
@@ -350,7 +371,7 @@ __global__ void __launch_bounds__(kNarrowThreads, 1) k_narrow(NarrowParams p) {
       for (uint32_t k = k0; __any_sync(DAWN_FULL, !big && k < d); k += 4) {
         const bool act = !big && k < d;
         const uint4 a = !act ? make_uint4(0u, 0u, 0u, 0u)
-                        : staged ? acur[(size_t)g * kNarrowStage + k] : ld_nc4(p.arc + e.y + k);
+                        : staged ? acur[(size_t)g * kNarrowStage + k] : narrow_arc(p, e.y + k);
 #if DAWN_NARROW_PROF
         if (prof && base == 0 && lane == 0 && ts[2] == 0) {
           uint32_t x = a.x;
@@ -364,36 +385,57 @@ __global__ void __launch_bounds__(kNarrowThreads, 1) k_narrow(NarrowParams p) {
         if (prof && base == 0 && lane == 0 && ts[4] == 0) ts[4] = ts[3] = clock64();
 #endif
       }
+      // rows of > 16 arcs: listed for the CTA-wide pass below (a row beyond the list's
+      // capacity is expanded by this warp alone)
       uint32_t bm = __ballot_sync(DAWN_FULL, big && k0 == 0);
       while (bm) {
         const uint32_t k = __ffs(bm) - 1;
         bm &= bm - 1;
-        const uint32_t s = __shfl_sync(DAWN_FULL, e.y, k), t = __shfl_sync(DAWN_FULL, e.z, k);
-        const uint32_t par = __shfl_sync(DAWN_FULL, e.x, k);
-        const uint32_t skp = __shfl_sync(DAWN_FULL, skip, k);
-        for (uint32_t jj = s; jj < t; jj += 32) {
-          const bool act = jj + lane < t;
-          const uint4 a = act ? ld_nc4(p.arc + jj + lane) : make_uint4(0u, 0u, 0u, 0u);
-          narrow_visit(p, S, vis_s, rank, L1, nxt, qnxt_off, qnxt, anxt, a, act, par, skp, n_new,
+        const uint4 eb = make_uint4(__shfl_sync(DAWN_FULL, e.x, k), __shfl_sync(DAWN_FULL, e.y, k),
+                                    __shfl_sync(DAWN_FULL, e.z, k), __shfl_sync(DAWN_FULL, skip, k));
+        uint32_t slot = 0;
+        if (lane == 0) slot = atomicAdd(&S.nbig, 1u);
+        slot = __shfl_sync(DAWN_FULL, slot, 0);
+        if (slot < kNarrowBig) {
+          if (lane == 0) S.big[slot] = eb;
+          continue;
+        }
+        for (uint32_t jj = eb.y; jj < eb.z; jj += 32) {
+          const bool act = jj + lane < eb.z;
+          const uint4 a = act ? narrow_arc(p, jj + lane) : make_uint4(0u, 0u, 0u, 0u);
+          narrow_visit(p, S, vis_s, rank, L1, nxt, qnxt_off, qnxt, anxt, a, act, eb.x, eb.w, n_new,
                        m_new);
         }
       }
     }
-    // ---- level totals: warp reductions, then this CTA's slot of every CTA's exchange arrays
-    if (nq > warp * 8) {
+    // ---- level totals: warp reductions into this CTA's counters
+    auto fold = [&]() {
       n_new = __reduce_add_sync(DAWN_FULL, n_new);
       m_new = __reduce_add_sync(DAWN_FULL, m_new);
       if (lane == 0 && n_new) {
         atomicAdd(&S.n_new, n_new);
         atomicAdd(&S.m_new, m_new);
       }
+      n_new = m_new = 0;
+    };
+    fold();
+    __syncthreads();
+    if (S.nbig) {  // uniform after the barrier: listed long rows, one arc per thread per round
+      const uint32_t nb = min(S.nbig, kNarrowBig);
+      for (uint32_t b = 0; b < nb; ++b) {
+        const uint4 eb = S.big[b];
+        for (uint32_t j0 = eb.y + warp * 32; j0 < eb.z; j0 += kNarrowThreads) {
+          const bool act = j0 + lane < eb.z;
+          const uint4 a = act ? narrow_arc(p, j0 + lane) : make_uint4(0u, 0u, 0u, 0u);
+          narrow_visit(p, S, vis_s, rank, L1, nxt, qnxt_off, qnxt, anxt, a, act, eb.x, eb.w, n_new,
+                       m_new);
+        }
+      }
+      fold();
+      __syncthreads();
     }
 #if DAWN_NARROW_PROF
-    if (prof) ts[5] = clock64();
-#endif
-    __syncthreads();
-#if DAWN_NARROW_PROF
-    if (prof) ts[6] = clock64();
+    if (prof) ts[5] = ts[6] = clock64();
 #endif
     long long tc1 = 0;
     if (p.trace && tid == 0) {
@@ -411,6 +453,7 @@ __global__ void __launch_bounds__(kNarrowThreads, 1) k_narrow(NarrowParams p) {
       // (peers append to it only after this level's barrier, which needs this CTA's slot)
       if (lane == 31) {
         S.n_new = S.m_new = S.ovf = 0;  // this level's local totals are sent below
+        S.nbig = 0;
         S.qn[cur] = 0;
       }
       __syncwarp();
@@ -476,8 +519,9 @@ __global__ void __launch_bounds__(kNarrowThreads, 1) k_narrow(NarrowParams p) {
     ++L;
     cur = nxt;
     if (reached + 1 >= max_reach || L + 1 >= p.n) { ecc = L; break; }  // condition 1 / Q8
-    if (O) {
-      // ---- hand over frontier L (queues + overflow bitmap) to k_sssp
+    if (O || M > p.handover_m) {
+      // ---- hand over frontier L (queues + overflow bitmap) to k_sssp: a queue overflowed, or
+      // the frontier is wide enough for the grid-wide kernel (push or pull by its own rule)
       const uint32_t nq2 = min(S.qn[cur], p.qcap);
       const uint4 *q2 = qbuf0 + (size_t)cur * p.qcap;
       for (uint32_t i = tid; i < nq2; i += kNarrowThreads) {

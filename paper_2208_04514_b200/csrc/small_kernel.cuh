@@ -35,11 +35,27 @@ __global__ void __launch_bounds__(NT) k_small(SmallParams p) {
   uint32_t *qa = dist + n;        // n
   uint32_t *qb = qa + n;          // n
   uint32_t *vis = qb + n;         // nw
-  __shared__ uint32_t nq_next;
+  __shared__ uint32_t nq_cnt[3];  // level L appends to nq_cnt[L % 3]
   __shared__ unsigned long long m_acc;
-  const uint32_t tid = threadIdx.x;
-  for (uint32_t i = tid; i <= n; i += NT) rp[i] = ld_nc(p.rp + i);
-  for (uint32_t i = tid; i < m; i += NT) col[i] = (uint32_t)ld_nc(p.col + i);
+  const uint32_t tid = threadIdx.x, lane = lane_id();
+  // CSR -> shared memory, 4 independent loads in flight per thread
+  {
+    constexpr int U = 4;
+    for (uint32_t i0 = tid; i0 <= n; i0 += NT * U) {
+      uint32_t v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) v[u] = (i0 + u * NT <= n) ? ld_nc(p.rp + i0 + u * NT) : 0u;
+#pragma unroll
+      for (int u = 0; u < U; ++u) if (i0 + u * NT <= n) rp[i0 + u * NT] = v[u];
+    }
+    for (uint32_t i0 = tid; i0 < m; i0 += NT * U) {
+      uint32_t v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) v[u] = (i0 + u * NT < m) ? (uint32_t)ld_nc(p.col + i0 + u * NT) : 0u;
+#pragma unroll
+      for (int u = 0; u < U; ++u) if (i0 + u * NT < m) col[i0 + u * NT] = v[u];
+    }
+  }
   for (uint32_t i = tid; i < n; i += NT) dist[i] = kUnreached;
   for (uint32_t i = tid; i < nw; i += NT) vis[i] = 0;
   __syncthreads();
@@ -49,32 +65,47 @@ __global__ void __launch_bounds__(NT) k_small(SmallParams p) {
     vis[s >> 5] = 1u << (s & 31);
     qa[0] = s;
     m_acc = rp[s + 1] - rp[s];
+    nq_cnt[0] = nq_cnt[1] = nq_cnt[2] = 0;
   }
   uint32_t nq = 1, L = 0, reached = 0, levels = 0, ecc = 0;
   uint32_t *cur = qa, *nxt = qb;
   __syncthreads();
+  // kLpv lanes per frontier vertex (4 vertices per warp round), one arc per lane per step
+  constexpr uint32_t kLpv = 8;
   for (;;) {
-    if (tid == 0) nq_next = 0;
-    __syncthreads();
-    unsigned long long my_m = 0;
-    // thread per frontier vertex (rows are short at this size; no hub splitting needed)
-    for (uint32_t i = tid; i < nq; i += NT) {
-      const uint32_t v = cur[i];
-      for (uint32_t e = rp[v]; e < rp[v + 1]; ++e) {
-        const uint32_t u = col[e];
-        const uint32_t bit = 1u << (u & 31);
-        if (vis[u >> 5] & bit) continue;
-        if (atomicOr(&vis[u >> 5], bit) & bit) continue;
-        dist[u] = L + 1;
-        nxt[atomicAdd(&nq_next, 1u)] = u;
-        my_m += rp[u + 1] - rp[u];
+    uint32_t *cnt = &nq_cnt[L % 3];
+    if (tid == 0) nq_cnt[(L + 1) % 3] = 0;  // last read two barriers ago
+    uint32_t my_m = 0;
+    for (uint32_t base = (tid / 32) * (32 / kLpv); base < nq; base += (NT / 32) * (32 / kLpv)) {
+      const uint32_t i = base + lane / kLpv;
+      const uint32_t v = i < nq ? cur[i] : 0u;
+      const uint32_t e0 = i < nq ? rp[v] : 0u, e1 = i < nq ? rp[v + 1] : 0u;
+      for (uint32_t e = e0 + lane % kLpv; __any_sync(DAWN_FULL, e < e1); e += kLpv) {
+        bool put = false;
+        uint32_t u = 0;
+        if (e < e1) {
+          u = col[e];
+          const uint32_t bit = 1u << (u & 31);
+          if (!(vis[u >> 5] & bit)) put = !(atomicOr(&vis[u >> 5], bit) & bit);
+        }
+        const uint32_t b = __ballot_sync(DAWN_FULL, put);
+        if (b) {
+          uint32_t base2 = 0;
+          if (lane == 0) base2 = atomicAdd(cnt, (uint32_t)__popc(b));
+          base2 = __shfl_sync(DAWN_FULL, base2, 0);
+          if (put) {
+            dist[u] = L + 1;
+            nxt[base2 + __popc(b & lanemask_lt())] = u;
+            my_m += rp[u + 1] - rp[u];
+          }
+        }
       }
     }
-    my_m = warp_sum(my_m);
-    if (lane_id() == 0 && my_m) atomicAdd(&m_acc, my_m);
+    my_m = __reduce_add_sync(DAWN_FULL, my_m);
+    if (lane == 0 && my_m) atomicAdd(&m_acc, (unsigned long long)my_m);
     __syncthreads();
     ++levels;
-    const uint32_t k = nq_next;
+    const uint32_t k = *cnt;
     if (k == 0) break;
     reached += k;
     ecc = L + 1;
@@ -83,7 +114,6 @@ __global__ void __launch_bounds__(NT) k_small(SmallParams p) {
     cur = nxt;
     nxt = t;
     ++L;
-    __syncthreads();
   }
   for (uint32_t i = tid; i < n; i += NT) p.dist[i] = dist[i];
   if (p.stats && tid == 0) {

@@ -21,6 +21,15 @@
 
 namespace dawn {
 
+#ifndef DAWN_SSSP_NODIST
+#define DAWN_SSSP_NODIST 0  // experiment (WRONG RESULTS): drop the per-level dist stores, timing only
+#endif
+#if DAWN_SSSP_NODIST
+#define DIST_ST(i, v) ((void)0)
+#else
+#define DIST_ST(i, v) (p.dist[i] = (v))
+#endif
+
 struct SsspParams {
   uint32_t n, nwords;
   unsigned long long m;
@@ -195,7 +204,7 @@ __device__ __forceinline__ void push_visit(const SsspParams &p, Slot *ns, int qn
   if (disc) {
     rs = ld_nc(p.rp + u);
     d = ld_nc(p.rp + u + 1) - rs;
-    p.dist[u] = L1;
+    DIST_ST(u, L1);
     n_new += 1;
     m_new += d;
   }
@@ -273,7 +282,7 @@ __device__ __forceinline__ void push_item(const SsspParams &p, const LevelState 
     for (int j = 0; j < J; ++j) {
       if (disc[j]) {
         dd[j] -= rsd[j];
-        p.dist[u[j]] = L1;
+        DIST_ST(u[j], L1);
         n_new += 1;
         m_new += dd[j];
       }
@@ -408,7 +417,7 @@ __device__ void pull_level(const SsspParams &p, const LevelState &st, uint32_t g
       }
       if (found[j]) {
         red_or(fnext + (u[j] >> 5), 1u << (u[j] & 31));
-        p.dist[u[j]] = L1;
+        DIST_ST(u[j], L1);
         n_new += 1;
         m_new += p.sym ? (e[j] - s[j]) : (ld_nc(p.rp + u[j] + 1) - ld_nc(p.rp + u[j]));
       }
@@ -451,7 +460,7 @@ __device__ void pull_level(const SsspParams &p, const LevelState &st, uint32_t g
             const uint32_t old = atomicOr(p.vis + w, bit);
             if (!(old & bit)) {
               red_or(fnext + w, bit);
-              p.dist[uk] = L1;
+              DIST_ST(uk, L1);
               n_new += 1;
               m_new += p.sym ? (ld_nc(p.irp + uk + 1) - ld_nc(p.irp + uk))
                              : (ld_nc(p.rp + uk + 1) - ld_nc(p.rp + uk));
@@ -509,7 +518,7 @@ __device__ void cand_filter(const SsspParams &p, const LevelState &st, uint32_t 
         if (i < k) {
           a[i] = ld_nc(p.rp + u[i]);
           b[i] = ld_nc(p.rp + u[i] + 1);
-          p.dist[u[i]] = L1;
+          DIST_ST(u[i], L1);
         }
 #pragma unroll
       for (int i = 0; i < 4; ++i)
@@ -597,6 +606,11 @@ __device__ __forceinline__ void level_header(const SsspParams &p, Ctrl *C, Level
     for (int k = 0; k < 4; ++k) r.cyc[k] = p.trace[st.L].cyc[k];
     p.trace[st.L] = r;
     C->trace_n = st.L + 1;
+    if (st.L + 1 < kTraceCap - 1) {  // the next level's record (accumulated at its end)
+      p.trace[st.L + 1].t_first = ~0ull;
+      p.trace[st.L + 1].t_last = 0;
+      for (int k = 0; k < 4; ++k) p.trace[st.L + 1].cyc[k] = 0;
+    }
   }
 }
 
@@ -656,6 +670,7 @@ __global__ void __launch_bounds__(NT, DAWN_SSSP_MINB) k_sssp(SsspParams p) {
   // condition 1 bound: only vertices with an in-edge (plus s itself) can ever be reached
   const uint32_t max_reach = ld_cg(&C->n_hasin) + ((p.noin[src >> 5] >> (src & 31)) & 1u);
 
+  if (p.trace && gtid == 0) p.trace[kTraceCap - 1].t_ns = globaltimer();  // kernel timeline
   // ---- k_narrow ran first for this call: finished (nothing to do) or hand-over (resume)
   uint32_t narrow = 0;
   if (ld_acquire(&C->narrow_seq) == p.seq) narrow = ld_cg(&C->narrow_status);
@@ -690,13 +705,10 @@ __global__ void __launch_bounds__(NT, DAWN_SSSP_MINB) k_sssp(SsspParams p) {
       s0.qpack = (1ull << 32) | d;
     }
   }
-  if (p.trace) {
-    const uint32_t ntr = min(p.n + 1, kTraceCap);
-    for (uint32_t i = gtid; i < ntr; i += nthreads) {
-      p.trace[i].t_first = ~0ull;
-      p.trace[i].t_last = 0;
-      for (int k = 0; k < 4; ++k) p.trace[i].cyc[k] = 0;
-    }
+  if (p.trace && gtid == 0) {  // record 0 (later records are reset by the previous header)
+    p.trace[0].t_first = ~0ull;
+    p.trace[0].t_last = 0;
+    for (int k = 0; k < 4; ++k) p.trace[0].cyc[k] = 0;
   }
   if (threadIdx.x < 4) phase_smem()[threadIdx.x] = 0;
   if (threadIdx.x == 0) {
@@ -706,6 +718,7 @@ __global__ void __launch_bounds__(NT, DAWN_SSSP_MINB) k_sssp(SsspParams p) {
   }
   }
   grid_sync(&C->bar, nblocks, bar_target);
+  if (p.trace && gtid == 0) p.trace[kTraceCap - 1].t_first = globaltimer();
 
   unsigned long long examined = 0;
   bool have_header = false;
@@ -822,10 +835,10 @@ __global__ void __launch_bounds__(NT, DAWN_SSSP_MINB) k_sssp(SsspParams p) {
     } else {
 #if DAWN_PULL_DEEP
       if (st.deep)
-        pull_level<8>(p, st, gwarp, nwarps, n_new, m_new, examined, tconv);
+        pull_level<DAWN_PULL_DEEP_PR>(p, st, gwarp, nwarps, n_new, m_new, examined, tconv);
       else
 #endif
-        pull_level<4>(p, st, gwarp, nwarps, n_new, m_new, examined, tconv);
+        pull_level<DAWN_PULL_PR>(p, st, gwarp, nwarps, n_new, m_new, examined, tconv);
     }
     block_flush(n_new, m_new, &ns->n_new, &ns->m_new, red);
     phase_add(p, st.L, 2, tconv);
@@ -835,6 +848,7 @@ __global__ void __launch_bounds__(NT, DAWN_SSSP_MINB) k_sssp(SsspParams p) {
     __syncthreads();
   }
 
+  if (p.trace && gtid == 0) p.trace[kTraceCap - 1].t_last = globaltimer();
   // ---- a7 statistics
   if (p.stats) {
     block_flush(0u, examined, nullptr, &C->examined, red);

@@ -23,13 +23,16 @@ for v in variants:
         if trr is not None and os.environ.get("PROF"):
             G.trace_raw = trr
             trr = trr[: sd["levels"] + 1]
-        traces.append((ts[-1], int(s), sd, trr))
+        traces.append((ts[-1], int(s), sd, trr, getattr(G, 'timeline', None)))
     print(f"== {cfg} {v}: median {np.median(ts)*1e3:.1f} us mean {np.mean(ts)*1e3:.1f} max {np.max(ts)*1e3:.1f}  GTEPS(agg) {er/(sum(ts)*1e-3)/1e9:.1f}")
     print("   per-source us:", [round(x * 1e3) for x in ts])
-    for label, (tt, s, sd, tr) in (("median", sorted(traces, key=lambda x: x[0])[len(traces)//2]), ("slowest", max(traces, key=lambda x: x[0]))):
+    for label, (tt, s, sd, tr, tl) in (("median", sorted(traces, key=lambda x: x[0])[len(traces)//2]), ("slowest", max(traces, key=lambda x: x[0]))):
         print(f"   {label} source {s}: {tt*1e3:.1f} us, {sd}")
         if tr is None: continue
         t0 = int(tr["t_ns"][0])
+        if tl is not None and int(tl["t_ns"]) > 0:
+            print("   k_sssp timeline us (rel. level 0 start): entry %.1f init-done %.1f last-level-done %.1f" % (
+                (int(tl["t_ns"]) - t0) / 1e3, (int(tl["t_first"]) - t0) / 1e3, (int(tl["t_last"]) - t0) / 1e3))
         if len(tr) > 40:
             print("   levels:", len(tr), " avg level us: %.2f" % ((int(tr['t_ns'][-1]) - t0) / 1e3 / (len(tr) - 1)))
             rows = list(tr[:6]) + list(tr[len(tr)//2 - 2: len(tr)//2 + 2]) + list(tr[-4:])

@@ -257,8 +257,8 @@ def test_tunables_never_change_results(knobs):
 
 
 def test_narrow_kernel_and_handover():
-    # low average degree => dawn_sssp starts on one CTA with the frontier in shared memory
-    # (k_narrow); wide frontiers overflow it and the grid-wide kernel resumes from its queue.
+    # dawn_sssp starts on one 16-CTA cluster (k_narrow); wide frontiers (or full queues) hand
+    # over to the grid-wide kernel, which resumes from the frontier bitmap.
     rng = np.random.default_rng(11)
     n = 200_000
     e = rng.integers(0, n, size=(2 * n, 2))
@@ -266,13 +266,15 @@ def test_narrow_kernel_and_handover():
     tree = graphgen.from_edges(2 ** 17 - 1, [[v, 2 * v + 1] for v in range(2 ** 16 - 1)] +
                                [[v, 2 * v + 2] for v in range(2 ** 16 - 1)])  # directed tree
     grid = graphgen.grid(700, 500)
-    for g in (rand, tree, grid):
-        assert g.m <= 6 * g.n
+    kr = graphgen.kron(14, 16, 14)                                # hubs: CTA-wide long rows
+    for g in (rand, tree, grid, kr):
         G = dev_graph(g)
-        G.set_tuning(narrow_avg_degree=6)
         srcs = [0, 1, g.n // 2, g.n - 1]
-        check_sssp(g, G, srcs, variants=("auto", "push"))
-        G.set_tuning(narrow_avg_degree=0)                          # grid-wide kernel only
+        check_sssp(g, G, srcs, variants=("auto", "push"))         # load-time defaults
+        for h in (0, 64, 1024, 2e19):                              # hand over at every width
+            G.set_tuning(cluster_start=1, cluster_handover_edges=h)
+            check_sssp(g, G, srcs[:2], variants=("auto", "push"))
+        G.set_tuning(cluster_start=0)                              # grid-wide kernel only
         check_sssp(g, G, srcs[:2], variants=("auto",))
 
 
@@ -286,5 +288,35 @@ def test_narrow_forced_handover(monkeypatch):
     dirg = graphgen.from_edges(n, rng.integers(0, n, size=(3 * n, 2)))
     for g in (graphgen.grid(300, 200), rand, dirg):
         G = dev_graph(g)
+        G.set_tuning(cluster_start=1, cluster_handover_edges=2e19)  # only overflow hands over
         srcs = [0, g.n // 3, g.n - 1] + list(g.sample_sources(3, seed=3))
         check_sssp(g, G, srcs, variants=("auto", "push"))
+
+
+def test_cuda_graph_replay():
+    # dawn_sssp calls captured in a CUDA graph and replayed must give the same distances on
+    # every replay (no host-side per-call state baked into the captured launches): a grid
+    # (k_narrow + k_sssp), a Kronecker graph (k_sssp) and a tiny ER graph (k_small)
+    cases = [graphgen.grid(300, 200), graphgen.kron(12, 16, 12), graphgen.er(1000, 8000, 1)]
+    for g in cases:
+        G = dev_graph(g)
+        srcs = [0, g.n // 2, g.n - 1]
+        outs = [torch.empty(g.n, dtype=torch.int32, device="cuda") for _ in srcs]
+        for s, o in zip(srcs, outs):
+            dawn.sssp(G, s, "auto", out=o)
+        torch.cuda.synchronize()
+        cap = torch.cuda.Stream()
+        cap.wait_stream(torch.cuda.current_stream())
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=cap):
+            for s, o in zip(srcs, outs):
+                dawn.sssp(G, s, "auto", out=o)
+        exp = [oracle.bfs_fifo(g.n, g.row_ptr, g.col, s)[0] for s in srcs]
+        for rep in range(3):
+            for o in outs:
+                o.fill_(7)
+            graph.replay()
+            torch.cuda.synchronize()
+            for s, o, e in zip(srcs, outs, exp):
+                d = o.cpu().numpy().view(np.uint32)
+                assert np.array_equal(d, e), (g.name, s, rep)
