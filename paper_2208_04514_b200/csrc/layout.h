@@ -52,6 +52,9 @@ static_assert(kMsBatch == DAWN_MS_BATCH, "dawn.h DAWN_MS_BATCH must match kMsW")
 #ifndef DAWN_PULL_PR
 #define DAWN_PULL_PR 4       // ... on dense frontiers
 #endif
+#ifndef DAWN_HEAVY_ILP
+#define DAWN_HEAVY_ILP 1     // in-edges per lane in flight when a warp scans a heavy pull piece
+#endif
 #ifndef DAWN_PULL_J
 #define DAWN_PULL_J 2  // vis words per warp iteration of the pull sweep (independent scans)
 #endif

@@ -21,6 +21,9 @@
 
 namespace dawn {
 
+#ifndef DAWN_TRACE_MAX
+#define DAWN_TRACE_MAX 0  // experiment: trace per-phase max over warps instead of the sum
+#endif
 #ifndef DAWN_SSSP_NODIST
 #define DAWN_SSSP_NODIST 0  // experiment (WRONG RESULTS): drop the per-level dist stores, timing only
 #endif
@@ -83,7 +86,11 @@ __device__ __forceinline__ void phase_add(const SsspParams &p, uint32_t L, int p
                                           long long &t0) {
   if (p.trace) {
     const long long t = clock64();
+#if DAWN_TRACE_MAX  // per-phase maximum over the warps (stragglers) instead of the sum
+    if (lane_id() == 0 && L < kTraceCap) atomicMax(phase_smem() + ph, (unsigned long long)(t - t0));
+#else
     if (lane_id() == 0 && L < kTraceCap) atomicAdd(phase_smem() + ph, (unsigned long long)(t - t0));
+#endif
     t0 = t;
   }
 }
@@ -432,11 +439,15 @@ __device__ void pull_level(const SsspParams &p, const LevelState &st, uint32_t g
   phase_add(p, st.L, 0, t0);
   // (2) heavy rows: static pieces; 32 pieces tested per warp (vis), then a warp scans each
   //     live piece 32 in-edges per round trip
-  for (uint32_t pb = gwarp * 32; pb < st.n_hp; pb += nwarps * 32) {
+  // every warp gets an equal consecutive share of the piece list (a 32-piece stride left most
+  // warps idle and the rest with up to 32 live pieces each: the level's straggler)
+  const uint32_t per = (st.n_hp + nwarps - 1) / nwarps;
+  const uint32_t pe = min(st.n_hp, (gwarp + 1) * per);
+  for (uint32_t pb = gwarp * per; pb < pe; pb += 32) {
     const uint32_t pc = pb + lane;
     uint32_t u = 0, s = 0, e = 0;
     bool need = false;
-    if (pc < st.n_hp) {
+    if (pc < pe) {
       u = ld_nc(p.hin_v + pc);
       s = ld_nc(p.hin_s + pc);
       e = ld_nc(p.hin_e + pc);
@@ -450,13 +461,25 @@ __device__ void pull_level(const SsspParams &p, const LevelState &st, uint32_t g
       const uint32_t sk = __shfl_sync(DAWN_FULL, s, k);
       const uint32_t ek = __shfl_sync(DAWN_FULL, e, k);
       const uint32_t w = uk >> 5, bit = 1u << (uk & 31);
-      for (uint32_t j = sk; j < ek; j += 32) {
-        const bool act = j + lane < ek;
-        const bool hit = act && fb_test(fcur, (uint32_t)ld_nc(p.icol + j + lane));
-        const uint32_t hm = __ballot_sync(DAWN_FULL, hit);
+      // kHW in-edges per lane in flight: a whole 256-arc piece per round trip
+      constexpr uint32_t kHW = DAWN_HEAVY_ILP;
+      for (uint32_t j = sk; j < ek; j += 32 * kHW) {
+        uint32_t v[kHW];
+#pragma unroll
+        for (uint32_t i = 0; i < kHW; ++i) {
+          const uint32_t jj = j + i * 32 + lane;
+          v[i] = jj < ek ? (uint32_t)ld_nc(p.icol + jj) : 0xffffffffu;
+        }
+        uint32_t first = 0xffffffffu;  // first round (i) with a hit in this lane
+#pragma unroll
+        for (int i = (int)kHW - 1; i >= 0; --i)
+          if (v[i] != 0xffffffffu && fb_test(fcur, v[i])) first = (uint32_t)i;
+        const uint32_t hm = __ballot_sync(DAWN_FULL, first != 0xffffffffu);
         if (hm) {
+          const uint32_t fmin = __reduce_min_sync(DAWN_FULL, first);
+          const uint32_t hm2 = __ballot_sync(DAWN_FULL, first == fmin);
           if (lane == 0) {
-            examined += __ffs(hm);
+            examined += fmin * 32 + __ffs(hm2);
             const uint32_t old = atomicOr(p.vis + w, bit);
             if (!(old & bit)) {
               red_or(fnext + w, bit);
@@ -468,8 +491,8 @@ __device__ void pull_level(const SsspParams &p, const LevelState &st, uint32_t g
           }
           break;
         }
-        if (lane == 0) examined += min(32u, ek - j);
-        if ((((j - sk) >> 5) & 3) == 3 && (ld_cg(p.vis + w) & bit)) break;
+        if (lane == 0) examined += min(32u * kHW, ek - j);
+        if (ld_cg(p.vis + w) & bit) break;  // settled meanwhile by another piece
       }
     }
   }
@@ -624,7 +647,11 @@ __device__ __forceinline__ void trace_done(const SsspParams &p, uint32_t L) {
     atomicMax(&p.trace[L].t_last, t);
     unsigned long long *a = phase_smem();
     for (int k = 0; k < 4; ++k) {
+#if DAWN_TRACE_MAX
+      if (a[k]) atomicMax(&p.trace[L].cyc[k], a[k]);
+#else
       if (a[k]) atomicAdd(&p.trace[L].cyc[k], a[k]);
+#endif
       a[k] = 0;
     }
   }

@@ -49,7 +49,7 @@ for v in variants:
                     print("      stamps (cyc from start) entry/arc/claim/append/sums/sync/exch/barrier/next:", list(raw[:9]), "rank", raw[9])
                 continue
             solo = bool(r["rep"] & 2)
-            div = 16 if solo else nw
+            div = 1 if os.environ.get("TRACE_MAX") else (16 if solo else nw)
             cyc = " ".join("%.1f" % (c / div / CLK) for c in r["cyc"])
             print("   L%d %s%s nf=%d mf=%d start=%s first=%s last=%s  per-warp us [work heavy flush conv]=[%s]" % (
                 r["level"], "PUSH PULL STOP".split()[r["dir"]], " solo" if solo else "", r["nf"], r["mf"],
