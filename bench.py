@@ -151,6 +151,13 @@ def cpu_oracle_apsp(g, verts, budget_s: float):
 
 
 # ------------------------------------------------------------------------------- GPU arms
+# the kernel that does the work of one dawn_sssp call on each config (the dominant kernel)
+KERNEL_OF = {"C1": "k_small (whole SSSP on one CTA, CSR in shared memory)",
+             "C2": "k_sssp (one persistent launch per SSSP)",
+             "C3": "k_narrow (one 16-CTA cluster per SSSP; the k_sssp behind it exits at once)",
+             "C4": "k_sssp (one persistent launch per SSSP)"}
+
+
 def run_sssp(args, rank, world, dev, cfg=None, steps=None, warmup=None, e2e=True, reps=1):
     """One SSSP config.  A step = every bench source once (64 for C2/C4; the single source
     repeated `reps` times for C1/C3)."""
@@ -261,7 +268,8 @@ def run_sssp(args, rank, world, dev, cfg=None, steps=None, warmup=None, e2e=True
                 "avg_launch_us": avg_launch_ms * 1e3, "edges_reach_mean": float(np.mean(er)),
                 "levels": {"push_mean": float(np.mean(pushl)), "pull_mean": float(np.mean(pulll))},
                 "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                             "frac": achieved / peak, "achieved_exec": achieved_exec,
+                             "frac": achieved / peak, "kernel": KERNEL_OF.get(cfg),
+                             "traffic": traffic, "achieved_exec": achieved_exec,
                              "frac_exec": achieved_exec / peak,
                              "bytes_model": "B_SOVM = 4*E_reach + 8*S_reach + 4*n"},
                 "clocks": clk.summary()}, g, srcs, er
@@ -311,7 +319,7 @@ def run_sssp(args, rank, world, dev, cfg=None, steps=None, warmup=None, e2e=True
         "gpu_launches": k * steps * (2 if (g.m <= 6 * g.n and g.n <= 20971520 and cfg != "C1") else 1),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
-                     "kernel": "k_sssp (one persistent launch per SSSP)",
+                     "kernel": KERNEL_OF.get(cfg, KERNEL_OF["C2"]),
                      "algorithmic_bytes_per_launch": float(np.mean(b_sovm)),
                      "bytes_model": "B_SOVM = 4*E_reach + 8*S_reach + 4*n",
                      "avg_launch_us": avg_launch_ms * 1e3,
