@@ -438,7 +438,15 @@ dawn_status dawn_graph_load_csr(int64_t n, int64_t m, const int64_t *row_ptr, co
     }
     cudaGetLastError();
   }
-  g->ms_grid = grid_for((const void *)k_ms64<kNT>, g->nsm, "DAWN_MS_BPS");
+  cudaFuncSetAttribute((const void *)k_ms64<kNT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)ms_smem_bytes(kNT));
+  {
+    int bps = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, (const void *)k_ms64<kNT>, kNT,
+                                                  ms_smem_bytes(kNT));
+    bps = std::max(1, std::min(bps, env_int("DAWN_MS_BPS", 2)));
+    g->ms_grid = std::min<int>(g->nsm * bps, (int)kMaxBlocks);
+  }
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const uint32_t nwords = (uint32_t)((n + 31) / 32);
   const int blocks = std::max(1, std::min<int>(g->nsm * 4, (int)((n + 255) / 256)));
@@ -730,7 +738,8 @@ static dawn_status launch_ms(dawn_graph g, const std::vector<uint32_t> &src, uin
     const int small_m = env_int("DAWN_SMALL_M", 1 << 15);
     if (g->m + g->n <= small_m) grid = 1;
     void *args[] = {&p};
-    e = cudaLaunchCooperativeKernel((const void *)k_ms64<kNT>, dim3(grid), dim3(kNT), args, 0, st);
+    e = cudaLaunchCooperativeKernel((const void *)k_ms64<kNT>, dim3(grid), dim3(kNT), args,
+                                    ms_smem_bytes(kNT), st);
     if (e != cudaSuccess) return cuda_fail(e, "k_ms64 launch");
   }
   return DAWN_OK;

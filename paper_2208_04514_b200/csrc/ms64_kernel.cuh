@@ -18,6 +18,17 @@
 #pragma once
 #include "layout.h"
 
+#ifndef DAWN_MS_NOREC
+#define DAWN_MS_NOREC 0
+#endif
+#ifndef DAWN_MS_PUSH_U
+#define DAWN_MS_PUSH_U 4  // 32-arc rounds batched per warp iteration (push phases, heavy pulls)
+#endif
+#ifndef DAWN_MS_PULL_U
+#define DAWN_MS_PULL_U 2  // in-neighbour gathers per lane per round trip in the light pull pass
+#endif
+
+
 namespace dawn {
 
 template <int W>
@@ -101,18 +112,43 @@ struct MsState {
   unsigned long long n_active, m_active, m_uns;
 };
 
-struct MsSmem {  // per-CTA record accumulators of the current batch
+// Per-warp record accumulators of the current batch (dynamic shared memory, one slice per warp):
+// lane j of a warp owns sources 32i + j (i < 2W) of its slice, so the updates need no atomics;
+// the CTA folds its slices once per batch.
+struct MsWarpAcc {
   unsigned long long sum[kMsBatch], hash[kMsBatch];
   uint32_t cnt[kMsBatch], ecc[kMsBatch];
 };
+inline size_t ms_smem_bytes(int nt) { return sizeof(MsWarpAcc) * (size_t)(nt / 32); }
+
 
 // Warp-collective: fold this lane's vertex u new-bits nw into the per-CTA accumulators and, if
 // requested, the dense distance rows.  Lane j receives, for source block i, the 32-vertex
 // mask of source 32i + j (one ballot per source).
+// Lane j gets column j of the 32x32 bit matrix whose row k is lane k's x (butterfly transpose:
+// five shfl_xor stages instead of 32 ballots).
+__device__ __forceinline__ uint32_t transpose32(uint32_t x) {
+  const uint32_t lane = lane_id();
+  uint32_t m = 0x0000FFFFu;
+#pragma unroll
+  for (uint32_t s = 16; s > 0; s >>= 1) {
+    const uint32_t y = __shfl_xor_sync(DAWN_FULL, x, s);
+    x = (lane & s) ? ((x & ~m) | ((y & ~m) >> s)) : ((x & m) | ((y & m) << s));
+    m ^= m << (s >> 1);
+  }
+  return x;
+}
+
+// Warp-collective: fold this lane's vertex u new-bits nw into the warp's record slice and, if
+// requested, the dense distance rows.  Lane j receives, for source block i, the 32-vertex
+// mask of source 32i + j (a bit-matrix transpose of the warp's new-words).
 template <int W>
 __device__ __forceinline__ void ms_record_group(const MsParams &p, const Word<W> &nw, uint32_t u,
                                                 uint32_t L1, uint32_t batch_base,
-                                                unsigned long long *hs, MsSmem &acc) {
+                                                unsigned long long *hs, MsWarpAcc &wa) {
+#if DAWN_MS_NOREC
+  return;  // experiment (WRONG RECORDS): no record accumulation, timing only
+#endif
   const bool mine = wany<W>(nw);
   if (!__any_sync(DAWN_FULL, mine)) return;
   const uint32_t lane = lane_id();
@@ -123,12 +159,7 @@ __device__ __forceinline__ void ms_record_group(const MsParams &p, const Word<W>
     const unsigned long long word = nw.w[i >> 1];
     const uint32_t half = (uint32_t)(word >> ((i & 1) * 32));
     if (!__any_sync(DAWN_FULL, half != 0)) continue;
-    uint32_t mk = 0;
-#pragma unroll 8
-    for (int k = 0; k < 32; ++k) {
-      const uint32_t b = __ballot_sync(DAWN_FULL, (half >> k) & 1u);
-      if (lane == (uint32_t)k) mk = b;
-    }
+    uint32_t mk = transpose32(half);
     if (mk) {
       const uint32_t src = 32 * i + lane;
       const uint32_t c = __popc(mk);
@@ -138,10 +169,10 @@ __device__ __forceinline__ void ms_record_group(const MsParams &p, const Word<W>
         h += hs[__ffs(t) - 1];
         t &= t - 1;
       }
-      atomicAdd(&acc.cnt[src], c);
-      atomicMax(&acc.ecc[src], L1);
-      atomicAdd(&acc.sum[src], (unsigned long long)c * L1);
-      atomicAdd(&acc.hash[src], h);
+      wa.cnt[src] += c;
+      wa.ecc[src] = L1;  // levels only grow
+      wa.sum[src] += (unsigned long long)c * L1;
+      wa.hash[src] += h;
       if (p.dist) {
         // lane j owns source src: its row gets L1 at the vertices of mk
         uint32_t *row = p.dist + (size_t)(batch_base + src) * p.n + (u - lane);
@@ -164,7 +195,8 @@ __global__ void __launch_bounds__(NT, DAWN_MS_MINB) k_ms64(MsParams p) {
   __shared__ MsState st;
   __shared__ unsigned long long hsm[NT];  // per-warp 32-entry hash stash
   __shared__ unsigned long long red[4];
-  __shared__ MsSmem acc;
+  extern __shared__ __align__(16) unsigned char ms_dyn[];
+  MsWarpAcc &wacc = reinterpret_cast<MsWarpAcc *>(ms_dyn)[threadIdx.x / 32];
   const uint32_t nblocks = gridDim.x;
   const uint32_t lane = lane_id();
   const uint32_t gwarp = blockIdx.x * (NT / 32) + threadIdx.x / 32;
@@ -197,11 +229,11 @@ __global__ void __launch_bounds__(NT, DAWN_MS_MINB) k_ms64(MsParams p) {
       uint32_t *d0 = p.dist + (size_t)bbase * p.n;
       for (size_t i = gtid; i < tot; i += nthreads) d0[i] = kUnreached;
     }
-    for (uint32_t i = threadIdx.x; i < kMsBatch; i += NT) {
-      acc.sum[i] = 0;
-      acc.hash[i] = 0;
-      acc.cnt[i] = 0;
-      acc.ecc[i] = 0;
+    for (uint32_t i = lane; i < kMsBatch; i += 32) {
+      wacc.sum[i] = 0;
+      wacc.hash[i] = 0;
+      wacc.cnt[i] = 0;
+      wacc.ecc[i] = 0;
     }
     if (blockIdx.x == 0 && threadIdx.x < 12) (&C->cnt[0][0])[threadIdx.x] = 0;
     grid_sync(&C->bar, nblocks, bar_target);
@@ -272,26 +304,39 @@ __global__ void __launch_bounds__(NT, DAWN_MS_MINB) k_ms64(MsParams p) {
           const uint32_t incl = warp_incl_scan(d);
           const uint32_t total = __shfl_sync(DAWN_FULL, incl, 31);
           const uint32_t excl = incl - d;
-          for (uint32_t base = 0; base < total; base += 32) {
-            const uint32_t t = base + lane;
-            uint32_t k = 0;
+          // kPU rounds of 32 arcs per iteration: every target and seen-word load of the batch is
+          // issued before the first red.or (the asm memory clobber would otherwise serialise
+          // the rounds into load -> gather -> red chains)
+          constexpr uint32_t kPU = DAWN_MS_PUSH_U;
+          for (uint32_t base = 0; base < total; base += 32 * kPU) {
+            uint32_t u[kPU];
+            Word<W> fk[kPU];
 #pragma unroll
-            for (uint32_t step = 16; step; step >>= 1) {
-              const uint32_t e = __shfl_sync(DAWN_FULL, excl, k + step);
-              if (e <= t) k += step;
+            for (uint32_t r = 0; r < kPU; ++r) {
+              const uint32_t t = base + 32 * r + lane;
+              uint32_t k = 0;
+#pragma unroll
+              for (uint32_t step = 16; step; step >>= 1) {
+                const uint32_t e = __shfl_sync(DAWN_FULL, excl, k + step);
+                if (e <= t) k += step;
+              }
+              const uint32_t ek = __shfl_sync(DAWN_FULL, excl, k);
+              const uint32_t sk = __shfl_sync(DAWN_FULL, s, k);
+#pragma unroll
+              for (int i = 0; i < W; ++i) fk[r].w[i] = __shfl_sync(DAWN_FULL, fv.w[i], k);
+              u[r] = (t < total) ? (uint32_t)ld_nc(p.col + sk + (t - ek)) : 0xffffffffu;
             }
-            const uint32_t ek = __shfl_sync(DAWN_FULL, excl, k);
-            const uint32_t sk = __shfl_sync(DAWN_FULL, s, k);
-            Word<W> fk;
+            Word<W> su[kPU];
 #pragma unroll
-            for (int i = 0; i < W; ++i) fk.w[i] = __shfl_sync(DAWN_FULL, fv.w[i], k);
-            if (t < total) {
-              const uint32_t u = (uint32_t)ld_nc(p.col + sk + (t - ek));
-              const Word<W> su = wload<W>(p.seen, u);
+            for (uint32_t r = 0; r < kPU; ++r)
+              su[r] = (u[r] != 0xffffffffu) ? wload<W>(p.seen, u[r]) : wzero<W>();
+#pragma unroll
+            for (uint32_t r = 0; r < kPU; ++r) {
+              if (u[r] == 0xffffffffu) continue;
 #pragma unroll
               for (int i = 0; i < W; ++i) {
-                const unsigned long long x = fk.w[i] & ~su.w[i];
-                if (x) red_or64(p.nxt + (size_t)u * W + i, x);
+                const unsigned long long x = fk[r].w[i] & ~su[r].w[i];
+                if (x) red_or64(p.nxt + (size_t)u[r] * W + i, x);
               }
             }
           }
@@ -302,13 +347,24 @@ __global__ void __launch_bounds__(NT, DAWN_MS_MINB) k_ms64(MsParams p) {
           const Word<W> fv = wload<W>(Fc, v);
           if (!wany<W>(fv)) continue;
           const uint32_t s = ld_nc(p.hout_s + pc), e = ld_nc(p.hout_e + pc);
-          for (uint32_t j = s + lane; j < e; j += 32) {
-            const uint32_t u = (uint32_t)ld_nc(p.col + j);
-            const Word<W> su = wload<W>(p.seen, u);
+          constexpr uint32_t kPU = DAWN_MS_PUSH_U;  // rounds batched as in phase A1
+          for (uint32_t j0 = s + lane; j0 < e; j0 += 32 * kPU) {
+            uint32_t u[kPU];
 #pragma unroll
-            for (int i = 0; i < W; ++i) {
-              const unsigned long long x = fv.w[i] & ~su.w[i];
-              if (x) red_or64(p.nxt + (size_t)u * W + i, x);
+            for (uint32_t r = 0; r < kPU; ++r)
+              u[r] = (j0 + 32 * r < e) ? (uint32_t)ld_nc(p.col + j0 + 32 * r) : 0xffffffffu;
+            Word<W> su[kPU];
+#pragma unroll
+            for (uint32_t r = 0; r < kPU; ++r)
+              su[r] = (u[r] != 0xffffffffu) ? wload<W>(p.seen, u[r]) : wzero<W>();
+#pragma unroll
+            for (uint32_t r = 0; r < kPU; ++r) {
+              if (u[r] == 0xffffffffu) continue;
+#pragma unroll
+              for (int i = 0; i < W; ++i) {
+                const unsigned long long x = fv.w[i] & ~su[r].w[i];
+                if (x) red_or64(p.nxt + (size_t)u[r] * W + i, x);
+              }
             }
           }
         }
@@ -341,7 +397,7 @@ __global__ void __launch_bounds__(NT, DAWN_MS_MINB) k_ms64(MsParams p) {
             }
             wstore<W>(Fn, u, nw);
           }
-          ms_record_group<W>(p, nw, u, L1, bbase, hs, acc);
+          ms_record_group<W>(p, nw, u, L1, bbase, hs, wacc);
         }
       } else {
         // pass 1a: light in-rows, one lane per vertex, early exit once U is covered
@@ -357,16 +413,22 @@ __global__ void __launch_bounds__(NT, DAWN_MS_MINB) k_ms64(MsParams p) {
             if (wany<W>(U)) {
               Word<W> a = wzero<W>();
               const uint32_t s = ld_nc(p.irp + u), e = ld_nc(p.irp + u + 1);
-              for (uint32_t j = s; j < e; j += 2) {
-                const uint32_t v0 = (uint32_t)ld_nc(p.icol + j);
-                const uint32_t v1 = j + 1 < e ? (uint32_t)ld_nc(p.icol + j + 1) : v0;
-                const Word<W> f0 = wload<W>(Fc, v0), f1 = wload<W>(Fc, v1);
+              constexpr uint32_t PU = DAWN_MS_PULL_U;  // in-neighbour gathers in flight per lane
+              for (uint32_t j = s; j < e; j += PU) {
+                uint32_t vv[PU];
+#pragma unroll
+                for (uint32_t x = 0; x < PU; ++x)
+                  vv[x] = (x == 0 || j + x < e) ? (uint32_t)ld_nc(p.icol + j + x) : 0xffffffffu;
+#pragma unroll
+                for (uint32_t x = 0; x < PU; ++x) {
+                  if (vv[x] == 0xffffffffu) continue;
+                  const Word<W> f = wload<W>(Fc, vv[x]);
+#pragma unroll
+                  for (int i = 0; i < W; ++i) a.w[i] |= f.w[i];
+                }
                 bool cov = true;
 #pragma unroll
-                for (int i = 0; i < W; ++i) {
-                  a.w[i] |= f0.w[i] | f1.w[i];
-                  cov = cov && (a.w[i] & U.w[i]) == U.w[i];
-                }
+                for (int i = 0; i < W; ++i) cov = cov && (a.w[i] & U.w[i]) == U.w[i];
                 if (cov) break;
               }
               bool full = true;
@@ -388,7 +450,7 @@ __global__ void __launch_bounds__(NT, DAWN_MS_MINB) k_ms64(MsParams p) {
             }
             wstore<W>(Fn, u, nw);
           }
-          ms_record_group<W>(p, nw, u, L1, bbase, hs, acc);
+          ms_record_group<W>(p, nw, u, L1, bbase, hs, wacc);
         }
         // pass 1b: heavy in-rows by static pieces; partial ORs meet in nxt[u]
         for (uint32_t pc = gwarp; pc < st.n_hp_in; pc += nwarps) {
@@ -402,9 +464,23 @@ __global__ void __launch_bounds__(NT, DAWN_MS_MINB) k_ms64(MsParams p) {
           if (!wany<W>(U)) continue;
           const uint32_t s = ld_nc(p.hin_s + pc), e = ld_nc(p.hin_e + pc);
           Word<W> a = wzero<W>();
-          for (uint32_t j = s; j < e; j += 32) {
+          constexpr uint32_t kHU = DAWN_MS_PUSH_U;  // 32 * kHU in-edges per round trip
+          for (uint32_t j = s; j < e; j += 32 * kHU) {
             Word<W> f = wzero<W>();
-            if (j + lane < e) f = wload<W>(Fc, (uint32_t)ld_nc(p.icol + j + lane));
+            {
+              uint32_t vv[kHU];
+#pragma unroll
+              for (uint32_t r = 0; r < kHU; ++r)
+                vv[r] = (j + 32 * r + lane < e) ? (uint32_t)ld_nc(p.icol + j + 32 * r + lane)
+                                                : 0xffffffffu;
+#pragma unroll
+              for (uint32_t r = 0; r < kHU; ++r) {
+                if (vv[r] == 0xffffffffu) continue;
+                const Word<W> g = wload<W>(Fc, vv[r]);
+#pragma unroll
+                for (int i = 0; i < W; ++i) f.w[i] |= g.w[i];
+              }
+            }
             bool cov = true;
 #pragma unroll
             for (int i = 0; i < W; ++i) {
@@ -453,7 +529,7 @@ __global__ void __launch_bounds__(NT, DAWN_MS_MINB) k_ms64(MsParams p) {
             }
             wstore<W>(Fn, u, nw);
           }
-          ms_record_group<W>(p, nw, u, L1, bbase, hs, acc);
+          ms_record_group<W>(p, nw, u, L1, bbase, hs, wacc);
         }
       }
       // frontier counters for the direction choice / stop test
@@ -479,11 +555,20 @@ __global__ void __launch_bounds__(NT, DAWN_MS_MINB) k_ms64(MsParams p) {
     }
     // ---- records: per-CTA partials, reduced by CTA 0 after a barrier
     if (p.rec) {
+      __syncthreads();  // every warp's slice is final
+      const MsWarpAcc *slices = reinterpret_cast<const MsWarpAcc *>(ms_dyn);
       for (uint32_t k = threadIdx.x; k < kMsBatch; k += NT) {
-        p.part[blockIdx.x * kMsBatch + k] = make_uint4(acc.cnt[k], acc.ecc[k], 0, 0);
+        uint32_t c = 0, e = 0;
+        unsigned long long sm = 0, hh = 0;
+        for (uint32_t w = 0; w < NT / 32; ++w) {
+          c += slices[w].cnt[k];
+          e = max(e, slices[w].ecc[k]);
+          sm += slices[w].sum[k];
+          hh += slices[w].hash[k];
+        }
+        p.part[blockIdx.x * kMsBatch + k] = make_uint4(c, e, 0, 0);
         p.part[(nblocks + blockIdx.x) * kMsBatch + k] =
-            make_uint4((uint32_t)acc.sum[k], (uint32_t)(acc.sum[k] >> 32), (uint32_t)acc.hash[k],
-                       (uint32_t)(acc.hash[k] >> 32));
+            make_uint4((uint32_t)sm, (uint32_t)(sm >> 32), (uint32_t)hh, (uint32_t)(hh >> 32));
       }
       grid_sync(&C->bar, nblocks, bar_target);
       if (blockIdx.x == 0) {
