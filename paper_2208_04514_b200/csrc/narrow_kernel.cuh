@@ -48,6 +48,12 @@ namespace dawn {
 #ifndef DAWN_NARROW_NODIST
 #define DAWN_NARROW_NODIST 0  // experiment (WRONG RESULTS): skip the dist stores, timing only
 #endif
+#ifndef DAWN_NARROW_TMA
+#define DAWN_NARROW_TMA 1  // stage rows with one TMA bulk copy each (else 16-B cp.async pieces)
+#endif
+#ifndef DAWN_NARROW_PF2
+#define DAWN_NARROW_PF2 0  // experiment: L2 prefetch of every target row before its claim (C3: 19.8 -> 27.7 ms)
+#endif
 #ifndef DAWN_NARROW_CBAR
 #define DAWN_NARROW_CBAR 0  // experiment: exchange by returning atomics + barrier.cluster
 #endif
@@ -192,7 +198,7 @@ __device__ __forceinline__ void narrow_visit(const NarrowParams &p, NarrowCtl &S
                                              uint32_t rank, uint32_t L1, uint32_t nxt,
                                              size_t qnxt_off, uint4 *qn_buf, uint4 *an_buf,
                                              uint4 a, bool act, uint32_t parent, uint32_t skip,
-                                             uint32_t &n_new, uint32_t &m_new) {
+                                             uint32_t &n_new, uint32_t &m_new, uint32_t lvl_bar) {
   act = act && a.x != skip;  // the row owner's discoverer is visited: skip that arc
   const uint32_t w = a.x >> 5, o = w % kNarrowCluster, bit = 1u << (a.x & 31);
   const bool loc = o == rank;           // claim in this CTA's visited slice
@@ -225,11 +231,20 @@ __device__ __forceinline__ void narrow_visit(const NarrowParams &p, NarrowCtl &S
         if (stage) {
           const uint32_t dst =
               (uint32_t)__cvta_generic_to_shared(an_buf + (size_t)slot * kNarrowStage);
+#if DAWN_NARROW_TMA
+          // one TMA bulk copy of the whole row, completing on this level's barrier
+          asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;"
+                       ::"r"(lvl_bar), "r"(16u * d) : "memory");
+          asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes"
+                       " [%0], [%1], %2, [%3];"
+                       ::"r"(dst), "l"(p.arc + a.y), "r"(16u * d), "r"(lvl_bar) : "memory");
+#else
 #pragma unroll
           for (uint32_t i = 0; i < kNarrowStage; ++i)
             if (i < d)
               asm volatile("cp.async.cg.shared.global [%0], [%1], 16;"
                            ::"r"(dst + 16 * i), "l"(p.arc + a.y + i) : "memory");
+#endif
         } else if (p.arc) {
           prefetch_row_l2(p.arc + a.y, d);
         }
@@ -337,6 +352,11 @@ __global__ void __launch_bounds__(kNarrowThreads, 1) k_narrow(NarrowParams p) {
     uint4 *anxt = abuf0 + (size_t)nxt * p.qcap * kNarrowStage;
     const uint32_t nq = min(S.qn[cur], p.qcap);  // this CTA's share of frontier L
     const uint32_t L1 = L + 1;
+    const uint32_t lvl_bar = smem_u32(&S.mbar[L & 1]);  // this level's barrier (row copies land)
+#if DAWN_NARROW_TMA
+    // the row slots the TMA writes this level were last read (generic proxy) two levels ago
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+#endif
     uint32_t n_new = 0, m_new = 0;
     long long tc0 = 0;
     if (p.trace && tid == 0) {
@@ -372,6 +392,11 @@ __global__ void __launch_bounds__(kNarrowThreads, 1) k_narrow(NarrowParams p) {
         const bool act = !big && k < d;
         const uint4 a = !act ? make_uint4(0u, 0u, 0u, 0u)
                         : staged ? acur[(size_t)g * kNarrowStage + k] : narrow_arc(p, e.y + k);
+#if DAWN_NARROW_PF2
+        // two hops ahead: the target's row goes to L2 now; if the claim below wins, its TMA
+        // staging copy (issued a few hundred cycles later) then reads L2, not HBM
+        if (p.arc && act && a.x != skip && a.z > a.y) prefetch_row_l2(p.arc + a.y, a.z - a.y);
+#endif
 #if DAWN_NARROW_PROF
         if (prof && base == 0 && lane == 0 && ts[2] == 0) {
           uint32_t x = a.x;
@@ -380,7 +405,7 @@ __global__ void __launch_bounds__(kNarrowThreads, 1) k_narrow(NarrowParams p) {
         }
 #endif
         narrow_visit(p, S, vis_s, rank, L1, nxt, qnxt_off, qnxt, anxt, a, act, e.x, skip, n_new,
-                     m_new);
+                     m_new, lvl_bar);
 #if DAWN_NARROW_PROF
         if (prof && base == 0 && lane == 0 && ts[4] == 0) ts[4] = ts[3] = clock64();
 #endif
@@ -404,7 +429,7 @@ __global__ void __launch_bounds__(kNarrowThreads, 1) k_narrow(NarrowParams p) {
           const bool act = jj + lane < eb.z;
           const uint4 a = act ? narrow_arc(p, jj + lane) : make_uint4(0u, 0u, 0u, 0u);
           narrow_visit(p, S, vis_s, rank, L1, nxt, qnxt_off, qnxt, anxt, a, act, eb.x, eb.w, n_new,
-                       m_new);
+                       m_new, lvl_bar);
         }
       }
     }
@@ -428,7 +453,7 @@ __global__ void __launch_bounds__(kNarrowThreads, 1) k_narrow(NarrowParams p) {
           const bool act = j0 + lane < eb.z;
           const uint4 a = act ? narrow_arc(p, j0 + lane) : make_uint4(0u, 0u, 0u, 0u);
           narrow_visit(p, S, vis_s, rank, L1, nxt, qnxt_off, qnxt, anxt, a, act, eb.x, eb.w, n_new,
-                       m_new);
+                       m_new, lvl_bar);
         }
       }
       fold();
@@ -482,7 +507,12 @@ __global__ void __launch_bounds__(kNarrowThreads, 1) k_narrow(NarrowParams p) {
 #else
     {
       const uint32_t bar = smem_u32(&S.mbar[bb]);
+#if DAWN_NARROW_TMA
+      asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.release.cta.shared::cta.b64 st, [%0];\n\t}"
+                   ::"r"(bar) : "memory");
+#else
       asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(bar) : "memory");
+#endif
       if (tid == 0)
         asm volatile("{\n\t.reg .b64 st;\n\t"
                      "mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 st, [%0], %1;\n\t}"
