@@ -299,6 +299,7 @@ struct dawn_graph_s {
   bool has_csc;
   float alpha = 2.f, beta = 24.f, ms_alpha = 2.f;
   int sssp_grid, ms_grid;
+  bool sssp_one = false;  // the 1-CTA-per-SM instantiation of k_sssp (small graphs)
   bool trace;
   size_t small_cap;  // max dynamic smem for k_small (0 = disabled)
   uint32_t bmpush_e = 1u << 18, solo_e = 512;
@@ -388,7 +389,10 @@ dawn_status dawn_graph_load_csr(int64_t n, int64_t m, const int64_t *row_ptr, co
   g->alpha = (float)env_int("DAWN_ALPHA", 2);
   g->beta = (float)env_int("DAWN_BETA", 24);
   g->ms_alpha = (float)env_int("DAWN_MS_ALPHA", 2);
-  g->sssp_grid = grid_for((const void *)k_sssp<kNT>, g->nsm, "DAWN_SSSP_BPS");
+  // small graphs: k_sssp<kNT, 1> (one CTA per SM, 128 registers); big ones k_sssp<kNT, 2>
+  g->sssp_one = n <= env_int("DAWN_SSSP_ONE_MAX_N", 1 << 22);
+  g->sssp_grid = g->sssp_one ? std::min<int>(g->nsm, (int)kMaxBlocks)
+                             : grid_for((const void *)k_sssp<kNT, 2>, g->nsm, "DAWN_SSSP_BPS");
   {
     int optin = 0;
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, g->device);
@@ -687,7 +691,8 @@ dawn_status dawn_sssp(dawn_graph g, int64_t source, uint32_t variant, uint32_t *
   const int small_m = env_int("DAWN_SMALL_M", 1 << 15);
   if (g->m + g->n <= small_m) grid = 1;  // tiny graphs: one CTA, barriers are __syncthreads
   void *args[] = {&p};
-  cudaError_t e = cudaLaunchCooperativeKernel((const void *)k_sssp<kNT>, dim3(grid), dim3(kNT),
+  const void *kfn = g->sssp_one ? (const void *)k_sssp<kNT, 1> : (const void *)k_sssp<kNT, 2>;
+  cudaError_t e = cudaLaunchCooperativeKernel(kfn, dim3(grid), dim3(kNT),
                                               args, 0, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "k_sssp launch");
   return DAWN_OK;

@@ -677,8 +677,11 @@ __device__ __forceinline__ void level_advance(LevelState &st) {
   st.L++;
 }
 
-template <int NT>
-__global__ void __launch_bounds__(NT, DAWN_SSSP_MINB) k_sssp(SsspParams p) {
+// MINB = CTAs per SM the register allocation targets: 2 (64 registers, 296 CTAs) hides more
+// latency on big graphs (Kronecker-24: 1196 vs 992 GTEPS); 1 (no spills, 148 CTAs, cheaper
+// grid barriers and fewer same-address atomics) wins on small ones (Kronecker-20: 364 vs 352).
+template <int NT, int MINB = DAWN_SSSP_MINB>
+__global__ void __launch_bounds__(NT, MINB) k_sssp(SsspParams p) {
   __shared__ LevelState st;
   __shared__ unsigned long long red[2];
   __shared__ WarpStage stage[NT / 32];
