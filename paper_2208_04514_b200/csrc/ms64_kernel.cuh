@@ -341,11 +341,26 @@ __global__ void __launch_bounds__(NT, DAWN_MS_MINB) k_ms64(MsParams p) {
             }
           }
         }
-        // phase A2: heavy active rows by static pieces
-        for (uint32_t pc = gwarp; pc < st.n_hp_out; pc += nwarps) {
-          const uint32_t v = ld_nc(p.hout_v + pc);
+        // phase A2: heavy active rows by static pieces.  Warp w takes pieces w + k * nwarps (the
+        // live ones of a level spread over all warps) and tests 32 of them at once (lane k: is the
+        // piece's vertex in the frontier?) before expanding the live ones — a per-piece test was
+        // two dependent round trips, ~20 per warp per level even when nothing was live
+        const uint32_t hend = st.n_hp_out;
+        for (uint32_t pb = gwarp; pb < hend; pb += 32 * nwarps) {
+          const uint32_t pcl = pb + lane * nwarps;
+          uint32_t vl = 0;
+          bool live = false;
+          if (pcl < hend) {
+            vl = ld_nc(p.hout_v + pcl);
+            live = wany<W>(wload<W>(Fc, vl));
+          }
+          uint32_t lm = __ballot_sync(DAWN_FULL, live);
+          while (lm) {
+          const uint32_t kk = __ffs(lm) - 1;
+          lm &= lm - 1;
+          const uint32_t pc = pb + kk * nwarps;
+          const uint32_t v = __shfl_sync(DAWN_FULL, vl, kk);
           const Word<W> fv = wload<W>(Fc, v);
-          if (!wany<W>(fv)) continue;
           const uint32_t s = ld_nc(p.hout_s + pc), e = ld_nc(p.hout_e + pc);
           constexpr uint32_t kPU = DAWN_MS_PUSH_U;  // rounds batched as in phase A1
           for (uint32_t j0 = s + lane; j0 < e; j0 += 32 * kPU) {
@@ -366,6 +381,7 @@ __global__ void __launch_bounds__(NT, DAWN_MS_MINB) k_ms64(MsParams p) {
                 if (x) red_or64(p.nxt + (size_t)u[r] * W + i, x);
               }
             }
+          }
           }
         }
         grid_sync(&C->bar, nblocks, bar_target);
@@ -453,8 +469,24 @@ __global__ void __launch_bounds__(NT, DAWN_MS_MINB) k_ms64(MsParams p) {
           ms_record_group<W>(p, nw, u, L1, bbase, hs, wacc);
         }
         // pass 1b: heavy in-rows by static pieces; partial ORs meet in nxt[u]
-        for (uint32_t pc = gwarp; pc < st.n_hp_in; pc += nwarps) {
-          const uint32_t u = ld_nc(p.hin_v + pc);
+        // (pieces w + k * nwarps, 32 tested at once, as in phase A2)
+        const uint32_t iend = st.n_hp_in;
+        for (uint32_t pb = gwarp; pb < iend; pb += 32 * nwarps) {
+          const uint32_t pcl = pb + lane * nwarps;
+          uint32_t ul = 0;
+          bool live = false;
+          if (pcl < iend) {
+            ul = ld_nc(p.hin_v + pcl);
+            const Word<W> sn = wload<W>(p.seen, ul), have = wload_cg<W>(p.nxt, ul);
+#pragma unroll
+            for (int i = 0; i < W; ++i) live = live || (~sn.w[i] & active.w[i] & ~have.w[i]) != 0;
+          }
+          uint32_t lm = __ballot_sync(DAWN_FULL, live);
+          while (lm) {
+          const uint32_t kk = __ffs(lm) - 1;
+          lm &= lm - 1;
+          const uint32_t pc = pb + kk * nwarps;
+          const uint32_t u = __shfl_sync(DAWN_FULL, ul, kk);
           // bits already found by earlier pieces of this row (pieces are stored piece-major:
           // all first pieces, then all second pieces, ...) need not be looked for again
           const Word<W> sn = wload<W>(p.seen, u), have = wload_cg<W>(p.nxt, u);
@@ -496,6 +528,7 @@ __global__ void __launch_bounds__(NT, DAWN_MS_MINB) k_ms64(MsParams p) {
           for (int i = 0; i < W; ++i) {
             const unsigned long long x = a.w[i] & U.w[i];
             if (lane == (uint32_t)i && x) red_or64(p.nxt + (size_t)u * W + i, x);
+          }
           }
         }
         grid_sync(&C->bar, nblocks, bar_target);
