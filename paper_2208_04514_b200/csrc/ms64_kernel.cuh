@@ -25,7 +25,7 @@
 #define DAWN_MS_PUSH_U 4  // 32-arc rounds batched per warp iteration (push phases, heavy pulls)
 #endif
 #ifndef DAWN_MS_PULL_U
-#define DAWN_MS_PULL_U 2  // in-neighbour gathers per lane per round trip in the light pull pass
+#define DAWN_MS_PULL_U 4  // in-neighbour gathers per lane per round trip in the light pull pass
 #endif
 
 
