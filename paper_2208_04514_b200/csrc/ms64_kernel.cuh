@@ -118,6 +118,7 @@ struct MsState {
 struct MsWarpAcc {
   unsigned long long sum[kMsBatch], hash[kMsBatch];
   uint32_t cnt[kMsBatch], ecc[kMsBatch];
+  unsigned long long tab[8][16];  // subset sums of the group's hash terms, per 4-lane block
 };
 inline size_t ms_smem_bytes(int nt) { return sizeof(MsWarpAcc) * (size_t)(nt / 32); }
 
@@ -154,6 +155,18 @@ __device__ __forceinline__ void ms_record_group(const MsParams &p, const Word<W>
   const uint32_t lane = lane_id();
   hs[lane] = mine ? rec_hash(u, L1) : 0ull;
   __syncwarp();
+  // tab[b][m] = sum of the hash terms of lanes 4b + i for the bits i of m: a source's hash
+  // contribution over a 32-vertex mask is then 8 table reads instead of popc(mask) dependent ones
+#pragma unroll
+  for (uint32_t e = lane; e < 128; e += 32) {
+    const uint32_t b = e >> 4, m = e & 15;
+    unsigned long long v = 0;
+#pragma unroll
+    for (uint32_t i = 0; i < 4; ++i)
+      if ((m >> i) & 1u) v += hs[4 * b + i];
+    wa.tab[b][m] = v;
+  }
+  __syncwarp();
 #pragma unroll
   for (int i = 0; i < 2 * W; ++i) {
     const unsigned long long word = nw.w[i >> 1];
@@ -164,11 +177,8 @@ __device__ __forceinline__ void ms_record_group(const MsParams &p, const Word<W>
       const uint32_t src = 32 * i + lane;
       const uint32_t c = __popc(mk);
       unsigned long long h = 0;
-      uint32_t t = mk;
-      while (t) {
-        h += hs[__ffs(t) - 1];
-        t &= t - 1;
-      }
+#pragma unroll
+      for (uint32_t b = 0; b < 8; ++b) h += wa.tab[b][(mk >> (4 * b)) & 15u];
       wa.cnt[src] += c;
       wa.ecc[src] = L1;  // levels only grow
       wa.sum[src] += (unsigned long long)c * L1;
@@ -285,6 +295,8 @@ __global__ void __launch_bounds__(NT, DAWN_MS_MINB) k_ms64(MsParams p) {
       }
       __syncthreads();
       if (st.stop) break;
+      const bool trc = p.trace && bt == 0 && st.L < kTraceCap;  // per-phase slowest-warp cycles
+      long long tA = trc ? clock64() : 0, tB = 0, tC = 0;
       const uint32_t L1 = st.L + 1;
       const unsigned long long *Fc = p.F[st.cur];
       unsigned long long *Fn = p.F[st.cur ^ 1];
@@ -384,7 +396,9 @@ __global__ void __launch_bounds__(NT, DAWN_MS_MINB) k_ms64(MsParams p) {
           }
           }
         }
+        if (trc) tB = clock64();
         grid_sync(&C->bar, nblocks, bar_target);
+        if (trc) tC = clock64();
         // phase B: vertex pass
         for (uint32_t g = gwarp; g < ngroups; g += nwarps) {
           const uint32_t u = g * 32 + lane;
@@ -531,7 +545,9 @@ __global__ void __launch_bounds__(NT, DAWN_MS_MINB) k_ms64(MsParams p) {
           }
           }
         }
+        if (trc) tB = clock64();
         grid_sync(&C->bar, nblocks, bar_target);
+        if (trc) tC = clock64();
         // pass 2: finalise heavy vertices
         for (uint32_t g = gwarp; g < ngroups; g += nwarps) {
           const uint32_t hw = ld_nc(p.hin_bits + g);
@@ -564,6 +580,12 @@ __global__ void __launch_bounds__(NT, DAWN_MS_MINB) k_ms64(MsParams p) {
           }
           ms_record_group<W>(p, nw, u, L1, bbase, hs, wacc);
         }
+      }
+      if (trc && lane == 0) {
+        const long long tD = clock64();
+        atomicMax(&p.trace[st.L].cyc[0], (unsigned long long)(tB - tA));
+        atomicMax(&p.trace[st.L].cyc[1], (unsigned long long)(tC - tB));
+        atomicMax(&p.trace[st.L].cyc[2], (unsigned long long)(tD - tC));
       }
       // frontier counters for the direction choice / stop test
       na = warp_sum(na);
