@@ -142,6 +142,9 @@ dawn_status dawn_graph_destroy(dawn_graph g);
  *                     instead of one returning atomic per arc.  Default 262144.
  *   DAWN_PARAM_SOLO_EDGES  push levels with <= this many arcs run on one CTA with block-level
  *                     barriers only.  Default 512.
+ *   DAWN_PARAM_BITMAP_PUSH_GROW_EDGES  the bitmap push threshold for a push level whose frontier
+ *                     grew (such a level usually turns to pull next, which wants the bitmap and
+ *                     no queue).  Default 4096 (Kronecker-20: 362 -> 389 GTEPS).
  *   DAWN_PARAM_CLUSTER_START  1: every push/auto dawn_sssp on a graph with n <= 20,971,520
  *                     starts on ONE 16-CTA thread-block cluster with the visited bitmap and the
  *                     frontier queues in distributed shared memory (k_narrow), and hands over to
@@ -160,7 +163,8 @@ typedef enum {
   DAWN_PARAM_BITMAP_PUSH_EDGES = 3,
   DAWN_PARAM_SOLO_EDGES = 4,
   DAWN_PARAM_CLUSTER_START = 5,
-  DAWN_PARAM_CLUSTER_HANDOVER_EDGES = 6
+  DAWN_PARAM_CLUSTER_HANDOVER_EDGES = 6,
+  DAWN_PARAM_BITMAP_PUSH_GROW_EDGES = 7
 } dawn_param;
 
 /* Set one tunable (INVALID_ARGUMENT for an unknown key or a negative value). */

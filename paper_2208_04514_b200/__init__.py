@@ -182,11 +182,11 @@ class Graph:
         return buf[: min(cnt.value, len(buf) - 1)].copy()
 
     _PARAMS = {"alpha": 0, "beta": 1, "ms_alpha": 2, "bitmap_push_edges": 3, "solo_edges": 4,
-               "cluster_start": 5, "cluster_handover_edges": 6}
+               "cluster_start": 5, "cluster_handover_edges": 6, "bitmap_push_grow_edges": 7}
 
     def set_tuning(self, **kw):
         """dawn_graph_set_param for each keyword (alpha, beta, ms_alpha, bitmap_push_edges,
-        solo_edges, cluster_start, cluster_handover_edges).  Speed only; results never change."""
+        solo_edges, cluster_start, cluster_handover_edges, bitmap_push_grow_edges).  Speed only; results never change."""
         for k, v in kw.items():
             _check(lib().dawn_graph_set_param(self._h, self._PARAMS[k], float(v)))
 

@@ -302,7 +302,7 @@ struct dawn_graph_s {
   bool sssp_one = false;  // the 1-CTA-per-SM instantiation of k_sssp (small graphs)
   bool trace;
   size_t small_cap;  // max dynamic smem for k_small (0 = disabled)
-  uint32_t bmpush_e = 1u << 18, solo_e = 512;
+  uint32_t bmpush_e = 1u << 18, solo_e = 512, bmpush_grow = 4096;
   uint32_t n_hasin = 0;
   bool cluster_start = false;     // DAWN_PARAM_CLUSTER_START (default set at load)
   unsigned long long handover_m = 0;  // DAWN_PARAM_CLUSTER_HANDOVER_EDGES (set at load)
@@ -387,6 +387,9 @@ dawn_status dawn_graph_load_csr(int64_t n, int64_t m, const int64_t *row_ptr, co
   if ((e = cudaSetDevice(g->device)) != cudaSuccess) { delete g; return cuda_fail(e, "cudaSetDevice"); }
   cudaDeviceGetAttribute(&g->nsm, cudaDevAttrMultiProcessorCount, g->device);
   g->alpha = (float)env_int("DAWN_ALPHA", 2);
+  g->bmpush_e = (uint32_t)env_int("DAWN_BMPUSH_E", 1 << 18);
+  g->bmpush_grow = (uint32_t)env_int("DAWN_BMPUSH_GROW", 4096);
+  g->solo_e = (uint32_t)env_int("DAWN_SOLO_E", 512);
   g->beta = (float)env_int("DAWN_BETA", 24);
   g->ms_alpha = (float)env_int("DAWN_MS_ALPHA", 2);
   // small graphs: k_sssp<kNT, 1> (one CTA per SM, 128 registers); big ones k_sssp<kNT, 2>
@@ -579,6 +582,9 @@ dawn_status dawn_graph_set_param(dawn_graph g, dawn_param key, double value) {
     case DAWN_PARAM_MS_ALPHA: g->ms_alpha = (float)value; break;
     case DAWN_PARAM_BITMAP_PUSH_EDGES: g->bmpush_e = (uint32_t)std::min(value, 4294967295.0); break;
     case DAWN_PARAM_SOLO_EDGES: g->solo_e = (uint32_t)std::min(value, 4294967295.0); break;
+    case DAWN_PARAM_BITMAP_PUSH_GROW_EDGES:
+      g->bmpush_grow = (uint32_t)std::min(value, 4294967295.0);
+      break;
     case DAWN_PARAM_CLUSTER_START: g->cluster_start = value != 0; break;
     case DAWN_PARAM_CLUSTER_HANDOVER_EDGES:
       g->handover_m = value >= 1.8e19 ? ~0ull : (unsigned long long)value;
@@ -646,6 +652,7 @@ dawn_status dawn_sssp(dawn_graph g, int64_t source, uint32_t variant, uint32_t *
   p.alpha = g->alpha;
   p.beta = g->beta;
   p.bmpush_e = g->bmpush_e;
+  p.bmpush_grow = std::min(g->bmpush_grow, g->bmpush_e);
   p.solo_e = g->solo_e;
   p.seq = ++g->seq;
   if (variant != DAWN_PULL && g->narrow_ok && g->cluster_start) {

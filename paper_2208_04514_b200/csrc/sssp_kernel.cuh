@@ -54,6 +54,7 @@ struct SsspParams {
   uint32_t source, variant, can_pull, sym;
   float alpha, beta;
   uint32_t bmpush_e, solo_e;  // DAWN_PARAM_BITMAP_PUSH_EDGES / DAWN_PARAM_SOLO_EDGES
+  uint32_t bmpush_grow;       // bitmap push threshold while the frontier grows
   uint32_t seq;               // call number (k_narrow hand-over)
 };
 
@@ -608,9 +609,15 @@ __device__ __forceinline__ void level_header(const SsspParams &p, Ctrl *C, Level
         if ((double)st.nf * p.beta < (double)p.n && st.nf < st.prev_nf) st.dir = kPush;
       }
     }
+    const bool grows = st.nf > st.prev_nf;
     st.prev_nf = st.nf;
     st.solo = (nblocks > 1 && st.dir == kPush && st.rep == kRepQueue && st.qe <= p.solo_e) ? 1u : 0u;
-    st.bm = (st.dir == kPush && !st.solo && st.mf >= p.bmpush_e) ? 1u : 0u;
+    // bitmap push (candidates + word-owner filter, the next frontier as a bitmap): wide levels,
+    // and growing ones from bmpush_grow arcs up — a growing frontier usually turns to pull next,
+    // which wants the bitmap and no queue (C2 +3%); a shrinking one keeps the queue
+    st.bm = (st.dir == kPush && !st.solo &&
+             st.mf >= (grows ? (unsigned long long)p.bmpush_grow : (unsigned long long)p.bmpush_e))
+                ? 1u : 0u;
     // sparse frontier (a probe hits with probability ~ m_f / (m_f + m_u) < 1/6): probe 8
     // in-edges per round trip instead of 4
     st.deep = (st.dir == kPull && 6.0 * (double)st.mf < (double)(p.m - st.explored) + (double)st.mf)

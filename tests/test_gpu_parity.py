@@ -245,7 +245,9 @@ def test_trace_levels_consistent():
 
 
 @pytest.mark.parametrize("knobs", [dict(bitmap_push_edges=64), dict(bitmap_push_edges=0, solo_edges=0),
-                                   dict(solo_edges=100000, alpha=1000), dict(alpha=0, beta=1e9)])
+                                   dict(solo_edges=100000, alpha=1000), dict(alpha=0, beta=1e9),
+                                   dict(bitmap_push_grow_edges=0, solo_edges=0),
+                                   dict(bitmap_push_grow_edges=2 ** 31, bitmap_push_edges=2 ** 31)])
 def test_tunables_never_change_results(knobs):
     # every schedule knob (bitmap push on every level, no solo levels, long solo stretches,
     # never/always pull) must give the oracle's distances (tolerance 0)
