@@ -322,3 +322,18 @@ def test_cuda_graph_replay():
             for s, o, e in zip(srcs, outs, exp):
                 d = o.cpu().numpy().view(np.uint32)
                 assert np.array_equal(d, e), (g.name, s, rep)
+
+
+def test_narrow_directed_mesh():
+    # a directed mesh (right and down arcs only, ids follow space): owner-computes cluster search
+    # on a graph without in-edge symmetry; sources inside the mesh reach only their lower-right
+    # quadrant, the rest must stay UNREACHED
+    W, H = 300, 200
+    e = [[r * W + c, r * W + c + 1] for r in range(H) for c in range(W - 1)]
+    e += [[r * W + c, (r + 1) * W + c] for r in range(H - 1) for c in range(W)]
+    g = graphgen.from_edges(W * H, e)
+    G = dev_graph(g)
+    srcs = [0, W * H // 2 + W // 3, W * H - 1, W - 1]
+    check_sssp(g, G, srcs, variants=("auto", "push"))
+    G.set_tuning(cluster_start=1, cluster_handover_edges=2e19)
+    check_sssp(g, G, srcs, variants=("auto",))
