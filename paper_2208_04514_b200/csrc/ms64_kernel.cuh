@@ -296,7 +296,7 @@ __global__ void __launch_bounds__(NT, DAWN_MS_MINB) k_ms64(MsParams p) {
       __syncthreads();
       if (st.stop) break;
       const bool trc = p.trace && bt == 0 && st.L < kTraceCap;  // per-phase slowest-warp cycles
-      long long tA = trc ? clock64() : 0, tB = 0, tC = 0;
+      long long tA = trc ? clock64() : 0, tB = 0, tC = 0, trec = 0;
       const uint32_t L1 = st.L + 1;
       const unsigned long long *Fc = p.F[st.cur];
       unsigned long long *Fn = p.F[st.cur ^ 1];
@@ -427,7 +427,11 @@ __global__ void __launch_bounds__(NT, DAWN_MS_MINB) k_ms64(MsParams p) {
             }
             wstore<W>(Fn, u, nw);
           }
-          ms_record_group<W>(p, nw, u, L1, bbase, hs, wacc);
+          {
+            const long long tr0 = trc ? clock64() : 0;
+            ms_record_group<W>(p, nw, u, L1, bbase, hs, wacc);
+            if (trc) trec += clock64() - tr0;
+          }
         }
       } else {
         // pass 1a: light in-rows, one lane per vertex, early exit once U is covered
@@ -480,7 +484,11 @@ __global__ void __launch_bounds__(NT, DAWN_MS_MINB) k_ms64(MsParams p) {
             }
             wstore<W>(Fn, u, nw);
           }
-          ms_record_group<W>(p, nw, u, L1, bbase, hs, wacc);
+          {
+            const long long tr0 = trc ? clock64() : 0;
+            ms_record_group<W>(p, nw, u, L1, bbase, hs, wacc);
+            if (trc) trec += clock64() - tr0;
+          }
         }
         // pass 1b: heavy in-rows by static pieces; partial ORs meet in nxt[u]
         // (pieces w + k * nwarps, 32 tested at once, as in phase A2)
@@ -578,7 +586,11 @@ __global__ void __launch_bounds__(NT, DAWN_MS_MINB) k_ms64(MsParams p) {
             }
             wstore<W>(Fn, u, nw);
           }
-          ms_record_group<W>(p, nw, u, L1, bbase, hs, wacc);
+          {
+            const long long tr0 = trc ? clock64() : 0;
+            ms_record_group<W>(p, nw, u, L1, bbase, hs, wacc);
+            if (trc) trec += clock64() - tr0;
+          }
         }
       }
       if (trc && lane == 0) {
@@ -586,6 +598,7 @@ __global__ void __launch_bounds__(NT, DAWN_MS_MINB) k_ms64(MsParams p) {
         atomicMax(&p.trace[st.L].cyc[0], (unsigned long long)(tB - tA));
         atomicMax(&p.trace[st.L].cyc[1], (unsigned long long)(tC - tB));
         atomicMax(&p.trace[st.L].cyc[2], (unsigned long long)(tD - tC));
+        atomicMax(&p.trace[st.L].cyc[3], (unsigned long long)trec);
       }
       // frontier counters for the direction choice / stop test
       na = warp_sum(na);
