@@ -153,18 +153,25 @@ __device__ __forceinline__ void ms_record_group(const MsParams &p, const Word<W>
   const bool mine = wany<W>(nw);
   if (!__any_sync(DAWN_FULL, mine)) return;
   const uint32_t lane = lane_id();
-  hs[lane] = mine ? rec_hash(u, L1) : 0ull;
-  __syncwarp();
   // tab[b][m] = sum of the hash terms of lanes 4b + i for the bits i of m: a source's hash
   // contribution over a 32-vertex mask is then 8 table reads instead of popc(mask) dependent ones
+  {
+    // lane l builds entries m = 4 (l & 3) .. + 3 of block b = l >> 2 from the block's four hash
+    // terms, fetched by shuffles
+    const unsigned long long mh = mine ? rec_hash(u, L1) : 0ull;
+    const uint32_t b = lane >> 2, q = lane & 3;
+    unsigned long long h4[4];
 #pragma unroll
-  for (uint32_t e = lane; e < 128; e += 32) {
-    const uint32_t b = e >> 4, m = e & 15;
-    unsigned long long v = 0;
+    for (uint32_t i = 0; i < 4; ++i) h4[i] = __shfl_sync(DAWN_FULL, mh, 4 * b + i);
 #pragma unroll
-    for (uint32_t i = 0; i < 4; ++i)
-      if ((m >> i) & 1u) v += hs[4 * b + i];
-    wa.tab[b][m] = v;
+    for (uint32_t r = 0; r < 4; ++r) {
+      const uint32_t m = 4 * q + r;
+      unsigned long long v = 0;
+#pragma unroll
+      for (uint32_t i = 0; i < 4; ++i)
+        if ((m >> i) & 1u) v += h4[i];
+      wa.tab[b][m] = v;
+    }
   }
   __syncwarp();
 #pragma unroll
