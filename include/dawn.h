@@ -184,6 +184,18 @@ dawn_status dawn_sssp(dawn_graph g, int64_t source, uint32_t variant, uint32_t *
                       dawn_sssp_stats *stats, void *stream);
 
 /*
+ * k single-source searches one after the other in ONE launch of the grid-wide kernel (a grid
+ * barrier between searches instead of a kernel boundary): the same results as k dawn_sssp calls.
+ *   sources  DEVICE uint32[k], each in [0, n) (not checked: the array is not read on the host)
+ *   dist     device uint32[k][n] (row i for sources[i], fully overwritten)
+ *   stats    device dawn_sssp_stats[k] or NULL
+ * Graphs that dawn_sssp would start on the cluster kernel or on the one-CTA kernel are searched
+ * by the grid-wide kernel here.
+ */
+dawn_status dawn_sssp_batch(dawn_graph g, const uint32_t *sources, int64_t k, uint32_t variant,
+                            uint32_t *dist, dawn_sssp_stats *stats, void *stream);
+
+/*
  * Multi-source: k sources (HOST array; all validated before any work),
  * processed DAWN_MS_BATCH (256) at a time by the bit-parallel kernel: each vertex holds four
  * 64-bit words, bit j of the batch's word w = source DAWN_MS_BATCH*b + 64w + j, so one adjacency

@@ -97,6 +97,8 @@ def lib():
         L.dawn_graph_set_param.argtypes = [vp, ctypes.c_int, ctypes.c_double]
         L.dawn_sssp.restype = st
         L.dawn_sssp.argtypes = [vp, i64, u32, vp, vp, vp]
+        L.dawn_sssp_batch.restype = st
+        L.dawn_sssp_batch.argtypes = [vp, vp, i64, u32, vp, vp, vp]
         L.dawn_msssp.restype = st
         L.dawn_msssp.argtypes = [vp, vp, i64, vp, vp, vp]
         L.dawn_apsp_shard.restype = st
@@ -208,6 +210,21 @@ def sssp(g: Graph, source: int, variant="auto", stats: bool = False, out: torch.
     st = torch.zeros(4, dtype=torch.int64, device=g.device) if stats else None
     _check(lib().dawn_sssp(g.handle, int(source), _VARIANTS[variant], _dptr(dist), _dptr(st),
                            _stream(stream)))
+    return (dist, st) if stats else dist
+
+
+def sssp_batch(g: Graph, sources: torch.Tensor, variant="auto", stats: bool = False,
+               out: torch.Tensor | None = None, stream=None):
+    """dawn_sssp_batch: k single-source searches, one after the other in ONE launch (no kernel
+    boundary between them).  `sources`: uint32/int32 CUDA tensor [k] of vertex ids in [0, n).
+    Returns dist int32 [k, n] (and stats int64 [k, 4] = k dawn_sssp_stats when stats=True)."""
+    assert sources.is_cuda and sources.dtype in (torch.int32, torch.uint32)
+    k = sources.numel()
+    dist = out if out is not None else torch.empty((k, g.n), dtype=torch.int32, device=g.device)
+    assert dist.shape == (k, g.n) and dist.dtype == torch.int32 and dist.is_contiguous()
+    st = torch.zeros((k, 4), dtype=torch.int64, device=g.device) if stats else None
+    _check(lib().dawn_sssp_batch(g.handle, _dptr(sources), k, _VARIANTS[variant], _dptr(dist),
+                                 _dptr(st), _stream(stream)))
     return (dist, st) if stats else dist
 
 

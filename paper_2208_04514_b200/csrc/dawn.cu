@@ -594,28 +594,9 @@ dawn_status dawn_graph_set_param(dawn_graph g, dawn_param key, double value) {
   return DAWN_OK;
 }
 
-dawn_status dawn_sssp(dawn_graph g, int64_t source, uint32_t variant, uint32_t *dist,
-                      dawn_sssp_stats *stats, void *stream) {
-  g_err.clear();
-  if (!g || !dist) return fail(DAWN_ERR_INVALID_ARGUMENT, "graph or dist is NULL");
-  if (variant > DAWN_PULL) return fail(DAWN_ERR_INVALID_ARGUMENT, "unknown variant");
-  if (source < 0 || source >= g->n)
-    return fail(DAWN_ERR_BOUNDS, "source " + std::to_string(source) + " not in [0, n)");
-  if (variant == DAWN_PULL && !g->has_csc)
-    return fail(DAWN_ERR_CONFIG, "PULL needs CSC (in-edges) on a directed graph");
-  dawn_status s = set_device(g);
-  if (s != DAWN_OK) return s;
+static SsspParams sssp_params(dawn_graph g, uint32_t variant, uint32_t *dist,
+                              dawn_sssp_stats *stats) {
   const Layout &L = g->L;
-  const size_t small_bytes = small_smem_bytes(g->n, g->m);
-  if (variant != DAWN_PULL && !g->trace && small_bytes <= g->small_cap) {
-    // whole SSSP in one CTA's shared memory (tiny graphs, e.g. configs[0])
-    SmallParams sp{(uint32_t)g->n, (uint32_t)g->m, at<uint32_t>(g, L.rp), g->col, dist, stats,
-                   (uint32_t)source};
-    k_small<1024><<<1, 1024, small_bytes, static_cast<cudaStream_t>(stream)>>>(sp);
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) return cuda_fail(e, "k_small launch");
-    return DAWN_OK;
-  }
   SsspParams p{};
   p.n = (uint32_t)g->n;
   p.nwords = (uint32_t)((g->n + 31) / 32);
@@ -645,16 +626,53 @@ dawn_status dawn_sssp(dawn_graph g, int64_t source, uint32_t variant, uint32_t *
   p.ctrl = at<Ctrl>(g, L.ctrl);
   p.dist = dist;
   p.stats = stats;
-  p.source = (uint32_t)source;
   p.variant = variant;
   p.can_pull = g->has_csc ? 1u : 0u;
   p.sym = (g->flags & DAWN_GRAPH_SYMMETRIC) ? 1u : 0u;
   p.alpha = g->alpha;
   p.beta = g->beta;
   p.bmpush_e = g->bmpush_e;
-  p.bmpush_grow = std::min(g->bmpush_grow, g->bmpush_e);
   p.solo_e = g->solo_e;
+  p.bmpush_grow = std::min(g->bmpush_grow, g->bmpush_e);
   p.seq = ++g->seq;
+  return p;
+}
+
+static dawn_status launch_sssp(dawn_graph g, SsspParams &p, cudaStream_t stream) {
+  int grid = g->sssp_grid;
+  const int small_m = env_int("DAWN_SMALL_M", 1 << 15);
+  if (g->m + g->n <= small_m) grid = 1;  // tiny graphs: one CTA, barriers are __syncthreads
+  void *args[] = {&p};
+  const void *kfn = g->sssp_one ? (const void *)k_sssp<kNT, 1> : (const void *)k_sssp<kNT, 2>;
+  cudaError_t e = cudaLaunchCooperativeKernel(kfn, dim3(grid), dim3(kNT), args, 0, stream);
+  if (e != cudaSuccess) return cuda_fail(e, "k_sssp launch");
+  return DAWN_OK;
+}
+
+dawn_status dawn_sssp(dawn_graph g, int64_t source, uint32_t variant, uint32_t *dist,
+                      dawn_sssp_stats *stats, void *stream) {
+  g_err.clear();
+  if (!g || !dist) return fail(DAWN_ERR_INVALID_ARGUMENT, "graph or dist is NULL");
+  if (variant > DAWN_PULL) return fail(DAWN_ERR_INVALID_ARGUMENT, "unknown variant");
+  if (source < 0 || source >= g->n)
+    return fail(DAWN_ERR_BOUNDS, "source " + std::to_string(source) + " not in [0, n)");
+  if (variant == DAWN_PULL && !g->has_csc)
+    return fail(DAWN_ERR_CONFIG, "PULL needs CSC (in-edges) on a directed graph");
+  dawn_status s = set_device(g);
+  if (s != DAWN_OK) return s;
+  const Layout &L = g->L;
+  const size_t small_bytes = small_smem_bytes(g->n, g->m);
+  if (variant != DAWN_PULL && !g->trace && small_bytes <= g->small_cap) {
+    // whole SSSP in one CTA's shared memory (tiny graphs, e.g. configs[0])
+    SmallParams sp{(uint32_t)g->n, (uint32_t)g->m, at<uint32_t>(g, L.rp), g->col, dist, stats,
+                   (uint32_t)source};
+    k_small<1024><<<1, 1024, small_bytes, static_cast<cudaStream_t>(stream)>>>(sp);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "k_small launch");
+    return DAWN_OK;
+  }
+  SsspParams p = sssp_params(g, variant, dist, stats);
+  p.source = (uint32_t)source;
   if (variant != DAWN_PULL && g->narrow_ok && g->cluster_start) {
     // the search starts on one 16-CTA cluster (state in distributed shared memory); k_sssp
     // below resumes from its hand-over (wide frontier or full queue) or exits at once
@@ -694,15 +712,27 @@ dawn_status dawn_sssp(dawn_graph g, int64_t source, uint32_t variant, uint32_t *
     cudaError_t e = cudaLaunchKernelEx(&cfg, k_narrow, np);
     if (e != cudaSuccess) return cuda_fail(e, "k_narrow launch");
   }
-  int grid = g->sssp_grid;
-  const int small_m = env_int("DAWN_SMALL_M", 1 << 15);
-  if (g->m + g->n <= small_m) grid = 1;  // tiny graphs: one CTA, barriers are __syncthreads
-  void *args[] = {&p};
-  const void *kfn = g->sssp_one ? (const void *)k_sssp<kNT, 1> : (const void *)k_sssp<kNT, 2>;
-  cudaError_t e = cudaLaunchCooperativeKernel(kfn, dim3(grid), dim3(kNT),
-                                              args, 0, static_cast<cudaStream_t>(stream));
-  if (e != cudaSuccess) return cuda_fail(e, "k_sssp launch");
-  return DAWN_OK;
+  return launch_sssp(g, p, static_cast<cudaStream_t>(stream));
+}
+
+
+dawn_status dawn_sssp_batch(dawn_graph g, const uint32_t *sources, int64_t k, uint32_t variant,
+                            uint32_t *dist, dawn_sssp_stats *stats, void *stream) {
+  g_err.clear();
+  if (!g || !dist || (!sources && k > 0) || k < 0)
+    return fail(DAWN_ERR_INVALID_ARGUMENT, "bad arguments");
+  if (variant > DAWN_PULL) return fail(DAWN_ERR_INVALID_ARGUMENT, "unknown variant");
+  if (variant == DAWN_PULL && !g->has_csc)
+    return fail(DAWN_ERR_CONFIG, "PULL needs CSC (in-edges) on a directed graph");
+  if (k == 0) return DAWN_OK;
+  if (k >= (int64_t(1) << 32)) return fail(DAWN_ERR_CAPACITY, "k too large");
+  dawn_status s = set_device(g);
+  if (s != DAWN_OK) return s;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  SsspParams p = sssp_params(g, variant, dist, stats);
+  p.sources = sources;
+  p.nsrc = (uint32_t)k;
+  return launch_sssp(g, p, st);
 }
 
 static dawn_status launch_ms(dawn_graph g, const std::vector<uint32_t> &src, uint32_t *dist,

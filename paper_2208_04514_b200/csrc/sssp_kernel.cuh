@@ -30,7 +30,7 @@ namespace dawn {
 #if DAWN_SSSP_NODIST
 #define DIST_ST(i, v) ((void)0)
 #else
-#define DIST_ST(i, v) (p.dist[i] = (v))
+#define DIST_ST(i, v) (st.drow[i] = (v))
 #endif
 
 struct SsspParams {
@@ -56,6 +56,10 @@ struct SsspParams {
   uint32_t bmpush_e, solo_e;  // DAWN_PARAM_BITMAP_PUSH_EDGES / DAWN_PARAM_SOLO_EDGES
   uint32_t bmpush_grow;       // bitmap push threshold while the frontier grows
   uint32_t seq;               // call number (k_narrow hand-over)
+  // batch mode (dawn_sssp_batch): nsrc > 0 sources from the device array `sources`, searched one
+  // after the other in this launch; source i writes dist + i * n and stats[i]
+  const uint32_t *sources;
+  uint32_t nsrc;
 };
 
 struct __align__(16) LevelState {
@@ -64,6 +68,7 @@ struct __align__(16) LevelState {
   uint32_t qn, n_hp;            // queue entries of frontier L; static heavy pieces
   uint32_t qe;                  // queue edges of frontier L
   unsigned long long mf, explored, push_edges, pad;
+  uint32_t *drow;               // this search's distance row
 };
 static_assert(sizeof(LevelState) % 16 == 0, "LevelState is copied as uint4");
 
@@ -198,27 +203,6 @@ __device__ __forceinline__ void enqueue_frontier(const SsspParams &p, Slot *s, i
 
 // Push-mode visit of arc (frontier vertex) -> u, warp-collective (all lanes call; `act`
 // false for idle lanes).
-__device__ __forceinline__ void push_visit(const SsspParams &p, Slot *ns, int qn, uint32_t L1,
-                                           bool act, uint32_t u, uint32_t &n_new,
-                                           unsigned long long &m_new, WarpStage &stg,
-                                           uint32_t &cnt) {
-  bool disc = false;
-  uint32_t rs = 0, d = 0;
-  if (act) {
-    const uint32_t w = u >> 5, bit = 1u << (u & 31);
-    const uint32_t cur = p.vis[w];  // weak load: a stale 0 only costs an atomic
-    if (!(cur & bit)) disc = !(atomicOr(&p.vis[w], bit) & bit);
-  }
-  if (disc) {
-    rs = ld_nc(p.rp + u);
-    d = ld_nc(p.rp + u + 1) - rs;
-    DIST_ST(u, L1);
-    n_new += 1;
-    m_new += d;
-  }
-  enqueue_frontier(p, ns, qn, disc, u, rs, d, stg, cnt);
-}
-
 // One push level over the queue.  Chunk c = edges [32c, 32c+32) of the frontier; a warp item
 // is J consecutive chunks (J = kIlp when the frontier has enough edges to keep every warp busy,
 // else 1), processed with all J chains' loads in flight together (memory-level parallelism):
@@ -701,8 +685,14 @@ __global__ void __launch_bounds__(NT, MINB) k_sssp(SsspParams p) {
   const uint32_t nthreads = nblocks * NT;
   WarpStage &stg = stage[threadIdx.x / 32];
   Ctrl *C = p.ctrl;
-  const uint32_t src = p.source;
   unsigned long long bar_target = 0;
+  const uint32_t nsrc = p.nsrc ? p.nsrc : 1u;
+  // batch mode: the searches run back to back in this launch, a grid barrier apart (no kernel
+  // boundary or launch ramp between them)
+  for (uint32_t si = 0; si < nsrc; ++si) {
+  const uint32_t src = p.nsrc ? ld_nc(p.sources + si) : p.source;
+  uint32_t *const drow = p.dist + (size_t)si * p.n;
+  dawn_sssp_stats *const stats_out = p.stats ? p.stats + si : nullptr;
   uint32_t solo_epoch = 0;
   // condition 1 bound: only vertices with an in-edge (plus s itself) can ever be reached
   const uint32_t max_reach = ld_cg(&C->n_hasin) + ((p.noin[src >> 5] >> (src & 31)) & 1u);
@@ -710,7 +700,7 @@ __global__ void __launch_bounds__(NT, MINB) k_sssp(SsspParams p) {
   if (p.trace && gtid == 0) p.trace[kTraceCap - 1].t_ns = globaltimer();  // kernel timeline
   // ---- k_narrow ran first for this call: finished (nothing to do) or hand-over (resume)
   uint32_t narrow = 0;
-  if (ld_acquire(&C->narrow_seq) == p.seq) narrow = ld_cg(&C->narrow_status);
+  if (!p.nsrc && ld_acquire(&C->narrow_seq) == p.seq) narrow = ld_cg(&C->narrow_status);
   if (narrow == 1) return;
   if (narrow == 2) {
     if (threadIdx.x < 4) phase_smem()[threadIdx.x] = 0;
@@ -719,12 +709,13 @@ __global__ void __launch_bounds__(NT, MINB) k_sssp(SsspParams p) {
       uint4 *d4 = reinterpret_cast<uint4 *>(&st);
       for (int i = 0; i < (int)(sizeof(LevelState) / 16); ++i) d4[i] = __ldcg(s4 + i);
       st.n_hp = ld_cg(&C->n_hp_in);
+      st.drow = drow;
     }
     __syncthreads();
   }
   // ---- a1 init: dist <- UNREACHED (d(s) = 0), vis <- no-in-edge vertices | {s}  (Q4, Q7)
   if (narrow != 2) {
-  for (uint32_t i = gtid; i < p.n; i += nthreads) p.dist[i] = (i == src) ? 0u : kUnreached;
+  for (uint32_t i = gtid; i < p.n; i += nthreads) drow[i] = (i == src) ? 0u : kUnreached;
   for (uint32_t w = gtid; w < p.nwords; w += nthreads)
     p.vis[w] = p.noin[w] | ((w == (src >> 5)) ? (1u << (src & 31)) : 0u);
   if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -752,6 +743,7 @@ __global__ void __launch_bounds__(NT, MINB) k_sssp(SsspParams p) {
     st = LevelState{};
     st.dir = (p.variant == DAWN_PULL) ? kPull : kPush;
     st.n_hp = ld_cg(&C->n_hp_in);
+    st.drow = drow;
   }
   }
   grid_sync(&C->bar, nblocks, bar_target);
@@ -887,7 +879,7 @@ __global__ void __launch_bounds__(NT, MINB) k_sssp(SsspParams p) {
 
   if (p.trace && gtid == 0) p.trace[kTraceCap - 1].t_last = globaltimer();
   // ---- a7 statistics
-  if (p.stats) {
+  if (stats_out) {
     block_flush(0u, examined, nullptr, &C->examined, red);
     grid_sync(&C->bar, nblocks, bar_target);
     if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -898,9 +890,11 @@ __global__ void __launch_bounds__(NT, MINB) k_sssp(SsspParams p) {
       s.edges_examined = st.push_edges + ld_cg(&C->examined);
       s.push_levels = st.push_levels;
       s.pull_levels = st.pull_levels;
-      *p.stats = s;
+      *stats_out = s;
     }
   }
+  if (si + 1 < nsrc) grid_sync(&C->bar, nblocks, bar_target);  // before the next init
+  }  // sources
   grid_exit(&C->bar, nblocks);
 }
 

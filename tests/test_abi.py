@@ -60,6 +60,8 @@ def test_host_validation_errors_before_device_work():
                                  ctypes.byref(h)) == 5
     assert b"workspace" in L.dawn_last_error()
     assert L.dawn_sssp(None, 0, 0, None, None, None) == 1
+    assert L.dawn_sssp_batch(None, None, 4, 0, None, None, None) == 1
+    assert L.dawn_sssp_batch(None, None, -1, 0, None, None, None) == 1
     assert L.dawn_graph_destroy(None) == 0
 
 
