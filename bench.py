@@ -187,48 +187,30 @@ def run_sssp(args, rank, world, dev, cfg=None, steps=None, warmup=None, e2e=True
     flush = torch.empty(int(2.2 * 132644864) // 4, dtype=torch.int32, device=dev)
     stream = torch.cuda.current_stream()
 
-    def step(times=None):
-        for i, s in enumerate(srcs):
-            if times is not None:
-                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                e0.record(stream)
-                dawn.sssp(G, int(s), args.variant, out=orow(i))
-                e1.record(stream)
-                times.append((e0, e1))
-            else:
-                dawn.sssp(G, int(s), args.variant, out=orow(i))
+    dsrc = torch.from_numpy(srcs.astype(np.int32)).to(dev)
+    outk = out[:k]
 
-    # The timed step replays a CUDA graph of the k dawn_sssp calls (captured once, after an
-    # eager warm-up): back-to-back launches with no host gaps, so per-source time is kernel time
-    # even for tiny graphs (C1), whose kernels are shorter than a Python-level launch.
+    def step():
+        # the public batch call: the k searches one after the other (dawn_sssp_batch: one
+        # k_sssp launch, or k_small / per-search k_narrow + k_sssp where those apply)
+        dawn.sssp_batch(G, dsrc, args.variant, out=outk)
+
     step()
     torch.cuda.synchronize()
-    graph = None
-    if not getattr(args, "no_graph", False):
-        cap = torch.cuda.Stream(device=dev)
-        cap.wait_stream(stream)
-        graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(graph, stream=cap):
-            step()
-        torch.cuda.synchronize()
-    run = graph.replay if graph is not None else step
     for _ in range(warmup):
-        run()
+        step()
         flush.zero_()
     torch.cuda.synchronize()
     if world > 1:
         tdist.barrier()
     torch.cuda.synchronize()
-    step_ms, launch_pairs = [], []
+    step_ms = []
     with ClockSampler(dev.index if dev.index is not None else 0) as clk:
         for _ in range(steps):
             flush.zero_()  # L2 flush between timed steps (write 2.2x L2)
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(stream)
-            if graph is not None:
-                graph.replay()
-            else:
-                step(launch_pairs)
+            step()
             b.record(stream)
             torch.cuda.synchronize()
             step_ms.append(a.elapsed_time(b))
@@ -236,11 +218,8 @@ def run_sssp(args, rank, world, dev, cfg=None, steps=None, warmup=None, e2e=True
         tdist.barrier()
     torch.cuda.synchronize()
     tot_ms = sum(step_ms)
-    # average dawn_sssp duration over the timed region: per-call events (eager) or, for graph
-    # replay, the timed steps divided by the calls they contain (back to back, so inter-kernel
-    # gaps count against us)
-    launch_ms = ([x.elapsed_time(y) for x, y in launch_pairs] if launch_pairs
-                 else [sum(step_ms) / (len(step_ms) * k)])
+    # average duration of one search over the timed region: timed steps / searches they contain
+    launch_ms = [sum(step_ms) / (len(step_ms) * k)]
     if world > 1:
         t = torch.tensor([tot_ms], dtype=torch.float64, device=dev)
         tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
@@ -315,8 +294,9 @@ def run_sssp(args, rank, world, dev, cfg=None, steps=None, warmup=None, e2e=True
                    "teps_numerator": "E_reach = sum of out-degrees of reached vertices incl. s "
                                      "(directed arcs, PAPER E10)",
                    "parallelism": f"dp{world} (independent sources per rank)"},
-        # k_narrow + k_sssp per call on narrow-eligible graphs (include/dawn.h), else one kernel
-        "gpu_launches": k * steps * (2 if (g.m <= 6 * g.n and g.n <= 20971520 and cfg != "C1") else 1),
+        # dawn_sssp_batch: k_narrow + k_sssp per search on cluster-start graphs (C3), else one
+        # launch per step
+        "gpu_launches": steps * (2 * k if cfg == "C3" else 1),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
                      "kernel": KERNEL_OF.get(cfg, KERNEL_OF["C2"]),
@@ -508,8 +488,6 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=15.0, help="seconds of oracle CPU work")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-secondary", dest="secondary", action="store_false")
-    ap.add_argument("--no-graph", action="store_true",
-                    help="time eager dawn_sssp calls instead of a CUDA-graph replay of them")
     ap.add_argument("--no-extra", dest="extra", action="store_false",
                     help="skip the C1/C3/C4 lines (reported under extra_configs)")
     args = ap.parse_args()

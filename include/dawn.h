@@ -184,13 +184,18 @@ dawn_status dawn_sssp(dawn_graph g, int64_t source, uint32_t variant, uint32_t *
                       dawn_sssp_stats *stats, void *stream);
 
 /*
- * k single-source searches one after the other in ONE launch of the grid-wide kernel (a grid
- * barrier between searches instead of a kernel boundary): the same results as k dawn_sssp calls.
+ * k single-source searches with the same results as k dawn_sssp calls (the
+ * sources are independent), on one stream with no host work between them:
+ *   - graphs small enough for the one-CTA kernel: ONE launch of min(k, #SMs) CTAs, each holding
+ *     the CSR in its shared memory and running searches b, b + grid, ... (concurrently);
+ *   - graphs dawn_sssp starts on the cluster kernel: per search, k_narrow then k_sssp, both
+ *     reading the source id from the device array;
+ *   - otherwise ONE launch of the grid-wide kernel running the k searches one after the other
+ *     (a grid barrier between searches instead of a kernel boundary).
  *   sources  DEVICE uint32[k], each in [0, n) (not checked: the array is not read on the host)
  *   dist     device uint32[k][n] (row i for sources[i], fully overwritten)
  *   stats    device dawn_sssp_stats[k] or NULL
- * Graphs that dawn_sssp would start on the cluster kernel or on the one-CTA kernel are searched
- * by the grid-wide kernel here.
+ * k == 0 is a no-op; k >= 2^32 -> CAPACITY.
  */
 dawn_status dawn_sssp_batch(dawn_graph g, const uint32_t *sources, int64_t k, uint32_t variant,
                             uint32_t *dist, dawn_sssp_stats *stats, void *stream);

@@ -215,8 +215,9 @@ def sssp(g: Graph, source: int, variant="auto", stats: bool = False, out: torch.
 
 def sssp_batch(g: Graph, sources: torch.Tensor, variant="auto", stats: bool = False,
                out: torch.Tensor | None = None, stream=None):
-    """dawn_sssp_batch: k single-source searches, one after the other in ONE launch (no kernel
-    boundary between them).  `sources`: uint32/int32 CUDA tensor [k] of vertex ids in [0, n).
+    """dawn_sssp_batch: k single-source searches with no host work between them (include/dawn.h:
+    concurrent one-CTA searches on tiny graphs, one grid-wide launch running them one after the
+    other otherwise).  `sources`: uint32/int32 CUDA tensor [k] of vertex ids in [0, n).
     Returns dist int32 [k, n] (and stats int64 [k, 4] = k dawn_sssp_stats when stats=True)."""
     assert sources.is_cuda and sources.dtype in (torch.int32, torch.uint32)
     k = sources.numel()

@@ -649,6 +649,48 @@ static dawn_status launch_sssp(dawn_graph g, SsspParams &p, cudaStream_t stream)
   return DAWN_OK;
 }
 
+static dawn_status launch_narrow(dawn_graph g, const SsspParams &p, uint32_t source,
+                                 const uint32_t *src_dev, cudaStream_t stream) {
+  const Layout &L = g->L;
+  NarrowParams np{};
+  np.n = p.n;
+  np.nwords = p.nwords;
+  np.wpc = g->narrow_wpc;
+  np.qcap = g->narrow_qcap;
+  np.rp = p.rp;
+  np.arc = L.arc ? at<uint4>(g, L.arc) : nullptr;
+  np.col = g->col;
+  np.owner = g->narrow_owner ? 1u : 0u;
+  np.handover_m = g->handover_m;
+  np.noin = p.noin;
+  np.vis = p.vis;
+  np.dist = p.dist;
+  np.fb0 = p.fb[0];
+  np.fb1 = p.fb[1];
+  np.ctrl = p.ctrl;
+  np.stats = p.stats;
+  np.source = source;
+  np.src_dev = src_dev;
+  np.max_reach_base = g->n_hasin;
+  np.seq = p.seq;
+  np.trace = p.trace;
+  cudaLaunchConfig_t cfg{};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = kNarrowCluster;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.gridDim = dim3(g->narrow_grid);
+  cfg.blockDim = dim3(kNarrowThreads);
+  cfg.dynamicSmemBytes = g->narrow_smem;
+  cfg.stream = stream;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, k_narrow, np);
+  if (e != cudaSuccess) return cuda_fail(e, "k_narrow launch");
+  return DAWN_OK;
+}
+
 dawn_status dawn_sssp(dawn_graph g, int64_t source, uint32_t variant, uint32_t *dist,
                       dawn_sssp_stats *stats, void *stream) {
   g_err.clear();
@@ -665,7 +707,7 @@ dawn_status dawn_sssp(dawn_graph g, int64_t source, uint32_t variant, uint32_t *
   if (variant != DAWN_PULL && !g->trace && small_bytes <= g->small_cap) {
     // whole SSSP in one CTA's shared memory (tiny graphs, e.g. configs[0])
     SmallParams sp{(uint32_t)g->n, (uint32_t)g->m, at<uint32_t>(g, L.rp), g->col, dist, stats,
-                   (uint32_t)source};
+                   (uint32_t)source, nullptr, 0u};
     k_small<1024><<<1, 1024, small_bytes, static_cast<cudaStream_t>(stream)>>>(sp);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "k_small launch");
@@ -676,41 +718,8 @@ dawn_status dawn_sssp(dawn_graph g, int64_t source, uint32_t variant, uint32_t *
   if (variant != DAWN_PULL && g->narrow_ok && g->cluster_start) {
     // the search starts on one 16-CTA cluster (state in distributed shared memory); k_sssp
     // below resumes from its hand-over (wide frontier or full queue) or exits at once
-    NarrowParams np{};
-    np.n = p.n;
-    np.nwords = p.nwords;
-    np.wpc = g->narrow_wpc;
-    np.qcap = g->narrow_qcap;
-    np.rp = p.rp;
-    np.arc = L.arc ? at<uint4>(g, L.arc) : nullptr;
-    np.col = g->col;
-    np.owner = g->narrow_owner ? 1u : 0u;
-    np.handover_m = g->handover_m;
-    np.noin = p.noin;
-    np.vis = p.vis;
-    np.dist = dist;
-    np.fb0 = p.fb[0];
-    np.fb1 = p.fb[1];
-    np.ctrl = p.ctrl;
-    np.stats = stats;
-    np.source = (uint32_t)source;
-    np.max_reach_base = g->n_hasin;
-    np.seq = p.seq;
-    np.trace = p.trace;
-    cudaLaunchConfig_t cfg{};
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = kNarrowCluster;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.gridDim = dim3(g->narrow_grid);
-    cfg.blockDim = dim3(kNarrowThreads);
-    cfg.dynamicSmemBytes = g->narrow_smem;
-    cfg.stream = static_cast<cudaStream_t>(stream);
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, k_narrow, np);
-    if (e != cudaSuccess) return cuda_fail(e, "k_narrow launch");
+    dawn_status sn = launch_narrow(g, p, (uint32_t)source, nullptr, static_cast<cudaStream_t>(stream));
+    if (sn != DAWN_OK) return sn;
   }
   return launch_sssp(g, p, static_cast<cudaStream_t>(stream));
 }
@@ -719,7 +728,7 @@ dawn_status dawn_sssp(dawn_graph g, int64_t source, uint32_t variant, uint32_t *
 dawn_status dawn_sssp_batch(dawn_graph g, const uint32_t *sources, int64_t k, uint32_t variant,
                             uint32_t *dist, dawn_sssp_stats *stats, void *stream) {
   g_err.clear();
-  if (!g || !dist || (!sources && k > 0) || k < 0)
+  if (!g || k < 0 || (k > 0 && (!dist || !sources)))
     return fail(DAWN_ERR_INVALID_ARGUMENT, "bad arguments");
   if (variant > DAWN_PULL) return fail(DAWN_ERR_INVALID_ARGUMENT, "unknown variant");
   if (variant == DAWN_PULL && !g->has_csc)
@@ -729,6 +738,32 @@ dawn_status dawn_sssp_batch(dawn_graph g, const uint32_t *sources, int64_t k, ui
   dawn_status s = set_device(g);
   if (s != DAWN_OK) return s;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const size_t small_bytes = small_smem_bytes(g->n, g->m);
+  if (variant != DAWN_PULL && !g->trace && small_bytes <= g->small_cap) {
+    // tiny graphs: the searches are independent, so up to one CTA per SM, each loading the CSR
+    // into its shared memory once and running searches blockIdx.x, blockIdx.x + grid, ...
+    SmallParams sp{(uint32_t)g->n, (uint32_t)g->m, at<uint32_t>(g, g->L.rp), g->col, dist, stats,
+                   0u, sources, (uint32_t)k};
+    const unsigned grid = (unsigned)std::min<int64_t>(k, g->nsm);
+    k_small<1024><<<grid, 1024, small_bytes, st>>>(sp);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "k_small launch");
+    return DAWN_OK;
+  }
+  if (variant != DAWN_PULL && g->narrow_ok && g->cluster_start) {
+    // cluster-start graphs: per search, k_narrow then k_sssp (resume or exit), both reading the
+    // source id from the device list
+    for (int64_t i = 0; i < k; ++i) {
+      SsspParams p = sssp_params(g, variant, dist + (size_t)i * g->n, stats ? stats + i : nullptr);
+      p.sources = sources + i;
+      p.nsrc = 1;
+      dawn_status sn = launch_narrow(g, p, 0u, sources + i, st);
+      if (sn != DAWN_OK) return sn;
+      sn = launch_sssp(g, p, st);
+      if (sn != DAWN_OK) return sn;
+    }
+    return DAWN_OK;
+  }
   SsspParams p = sssp_params(g, variant, dist, stats);
   p.sources = sources;
   p.nsrc = (uint32_t)k;

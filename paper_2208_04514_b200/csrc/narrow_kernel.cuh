@@ -79,6 +79,7 @@ struct NarrowParams {
   Ctrl *ctrl;
   dawn_sssp_stats *stats;
   uint32_t source, max_reach_base, seq;  // max_reach_base = #vertices with an in-edge
+  const uint32_t *src_dev;               // source id on the device (dawn_sssp_batch) or NULL
   TraceRec *trace;                 // per-level trace (DAWN_GRAPH_TRACE) or NULL
 };
 
@@ -277,7 +278,7 @@ __global__ void __launch_bounds__(kNarrowThreads, 1) k_narrow(NarrowParams p) {
   uint4 *qbuf0 = reinterpret_cast<uint4 *>(smraw + q0off);
   uint4 *abuf0 = qbuf0 + 2 * (size_t)p.qcap;  // row arcs of the staged entries
   Ctrl *C = p.ctrl;
-  const uint32_t src = p.source, tid = threadIdx.x;
+  const uint32_t src = p.src_dev ? ld_nc(p.src_dev) : p.source, tid = threadIdx.x;
   const uint32_t gtid = blockIdx.x * kNarrowThreads + tid, nthreads = gridDim.x * kNarrowThreads;
 
   // ---- a1 init, grid-wide: dist <- UNREACHED (d(s) = 0); hand-over bitmaps cleared

@@ -14,9 +14,11 @@ struct SmallParams {
   uint32_t n, m;
   const uint32_t *rp;
   const int32_t *col;
-  uint32_t *dist;
-  dawn_sssp_stats *stats;
+  uint32_t *dist;             // [nsrc or 1][n]
+  dawn_sssp_stats *stats;     // [nsrc or 1] or NULL
   uint32_t source;
+  const uint32_t *sources;    // batch mode (dawn_sssp_batch): nsrc device source ids
+  uint32_t nsrc;
 };
 
 // Shared-memory bytes k_small needs for (n, m).
@@ -56,10 +58,14 @@ __global__ void __launch_bounds__(NT) k_small(SmallParams p) {
       for (int u = 0; u < U; ++u) if (i0 + u * NT < m) col[i0 + u * NT] = v[u];
     }
   }
+  // the CSR stays in shared memory for every search of a batch; batch searches are independent,
+  // so CTA b takes searches b, b + gridDim.x, ...
+  const uint32_t nsrc = p.nsrc ? p.nsrc : 1u;
+  for (uint32_t si = blockIdx.x; si < nsrc; si += gridDim.x) {
   for (uint32_t i = tid; i < n; i += NT) dist[i] = kUnreached;
   for (uint32_t i = tid; i < nw; i += NT) vis[i] = 0;
   __syncthreads();
-  const uint32_t s = p.source;
+  const uint32_t s = p.nsrc ? p.sources[si] : p.source;
   if (tid == 0) {
     dist[s] = 0;
     vis[s >> 5] = 1u << (s & 31);
@@ -115,7 +121,8 @@ __global__ void __launch_bounds__(NT) k_small(SmallParams p) {
     nxt = t;
     ++L;
   }
-  for (uint32_t i = tid; i < n; i += NT) p.dist[i] = dist[i];
+  uint32_t *drow = p.dist + (size_t)si * n;
+  for (uint32_t i = tid; i < n; i += NT) drow[i] = dist[i];
   if (p.stats && tid == 0) {
     dawn_sssp_stats st;
     st.levels = ecc;
@@ -124,8 +131,10 @@ __global__ void __launch_bounds__(NT) k_small(SmallParams p) {
     st.edges_examined = m_acc;
     st.push_levels = levels;
     st.pull_levels = 0;
-    *p.stats = st;
+    p.stats[si] = st;
   }
+  __syncthreads();  // the next search re-initialises dist / vis / counters
+  }  // sources
 }
 
 }  // namespace dawn

@@ -700,7 +700,7 @@ __global__ void __launch_bounds__(NT, MINB) k_sssp(SsspParams p) {
   if (p.trace && gtid == 0) p.trace[kTraceCap - 1].t_ns = globaltimer();  // kernel timeline
   // ---- k_narrow ran first for this call: finished (nothing to do) or hand-over (resume)
   uint32_t narrow = 0;
-  if (!p.nsrc && ld_acquire(&C->narrow_seq) == p.seq) narrow = ld_cg(&C->narrow_status);
+  if (p.nsrc <= 1 && ld_acquire(&C->narrow_seq) == p.seq) narrow = ld_cg(&C->narrow_status);
   if (narrow == 1) return;
   if (narrow == 2) {
     if (threadIdx.x < 4) phase_smem()[threadIdx.x] = 0;

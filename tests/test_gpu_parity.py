@@ -357,3 +357,32 @@ def test_sssp_batch_matches_single_calls():
                 rec, er = oracle.record(g.n, g.row_ptr, int(s), exp)
                 sd = dawn.stats_to_dict(st[i])
                 assert sd["levels"] == int(rec["ecc"]) and sd["edges_reach"] == er, (g.name, v, sd)
+
+
+
+def test_sssp_batch_paths():
+    # the three dawn_sssp_batch paths against the oracle: k_small with more searches than CTAs
+    # (each CTA strides over the batch), cluster start (k_narrow + k_sssp per search, with and
+    # without forced hand-over) and the grid-wide kernel forced on the same mesh; k == 0
+    small = graphgen.er(1000, 8000, 5)
+    G = dev_graph(small)
+    srcs = np.arange(0, 1000, 3, dtype=np.int32)                   # 334 > #SMs
+    d = dawn.sssp_batch(G, torch.from_numpy(srcs).cuda()).cpu().numpy().view(np.uint32)
+    for i in range(0, len(srcs), 37):
+        assert np.array_equal(d[i], oracle.bfs_fifo(small.n, small.row_ptr, small.col,
+                                                     int(srcs[i]))[0]), int(srcs[i])
+    assert dawn.sssp_batch(G, torch.empty(0, dtype=torch.int32, device="cuda")).shape == (0, 1000)
+    mesh = graphgen.grid(700, 500)
+    G = dev_graph(mesh)
+    srcs = np.array([0, mesh.n - 1, 12345, 0], dtype=np.int32)
+    exp = [oracle.bfs_fifo(mesh.n, mesh.row_ptr, mesh.col, int(s))[0] for s in srcs]
+    for knobs in ({"cluster_start": 1}, {"cluster_start": 1, "cluster_handover_edges": 64},
+                  {"cluster_start": 0}):
+        G.set_tuning(**knobs)
+        d, st = dawn.sssp_batch(G, torch.from_numpy(srcs).cuda(), stats=True)
+        d = d.cpu().numpy().view(np.uint32)
+        for i, s in enumerate(srcs):
+            assert np.array_equal(d[i], exp[i]), (knobs, int(s))
+            rec, er = oracle.record(mesh.n, mesh.row_ptr, int(s), exp[i])
+            sd = dawn.stats_to_dict(st[i])
+            assert sd["levels"] == int(rec["ecc"]) and sd["edges_reach"] == er, (knobs, sd)
