@@ -240,6 +240,41 @@ def run_sssp(args, rank, world, dev, cfg=None, steps=None, warmup=None, e2e=True
     if os.path.exists(tp):
         traffic = json.load(open(tp)).get(f"sssp-{cfg}-{args.variant}")
 
+    # context, not the headline: (1) the latency of ONE dawn_sssp call (L2 flushed before each),
+    # (2) the same distinct sources through the bit-parallel multi-source kernel (dawn_msssp)
+    lat = []
+    for i in range(min(k, 16)):
+        flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        dawn.sssp(G, int(srcs[i]), args.variant, out=outk[i])
+        b.record(stream)
+        torch.cuda.synchronize()
+        lat.append(a.elapsed_time(b))
+    single = {"median_us": float(np.median(lat)) * 1e3, "calls": len(lat),
+              "gteps": float(np.mean(er[:len(lat)])) / (float(np.median(lat)) * 1e-3) / 1e9}
+    uniq = len(set(int(x) for x in srcs))
+    if uniq == k and k >= 64 and args.variant == "auto":
+        ms_dist = torch.empty((k, g.n), dtype=torch.int32, device=dev)
+        dawn.msssp(G, srcs, dist=True, records=False, d_out=ms_dist)
+        torch.cuda.synchronize()
+        assert torch.equal(ms_dist, outk), "dawn_msssp distances differ from dawn_sssp_batch"
+        mt = []
+        for _ in range(3):
+            flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            dawn.msssp(G, srcs, dist=True, records=False, d_out=ms_dist)
+            b.record(stream)
+            torch.cuda.synchronize()
+            mt.append(a.elapsed_time(b))
+        single["msssp_same_sources"] = {
+            "gteps": edges_step / (float(np.median(mt)) * 1e-3) / 1e9,
+            "ms": float(np.median(mt)),
+            "how": "dawn_msssp on the same k sources (one bit-parallel pass, dist rows written), "
+                   "distances checked equal to the batch's"}
+        del ms_dist
+
     if not e2e:
         peak, _ = peaks()
         return {"value": value, "unit": "GTEPS", "ms_per_step": tot_ms / steps, "steps": steps,
@@ -251,7 +286,7 @@ def run_sssp(args, rank, world, dev, cfg=None, steps=None, warmup=None, e2e=True
                              "traffic": traffic, "achieved_exec": achieved_exec,
                              "frac_exec": achieved_exec / peak,
                              "bytes_model": "B_SOVM = 4*E_reach + 8*S_reach + 4*n"},
-                "clocks": clk.summary()}, g, srcs, er
+                "single_search": single, "clocks": clk.summary()}, g, srcs, er
     # e2e through the public API with HOST buffers: sources H2D (pinned) + 64 dist rows D2H
     host_src = torch.from_numpy(srcs.copy()).pin_memory()
     dev_src = torch.empty_like(host_src, device=dev)
@@ -313,6 +348,7 @@ def run_sssp(args, rank, world, dev, cfg=None, steps=None, warmup=None, e2e=True
         "levels": {"push_mean": float(np.mean(pushl)), "pull_mean": float(np.mean(pulll)),
                    "edges_examined_mean": float(np.mean(examined)),
                    "edges_reach_mean": float(np.mean(er))},
+        "single_search": single,
         "clocks": clk.summary(),
     }
     return res, g, srcs, er

@@ -239,12 +239,17 @@ def records_to_numpy(rec: torch.Tensor) -> np.ndarray:
     return np.frombuffer(rec.cpu().numpy().tobytes(), dtype=REC_DTYPE)
 
 
-def msssp(g: Graph, sources, dist: bool = True, records: bool = True, stream=None):
-    """dawn_msssp (64-source bit-parallel kernel).  Returns (dist int32[k, n] | None,
-    records int64[k, 4] CUDA tensor (32-byte dawn_record rows) | None)."""
+def msssp(g: Graph, sources, dist: bool = True, records: bool = True, stream=None,
+          d_out: torch.Tensor | None = None):
+    """dawn_msssp (bit-parallel kernel, DAWN_MS_BATCH = 256 sources per pass).  Returns
+    (dist int32[k, n] | None, records int64[k, 4] CUDA tensor (32-byte dawn_record rows) | None).
+    `d_out`: optional preallocated contiguous int32 [k, n] CUDA tensor for the distances."""
     src = np.ascontiguousarray(np.asarray(sources, dtype=np.int64).reshape(-1))
     k = len(src)
-    d = torch.empty((k, g.n), dtype=torch.int32, device=g.device) if dist else None
+    d = None
+    if dist:
+        d = d_out if d_out is not None else torch.empty((k, g.n), dtype=torch.int32, device=g.device)
+        assert d.shape == (k, g.n) and d.dtype == torch.int32 and d.is_contiguous()
     r = torch.empty((k, 4), dtype=torch.int64, device=g.device) if records else None
     _check(lib().dawn_msssp(g.handle, src.ctypes.data_as(ctypes.c_void_p), k, _dptr(d), _dptr(r),
                             _stream(stream)))
