@@ -152,10 +152,11 @@ def cpu_oracle_apsp(g, verts, budget_s: float):
 
 # ------------------------------------------------------------------------------- GPU arms
 # the kernel that does the work of one dawn_sssp call on each config (the dominant kernel)
-KERNEL_OF = {"C1": "k_small (whole SSSP on one CTA, CSR in shared memory)",
-             "C2": "k_sssp (one persistent launch per SSSP)",
+KERNEL_OF = {"C1": "k_small (one SSSP per CTA, CSR in shared memory; the batch's searches run "
+                   "on min(k, #SMs) CTAs at once)",
+             "C2": "k_sssp (one persistent launch running the batch's SSSPs back to back)",
              "C3": "k_narrow (one 16-CTA cluster per SSSP; the k_sssp behind it exits at once)",
-             "C4": "k_sssp (one persistent launch per SSSP)"}
+             "C4": "k_sssp (one persistent launch running the batch's SSSPs back to back)"}
 
 
 def run_sssp(args, rank, world, dev, cfg=None, steps=None, warmup=None, e2e=True, reps=1):
