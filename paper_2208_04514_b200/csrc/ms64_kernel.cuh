@@ -236,10 +236,12 @@ __global__ void __launch_bounds__(NT, DAWN_MS_MINB) k_ms64(MsParams p) {
       active.w[i] = (int)bk >= lo + 64 ? ~0ull : ((int)bk <= lo ? 0ull : ((1ull << (bk - lo)) - 1));
     }
     // ---- init
+    // nxt is all-zero at the end of every batch (each level's vertex pass clears what it
+    // consumed), so only the launch's first batch clears it
     for (uint32_t x = gtid; x < p.n * W; x += nthreads) {
       p.seen[x] = 0;
       p.F[0][x] = 0;
-      p.nxt[x] = 0;
+      if (bt == 0) p.nxt[x] = 0;
     }
     if (p.dist) {
       const size_t tot = (size_t)bk * p.n;
@@ -254,19 +256,31 @@ __global__ void __launch_bounds__(NT, DAWN_MS_MINB) k_ms64(MsParams p) {
     }
     if (blockIdx.x == 0 && threadIdx.x < 12) (&C->cnt[0][0])[threadIdx.x] = 0;
     grid_sync(&C->bar, nblocks, bar_target);
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if (blockIdx.x == 0) {
+      // batch sources in parallel (one thread per source): set bit k of s's seen / frontier
+      // words; the level-0 frontier counters count each distinct vertex once (a repeated source
+      // is counted by its first occurrence only).  A serial loop here had held every other CTA
+      // at the next barrier for ~200 us per batch.
+      uint32_t *ssrc = reinterpret_cast<uint32_t *>(hsm);  // hsm is free outside the levels
+      for (uint32_t k = threadIdx.x; k < bk; k += NT) ssrc[k] = p.sources[bbase + k];
+      __syncthreads();
       unsigned long long na = 0, ma = 0;
-      for (uint32_t k = 0; k < bk; ++k) {
-        const uint32_t s = p.sources[bbase + k];
+      for (uint32_t k = threadIdx.x; k < bk; k += NT) {
+        const uint32_t s = ssrc[k];
         bool fresh = true;
-        for (int i = 0; i < W; ++i) fresh = fresh && p.F[0][(size_t)s * W + i] == 0;
-        if (fresh) { na++; ma += p.rp[s + 1] - p.rp[s]; }
-        p.seen[(size_t)s * W + k / 64] |= 1ull << (k % 64);
-        p.F[0][(size_t)s * W + k / 64] |= 1ull << (k % 64);
+        for (uint32_t j = 0; j < k && fresh; ++j) fresh = ssrc[j] != s;
+        if (fresh) { na += 1; ma += p.rp[s + 1] - p.rp[s]; }
+        atomicOr(p.seen + (size_t)s * W + k / 64, 1ull << (k % 64));
+        atomicOr(p.F[0] + (size_t)s * W + k / 64, 1ull << (k % 64));
         if (p.dist) p.dist[(size_t)(bbase + k) * p.n + s] = 0;
       }
-      C->cnt[0][0] = na;
-      C->cnt[0][1] = ma;
+      na = warp_sum(na);
+      ma = warp_sum(ma);
+      if (lane == 0 && na) {
+        atomicAdd(&C->cnt[0][0], na);
+        atomicAdd(&C->cnt[0][1], ma);
+      }
+      __syncthreads();
     }
     if (threadIdx.x == 0) {
       st = MsState{0, kPush, 0, 0, ld_cg(&p.sctrl->n_hp_out), ld_cg(&p.sctrl->n_hp_in), 0, 0,
@@ -646,19 +660,26 @@ __global__ void __launch_bounds__(NT, DAWN_MS_MINB) k_ms64(MsParams p) {
             make_uint4((uint32_t)sm, (uint32_t)(sm >> 32), (uint32_t)hh, (uint32_t)(hh >> 32));
       }
       grid_sync(&C->bar, nblocks, bar_target);
-      if (blockIdx.x == 0) {
-        for (uint32_t k = threadIdx.x; k < bk; k += NT) {
+      // one warp per source over the whole grid, lanes split the CTA partials (one CTA doing
+      // all 256 sources serially over 148 partials each held the grid ~20 us per batch)
+      for (uint32_t k = gwarp; k < bk; k += nwarps) {
+        uint32_t c = 0, e = 0;
+        unsigned long long sm = 0, hh = 0;
+        for (uint32_t b = lane; b < nblocks; b += 32) {
+          const uint4 x = __ldcg(p.part + b * kMsBatch + k);
+          const uint4 y = __ldcg(p.part + (nblocks + b) * kMsBatch + k);
+          c += x.x;
+          e = max(e, x.y);
+          sm += ((unsigned long long)y.y << 32) | y.x;
+          hh += ((unsigned long long)y.w << 32) | y.z;
+        }
+        c = warp_sum(c);
+        sm = warp_sum(sm);
+        hh = warp_sum(hh);
+#pragma unroll
+        for (int o = 16; o; o >>= 1) e = max(e, __shfl_xor_sync(DAWN_FULL, e, o));
+        if (lane == 0) {
           const uint32_t s = p.sources[bbase + k];
-          uint32_t c = 0, e = 0;
-          unsigned long long sm = 0, hh = 0;
-          for (uint32_t b = 0; b < nblocks; ++b) {
-            const uint4 x = __ldcg(p.part + b * kMsBatch + k);
-            const uint4 y = __ldcg(p.part + (nblocks + b) * kMsBatch + k);
-            c += x.x;
-            e = max(e, x.y);
-            sm += ((unsigned long long)y.y << 32) | y.x;
-            hh += ((unsigned long long)y.w << 32) | y.z;
-          }
           dawn_record r;
           r.source = s;
           r.ecc = e;
