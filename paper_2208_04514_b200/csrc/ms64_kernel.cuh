@@ -317,7 +317,7 @@ __global__ void __launch_bounds__(NT, DAWN_MS_MINB) k_ms64(MsParams p) {
       __syncthreads();
       if (st.stop) break;
       const bool trc = p.trace && bt == 0 && st.L < kTraceCap;  // per-phase slowest-warp cycles
-      long long tA = trc ? clock64() : 0, tB = 0, tC = 0, trec = 0;
+      long long tA = trc ? clock64() : 0, tB = 0, tC = 0, trec = 0, tL = 0;
       const uint32_t L1 = st.L + 1;
       const unsigned long long *Fc = p.F[st.cur];
       unsigned long long *Fn = p.F[st.cur ^ 1];
@@ -374,6 +374,7 @@ __global__ void __launch_bounds__(NT, DAWN_MS_MINB) k_ms64(MsParams p) {
             }
           }
         }
+        if (trc) tL = clock64();
         // phase A2: heavy active rows by static pieces.  Warp w takes pieces w + k * nwarps (the
         // live ones of a level spread over all warps) and tests 32 of them at once (lane k: is the
         // piece's vertex in the frontier?) before expanding the live ones — a per-piece test was
@@ -511,6 +512,7 @@ __global__ void __launch_bounds__(NT, DAWN_MS_MINB) k_ms64(MsParams p) {
             if (trc) trec += clock64() - tr0;
           }
         }
+        if (trc) tL = clock64();
         // pass 1b: heavy in-rows by static pieces; partial ORs meet in nxt[u]
         // (pieces w + k * nwarps, 32 tested at once, as in phase A2)
         const uint32_t iend = st.n_hp_in;
@@ -617,6 +619,9 @@ __global__ void __launch_bounds__(NT, DAWN_MS_MINB) k_ms64(MsParams p) {
       if (trc && lane == 0) {
         const long long tD = clock64();
         atomicMax(&p.trace[st.L].cyc[0], (unsigned long long)(tB - tA));
+        // pass-A balance: t_first = sum over warps of pass A cycles, t_last = slowest light pass
+        atomicAdd(&p.trace[st.L].t_first, (unsigned long long)(tB - tA));
+        atomicMax(&p.trace[st.L].t_last, (unsigned long long)(tL - tA));
         atomicMax(&p.trace[st.L].cyc[1], (unsigned long long)(tC - tB));
         atomicMax(&p.trace[st.L].cyc[2], (unsigned long long)(tD - tC));
         atomicMax(&p.trace[st.L].cyc[3], (unsigned long long)trec);

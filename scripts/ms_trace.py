@@ -9,4 +9,5 @@ for rep in range(2):
 tr = G.trace()
 t0 = int(tr["t_ns"][0])
 for r in tr:
-    print("L%d %s n_active=%d m_active=%d start=%.1f us  slowest warp us [pass A, barrier wait, pass B, records] = %s" % (r["level"], "PUSH PULL STOP".split()[r["dir"]], r["nf"], r["mf"], (int(r["t_ns"]) - t0) / 1e3, [round(int(c) / 1965.0, 1) for c in r["cyc"][:4]]))
+    nw = 148 * 16
+    print("L%d %s n_active=%d m_active=%d start=%.1f us  slowest warp us [pass A, barrier wait, pass B, records] = %s  pass A mean %.1f us, slowest light part %.1f us" % (r["level"], "PUSH PULL STOP".split()[r["dir"]], r["nf"], r["mf"], (int(r["t_ns"]) - t0) / 1e3, [round(int(c) / 1965.0, 1) for c in r["cyc"][:4]], int(r["t_first"]) / nw / 1965.0, int(r["t_last"]) / 1965.0))
