@@ -718,6 +718,12 @@ __global__ void __launch_bounds__(NT, MINB) k_sssp(SsspParams p) {
   for (uint32_t i = gtid; i < p.n; i += nthreads) drow[i] = (i == src) ? 0u : kUnreached;
   for (uint32_t w = gtid; w < p.nwords; w += nthreads)
     p.vis[w] = p.noin[w] | ((w == (src >> 5)) ? (1u << (src & 31)) : 0u);
+  {
+    // level-0 chunk map (every 32nd arc of s's row starts in entry 0), spread over the grid: a
+    // hub source has up to ~10^4 chunks
+    const uint32_t d0 = ld_nc(p.rp + src + 1) - ld_nc(p.rp + src);
+    for (uint32_t c = gtid; c * kChunk < d0; c += nthreads) p.Cf[0][c] = 0;
+  }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     for (int i = 0; i < 3; ++i) C->slot[i] = Slot{0, 0, 0, 0, 0};
     C->examined = 0;
@@ -729,7 +735,6 @@ __global__ void __launch_bounds__(NT, MINB) k_sssp(SsspParams p) {
     if (d > 0) {
       p.Lv[0][0] = src;
       p.Lsd[0][0] = make_uint2(rs, 0u);
-      for (uint32_t c = 0; c * kChunk < d; ++c) p.Cf[0][c] = 0;
       s0.qpack = (1ull << 32) | d;
     }
   }
