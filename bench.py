@@ -276,6 +276,24 @@ def run_sssp(args, rank, world, dev, cfg=None, steps=None, warmup=None, e2e=True
                    "distances checked equal to the batch's"}
         del ms_dist
 
+    # the forced-push (pure SOVM, Algorithm 2) schedule on the same sources
+    forced_push = None
+    if args.variant == "auto" and cfg in ("C2", "C4"):
+        dawn.sssp_batch(G, dsrc, "push", out=outk)
+        pt = []
+        for _ in range(2):
+            flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            dawn.sssp_batch(G, dsrc, "push", out=outk)
+            b.record(stream)
+            torch.cuda.synchronize()
+            pt.append(a.elapsed_time(b))
+        pms = float(np.median(pt))
+        forced_push = {"gteps": edges_step / (pms * 1e-3) / 1e9, "ms_per_step": pms,
+                       "achieved_GBps_B_SOVM": float(np.sum(b_sovm)) / (pms * 1e-3) / 1e9,
+                       "how": "dawn_sssp_batch with DAWN_PUSH (every level SOVM) on the same sources"}
+
     if not e2e:
         peak, _ = peaks()
         return {"value": value, "unit": "GTEPS", "ms_per_step": tot_ms / steps, "steps": steps,
@@ -287,7 +305,8 @@ def run_sssp(args, rank, world, dev, cfg=None, steps=None, warmup=None, e2e=True
                              "traffic": traffic, "achieved_exec": achieved_exec,
                              "frac_exec": achieved_exec / peak,
                              "bytes_model": "B_SOVM = 4*E_reach + 8*S_reach + 4*n"},
-                "single_search": single, "clocks": clk.summary()}, g, srcs, er
+                "single_search": single, "forced_push": forced_push,
+                "clocks": clk.summary()}, g, srcs, er
     # e2e through the public API with HOST buffers: sources H2D (pinned) + 64 dist rows D2H
     host_src = torch.from_numpy(srcs.copy()).pin_memory()
     dev_src = torch.empty_like(host_src, device=dev)
@@ -350,9 +369,33 @@ def run_sssp(args, rank, world, dev, cfg=None, steps=None, warmup=None, e2e=True
                    "edges_examined_mean": float(np.mean(examined)),
                    "edges_reach_mean": float(np.mean(er))},
         "single_search": single,
+        "forced_push": forced_push,
         "clocks": clk.summary(),
     }
     return res, g, srcs, er
+
+
+def l2_probe(dev):
+    """L2 bandwidth measured in the same run (context for the L2-resident
+    C5 words and C2's bitmaps): a device copy between two 24 MiB buffers (48 MiB, inside the
+    126 MB L2), 40 back-to-back copies timed with CUDA events after a warm-up."""
+    import torch
+    nb = 24 << 20
+    a = torch.ones(nb // 4, dtype=torch.int32, device=dev)
+    b = torch.empty_like(a)
+    for _ in range(5):
+        b.copy_(a)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(40):
+        b.copy_(a)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / 40
+    return {"copy_GBps": 2 * nb / (ms * 1e-3) / 1e9, "bytes_per_copy": 2 * nb,
+            "how": "torch copy_ of a 24 MiB int32 buffer (read + write counted), L2-resident; a "
+                   "lower bound on L2 bandwidth (the copy kernel's own limit may bind first)"}
 
 
 def run_apsp(args, rank, world, dev, steps=None, warmup=None):
@@ -450,6 +493,8 @@ def run_dawn(args):
             sec, _, _ = run_apsp(args, rank, world, dev, steps=max(1, min(args.steps, 3)),
                                  warmup=1)
             res["secondary"] = sec
+        if world == 1:
+            res["l2_probe"] = l2_probe(dev)
         if rank == 0 and world == 1 and not args.no_cpu:
             gte, done, t = cpu_oracle_sssp(g, srcs, args.cpu_budget)
             res["cpu_baseline"] = {"value": gte, "unit": "GTEPS", "cores": 1, "kind": "oracle",
