@@ -249,6 +249,14 @@ __device__ __forceinline__ void push_item(const SsspParams &p, const LevelState 
   for (int j = 0; j < J; ++j) cur[j] = act[j] ? p.vis[u[j] >> 5] : ~0u;  // weak: stale 0 = atomic
   if constexpr (CAND) {
     // bitmap push: mark the candidate, settle later in cand_filter (no returning atomic)
+#if DAWN_CAND_FILTER
+    // skip targets already marked by an earlier arc of this level (a stale read only costs a
+    // redundant reduction)
+#pragma unroll
+    for (int j = 0; j < J; ++j)
+      if (act[j] && !(cur[j] & (1u << (u[j] & 31))))
+        cur[j] |= (DAWN_CAND_FILTER == 2) ? ld_cg(p.cand + (u[j] >> 5)) : p.cand[u[j] >> 5];
+#endif
 #pragma unroll
     for (int j = 0; j < J; ++j) {
       const uint32_t bit = 1u << (u[j] & 31);
