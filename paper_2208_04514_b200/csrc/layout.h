@@ -52,6 +52,9 @@ static_assert(kMsBatch == DAWN_MS_BATCH, "dawn.h DAWN_MS_BATCH must match kMsW")
 #ifndef DAWN_PULL_PR
 #define DAWN_PULL_PR 4       // ... on dense frontiers
 #endif
+#ifndef DAWN_CAND_FILTER
+#define DAWN_CAND_FILTER 0   // experiment: 1 weak / 2 L2 load of the candidate word before each
+#endif                       // bitmap-push reduction (slower on C2 and C4)
 #ifndef DAWN_HEAVY_ILP
 #define DAWN_HEAVY_ILP 1     // in-edges per lane in flight when a warp scans a heavy pull piece
 #endif
