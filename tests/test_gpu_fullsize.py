@@ -8,6 +8,7 @@ of 256 records bit-exact against the oracle.
 """
 import numpy as np
 import pytest
+import torch
 
 import graphgen
 import oracle
@@ -43,9 +44,20 @@ def c2():
     return g, _dev(g)
 
 
+def _batch(G, srcs):
+    """dawn_sssp_batch, the call bench.py times, as uint32 numpy rows."""
+    d = dawn.sssp_batch(G, torch.from_numpy(np.asarray(srcs, dtype=np.int32)).cuda())
+    return d.cpu().numpy().view(np.uint32)
+
+
 def test_c1_full():
     g = graphgen.config_graph("C1")
-    _check(g, _dev(g), [0] + list(range(1, 1000, 97)))
+    G = _dev(g)
+    _check(g, G, [0] + list(range(1, 1000, 97)))
+    # the bench step: source 0 repeated 64 times, concurrent one-CTA searches
+    exp, _ = oracle.bfs_fifo(g.n, g.row_ptr, g.col, 0)
+    d = _batch(G, [0] * 64)
+    assert all(np.array_equal(row, exp) for row in d)
 
 
 def test_c2_full_sampled_sources(c2):
@@ -55,6 +67,11 @@ def test_c2_full_sampled_sources(c2):
     # certificate (an exact proof) on all 64 bench sources, auto variant
     for s in srcs:
         d = dawn.sssp(G, int(s)).cpu().numpy().view(np.uint32)
+        assert oracle.certify(g.n, g.row_ptr, g.col, g.row_ptr, g.col, int(s), d) == 0
+    # the bench step: one dawn_sssp_batch over the 64 sources; every row certified
+    D = _batch(G, srcs)
+    assert np.array_equal(D[0], oracle.bfs_fifo(g.n, g.row_ptr, g.col, int(srcs[0]))[0])
+    for s, d in zip(srcs, D):
         assert oracle.certify(g.n, g.row_ptr, g.col, g.row_ptr, g.col, int(s), d) == 0
 
 
@@ -78,6 +95,7 @@ def test_c3_grid_closed_form():
         for v in ("auto", "push"):
             d = dawn.sssp(G, s, v).cpu().numpy().view(np.uint32)
             assert np.array_equal(d, exp), (s, v)
+        assert np.array_equal(_batch(G, [s])[0], exp), s      # the bench's call
 
 
 def test_c4_full_sampled_sources():
@@ -86,6 +104,13 @@ def test_c4_full_sampled_sources():
     srcs = g.sample_sources(64, seed=1)
     _check(g, G, srcs[:2], variants=("auto", "push"))
     _check(g, G, srcs[2:3], variants=("pull",))
+    # the bench step (one dawn_sssp_batch over the 64 sources, 2-CTA/SM kernel): two rows
+    # element by element against the oracle, two more certified
+    D = _batch(G, srcs)
+    for i in (0, 63):
+        assert np.array_equal(D[i], oracle.bfs_fifo(g.n, g.row_ptr, g.col, int(srcs[i]))[0]), i
+    for i in (17, 40):
+        assert oracle.certify(g.n, g.row_ptr, g.col, g.row_ptr, g.col, int(srcs[i]), D[i]) == 0
 
 
 def test_c5_apsp_all_sources():
