@@ -52,6 +52,12 @@ static_assert(kMsBatch == DAWN_MS_BATCH, "dawn.h DAWN_MS_BATCH must match kMsW")
 #ifndef DAWN_PULL_PR
 #define DAWN_PULL_PR 4       // ... on dense frontiers
 #endif
+// Push levels read a bitmap frontier directly (no conversion to a queue) when none of its rows
+// is longer than kDirectRow arcs (DAWN_DIRECT_PUSH=0: always convert).
+constexpr uint32_t kDirectRow = 256;
+#ifndef DAWN_DIRECT_PUSH
+#define DAWN_DIRECT_PUSH 1
+#endif
 #ifndef DAWN_CAND_FILTER
 #define DAWN_CAND_FILTER 0   // experiment: 1 weak / 2 L2 load of the candidate word before each
 #endif                       // bitmap-push reduction (slower on C2 and C4)
@@ -66,7 +72,7 @@ enum : uint32_t { kPush = 0, kPull = 1, kRepQueue = 0, kRepBitmap = 1 };
 
 struct Slot {                 // counters of one frontier (3 rotate: written, read, reset)
   uint32_t n_new;             // vertices discovered into this frontier
-  uint32_t pad0;
+  uint32_t big;               // 1: a vertex of this (bitmap) frontier has > kDirectRow arcs
   unsigned long long qpack;   // queue: (entries << 32) | edges  (push-mode representation)
   unsigned long long m_new;   // sum of out-degrees of the frontier (m_f)
   unsigned long long pad1;

@@ -67,6 +67,7 @@ struct __align__(16) LevelState {
   uint32_t push_levels, pull_levels, reached;
   uint32_t qn, n_hp;            // queue entries of frontier L; static heavy pieces
   uint32_t qe;                  // queue edges of frontier L
+  uint32_t big;                 // frontier L (bitmap form) has a row of > kDirectRow arcs
   unsigned long long mf, explored, push_edges, pad;
   uint32_t *drow;               // this search's distance row
 };
@@ -318,6 +319,67 @@ __device__ void push_level(const SsspParams &p, const LevelState &st, Slot *ns, 
   phase_add(p, st.L, 2, t0);
 }
 
+// Push level straight from the frontier bitmap fb[b] (the frontier a pull or candidate level
+// left), for frontiers whose rows all have <= kDirectRow arcs (tracked by the levels that build
+// bitmap frontiers): no bitmap -> queue conversion and no grid barrier before the expansion.  A
+// warp takes 32 bitmap words; each round, every lane contributes the next frontier vertex of its
+// word and the round's rows are dealt 32 arcs at a time by the owner search of push_item.
+__device__ void push_bitmap(const SsspParams &p, const LevelState &st, Slot *ns, uint32_t gwarp,
+                            uint32_t nwarps, uint32_t &n_new, unsigned long long &m_new,
+                            WarpStage &stg, long long &t0, unsigned long long *fsm) {
+  const uint32_t lane = lane_id();
+  const uint32_t L1 = st.L + 1;
+  const int qn = st.q ^ 1;
+  const uint32_t *fb = p.fb[st.b];
+  uint32_t cnt = 0;
+  for (uint32_t base = gwarp * 32; base < p.nwords; base += nwarps * 32) {
+    const uint32_t w = base + lane;
+    uint32_t bits = (w < p.nwords) ? ld_cg(fb + w) : 0u;
+    while (__ballot_sync(DAWN_FULL, bits != 0)) {
+      uint32_t rs = 0, d = 0;
+      if (bits) {
+        const uint32_t v = w * 32 + (__ffs(bits) - 1);
+        bits &= bits - 1;
+        rs = ld_nc(p.rp + v);
+        d = ld_nc(p.rp + v + 1) - rs;
+      }
+      const uint32_t incl = warp_incl_scan(d);
+      const uint32_t total = __shfl_sync(DAWN_FULL, incl, 31);
+      const uint32_t excl = incl - d;
+      for (uint32_t r0 = 0; r0 < total; r0 += 32) {
+        const uint32_t t = r0 + lane;
+        uint32_t k = 0;
+#pragma unroll
+        for (uint32_t step = 16; step; step >>= 1) {
+          const uint32_t e = __shfl_sync(DAWN_FULL, excl, k + step);
+          if (e <= t) k += step;
+        }
+        const uint32_t ek = __shfl_sync(DAWN_FULL, excl, k);
+        const uint32_t sk = __shfl_sync(DAWN_FULL, rs, k);
+        const bool act = t < total;
+        const uint32_t u = act ? (uint32_t)ld_nc(p.col + sk + (t - ek)) : 0u;
+        bool disc = false;
+        if (act) {
+          const uint32_t bit = 1u << (u & 31);
+          if (!(p.vis[u >> 5] & bit)) disc = !(atomicOr(p.vis + (u >> 5), bit) & bit);
+        }
+        uint32_t urs = 0, ud = 0;
+        if (disc) {
+          urs = ld_nc(p.rp + u);
+          ud = ld_nc(p.rp + u + 1) - urs;
+          DIST_ST(u, L1);
+          n_new += 1;
+          m_new += ud;
+        }
+        enqueue_frontier(p, ns, qn, disc, u, urs, ud, stg, cnt);
+      }
+    }
+  }
+  phase_add(p, st.L, 0, t0);
+  cta_flush(p, ns, qn, stg, cnt, fsm);
+  phase_add(p, st.L, 2, t0);
+}
+
 __device__ __forceinline__ bool fb_test(const uint32_t *fb, uint32_t v) {
   return (fb[v >> 5] >> (v & 31)) & 1u;
 }
@@ -325,7 +387,7 @@ __device__ __forceinline__ bool fb_test(const uint32_t *fb, uint32_t v) {
 template <int PR>  // in-edges probed per lane per round trip (8 when the frontier is sparse)
 __device__ void pull_level(const SsspParams &p, const LevelState &st, uint32_t gwarp,
                            uint32_t nwarps, uint32_t &n_new, unsigned long long &m_new,
-                           unsigned long long &examined, long long &t0) {
+                           unsigned long long &examined, long long &t0, bool &bigf) {
   const uint32_t lane = lane_id();
   const uint32_t L1 = st.L + 1;
   const uint32_t *fcur = p.fb[st.b];
@@ -419,7 +481,9 @@ __device__ void pull_level(const SsspParams &p, const LevelState &st, uint32_t g
         red_or(fnext + (u[j] >> 5), 1u << (u[j] & 31));
         DIST_ST(u[j], L1);
         n_new += 1;
-        m_new += p.sym ? (e[j] - s[j]) : (ld_nc(p.rp + u[j] + 1) - ld_nc(p.rp + u[j]));
+        const uint32_t dg = p.sym ? (e[j] - s[j]) : (ld_nc(p.rp + u[j] + 1) - ld_nc(p.rp + u[j]));
+        m_new += dg;
+        bigf |= dg > kDirectRow;  // a long row in the frontier (CTA-reduced by the caller)
       }
       // survivors (still unreached) stay in the warp's segment, order preserved
       const bool keep = need[j] && !found[j];
@@ -478,8 +542,10 @@ __device__ void pull_level(const SsspParams &p, const LevelState &st, uint32_t g
               red_or(fnext + w, bit);
               DIST_ST(uk, L1);
               n_new += 1;
-              m_new += p.sym ? (ld_nc(p.irp + uk + 1) - ld_nc(p.irp + uk))
-                             : (ld_nc(p.rp + uk + 1) - ld_nc(p.rp + uk));
+              const uint32_t dg = p.sym ? (ld_nc(p.irp + uk + 1) - ld_nc(p.irp + uk))
+                                        : (ld_nc(p.rp + uk + 1) - ld_nc(p.rp + uk));
+              m_new += dg;
+              bigf |= dg > kDirectRow;
             }
           }
           break;
@@ -496,7 +562,8 @@ __device__ void pull_level(const SsspParams &p, const LevelState &st, uint32_t g
 // write the frontier bitmap fb[b+1] (every word), clear fb[b+2] and cand, set dist = L+1.
 // 32 words per warp iteration (one lane each), then lane-per-vertex for words with news.
 __device__ void cand_filter(const SsspParams &p, const LevelState &st, uint32_t gwarp,
-                            uint32_t nwarps, uint32_t &n_new, unsigned long long &m_new) {
+                            uint32_t nwarps, uint32_t &n_new, unsigned long long &m_new,
+                            bool &bigf) {
   const uint32_t lane = lane_id();
   const uint32_t L1 = st.L + 1;
   uint32_t *fnext = p.fb[(st.b + 1) % 3];
@@ -538,7 +605,10 @@ __device__ void cand_filter(const SsspParams &p, const LevelState &st, uint32_t 
         }
 #pragma unroll
       for (int i = 0; i < 4; ++i)
-        if (i < k) m_new += b[i] - a[i];
+        if (i < k) {
+          m_new += b[i] - a[i];
+          bigf |= b[i] - a[i] > kDirectRow;
+        }
       n_new += k;
     }
   }
@@ -572,6 +642,7 @@ __device__ __forceinline__ void level_header(const SsspParams &p, Ctrl *C, Level
   const unsigned long long qp = ld_cg(&cs->qpack);
   st.qn = (uint32_t)(qp >> 32);
   st.qe = (uint32_t)qp;
+  st.big = ld_cg(&cs->big);
   if (blockIdx.x == 0) C->slot[(st.L + 2) % 3] = Slot{0, 0, 0, 0, 0};
   if (st.L > 0) st.reached += st.nf;
   st.explored += st.mf;
@@ -819,6 +890,10 @@ __global__ void __launch_bounds__(NT, MINB) k_sssp(SsspParams p) {
     }
 
     long long tconv = clock64();
+    // a push from a bitmap frontier without long rows expands the bitmap directly
+    // (1-CTA/SM variant only: in the 64-register one the extra path costs spills, C4 -4%)
+    constexpr bool kDirect = DAWN_DIRECT_PUSH && MINB == 1;
+    const bool direct = kDirect && st.dir == kPush && st.rep == kRepBitmap && !st.bm && !st.big;
     if (st.dir == kPull && st.rep == kRepQueue) {
       // queue -> frontier bitmap fb[b] (and a clean fb[b+1] for the pull to write)
       uint32_t *fb = p.fb[st.b];
@@ -831,7 +906,7 @@ __global__ void __launch_bounds__(NT, MINB) k_sssp(SsspParams p) {
       }
       grid_sync(&C->bar, nblocks, bar_target);
       if (threadIdx.x == 0) st.rep = kRepBitmap;
-    } else if (st.dir == kPush && st.rep == kRepBitmap) {
+    } else if (st.dir == kPush && st.rep == kRepBitmap && !direct) {
       // frontier bitmap fb[b] -> queue q (ballot/popc compaction), barrier
       Slot *cs = &C->slot[st.L % 3];
       const uint32_t *fb = p.fb[st.b];
@@ -866,23 +941,29 @@ __global__ void __launch_bounds__(NT, MINB) k_sssp(SsspParams p) {
     Slot *ns = &C->slot[(st.L + 1) % 3];
     uint32_t n_new = 0;
     unsigned long long m_new = 0;
+    bool bigf = false;  // a bitmap frontier being built has a row of > kDirectRow arcs
     phase_add(p, st.L, 3, tconv);
-    if (st.dir == kPush) {
+    if (kDirect && direct) {
+      push_bitmap(p, st, ns, gwarp, nwarps, n_new, m_new, stg, tconv, fsm);
+    } else if (st.dir == kPush) {
       push_level(p, st, ns, gwarp, nwarps, n_new, m_new, stg, tconv, fsm);
       if (st.bm) {
         grid_sync(&C->bar, nblocks, bar_target);
-        cand_filter(p, st, gwarp, nwarps, n_new, m_new);
+        cand_filter(p, st, gwarp, nwarps, n_new, m_new, bigf);
         phase_add(p, st.L, 1, tconv);
       }
     } else {
 #if DAWN_PULL_DEEP
       if (st.deep)
-        pull_level<DAWN_PULL_DEEP_PR>(p, st, gwarp, nwarps, n_new, m_new, examined, tconv);
+        pull_level<DAWN_PULL_DEEP_PR>(p, st, gwarp, nwarps, n_new, m_new, examined, tconv, bigf);
       else
 #endif
-        pull_level<DAWN_PULL_PR>(p, st, gwarp, nwarps, n_new, m_new, examined, tconv);
+        pull_level<DAWN_PULL_PR>(p, st, gwarp, nwarps, n_new, m_new, examined, tconv, bigf);
     }
     block_flush(n_new, m_new, &ns->n_new, &ns->m_new, red);
+    if constexpr (kDirect) {
+      if (__syncthreads_or(bigf) && threadIdx.x == 0) ns->big = 1;  // one store per CTA at most
+    }
     phase_add(p, st.L, 2, tconv);
     trace_done(p, st.L);
     grid_sync(&C->bar, nblocks, bar_target);
