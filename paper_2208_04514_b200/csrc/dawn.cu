@@ -1,6 +1,7 @@
 // dawn.cu — libdawn.so: the C ABI of include/dawn.h over the sm_100a kernels.
-// Host side validates, lays out the caller's workspace and enqueues ONE cooperative persistent
-// kernel per call (no per-level host work).  No torch types cross this boundary.
+// Host side validates, lays out the caller's workspace and enqueues a fixed number of persistent
+// kernels per call (one; k_narrow + k_sssp on cluster-start graphs), never per-level host work.
+// No torch types cross this boundary.
 #include <cuda_runtime.h>
 
 #include <algorithm>
