@@ -4,7 +4,7 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
-struct Bar { unsigned int count, gen; unsigned long long mono; unsigned int flags[4096]; };
+struct Bar { unsigned int count, gen; unsigned long long mono; unsigned int flags[4096]; unsigned long long subs[16 * 16]; };
 
 __device__ __forceinline__ unsigned ld_acq(const unsigned *p) { unsigned r; asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(r) : "l"(p) : "memory"); return r; }
 __device__ __forceinline__ unsigned long long ld_acq64(const unsigned long long *p) { unsigned long long r; asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(r) : "l"(p) : "memory"); return r; }
@@ -67,6 +67,37 @@ __device__ void bar3(Bar *b, unsigned nb, unsigned &epoch) {
   __syncthreads();
 }
 
+__device__ __forceinline__ void red_add_rel64(unsigned long long *p, unsigned long long v) { asm volatile("red.release.gpu.global.add.u64 [%0], %1;" :: "l"(p), "l"(v) : "memory"); }
+// V4: the production barrier (common.cuh grid_sync): red.release on one monotonic counter
+__device__ void bar4(Bar *b, unsigned nb, unsigned long long &target) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    target += nb;
+    red_add_rel64(&b->mono, 1ull);
+    while (ld_acq64(&b->mono) < target) {}
+    fence_acqrel();
+  }
+  __syncthreads();
+}
+// V5/V6: S monotonic sub-counters on separate 128-byte lines (CTA b arrives on b mod S, no
+// same-address serialisation of the arrivals); lanes 0..S-1 of warp 0 poll them in parallel
+template <int S>
+__device__ void barS(Bar *b, unsigned nb, unsigned long long &target) {
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    target += nb;
+    if (threadIdx.x == 0) red_add_rel64(&b->subs[16 * (blockIdx.x % S)], 1ull);
+    for (;;) {
+      unsigned long long v = threadIdx.x < S ? ld_acq64(&b->subs[16 * threadIdx.x]) : 0ull;
+#pragma unroll
+      for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (v >= target) break;
+    }
+    fence_acqrel();
+  }
+  __syncthreads();
+}
+
 template <int V>
 __global__ void kbench(Bar *b, int iters, unsigned long long *out) {
   unsigned long long target = 0; unsigned epoch = 0;
@@ -77,6 +108,10 @@ __global__ void kbench(Bar *b, int iters, unsigned long long *out) {
     if (V == 1) bar1(b, gridDim.x);
     if (V == 2) bar2(b, gridDim.x, target);
     if (V == 3) bar3(b, gridDim.x, epoch);
+    if (V == 4) bar4(b, gridDim.x, target);
+    if (V == 5) barS<8>(b, gridDim.x, target);
+    if (V == 6) barS<16>(b, gridDim.x, target);
+    if (V == 7) barS<4>(b, gridDim.x, target);
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) *out = clock64() - t0;
 }
@@ -86,11 +121,13 @@ int main() {
   cudaMalloc(&b, sizeof(Bar)); cudaMalloc(&out, 8);
   int nsm; cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
   for (int bps : {1, 2, 4}) {
-    for (int v = 0; v < 4; ++v) {
+    for (int v = 0; v < 8; ++v) {
       cudaMemset(b, 0, sizeof(Bar));
       int iters = 2000, grid = nsm * bps;
       void *args[] = {&b, &iters, &out};
-      void *fn = v == 0 ? (void *)kbench<0> : v == 1 ? (void *)kbench<1> : v == 2 ? (void *)kbench<2> : (void *)kbench<3>;
+      void *fns[] = {(void *)kbench<0>, (void *)kbench<1>, (void *)kbench<2>, (void *)kbench<3>,
+                     (void *)kbench<4>, (void *)kbench<5>, (void *)kbench<6>, (void *)kbench<7>};
+      void *fn = fns[v];
       cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
       cudaLaunchCooperativeKernel(fn, grid, 512, args, 0, 0);  // warm
       cudaMemset(b, 0, sizeof(Bar));
