@@ -768,6 +768,7 @@ __global__ void __launch_bounds__(NT, MINB) k_sssp(SsspParams p) {
   const uint32_t nsrc = p.nsrc ? p.nsrc : 1u;
   // batch mode: the searches run back to back in this launch, a grid barrier apart (no kernel
   // boundary or launch ramp between them)
+  bool prefilled = false;  // this CTA's share of row si already holds UNREACHED
   for (uint32_t si = 0; si < nsrc; ++si) {
   const uint32_t src = p.nsrc ? ld_nc(p.sources + si) : p.source;
   uint32_t *const drow = p.dist + (size_t)si * p.n;
@@ -794,7 +795,12 @@ __global__ void __launch_bounds__(NT, MINB) k_sssp(SsspParams p) {
   }
   // ---- a1 init: dist <- UNREACHED (d(s) = 0), vis <- no-in-edge vertices | {s}  (Q4, Q7)
   if (narrow != 2) {
-  for (uint32_t i = gtid; i < p.n; i += nthreads) drow[i] = (i == src) ? 0u : kUnreached;
+  if (!prefilled) {
+    for (uint32_t i = gtid; i < p.n; i += nthreads) drow[i] = (i == src) ? 0u : kUnreached;
+  } else if (gtid == src % nthreads) {
+    drow[src] = 0u;  // this CTA's share was filled during the previous search's solo levels
+  }
+  prefilled = false;
   for (uint32_t w = gtid; w < p.nwords; w += nthreads)
     p.vis[w] = p.noin[w] | ((w == (src >> 5)) ? (1u << (src & 31)) : 0u);
   {
@@ -846,6 +852,13 @@ __global__ void __launch_bounds__(NT, MINB) k_sssp(SsspParams p) {
     if (st.solo) {
       // ---- solo stretch: narrow push levels on CTA 0 with __syncthreads only
       if (blockIdx.x != 0) {
+        if (MINB == 1 && si + 1 < nsrc && !prefilled) {  // (2-CTA variant: spills, C4 -1%)
+          // idle while CTA 0 runs the narrow levels: initialise this CTA's share of the next
+          // search's distance row (independent memory; its source entry is set at its init)
+          uint32_t *nrow = p.dist + (size_t)(si + 1) * p.n;
+          for (uint32_t i = gtid; i < p.n; i += nthreads) nrow[i] = kUnreached;
+          prefilled = true;
+        }
         if (threadIdx.x == 0) {
           ++solo_epoch;
           while (ld_acquire(&C->solo_epoch) < solo_epoch) {
