@@ -386,3 +386,39 @@ def test_sssp_batch_paths():
             rec, er = oracle.record(mesh.n, mesh.row_ptr, int(s), exp[i])
             sd = dawn.stats_to_dict(st[i])
             assert sd["levels"] == int(rec["ecc"]) and sd["edges_reach"] == er, (knobs, sd)
+
+def _pull_then_push_graph(hub_arcs: int, seed: int):
+    """0 -> 2,000 A -> 20,000 B (each A: 20 arcs into B) -> 300 C (one arc per B) -> D, where C's
+    first vertex H has `hub_arcs` arcs into D and the other C vertices one each.  With a large
+    alpha the growing levels run as pull, with beta = 1 the shrinking frontier C turns to
+    push: a push from the bitmap frontier the pull left."""
+    rng = np.random.default_rng(seed)
+    A = np.arange(1, 2001)
+    B = np.arange(2001, 22001)
+    C = np.arange(22001, 22301)
+    D0 = 22301
+    e = [[0, a] for a in A]
+    e += [[int(a), int(b)] for a in A for b in rng.choice(B, 20, replace=False)]
+    e += [[int(b), int(rng.choice(C))] for b in B]
+    nd = max(hub_arcs, 300)
+    e += [[int(C[0]), D0 + j] for j in range(hub_arcs)]
+    e += [[int(c), D0 + int(rng.integers(0, nd))] for c in C[1:]]
+    return graphgen.from_edges(D0 + nd, e)
+
+
+def test_push_from_pull_bitmap_frontier():
+    # the push level right after pull levels reads the bitmap frontier directly when no row
+    # exceeds 256 arcs, else converts it to a queue first (hub H in the frontier): both against
+    # the oracle, and the scenario checked through the level counts
+    for hub, seed in ((40, 1), (1000, 2)):
+        g = _pull_then_push_graph(hub, seed)
+        G = dev_graph(g)
+        G.set_tuning(alpha=1e9, beta=1.0)
+        exp = oracle.bfs_fifo(g.n, g.row_ptr, g.col, 0)[0]
+        d, st = gpu_dist(G, 0, "auto", stats=True)
+        assert np.array_equal(d, exp), hub
+        assert st["pull_levels"] == 3 and st["push_levels"] == 1, st  # L3: push from the bitmap
+        D = dawn.sssp_batch(G, torch.tensor([0, 0, 1], dtype=torch.int32, device="cuda"))
+        D = D.cpu().numpy().view(np.uint32)
+        assert np.array_equal(D[0], exp) and np.array_equal(D[1], exp)
+        assert np.array_equal(D[2], oracle.bfs_fifo(g.n, g.row_ptr, g.col, 1)[0])
