@@ -134,7 +134,7 @@ dawn_status dawn_graph_destroy(dawn_graph g);
  *                     (m_f: out-degree sum of the frontier; n_u / m_u: vertices / arcs not yet
  *                     reached).  A pull sweep costs ~ n_u early-exit scans of length ~ m_u/m_f.
  *                     The switch idea is Beamer's, cited by the paper at L123.  Default 2.
- *   DAWN_PARAM_BETA   pull -> push when beta * n_f < n and the frontier shrinks.  Default 24.
+ *   DAWN_PARAM_BETA   pull -> push when beta * n_f < n and the frontier shrinks.  Default 96.
  *   DAWN_PARAM_MS_ALPHA  the multi-source kernel pulls when ms_alpha * m_active > m_unsettled.
  *                     Default 2.
  *   DAWN_PARAM_BITMAP_PUSH_EDGES  push levels whose frontier has >= this many arcs mark

@@ -298,7 +298,7 @@ struct dawn_graph_s {
   Layout L;
   const int32_t *col, *icol;
   bool has_csc;
-  float alpha = 2.f, beta = 24.f, ms_alpha = 2.f;
+  float alpha = 2.f, beta = 96.f, ms_alpha = 2.f;
   int sssp_grid, ms_grid;
   bool sssp_one = false;  // the 1-CTA-per-SM instantiation of k_sssp (small graphs)
   bool trace;
@@ -391,7 +391,7 @@ dawn_status dawn_graph_load_csr(int64_t n, int64_t m, const int64_t *row_ptr, co
   g->bmpush_e = (uint32_t)env_int("DAWN_BMPUSH_E", 1 << 18);
   g->bmpush_grow = (uint32_t)env_int("DAWN_BMPUSH_GROW", 4096);
   g->solo_e = (uint32_t)env_int("DAWN_SOLO_E", 512);
-  g->beta = (float)env_int("DAWN_BETA", 24);
+  g->beta = (float)env_int("DAWN_BETA", 96);
   g->ms_alpha = (float)env_int("DAWN_MS_ALPHA", 2);
   // small graphs: k_sssp<kNT, 1> (one CTA per SM, 128 registers); big ones k_sssp<kNT, 2>
   g->sssp_one = n <= env_int("DAWN_SSSP_ONE_MAX_N", 1 << 22);
