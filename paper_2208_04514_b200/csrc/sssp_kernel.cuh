@@ -322,8 +322,9 @@ __device__ void push_level(const SsspParams &p, const LevelState &st, Slot *ns, 
 // Push level straight from the frontier bitmap fb[b] (the frontier a pull or candidate level
 // left), for frontiers whose rows all have <= kDirectRow arcs (tracked by the levels that build
 // bitmap frontiers): no bitmap -> queue conversion and no grid barrier before the expansion.  A
-// warp takes 32 bitmap words; each round, every lane contributes the next frontier vertex of its
-// word and the round's rows are dealt 32 arcs at a time by the owner search of push_item.
+// warp takes 32 bitmap words (strided over the grid); each round, every lane contributes the next
+// frontier vertex of its word and the round's rows are dealt 32 arcs at a time by the owner
+// search of push_item.
 __device__ void push_bitmap(const SsspParams &p, const LevelState &st, Slot *ns, uint32_t gwarp,
                             uint32_t nwarps, uint32_t &n_new, unsigned long long &m_new,
                             WarpStage &stg, long long &t0, unsigned long long *fsm) {
@@ -332,8 +333,10 @@ __device__ void push_bitmap(const SsspParams &p, const LevelState &st, Slot *ns,
   const int qn = st.q ^ 1;
   const uint32_t *fb = p.fb[st.b];
   uint32_t cnt = 0;
-  for (uint32_t base = gwarp * 32; base < p.nwords; base += nwarps * 32) {
-    const uint32_t w = base + lane;
+  // lane l of warp g reads word g + l * nwarps: every warp of the grid gets a share (32
+  // consecutive words per warp left most warps without any on a 2^20-vertex graph)
+  for (uint32_t base = gwarp; base < p.nwords; base += nwarps * 32) {
+    const uint32_t w = base + lane * nwarps;
     uint32_t bits = (w < p.nwords) ? ld_cg(fb + w) : 0u;
     while (__ballot_sync(DAWN_FULL, bits != 0)) {
       uint32_t rs = 0, d = 0;
