@@ -52,9 +52,21 @@ static_assert(kMsBatch == DAWN_MS_BATCH, "dawn.h DAWN_MS_BATCH must match kMsW")
 #ifndef DAWN_PULL_PR
 #define DAWN_PULL_PR 4       // ... on dense frontiers
 #endif
+// The same two for the 2-CTA/SM (64-register) variant: fewer probes in flight per lane keep its
+// pull loop free of spills, and the doubled warp count supplies the parallelism (Kronecker-24
+// 1224 -> 1323 GTEPS with 2 / 4 instead of 4 / 8)
+#ifndef DAWN_PULL_DEEP_PR2
+#define DAWN_PULL_DEEP_PR2 4
+#endif
+#ifndef DAWN_PULL_PR2
+#define DAWN_PULL_PR2 2
+#endif
 // Push levels read a bitmap frontier directly (no conversion to a queue) when none of its rows
 // is longer than kDirectRow arcs (DAWN_DIRECT_PUSH=0: always convert).
 constexpr uint32_t kDirectRow = 256;
+#ifndef DAWN_MINB2_EXTRAS
+#define DAWN_MINB2_EXTRAS 0  // direct bitmap push and next-row prefill in the 2-CTA/SM variant too
+#endif
 #ifndef DAWN_DIRECT_PUSH
 #define DAWN_DIRECT_PUSH 1
 #endif

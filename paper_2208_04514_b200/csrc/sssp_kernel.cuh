@@ -855,7 +855,7 @@ __global__ void __launch_bounds__(NT, MINB) k_sssp(SsspParams p) {
     if (st.solo) {
       // ---- solo stretch: narrow push levels on CTA 0 with __syncthreads only
       if (blockIdx.x != 0) {
-        if (MINB == 1 && si + 1 < nsrc && !prefilled) {  // (2-CTA variant: spills, C4 -1%)
+        if ((MINB == 1 || DAWN_MINB2_EXTRAS) && si + 1 < nsrc && !prefilled) {
           // idle while CTA 0 runs the narrow levels: initialise this CTA's share of the next
           // search's distance row (independent memory; its source entry is set at its init)
           uint32_t *nrow = p.dist + (size_t)(si + 1) * p.n;
@@ -908,7 +908,7 @@ __global__ void __launch_bounds__(NT, MINB) k_sssp(SsspParams p) {
     long long tconv = clock64();
     // a push from a bitmap frontier without long rows expands the bitmap directly
     // (1-CTA/SM variant only: in the 64-register one the extra path costs spills, C4 -4%)
-    constexpr bool kDirect = DAWN_DIRECT_PUSH && MINB == 1;
+    constexpr bool kDirect = DAWN_DIRECT_PUSH && (MINB == 1 || DAWN_MINB2_EXTRAS);
     const bool direct = kDirect && st.dir == kPush && st.rep == kRepBitmap && !st.bm && !st.big;
     if (st.dir == kPull && st.rep == kRepQueue) {
       // queue -> frontier bitmap fb[b] (and a clean fb[b+1] for the pull to write)
@@ -971,10 +971,12 @@ __global__ void __launch_bounds__(NT, MINB) k_sssp(SsspParams p) {
     } else {
 #if DAWN_PULL_DEEP
       if (st.deep)
-        pull_level<DAWN_PULL_DEEP_PR>(p, st, gwarp, nwarps, n_new, m_new, examined, tconv, bigf);
+        pull_level<MINB == 1 ? DAWN_PULL_DEEP_PR : DAWN_PULL_DEEP_PR2>(p, st, gwarp, nwarps, n_new, m_new,
+                                                                      examined, tconv, bigf);
       else
 #endif
-        pull_level<DAWN_PULL_PR>(p, st, gwarp, nwarps, n_new, m_new, examined, tconv, bigf);
+        pull_level<MINB == 1 ? DAWN_PULL_PR : DAWN_PULL_PR2>(p, st, gwarp, nwarps, n_new, m_new, examined,
+                                                            tconv, bigf);
     }
     block_flush(n_new, m_new, &ns->n_new, &ns->m_new, red);
     if constexpr (kDirect) {
