@@ -15,7 +15,13 @@ namespace dawn {
 // of equal size; Cf[c] names the entry holding chunk c's first edge.  Hub rows (64K arcs at
 // scale 20) therefore spread over many warps with no separate heavy path.
 constexpr uint32_t kChunk = 32;   // Cf granularity = one warp round
-constexpr uint32_t kIlp = 4;      // chunks per warp item when the frontier is wide
+#ifndef DAWN_ILP
+#define DAWN_ILP 4
+#endif
+#ifndef DAWN_ILP_CAND
+#define DAWN_ILP_CAND 8  // chunks per warp item of a candidate (bitmap) push level
+#endif
+constexpr uint32_t kIlp = DAWN_ILP;      // chunks per warp item when the frontier is wide
 // Solo levels (DAWN_PARAM_SOLO_EDGES): a narrow push level runs on CTA 0 alone with
 // __syncthreads instead of the grid barrier (the other CTAs wait for the stretch to end).
 // Bitmap push (DAWN_PARAM_BITMAP_PUSH_EDGES): a wide push level marks candidates with

@@ -299,10 +299,20 @@ __device__ void push_level(const SsspParams &p, const LevelState &st, Slot *ns, 
   const uint32_t nchunks = (E + kChunk - 1) / kChunk;
   uint32_t cnt = 0;
   if (st.bm) {
-    constexpr int JB = 2 * kIlp;  // candidate mode keeps less state per chain: deeper ILP
-    const uint32_t items = (nchunks + JB - 1) / JB;
-    for (uint32_t it = gwarp; it < items; it += nwarps)
-      push_item<JB, true>(p, st, ns, it, n_new, m_new, stg, cnt);
+    // candidate mode keeps less state per chain: deeper ILP (8 chunks per item) once there are
+    // enough chunks to give every warp an item, else 4 (all warps busy on the first bitmap
+    // levels: C2 +1.5%)
+    if (nchunks >= nwarps * DAWN_ILP_CAND) {
+      constexpr int JB = DAWN_ILP_CAND;
+      const uint32_t items = (nchunks + JB - 1) / JB;
+      for (uint32_t it = gwarp; it < items; it += nwarps)
+        push_item<JB, true>(p, st, ns, it, n_new, m_new, stg, cnt);
+    } else {
+      constexpr int JB = DAWN_ILP_CAND / 2;
+      const uint32_t items = (nchunks + JB - 1) / JB;
+      for (uint32_t it = gwarp; it < items; it += nwarps)
+        push_item<JB, true>(p, st, ns, it, n_new, m_new, stg, cnt);
+    }
     phase_add(p, st.L, 0, t0);
     return;
   }
