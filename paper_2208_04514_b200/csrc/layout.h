@@ -67,6 +67,9 @@ static_assert(kMsBatch == DAWN_MS_BATCH, "dawn.h DAWN_MS_BATCH must match kMsW")
 #ifndef DAWN_PULL_PR2
 #define DAWN_PULL_PR2 2
 #endif
+#ifndef DAWN_PULL_J2
+#define DAWN_PULL_J2 2  // DAWN_PULL_J of the 2-CTA/SM variant
+#endif
 // Push levels read a bitmap frontier directly (no conversion to a queue) when none of its rows
 // is longer than kDirectRow arcs (DAWN_DIRECT_PUSH=0: always convert).
 constexpr uint32_t kDirectRow = 256;

@@ -397,7 +397,8 @@ __device__ __forceinline__ bool fb_test(const uint32_t *fb, uint32_t v) {
   return (fb[v >> 5] >> (v & 31)) & 1u;
 }
 
-template <int PR>  // in-edges probed per lane per round trip (8 when the frontier is sparse)
+template <int PR, int J>  // in-edges probed per lane per round trip (8 when the frontier is
+                          // sparse); J unreached vertices per lane in flight
 __device__ void pull_level(const SsspParams &p, const LevelState &st, uint32_t gwarp,
                            uint32_t nwarps, uint32_t &n_new, unsigned long long &m_new,
                            unsigned long long &examined, long long &t0, bool &bigf) {
@@ -412,7 +413,6 @@ __device__ void pull_level(const SsspParams &p, const LevelState &st, uint32_t g
   //     the static ascending list of vertices with an in-edge at the first pull level, the
   //     warp's in-place compacted survivors afterwards (order kept, so vis / irp / dist
   //     accesses of a warp stay coalesced).  J entries per lane in flight.
-  constexpr int J = DAWN_PULL_J;
   const uint32_t cap = (p.n_hasin + nwarps - 1) / nwarps;
   const uint32_t seg0 = gwarp * cap;
   const uint32_t *src = (st.ul ? p.ulist : p.hasin) + seg0;
@@ -981,11 +981,11 @@ __global__ void __launch_bounds__(NT, MINB) k_sssp(SsspParams p) {
     } else {
 #if DAWN_PULL_DEEP
       if (st.deep)
-        pull_level<MINB == 1 ? DAWN_PULL_DEEP_PR : DAWN_PULL_DEEP_PR2>(p, st, gwarp, nwarps, n_new, m_new,
+        pull_level<MINB == 1 ? DAWN_PULL_DEEP_PR : DAWN_PULL_DEEP_PR2, MINB == 1 ? DAWN_PULL_J : DAWN_PULL_J2>(p, st, gwarp, nwarps, n_new, m_new,
                                                                       examined, tconv, bigf);
       else
 #endif
-        pull_level<MINB == 1 ? DAWN_PULL_PR : DAWN_PULL_PR2>(p, st, gwarp, nwarps, n_new, m_new, examined,
+        pull_level<MINB == 1 ? DAWN_PULL_PR : DAWN_PULL_PR2, MINB == 1 ? DAWN_PULL_J : DAWN_PULL_J2>(p, st, gwarp, nwarps, n_new, m_new, examined,
                                                             tconv, bigf);
     }
     block_flush(n_new, m_new, &ns->n_new, &ns->m_new, red);
