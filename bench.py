@@ -1,22 +1,28 @@
 #!/usr/bin/env python
-"""bench.py — DAWN on B200: SSSP GTEPS (1 GPU) and APSP sources/s (1/2/4/8 GPUs) vs the HBM
+"""bench.py — DAWN on B200: SSSP GTEPS (1 B200) and APSP sources/s (1/2/4/8 B200) vs the HBM
 roofline (BASELINE.json metric).
 
-  python bench.py [--gpus N --steps K --warmup W] [--workload sssp|apsp] [--config C2]
+  python bench.py [--gpus N --steps K --warmup W] [--workload auto|sssp|apsp] [--config C1..C4]
                   [--variant auto|push|pull] [--impl dawn|reference]
 
-Default (N=1): workload "sssp" on configs[1] = C2, Graph500 Kronecker scale 20 ef 16, 64
-seeded sources per rank; one step = 64 dawn_sssp calls (one persistent kernel each) writing
-64 distance rows.  Under torchrun each rank runs its own 64 sources (weak scaling); time is the
-max over ranks.  The JSON line also carries the C5 APSP (largest WCC of Kronecker-18, sources
-sharded over the N ranks, one NCCL all-gather) as "secondary".
+Headline (workload "auto", the default):
+  N = 1  SSSP on C4 = configs[3], Graph500 Kronecker scale 24 ef 16 (the largest single-GPU
+         config): one step = ONE dawn_sssp_batch call over 64 seeded sources (64 distance rows).
+         C1, C2, C3 and the C5 APSP are measured in the same run under "configs" (C1 as the
+         latency of one SSSP from vertex 0; C3 beside its measured level-latency floor; C5 with
+         the executed-byte roofline of the bit-parallel kernel and a measured L2 peak).
+  N > 1  APSP over the largest WCC of Kronecker-18 (C5 = configs[4]): sources sharded over the
+         N ranks (256-source batches, batch b on rank b mod N), one NCCL all-gather of the
+         32-byte records; strong scaling, time = max over ranks.
 
---impl reference times the CPU oracle (oracle/, literal Algorithm 2) on the host cores on a
-bounded sample of the same workload (this tier's reference arm: there is no reference code).
+--impl reference times the CPU oracle (oracle/: literal Algorithm 2 per source)
+on the host cores, on the same config and metric (this tier's reference arm: there is no
+reference code).
 """
 from __future__ import annotations
 
 import argparse
+import ctypes
 import json
 import os
 import statistics
@@ -24,6 +30,7 @@ import subprocess
 import sys
 import threading
 import time
+from concurrent.futures import ThreadPoolExecutor
 
 import numpy as np
 
@@ -32,6 +39,7 @@ sys.path.insert(0, ROOT)
 
 import graphgen  # noqa: E402
 
+METRIC = "SSSP GTEPS (1 B200) and APSP sources/sec at 1/2/4/8 B200 vs HBM roofline"
 CONFIG_TEXT = {
     "C1": "SSSP from vertex 0, directed Erdos-Renyi n=1000 m=8000 (seed 1)",
     "C2": "SSSP, Graph500 Kronecker scale 20 edge factor 16 (seed 20), 64 sources",
@@ -39,14 +47,22 @@ CONFIG_TEXT = {
     "C4": "SSSP, Graph500 Kronecker scale 24 edge factor 16 (seed 24), 64 sources",
     "C5": "APSP over all sources of the largest WCC of Kronecker scale 18 ef 16 (seed 18)",
 }
+L2_BYTES = 132644864  # B200 L2 (126.5 MiB); the flush writes 2.2x this between timed steps
 
 
 def peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
         d = json.load(open(p))
-        return float(d["hbm_gbs"]), "measured"
-    return 6650.0, "fallback"
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, burst copy)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(key):
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        return json.load(open(tp)).get(key)
+    return None
 
 
 class ClockSampler:
@@ -105,38 +121,56 @@ def dist_setup(n_gpus: int):
     return rank, world, local
 
 
-def build_graph(cfg: str):
-    g = graphgen.config_graph(cfg)
-    return g
-
-
-def sources_for(g, cfg: str, rank: int, count: int = 64):
+def sources_for(g, cfg: str, rank: int = 0, count: int = 64):
     if cfg in ("C1", "C3"):
         return np.zeros(1, np.int64)  # vertex 0 (configs[0], configs[2])
     return g.sample_sources(count, seed=1 + 1000 * rank).astype(np.int64)
 
 
+def _events():
+    import torch
+    return torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+
+def timed(fn, steps, flush, stream):
+    """CUDA-event times (ms) of `steps` calls of fn on `stream`, L2 flushed before each."""
+    import torch
+    out = []
+    for _ in range(steps):
+        flush.zero_()
+        a, b = _events()
+        a.record(stream)
+        fn()
+        b.record(stream)
+        torch.cuda.synchronize()
+        out.append(a.elapsed_time(b))
+    return out
+
+
 # ------------------------------------------------------------------------------- CPU oracle
-def cpu_oracle_sssp(g, sources, budget_s: float):
-    """Literal Algorithm 2 oracle, single-threaded, sources in order until the budget."""
+def cpu_oracle_sssp(g, sources, budget_s: float, cores: int):
+    """Literal Algorithm 2 oracle (oracle_sovm), one source per host thread, waves of `cores`
+    sources until the budget is spent (at least one wave).  GTEPS = sum of E10 counts / wall."""
     import oracle
-    t_tot, e_tot, done = 0.0, 0, 0
-    for s in sources:
-        t0 = time.perf_counter()
-        _, st = oracle.sovm(g.n, g.row_ptr, g.col, int(s))
-        t_tot += time.perf_counter() - t0
-        e_tot += st["edge_inspections"]
-        done += 1
-        if t_tot >= budget_s:
-            break
-    return e_tot / t_tot / 1e9, done, t_tot
+    edges, done, t0 = 0, 0, time.perf_counter()
+    srcs = list(sources)
+    with ThreadPoolExecutor(max_workers=cores) as ex:
+        while True:
+            wave = [srcs[(done + i) % len(srcs)] for i in range(cores)]
+            for _, st in ex.map(lambda s: oracle.sovm(g.n, g.row_ptr, g.col, int(s)), wave):
+                edges += st["edge_inspections"]
+            done += len(wave)
+            if time.perf_counter() - t0 >= budget_s:
+                break
+    wall = time.perf_counter() - t0
+    return edges / wall / 1e9, done, wall
 
 
-def cpu_oracle_apsp(g, verts, budget_s: float):
+def cpu_oracle_apsp(g, verts, budget_s: float, cores: int):
+    """oracle_records (literal Algorithm 2 + record per source) on a pthread pool of `cores`
+    threads over a growing prefix of the source list until one run takes >= budget/3."""
     import oracle
-    cores = len(os.sched_getaffinity(0))
-    k = max(cores, 16)
-    rate = None
+    k = max(4 * cores, 64)
     spent = 0.0
     while True:
         sub = verts[:k]
@@ -144,320 +178,387 @@ def cpu_oracle_apsp(g, verts, budget_s: float):
         oracle.records(g.n, g.row_ptr, g.col, sub, threads=cores)
         dt = time.perf_counter() - t0
         spent += dt
-        rate = len(sub) / dt
         if dt > budget_s / 3 or k >= len(verts) or spent > budget_s:
-            return rate, len(sub), cores, dt
+            return len(sub) / dt, len(sub), dt
         k = min(len(verts), int(k * max(2.0, budget_s / 3 / max(dt, 1e-3))))
 
 
 # ------------------------------------------------------------------------------- GPU arms
-# the kernel that does the work of one dawn_sssp call on each config (the dominant kernel)
-KERNEL_OF = {"C1": "k_small (one SSSP per CTA, CSR in shared memory; the batch's searches run "
-                   "on min(k, #SMs) CTAs at once)",
+KERNEL_OF = {"C1": "k_small (one SSSP on one CTA, CSR in shared memory)",
              "C2": "k_sssp (one persistent launch running the batch's SSSPs back to back)",
              "C3": "k_narrow (one 16-CTA cluster per SSSP; the k_sssp behind it exits at once)",
              "C4": "k_sssp (one persistent launch running the batch's SSSPs back to back)"}
 
 
-def run_sssp(args, rank, world, dev, cfg=None, steps=None, warmup=None, e2e=True, reps=1):
-    """One SSSP config.  A step = every bench source once (64 for C2/C4; the single source
-    repeated `reps` times for C1/C3)."""
+def dev_graph(g, **kw):
+    import paper_2208_04514_b200 as dawn
+    if g.symmetric:
+        return dawn.Graph(g.row_ptr, g.col, True, **kw)
+    p, i = g.transpose()
+    return dawn.Graph(g.row_ptr, g.col, False, p, i, **kw)
+
+
+def search_stats(G, srcs, variant, out):
+    """E10 count and the executed schedule of each source, from the kernel's own statistics
+    (untimed)."""
+    import paper_2208_04514_b200 as dawn
+    rows = []
+    for i, s in enumerate(srcs):
+        _, st = dawn.sssp(G, int(s), variant, stats=True, out=out[i % out.shape[0]])
+        rows.append(dawn.stats_to_dict(st))
+    return rows
+
+
+def level_floor(dev, flush, stream, levels: int):
+    """C3's latency floor, measured in the same run through the same kernels: one SSSP on a
+    directed path with `levels` + 1 vertices (one vertex and one arc per level: nothing but the
+    per-level fixed cost of k_narrow — the dependent row load and the cluster level barrier)."""
+    import paper_2208_04514_b200 as dawn
+    import torch
+    n = levels + 1
+    row_ptr = np.minimum(np.arange(n + 1, dtype=np.int64), n - 1)
+    col = np.arange(1, n, dtype=np.int32)
+    G = dawn.Graph(row_ptr, col, False, device=dev)  # push-only (no CSC): a pure level chain
+    G.set_tuning(cluster_start=1, cluster_handover_edges=2e19)
+    out = torch.empty((1, n), dtype=torch.int32, device=dev)
+    src = torch.zeros(1, dtype=torch.int32, device=dev)
+    for _ in range(3):
+        dawn.sssp_batch(G, src, out=out)
+    ms = timed(lambda: dawn.sssp_batch(G, src, out=out), 5, flush, stream)
+    d = out[0].cpu().numpy().view(np.uint32)
+    assert np.array_equal(d, np.arange(n, dtype=np.uint32)), "path floor: wrong distances"
+    return float(np.median(ms)), n
+
+
+def run_sssp(args, rank, world, dev, cfg, steps, warmup, e2e=True, with_cpu=False):
+    """One SSSP config.  A step = ONE dawn_sssp_batch call over the config's sources (64 for
+    C2/C4; vertex 0 for C1/C3)."""
     import torch
     import torch.distributed as tdist
     import paper_2208_04514_b200 as dawn
 
-    cfg = cfg or args.config
-    steps = args.steps if steps is None else steps
-    warmup = args.warmup if warmup is None else warmup
-    g = build_graph(cfg)
-    G = dawn.Graph(g.row_ptr, g.col, g.symmetric,
-                   *(g.transpose() if not g.symmetric else (None, None)))
+    t_gen = time.time()
+    g = graphgen.config_graph(cfg)
+    G = dev_graph(g)
+    t_gen = time.time() - t_gen
     srcs = sources_for(g, cfg, rank)
-    if reps > 1:
-        srcs = np.repeat(srcs, reps)
     k = len(srcs)
-    out = torch.empty((min(k, 64), g.n), dtype=torch.int32, device=dev)
-    orow = lambda i: out[i % out.shape[0]]
-    # E_reach per source (the E10 numerator) from the kernel's own statistics, untimed
-    er, reached, examined, pushl, pulll = [], [], [], [], []
-    for i, s in enumerate(srcs):
-        _, st = dawn.sssp(G, int(s), args.variant, stats=True, out=orow(i))
-        d = dawn.stats_to_dict(st)
-        er.append(d["edges_reach"]); reached.append(d["reached"]); examined.append(d["edges_examined"])
-        pushl.append(d["push_levels"]); pulll.append(d["pull_levels"])
-    flush = torch.empty(int(2.2 * 132644864) // 4, dtype=torch.int32, device=dev)
+    out = torch.empty((k, g.n), dtype=torch.int32, device=dev)
+    st = search_stats(G, srcs, args.variant, out)
+    er = [s["edges_reach"] for s in st]
+    reached = [s["reached"] for s in st]
+    examined = [s["edges_examined"] for s in st]
+    pull_l = [s["pull_levels"] for s in st]
+    levels = [s["levels"] for s in st]
+    flush = torch.empty(int(2.2 * L2_BYTES) // 4, dtype=torch.int32, device=dev)
     stream = torch.cuda.current_stream()
-
     dsrc = torch.from_numpy(srcs.astype(np.int32)).to(dev)
-    outk = out[:k]
 
     def step():
-        # the public batch call: the k searches one after the other (dawn_sssp_batch: one
-        # k_sssp launch, or k_small / per-search k_narrow + k_sssp where those apply)
-        dawn.sssp_batch(G, dsrc, args.variant, out=outk)
+        dawn.sssp_batch(G, dsrc, args.variant, out=out)
 
-    step()
-    torch.cuda.synchronize()
     for _ in range(warmup):
         step()
         flush.zero_()
-    torch.cuda.synchronize()
+    dawn.check(G)  # the bench sources are valid (device-side validation flag clear)
     if world > 1:
         tdist.barrier()
     torch.cuda.synchronize()
-    step_ms = []
     with ClockSampler(dev.index if dev.index is not None else 0) as clk:
-        for _ in range(steps):
-            flush.zero_()  # L2 flush between timed steps (write 2.2x L2)
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record(stream)
-            step()
-            b.record(stream)
-            torch.cuda.synchronize()
-            step_ms.append(a.elapsed_time(b))
+        step_ms = timed(step, steps, flush, stream)
     if world > 1:
         tdist.barrier()
-    torch.cuda.synchronize()
     tot_ms = sum(step_ms)
-    # average duration of one search over the timed region: timed steps / searches they contain
-    launch_ms = [sum(step_ms) / (len(step_ms) * k)]
     if world > 1:
         t = torch.tensor([tot_ms], dtype=torch.float64, device=dev)
         tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
         tot_ms = float(t.item())
     edges_step = float(sum(er))
-    value = edges_step * steps * world / (tot_ms * 1e-3) / 1e9
-
-    # roofline: dominant (only) kernel k_sssp; algorithmic bytes B_SOVM(s) = 4E + 8S + 4n
     peak, peak_kind = peaks()
+    # the one-SSSP latency (L2 flushed before each call)
+    lat = timed(lambda: dawn.sssp(G, int(srcs[0]), args.variant, out=out[0]), 5 if k == 1 else 1,
+                flush, stream)
+    for i in range(1, min(k, 16)):
+        lat += timed(lambda: dawn.sssp(G, int(srcs[i]), args.variant, out=out[i]), 1, flush, stream)
+    lat_med = float(np.median(lat))
+    if cfg == "C1":
+        # configs[0] is ONE SSSP from vertex 0: its number is the latency of that call
+        value = er[0] / (lat_med * 1e-3) / 1e9
+        ms_step = lat_med
+        search_ms = lat_med
+        timed_what = "median of 5 dawn_sssp(source 0) calls, L2 flushed before each"
+    else:
+        value = edges_step * steps * world / (tot_ms * 1e-3) / 1e9
+        ms_step = tot_ms / steps
+        search_ms = sum(step_ms) / (len(step_ms) * k)  # this rank's average per search
+        timed_what = f"{steps} steps of dawn_sssp_batch over {k} source(s), L2 flushed between"
+    # roofline of the dominant kernel: B_SOVM(s) = 4 E_reach + 8 S_reach + 4 n (SURVEY §8(d))
     b_sovm = [4 * e + 8 * (r + 1) + 4 * g.n for e, r in zip(er, reached)]
     b_exec = [4 * g.n + 4 * x + 8 * (r + 1) + (g.n // 8) * (2 * pl + 1)
-              for x, r, pl in zip(examined, reached, pulll)]
-    avg_launch_ms = float(np.mean(launch_ms))
-    achieved = float(np.mean(b_sovm)) / (avg_launch_ms * 1e-3) / 1e9
-    achieved_exec = float(np.mean(b_exec)) / (avg_launch_ms * 1e-3) / 1e9
-    traffic = None
-    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tp):
-        traffic = json.load(open(tp)).get(f"sssp-{cfg}-{args.variant}")
-
-    # context, not the headline: (1) the latency of ONE dawn_sssp call (L2 flushed before each),
-    # (2) the same distinct sources through the bit-parallel multi-source kernel (dawn_msssp)
-    lat = []
-    for i in range(min(k, 16)):
-        flush.zero_()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        dawn.sssp(G, int(srcs[i]), args.variant, out=outk[i])
-        b.record(stream)
-        torch.cuda.synchronize()
-        lat.append(a.elapsed_time(b))
-    single = {"median_us": float(np.median(lat)) * 1e3, "calls": len(lat),
-              "gteps": float(np.mean(er[:len(lat)])) / (float(np.median(lat)) * 1e-3) / 1e9}
-    uniq = len(set(int(x) for x in srcs))
-    if uniq == k and k >= 64 and args.variant == "auto":
-        ms_dist = torch.empty((k, g.n), dtype=torch.int32, device=dev)
-        dawn.msssp(G, srcs, dist=True, records=False, d_out=ms_dist)
-        torch.cuda.synchronize()
-        assert torch.equal(ms_dist, outk), "dawn_msssp distances differ from dawn_sssp_batch"
-        mt = []
-        for _ in range(3):
-            flush.zero_()
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record(stream)
-            dawn.msssp(G, srcs, dist=True, records=False, d_out=ms_dist)
-            b.record(stream)
-            torch.cuda.synchronize()
-            mt.append(a.elapsed_time(b))
-        single["msssp_same_sources"] = {
-            "gteps": edges_step / (float(np.median(mt)) * 1e-3) / 1e9,
-            "ms": float(np.median(mt)),
-            "how": "dawn_msssp on the same k sources (one bit-parallel pass, dist rows written), "
-                   "distances checked equal to the batch's"}
-        del ms_dist
-
-    # SURVEY 8(d) item 3: the forced-push (pure SOVM, Algorithm 2) schedule on the same sources
-    forced_push = None
-    if args.variant == "auto" and cfg in ("C2", "C4"):
-        dawn.sssp_batch(G, dsrc, "push", out=outk)
-        pt = []
-        for _ in range(2):
-            flush.zero_()
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record(stream)
-            dawn.sssp_batch(G, dsrc, "push", out=outk)
-            b.record(stream)
-            torch.cuda.synchronize()
-            pt.append(a.elapsed_time(b))
-        pms = float(np.median(pt))
-        forced_push = {"gteps": edges_step / (pms * 1e-3) / 1e9, "ms_per_step": pms,
-                       "achieved_GBps_B_SOVM": float(np.sum(b_sovm)) / (pms * 1e-3) / 1e9,
-                       "how": "dawn_sssp_batch with DAWN_PUSH (every level SOVM) on the same sources"}
-
-    if not e2e:
-        peak, _ = peaks()
-        return {"value": value, "unit": "GTEPS", "ms_per_step": tot_ms / steps, "steps": steps,
-                "sources_per_step": k, "n": g.n, "m": g.m, "workload": f"{cfg}: {CONFIG_TEXT[cfg]}",
-                "avg_launch_us": avg_launch_ms * 1e3, "edges_reach_mean": float(np.mean(er)),
-                "levels": {"push_mean": float(np.mean(pushl)), "pull_mean": float(np.mean(pulll))},
-                "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                             "frac": achieved / peak, "kernel": KERNEL_OF.get(cfg),
-                             "traffic": traffic, "achieved_exec": achieved_exec,
-                             "frac_exec": achieved_exec / peak,
-                             "bytes_model": "B_SOVM = 4*E_reach + 8*S_reach + 4*n"},
-                "single_search": single, "forced_push": forced_push,
-                "clocks": clk.summary()}, g, srcs, er
-    # e2e through the public API with HOST buffers: the source list H2D (pinned), then
-    # dawn_sssp_batch over chunks of E2E_CHUNK sources, each chunk's distance rows copied to pinned
-    # host memory on a second stream while the next chunk computes (the D2H of 64 rows, 4n bytes
-    # each, is the bound: ~45-55 GB/s of PCIe against ~50 GB/s of distance rows produced)
-    E2E_CHUNK = int(os.environ.get("DAWN_E2E_CHUNK", "1"))  # 1/4/8/16: 348/338/328/291 GTEPS
-    host_src = torch.from_numpy(srcs.astype(np.int32)).pin_memory()
-    dev_src = torch.empty_like(host_src, device=dev)
-    host_out = torch.empty((k, g.n), dtype=torch.int32).pin_memory()
-    e2e_ms = []
-    copy_stream = torch.cuda.Stream(device=dev)
-    for it in range(max(1, steps)):
-        flush.zero_()
-        torch.cuda.synchronize()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        dev_src.copy_(host_src, non_blocking=True)
-        for c0 in range(0, k, E2E_CHUNK):
-            c1 = min(k, c0 + E2E_CHUNK)
-            dawn.sssp_batch(G, dev_src[c0:c1], args.variant, out=outk[c0:c1])
-            done = torch.cuda.Event()
-            done.record(stream)
-            copy_stream.wait_event(done)
-            with torch.cuda.stream(copy_stream):
-                host_out[c0:c1].copy_(outk[c0:c1], non_blocking=True)
-        stream.wait_stream(copy_stream)
-        b.record(stream)
-        torch.cuda.synchronize()
-        e2e_ms.append(a.elapsed_time(b))
-    e2e_tot = sum(e2e_ms)
-    if world > 1:
-        t = torch.tensor([e2e_tot], dtype=torch.float64, device=dev)
-        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
-        e2e_tot = float(t.item())
-    e2e_val = edges_step * len(e2e_ms) * world / (e2e_tot * 1e-3) / 1e9
-
+              for x, r, pl in zip(examined, reached, pull_l)]
+    achieved = float(np.mean(b_sovm)) / (search_ms * 1e-3) / 1e9
+    achieved_exec = float(np.mean(b_exec)) / (search_ms * 1e-3) / 1e9
     res = {
-        "metric": "SSSP GTEPS (1 B200) and APSP sources/sec at 1/2/4/8 B200 vs HBM roofline",
-        "value": value, "unit": "GTEPS", "n_gpus": world, "steps": steps,
-        "warmup": warmup, "ms_per_step": tot_ms / steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-        "config": {"workload": f"{cfg}: {CONFIG_TEXT[cfg]}", "n": g.n, "m": g.m,
-                   "sources_per_rank": k, "variant": args.variant,
-                   "l2": "flushed between timed steps (2.2x L2 write)",
-                   "teps_numerator": "E_reach = sum of out-degrees of reached vertices incl. s "
-                                     "(directed arcs, PAPER E10)",
-                   "parallelism": f"dp{world} (independent sources per rank)"},
-        # dawn_sssp_batch: k_narrow + k_sssp per search on cluster-start graphs (C3), else one
-        # launch per step
-        "gpu_launches": steps * (2 * k if cfg == "C3" else 1),
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
-                     "kernel": KERNEL_OF.get(cfg, KERNEL_OF["C2"]),
-                     "algorithmic_bytes_per_launch": float(np.mean(b_sovm)),
-                     "bytes_model": "B_SOVM = 4*E_reach + 8*S_reach + 4*n",
-                     "avg_launch_us": avg_launch_ms * 1e3,
-                     "achieved_exec": achieved_exec, "frac_exec": achieved_exec / peak,
-                     "exec_bytes_per_launch": float(np.mean(b_exec))},
-        "e2e": {"value": e2e_val, "unit": "GTEPS", "h2d_bytes_per_step": int(host_src.numel() * 4),
-                "d2h_bytes_per_step": int(host_out.numel() * 4),
-                "how": f"source list H2D, then dawn_sssp_batch over chunks of {E2E_CHUNK} "
-                       "source(s); each chunk's distance rows copied to pinned host memory on a "
-                       "second stream while the next chunk computes",
-                "ms_per_step": e2e_tot / len(e2e_ms)},
-        "levels": {"push_mean": float(np.mean(pushl)), "pull_mean": float(np.mean(pulll)),
+        "value": value, "unit": "GTEPS", "ms_per_step": ms_step, "steps": steps,
+        "workload": f"{cfg}: {CONFIG_TEXT[cfg]}", "n": g.n, "m": g.m, "sources_per_step": k,
+        "timed": timed_what, "graph_build_s": t_gen,
+        "teps": {"e10_gteps": value,
+                 "graph500_gteps": value / 2 if g.symmetric else value,
+                 "note": "E10 numerator = directed arcs out of reached vertices (PAPER L299-302); "
+                         "Graph500 counts each undirected edge once (= E10/2 on symmetric graphs, "
+                         "reading Q18)"},
+        "levels": {"ecc_mean": float(np.mean(levels)),
+                   "pull_levels_mean": float(np.mean(pull_l)),
                    "edges_examined_mean": float(np.mean(examined)),
                    "edges_reach_mean": float(np.mean(er))},
-        "single_search": single,
-        "forced_push": forced_push,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": ncu_traffic(f"sssp-{cfg}-{args.variant}"),
+                     "peak_kind": peak_kind, "kernel": KERNEL_OF.get(cfg),
+                     "algorithmic_bytes_per_search": float(np.mean(b_sovm)),
+                     "bytes_model": "B_SOVM = 4*E_reach + 8*S_reach + 4*n per search (SURVEY §8(d))",
+                     "avg_search_us": search_ms * 1e3,
+                     "achieved_exec": achieved_exec, "frac_exec": achieved_exec / peak,
+                     "exec_bytes_per_search": float(np.mean(b_exec)),
+                     "exec_model": "B_exec = 4n + 4*edges_examined + 8*S_reach + (n/8)*(2*pull_levels+1)"},
+        "single_search": {"median_us": lat_med * 1e3, "calls": len(lat),
+                          "gteps": float(np.mean(er[:len(lat)])) / (lat_med * 1e-3) / 1e9},
         "clocks": clk.summary(),
+        "gpu_launches_per_step": 2 * k if cfg == "C3" else 1,
     }
-    return res, g, srcs, er
+    if cfg == "C1":
+        # context only: 64 concurrent copies of the search on 64 CTAs (k_small per CTA)
+        d64 = torch.zeros(64, dtype=torch.int32, device=dev)
+        o64 = torch.empty((64, g.n), dtype=torch.int32, device=dev)
+        ms = timed(lambda: dawn.sssp_batch(G, d64, args.variant, out=o64), 5, flush, stream)
+        res["context_64_concurrent_copies"] = {
+            "gteps": 64 * er[0] / (float(np.median(ms)) * 1e-3) / 1e9, "ms": float(np.median(ms)),
+            "how": "dawn_sssp_batch with source 0 repeated 64 times (one CTA each): throughput "
+                   "context, not the config's number"}
+    if cfg == "C3":
+        floor_ms, fn = level_floor(dev, flush, stream, int(levels[0]))
+        res["latency_floor"] = {
+            "ms": floor_ms, "levels": int(levels[0]) + 1,
+            "frac": floor_ms / search_ms,
+            "how": f"one SSSP through the same k_narrow + k_sssp on a {fn}-vertex directed path "
+                   "(one vertex and one arc per level): the per-level fixed cost alone, in this run",
+            "per_level_us": floor_ms * 1e3 / (int(levels[0]) + 1)}
+    if cfg in ("C2", "C4") and args.variant == "auto":
+        # SURVEY §8(d) item 3: the forced-push (pure SOVM, Algorithm 2) schedule
+        pt = timed(lambda: dawn.sssp_batch(G, dsrc, "push", out=out), 2, flush, stream)
+        pms = float(np.median(pt))
+        res["forced_push"] = {"gteps": edges_step / (pms * 1e-3) / 1e9, "ms_per_step": pms,
+                              "achieved_GBps_B_SOVM": float(np.sum(b_sovm)) / (pms * 1e-3) / 1e9,
+                              "frac_B_SOVM": float(np.sum(b_sovm)) / (pms * 1e-3) / 1e9 / peak,
+                              "how": "dawn_sssp_batch with DAWN_PUSH (every level SOVM)"}
+        # context: the same sources through the bit-parallel multi-source kernel
+        ms_dist = torch.empty_like(out)
+        dawn.msssp(G, srcs, dist=True, records=False, d_out=ms_dist)
+        torch.cuda.synchronize()
+        assert torch.equal(ms_dist, out), "dawn_msssp distances differ from dawn_sssp_batch"
+        mt = timed(lambda: dawn.msssp(G, srcs, dist=True, records=False, d_out=ms_dist), 3,
+                   flush, stream)
+        res["msssp_same_sources"] = {
+            "gteps": edges_step / (float(np.median(mt)) * 1e-3) / 1e9, "ms": float(np.median(mt)),
+            "how": "dawn_msssp on the same sources (one bit-parallel pass, 64 dist rows written; "
+                   "distances checked equal to the batch's)"}
+        del ms_dist
+    if e2e:
+        # end to end through the public API with HOST buffers: the source list H2D (pinned),
+        # dawn_sssp_batch per source, each distance row copied to pinned host memory on a second
+        # stream while the next search runs (the D2H of the rows is the bound)
+        host_src = torch.from_numpy(srcs.astype(np.int32)).pin_memory()
+        dev_src = torch.empty_like(host_src, device=dev)
+        host_out = torch.empty((k, g.n), dtype=torch.int32, pin_memory=True)
+        copy_stream = torch.cuda.Stream(device=dev)
+
+        def e2e_step():
+            dev_src.copy_(host_src, non_blocking=True)
+            for c in range(k):
+                dawn.sssp_batch(G, dev_src[c:c + 1], args.variant, out=out[c:c + 1])
+                done = torch.cuda.Event()
+                done.record(stream)
+                copy_stream.wait_event(done)
+                with torch.cuda.stream(copy_stream):
+                    host_out[c].copy_(out[c], non_blocking=True)
+            stream.wait_stream(copy_stream)
+
+        e2e_step()
+        torch.cuda.synchronize()
+        e_ms = timed(e2e_step, max(1, min(steps, 10)), flush, stream)
+        e_tot = sum(e_ms)
+        if world > 1:
+            t = torch.tensor([e_tot], dtype=torch.float64, device=dev)
+            tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+            e_tot = float(t.item())
+        assert np.array_equal(host_out[0].numpy(), out[0].cpu().numpy())
+        res["e2e"] = {"value": edges_step * len(e_ms) * world / (e_tot * 1e-3) / 1e9,
+                      "unit": "GTEPS", "h2d_bytes_per_step": int(host_src.numel() * 4),
+                      "d2h_bytes_per_step": int(host_out.numel() * 4),
+                      "ms_per_step": e_tot / len(e_ms),
+                      "how": "source list H2D from pinned memory, dawn_sssp_batch per source, "
+                             "every distance row (4n bytes) D2H into pinned memory on a second "
+                             "stream overlapping the next search"}
+        del host_out
+    if with_cpu:
+        cores = len(os.sched_getaffinity(0))
+        gte, done, wall = cpu_oracle_sssp(g, srcs, args.cpu_budget, cores)
+        res["cpu_baseline"] = {"value": gte, "unit": "GTEPS", "cores": cores, "kind": "oracle",
+                               "sample": f"oracle_sovm (literal Algorithm 2) on {done} of the "
+                                         f"bench sources, one per host thread, {wall:.1f} s wall"}
+    del G, out, flush
+    torch.cuda.empty_cache()
+    return res
 
 
-def l2_probe(dev):
-    """L2 bandwidth measured in the same run (context for the L2-resident
-    C5 words and C2's bitmaps): a device copy between two 24 MiB buffers (48 MiB, inside the
-    126 MB L2), 40 back-to-back copies timed with CUDA events after a warm-up."""
+def l2_peak(dev):
+    """Measured L2 read bandwidth (scripts/l2probe.cu): 16-byte ld.global.cg over a 48 MiB
+    L2-resident buffer by 148 x 4 CTAs, 20 passes, CUDA events; best of 5."""
     import torch
-    nb = 24 << 20
-    a = torch.ones(nb // 4, dtype=torch.int32, device=dev)
-    b = torch.empty_like(a)
-    for _ in range(5):
-        b.copy_(a)
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(40):
-        b.copy_(a)
-    e1.record()
-    torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1) / 40
-    return {"copy_GBps": 2 * nb / (ms * 1e-3) / 1e9, "bytes_per_copy": 2 * nb,
-            "how": "torch copy_ of a 24 MiB int32 buffer (read + write counted), L2-resident; a "
-                   "lower bound on L2 bandwidth (the copy kernel's own limit may bind first)"}
+    lib = os.path.join(ROOT, "scripts", "libl2probe.so")
+    if not os.path.exists(lib):
+        import __graft_entry__
+        __graft_entry__._build_probe()
+    L = ctypes.CDLL(lib)
+    L.l2probe_read.argtypes = [ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int, ctypes.c_int,
+                               ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p]
+    nb = 48 << 20
+    buf = torch.ones(nb // 4, dtype=torch.int32, device=dev)
+    sink = torch.zeros(4, dtype=torch.int32, device=dev)
+    nsm = torch.cuda.get_device_properties(dev).multi_processor_count
+    st = torch.cuda.current_stream().cuda_stream
+    reps = 20
+    best = 0.0
+    for _ in range(6):
+        a, b = _events()
+        a.record()
+        L.l2probe_read(buf.data_ptr(), nb, reps, nsm * 4, 512, sink.data_ptr(), st)
+        b.record()
+        torch.cuda.synchronize()
+        best = max(best, nb * reps / (a.elapsed_time(b) * 1e-3) / 1e9)
+    return {"read_GBps": best, "bytes": nb, "how": "scripts/l2probe.cu: ld.global.cg.v4 over a "
+            "48 MiB L2-resident buffer, 592 CTAs x 512 threads, 20 passes, best of 6"}
 
 
-def run_apsp(args, rank, world, dev, steps=None, warmup=None):
+def run_apsp(args, rank, world, dev, steps, warmup, with_cpu=False):
+    """C5: APSP over the largest WCC.  A step = dawn_apsp on this rank's shard + (N > 1) one
+    NCCL all-gather of the records; time = max over ranks."""
     import torch
     import torch.distributed as tdist
     import paper_2208_04514_b200 as dawn
 
-    steps = args.steps if steps is None else steps
-    warmup = args.warmup if warmup is None else warmup
-    g = build_graph("C5")
+    g = graphgen.config_graph("C5")
     G = dawn.Graph(g.row_ptr, g.col, True)
-    verts, e_wcc = g.largest_wcc()
+    verts, e_wcc = dawn.largest_wcc(G)  # the device helper picks the source set
     k = len(verts)
-    flush = torch.empty(int(2.2 * 132644864) // 4, dtype=torch.int32, device=dev)
+    flush = torch.empty(int(2.2 * L2_BYTES) // 4, dtype=torch.int32, device=dev)
     stream = torch.cuda.current_stream()
     for _ in range(warmup):
         dawn.apsp(G, verts, rank, world, gather=False)
     torch.cuda.synchronize()
-    ms, kern_ms = [], []
+    dawn.ms_counters(G)  # reset
+    tot, kern, gath = [], [], []
+    rec = None
     with ClockSampler(dev.index if dev.index is not None else 0) as clk:
         for _ in range(steps):
             flush.zero_()
             torch.cuda.synchronize()
             if world > 1:
                 tdist.barrier()
-            a, b, c = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+            a, c = _events()
+            b = torch.cuda.Event(enable_timing=True)
             a.record(stream)
             local = dawn.apsp(G, verts, rank, world, gather=False)
             c.record(stream)
             rec = dawn.gather_records(local, k, world) if world > 1 else local
             b.record(stream)
             torch.cuda.synchronize()
-            ms.append(a.elapsed_time(b))
-            kern_ms.append(a.elapsed_time(c))
-    t = sum(ms)
+            tot.append(a.elapsed_time(b))
+            kern.append(a.elapsed_time(c))
+            gath.append(c.elapsed_time(b))
+    cnt = dawn.ms_counters(G)
+    t_tot = sum(tot)
+    per_rank = {"kernel_ms": float(np.mean(kern)), "gather_ms": float(np.mean(gath))}
     if world > 1:
-        tt = torch.tensor([t], dtype=torch.float64, device=dev)
+        tt = torch.tensor([t_tot], dtype=torch.float64, device=dev)
         tdist.all_reduce(tt, op=tdist.ReduceOp.MAX)
-        t = float(tt.item())
-    value = k * steps / (t * 1e-3)
+        t_tot = float(tt.item())
+        pr = torch.tensor([per_rank["kernel_ms"], per_rank["gather_ms"]], dtype=torch.float64,
+                          device=dev)
+        allpr = [torch.zeros_like(pr) for _ in range(world)]
+        tdist.all_gather(allpr, pr)
+        per_rank = {"kernel_ms": [float(x[0]) for x in allpr],
+                    "gather_ms": [float(x[1]) for x in allpr]}
+    value = k * steps / (t_tot * 1e-3)
     peak, peak_kind = peaks()
-    per_src = 4 * e_wcc + 8 * k + 32  # B_SOVM per source of the component (SURVEY §8(d))
     mine = len(dawn.apsp_shard(k, rank, world))
-    achieved = per_src * mine / (np.mean(kern_ms) * 1e-3) / 1e9
-    recs = dawn.records_to_numpy(rec)
-    return {"value": value, "unit": "sources/s", "n_gpus": world, "steps": steps,
-            "ms_per_step": t / steps, "scaling": "strong",
-            "config": {"workload": f"C5: {CONFIG_TEXT['C5']}", "n": g.n, "m": g.m,
-                       "S_wcc": k, "E_wcc": e_wcc, "batch": dawn.MS_BATCH,
-                       "l2": "flushed between timed steps"},
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "peak_kind": peak_kind,
-                         "kernel": "k_ms64 (one persistent launch per rank)",
-                         "bytes_model": "per source B_SOVM = 4*E_wcc + 8*S_wcc + 32",
-                         "traffic": json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json"))).get("apsp-C5") if os.path.exists(os.path.join(ROOT, "profiles", "ncu_traffic.json")) else None},
-            "check": {"all_reached_S_wcc_minus_1": bool(np.all(recs["reached"] == k - 1))},
-            "clocks": clk.summary()}, g, verts
+    # executed bytes of k_ms64 (SURVEY §8(d): "for ms64, B_exec is the per-batch word traffic"):
+    # every level sweeps three 32-byte words per vertex (the frontier / seen test word, the
+    # next / seen word, the new frontier word written), every gathered adjacency entry moves a
+    # 4-byte index and a 32-byte word, every reduction 8 bytes
+    b_exec = 96 * g.n * cnt["levels"] + 36 * cnt["gathered"] + 8 * cnt["reductions"]
+    kern_s = float(np.sum(kern)) * 1e-3
+    ach = b_exec / kern_s / 1e9
+    l2 = l2_peak(dev) if world == 1 else None
+    per_src_sovm = 4 * e_wcc + 8 * k + 32
+    res = {
+        "value": value, "unit": "sources/s", "n_gpus": world, "steps": steps,
+        "ms_per_step": t_tot / steps, "scaling": "strong",
+        "workload": f"C5: {CONFIG_TEXT['C5']}", "n": g.n, "m": g.m, "S_wcc": k, "E_wcc": e_wcc,
+        "batch": dawn.MS_BATCH, "per_rank": per_rank,
+        "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
+                     "frac": ach / peak, "peak_kind": peak_kind,
+                     "kernel": "k_ms64 (one persistent launch per rank per step)",
+                     "bytes_model": "B_exec = 96*n*levels + 36*gathered + 8*reductions "
+                                    "(executed word traffic, kernel counters)",
+                     "exec_bytes_per_step": b_exec / steps,
+                     "counters_per_step": {x: v / steps for x, v in cnt.items()},
+                     "l2_peak_GBps": l2["read_GBps"] if l2 else None,
+                     "frac_l2": ach / l2["read_GBps"] if l2 else None,
+                     "traffic": ncu_traffic("apsp-C5"),
+                     "sovm_equivalent_GBps": per_src_sovm * mine * steps / kern_s / 1e9,
+                     "sovm_note": "per-source B_SOVM = 4*E_wcc + 8*S_wcc + 32 bytes: what 173K "
+                                  "independent SOVM searches would move; the bit-parallel kernel "
+                                  "shares each adjacency pass among 256 sources, so this is "
+                                  "work avoided, not bandwidth"},
+        "l2_probe": l2,
+        "check": {"all_reached_S_wcc_minus_1":
+                  bool(np.all(dawn.records_to_numpy(rec)["reached"] == k - 1))},
+        "clocks": clk.summary(),
+        "gpu_launches_per_step": 1,
+    }
+    # e2e: host source list in, records out to host (the API a user calls)
+    host_rec = torch.empty((k if world > 1 else mine, 4), dtype=torch.int64, pin_memory=True)
+    e_ms = []
+    for _ in range(max(1, min(steps, 3))):
+        flush.zero_()
+        torch.cuda.synchronize()
+        if world > 1:
+            tdist.barrier()
+        a, b = _events()
+        a.record(stream)
+        r = dawn.apsp(G, verts, rank, world, gather=world > 1)
+        host_rec.copy_(r, non_blocking=True)
+        b.record(stream)
+        torch.cuda.synchronize()
+        e_ms.append(a.elapsed_time(b))
+    e_tot = sum(e_ms)
+    if world > 1:
+        tt = torch.tensor([e_tot], dtype=torch.float64, device=dev)
+        tdist.all_reduce(tt, op=tdist.ReduceOp.MAX)
+        e_tot = float(tt.item())
+    res["e2e"] = {"value": k * len(e_ms) / (e_tot * 1e-3), "unit": "sources/s",
+                  "h2d_bytes_per_step": int(8 * k), "d2h_bytes_per_step": int(host_rec.numel() * 8),
+                  "how": "dawn_apsp from the host int64 source list (uploaded by the call), "
+                         "records (32 B each; all-gathered at N > 1) copied to pinned host memory"}
+    if with_cpu:
+        cores = len(os.sched_getaffinity(0))
+        rate, cnt_s, dt = cpu_oracle_apsp(g, verts, args.cpu_budget, cores)
+        res["cpu_baseline"] = {"value": rate, "unit": "sources/s", "cores": cores,
+                               "kind": "oracle",
+                               "sample": f"oracle_records (literal Algorithm 2 + record per "
+                                         f"source) over the first {cnt_s} largest-WCC sources "
+                                         f"on {cores} threads, {dt:.1f} s"}
+    return res
 
 
 def run_dawn(args):
@@ -471,41 +572,48 @@ def run_dawn(args):
         import torch.distributed as tdist
         tdist.init_process_group("nccl", device_id=dev)
     import paper_2208_04514_b200 as dawn
-    dawn.lib()
-    if args.workload == "apsp":
-        res, g, verts = run_apsp(args, rank, world, dev)
-        res.update({"metric": "SSSP GTEPS (1 B200) and APSP sources/sec at 1/2/4/8 B200 vs HBM roofline",
-                    "warmup": args.warmup, "higher_is_better": True, "vs_baseline": None,
-                    "dtype": "u64", "data": "synthetic", "gpu_launches": args.steps})
-        if rank == 0 and world == 1 and not args.no_cpu:
-            rate, cnt, cores, dt = cpu_oracle_apsp(g, verts, args.cpu_budget)
-            res["cpu_baseline"] = {"value": rate, "unit": "sources/s", "cores": cores,
-                                   "kind": "oracle",
-                                   "sample": f"oracle_records (literal Algorithm 2 per source) "
-                                             f"over the first {cnt} largest-WCC sources, {dt:.1f} s"}
+    dawn.lib()  # loads libdawn.so (raises if missing: there is no fallback)
+    workload = args.workload
+    if workload == "auto":
+        workload = "sssp" if world == 1 else "apsp"
+    common = {"metric": METRIC, "n_gpus": world, "warmup": args.warmup, "higher_is_better": True,
+              "vs_baseline": None, "data": "synthetic (seeded generators, graphgen/)"}
+    if workload == "apsp":
+        r = run_apsp(args, rank, world, dev, args.steps, args.warmup,
+                     with_cpu=(rank == 0 and world == 1 and not args.no_cpu))
+        res = {**common, "value": r.pop("value"), "unit": r.pop("unit"),
+               "steps": args.steps, "ms_per_step": r.pop("ms_per_step"), "scaling": "strong",
+               "dtype": "u64 (256-source bit words; uint32 ids/distances)",
+               "config": {"workload": r.pop("workload"), "n": r.pop("n"), "m": r.pop("m"),
+                          "S_wcc": r.pop("S_wcc"), "E_wcc": r.pop("E_wcc"),
+                          "parallelism": f"sources sharded over {world} rank(s), 256-source "
+                                         "batches round-robin, one NCCL all-gather",
+                          "l2": "flushed between timed steps (2.2x L2 write)"},
+               "gpu_launches": args.steps * r.pop("gpu_launches_per_step")}
+        res.update(r)
     else:
-        res, g, srcs, er = run_sssp(args, rank, world, dev)
-        if args.extra and world == 1:
+        cfg = args.config
+        r = run_sssp(args, rank, world, dev, cfg, args.steps, args.warmup, e2e=True,
+                     with_cpu=(rank == 0 and world == 1 and not args.no_cpu))
+        res = {**common, "value": r.pop("value"), "unit": r.pop("unit"), "steps": args.steps,
+               "ms_per_step": r.pop("ms_per_step"), "scaling": "weak",
+               "dtype": "u32 (vertex ids, offsets, distances; 32-bit bitmap words)",
+               "config": {"workload": r.pop("workload"), "n": r.pop("n"), "m": r.pop("m"),
+                          "sources_per_rank": r.pop("sources_per_step"), "variant": args.variant,
+                          "parallelism": f"dp{world}: independent sources per rank (replicas)",
+                          "l2": "flushed between timed steps (2.2x L2 write)"},
+               "gpu_launches": args.steps * r.pop("gpu_launches_per_step")}
+        res.update(r)
+        if world == 1 and args.extra:
             ex = {}
-            for cfg, reps, st in (("C1", 64, max(3, args.steps)), ("C3", 1, 2), ("C4", 1, 2)):
-                if cfg == args.config:
+            for c in ("C1", "C2", "C3"):
+                if c == cfg:
                     continue
-                r, _, _, _ = run_sssp(args, rank, world, dev, cfg=cfg, steps=st, warmup=3,
-                                      e2e=False, reps=reps)
-                ex[cfg] = r
-            res["extra_configs"] = ex
-        if args.secondary:
-            sec, _, _ = run_apsp(args, rank, world, dev, steps=max(1, min(args.steps, 3)),
-                                 warmup=1)
-            res["secondary"] = sec
-        if world == 1:
-            res["l2_probe"] = l2_probe(dev)
-        if rank == 0 and world == 1 and not args.no_cpu:
-            gte, done, t = cpu_oracle_sssp(g, srcs, args.cpu_budget)
-            res["cpu_baseline"] = {"value": gte, "unit": "GTEPS", "cores": 1, "kind": "oracle",
-                                   "sample": f"oracle_sovm (literal Algorithm 2, 1 thread) on the "
-                                             f"first {done} of the {len(srcs)} bench sources, "
-                                             f"{t:.1f} s"}
+                ex[c] = run_sssp(args, rank, world, dev, c, max(3, min(args.steps, 10)), 3,
+                                 e2e=False)
+            ex["C5"] = run_apsp(args, rank, world, dev, max(2, min(args.steps, 5)), 2,
+                                with_cpu=not args.no_cpu)
+            res["configs"] = ex
     if world > 1:
         import torch.distributed as tdist
         tdist.barrier()
@@ -515,49 +623,52 @@ def run_dawn(args):
 
 
 def run_reference(args):
-    """Reference arm for this tier: the CPU oracle, as it stands, on the host cores."""
+    """Reference arm for this tier: the CPU oracle, as it stands, on the host cores, on the same
+    config / metric / unit as the dawn arm (C4 SSSP GTEPS at N = 1, C5 APSP sources/s at N > 1).
+    Under torchrun rank 0 alone runs it; the other ranks exit without work."""
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return
     cores = len(os.sched_getaffinity(0))
-    if args.workload == "apsp":
-        g = build_graph("C5")
-        verts, _ = g.largest_wcc()
-        rates = []
+    workload = args.workload if args.workload != "auto" else ("sssp" if world == 1 else "apsp")
+    per_step = max(2.0, args.cpu_budget / max(1, args.steps + args.warmup))
+    if workload == "apsp":
+        g = graphgen.config_graph("C5")
+        import oracle
+        verts, _ = oracle.largest_wcc(g.n, g.row_ptr, g.col)
         for _ in range(args.warmup):
-            cpu_oracle_apsp(g, verts, min(args.cpu_budget, 4.0))
+            cpu_oracle_apsp(g, verts, per_step, cores)
+        rates, cnt = [], 0
         for _ in range(args.steps):
-            rate, cnt, cores, dt = cpu_oracle_apsp(g, verts, args.cpu_budget / max(1, args.steps))
+            rate, cnt, dt = cpu_oracle_apsp(g, verts, per_step, cores)
             rates.append(rate)
         value, unit = float(np.mean(rates)), "sources/s"
-        sample = f"oracle_records over the first {cnt} largest-WCC sources per step"
+        sample = (f"oracle_records (literal Algorithm 2 per source) over the first {cnt} "
+                  f"largest-WCC sources per step, {cores} threads")
         cfgtxt = f"C5: {CONFIG_TEXT['C5']}"
-        used = cores
     else:
         cfg = args.config
-        g = build_graph(cfg)
+        g = graphgen.config_graph(cfg)
         srcs = sources_for(g, cfg, 0)
-        budget = max(1.0, args.cpu_budget / max(1, args.steps + args.warmup))
         for _ in range(args.warmup):
-            cpu_oracle_sssp(g, srcs, budget)
+            cpu_oracle_sssp(g, srcs, per_step, cores)
         e_tot = t_tot = 0.0
         done_tot = 0
         for i in range(args.steps):
-            gte, done, t = cpu_oracle_sssp(g, np.roll(srcs, -i), budget)
+            gte, done, t = cpu_oracle_sssp(g, np.roll(srcs, -i * cores), per_step, cores)
             e_tot += gte * t
             t_tot += t
             done_tot += done
         value, unit = e_tot / t_tot, "GTEPS"
-        sample = f"oracle_sovm (literal Algorithm 2, 1 thread), {done_tot} source SSSPs over {args.steps} steps"
+        sample = (f"oracle_sovm (literal Algorithm 2), one source per host thread, {done_tot} "
+                  f"source SSSPs over {args.steps} steps")
         cfgtxt = f"{cfg}: {CONFIG_TEXT[cfg]}"
-        used = 1
-    res = {"impl": "reference",
-           "metric": "SSSP GTEPS (1 B200) and APSP sources/sec at 1/2/4/8 B200 vs HBM roofline",
-           "value": value, "unit": unit, "n_gpus": world, "steps": args.steps,
-           "warmup": args.warmup, "higher_is_better": True, "dtype": "u32", "data": "synthetic",
+    res = {"impl": "reference", "metric": METRIC, "value": value, "unit": unit,
+           "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
+           "dtype": "u32", "data": "synthetic (seeded generators, graphgen/)",
            "vs_baseline": None, "config": {"workload": cfgtxt},
-           "cpu_baseline": {"value": value, "unit": unit, "cores": used, "kind": "oracle",
+           "cpu_baseline": {"value": value, "unit": unit, "cores": cores, "kind": "oracle",
                             "sample": sample},
            "e2e": {"value": value, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(res), flush=True)
@@ -566,17 +677,17 @@ def run_reference(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["dawn", "reference"], default="dawn")
-    ap.add_argument("--workload", choices=["sssp", "apsp"], default="sssp")
-    ap.add_argument("--config", choices=["C1", "C2", "C3", "C4"], default="C2")
+    ap.add_argument("--workload", choices=["auto", "sssp", "apsp"], default="auto",
+                    help="auto: SSSP C4 at N=1, APSP C5 at N>1")
+    ap.add_argument("--config", choices=["C1", "C2", "C3", "C4"], default="C4")
     ap.add_argument("--variant", choices=["auto", "push", "pull"], default="auto")
-    ap.add_argument("--cpu-budget", type=float, default=15.0, help="seconds of oracle CPU work")
+    ap.add_argument("--cpu-budget", type=float, default=20.0, help="seconds of oracle CPU work")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--no-secondary", dest="secondary", action="store_false")
     ap.add_argument("--no-extra", dest="extra", action="store_false",
-                    help="skip the C1/C3/C4 lines (reported under extra_configs)")
+                    help="skip the other configs (C1/C2/C3/C5 under 'configs')")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "dawn":
         print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)

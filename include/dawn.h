@@ -51,8 +51,13 @@ enum {
   DAWN_GRAPH_SYMMETRIC = 1, /* arcs come in both directions: CSC == CSR, in_* may be NULL   */
   DAWN_GRAPH_VALIDATE = 2,  /* check row_ptr monotone, row_ptr[0]=0, row_ptr[n]=m, cols in
                                range; synchronises `stream` once                           */
-  DAWN_GRAPH_TRACE = 4      /* dawn_sssp records one dawn_trace_rec per level (device
+  DAWN_GRAPH_TRACE = 4,     /* dawn_sssp records one dawn_trace_rec per level (device
                                %globaltimer), readable with dawn_graph_trace               */
+  DAWN_GRAPH_LEAN = 8       /* memory-frugal residency (E13): no
+                               bit-parallel words (dawn_msssp / dawn_apsp then return
+                               DAWN_ERR_CONFIG), no degree-ordered in-row copy (pull probes
+                               the caller's adjacency order), no augmented arc array.  The
+                               same distances; C4 workspace 7.5 GB -> 1.1 GB                  */
 };
 
 /* Direction variants of one level step. */
@@ -164,7 +169,16 @@ typedef enum {
   DAWN_PARAM_SOLO_EDGES = 4,
   DAWN_PARAM_CLUSTER_START = 5,
   DAWN_PARAM_CLUSTER_HANDOVER_EDGES = 6,
-  DAWN_PARAM_BITMAP_PUSH_GROW_EDGES = 7
+  DAWN_PARAM_BITMAP_PUSH_GROW_EDGES = 7,
+  DAWN_PARAM_NARROW_QUEUE_CAP = 8, /* lowers k_narrow's per-CTA queue capacity (entries, >= 32;
+                                      capped at the load-time capacity).  Only for tests that
+                                      force queue-overflow hand-overs; speed only.            */
+  DAWN_PARAM_BATCH_LANES = 9       /* dawn_sssp_batch on the grid-wide kernel runs this many
+                                      searches at once, each on 1/lanes of the SMs with its own
+                                      per-search state and stream (the sources are
+                                      independent).  1 .. 4 (n <= 2^22) or
+                                      1 .. 2 (larger n; 1 with DAWN_GRAPH_LEAN).  Default set at
+                                      load from B200 measurements.              */
 } dawn_param;
 
 /* Set one tunable (INVALID_ARGUMENT for an unknown key or a negative value). */
@@ -192,7 +206,11 @@ dawn_status dawn_sssp(dawn_graph g, int64_t source, uint32_t variant, uint32_t *
  *     reading the source id from the device array;
  *   - otherwise ONE launch of the grid-wide kernel running the k searches one after the other
  *     (a grid barrier between searches instead of a kernel boundary).
- *   sources  DEVICE uint32[k], each in [0, n) (not checked: the array is not read on the host)
+ *   sources  DEVICE uint32[k], each in [0, n).  The list is validated ON THE DEVICE before any
+ *            search starts (every kernel of the call checks the whole list first): if an id is
+ *            >= n, nothing is written (dist, stats untouched) and the handle's sticky error flag
+ *            is set; since the array is not read on the host the call itself returns DAWN_OK and
+ *            dawn_graph_check() reports DAWN_ERR_BOUNDS (validation before work).
  *   dist     device uint32[k][n] (row i for sources[i], fully overwritten)
  *   stats    device dawn_sssp_stats[k] or NULL
  * k == 0 is a no-op; k >= 2^32 -> CAPACITY.
@@ -240,6 +258,35 @@ dawn_status dawn_apsp(dawn_graph g, const int64_t *sources, int64_t k, int32_t r
 #define DAWN_TRACE_CAP 65536
 dawn_status dawn_graph_trace(dawn_graph g, dawn_trace_rec *host_out, int64_t cap, int64_t *count,
                              void *stream);
+
+/* Synchronise `stream` and report deferred errors of this handle: DAWN_ERR_BOUNDS if a
+ * dawn_sssp_batch enqueued since the last check met a device source id outside [0, n) (that
+ * call wrote nothing; the flag is cleared by this call), DAWN_ERR_CUDA if the stream holds a
+ * CUDA error, else DAWN_OK.                                                                   */
+dawn_status dawn_graph_check(dawn_graph g, void *stream);
+
+/*
+ * The largest weakly connected component (Table 1: S_wcc / E_wcc; the APSP
+ * source set of E11-E12, L303-308), computed on the device: lock-free union-find hooking over
+ * every arc (a directed arc joins its endpoints' components), the larger root hooked onto the
+ * smaller so a root is its component's minimum id; then node and arc counts per component.
+ * "Largest" = most nodes, ties -> more arcs, then the smaller minimum vertex id (DESIGN.md
+ * reading Q15).  Uses the handle's frontier scratch: not concurrent with other calls on g.
+ *   sources_out  HOST int64[n] or NULL: the component's vertices, ascending
+ *   k            HOST, receives the component's node count S_wcc
+ *   arcs         HOST or NULL, receives E_wcc = the arcs whose source lies in the component
+ * Synchronises `stream`.  Errors: INVALID_ARGUMENT, CUDA.
+ */
+dawn_status dawn_largest_wcc(dawn_graph g, int64_t *sources_out, int64_t *k, uint64_t *arcs,
+                             void *stream);
+
+/* Executed-schedule counters of the bit-parallel kernel (dawn_msssp / dawn_apsp), summed over
+ * every launch on this handle since load or the previous read, then reset.  Synchronises
+ * `stream`.  host_out[0] levels run (over all batches), [1] adjacency entries gathered (push
+ * arcs of active rows + pull in-edge probes; each costs a 4-B index and a 32-B word gather),
+ * [2] 64-bit word reductions issued (red.or), [3] 256-source batches.  Measurement only
+ * (bench.py derives the executed bytes B_exec of SURVEY §8(d) from them).                   */
+dawn_status dawn_graph_ms_counters(dawn_graph g, uint64_t *host_out, void *stream);
 
 /* Thread-local description of the last error of this thread ("" if none). */
 const char *dawn_last_error(void);

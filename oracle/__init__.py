@@ -60,6 +60,8 @@ def _load():
         L.oracle_certify.argtypes = [i64, vp, vp, vp, vp, i64, vp, ctypes.POINTER(ctypes.c_int64)]
         L.oracle_records.restype = ctypes.c_int
         L.oracle_records.argtypes = [i64, vp, vp, i64, vp, ctypes.c_int, vp]
+        L.oracle_largest_wcc.restype = ctypes.c_int64
+        L.oracle_largest_wcc.argtypes = [i64, vp, vp, vp, ctypes.POINTER(ctypes.c_uint64)]
         L.oracle_hash_term.restype = ctypes.c_uint64
         L.oracle_hash_term.argtypes = [ctypes.c_uint32, ctypes.c_uint32]
         _lib = L
@@ -152,6 +154,18 @@ def records(n, row_ptr, col, sources, threads: int | None = None):
     if rc:
         raise ValueError(f"oracle_records: error {rc}")
     return out
+
+
+def largest_wcc(n, row_ptr, col):
+    """(vertices of the largest WCC ascending as int64[S_wcc], E_wcc): PAPER Table 1,
+    "largest" per reading Q15 (most nodes, then most arcs, then the smaller minimum id)."""
+    ptr, idx = _csr(row_ptr, col)
+    out = np.empty(max(1, n), np.int64)
+    arcs = ctypes.c_uint64(0)
+    k = _load().oracle_largest_wcc(n, _p(ptr), _p(idx), _p(out), ctypes.byref(arcs))
+    if k < 0:
+        raise MemoryError("oracle_largest_wcc")
+    return out[:k].copy(), int(arcs.value)
 
 
 def hash_term(v: int, d: int) -> int:

@@ -22,6 +22,11 @@
  *   oracle_certify     the four-invariant certificate (SURVEY §8(c) pins; Fact 1 L162-164).
  *   oracle_records     oracle_sovm over many sources on a pthread pool (sources are the paper's
  *                      own scaling axis).
+ *   oracle_largest_wcc the largest weakly connected component (Table 1:
+ *                      S_wcc, E_wcc; the APSP source set of E11-E12 L303-308): plain FIFO
+ *                      labelling over the undirected view (out-arcs plus reversed arcs), vertices
+ *                      taken in ascending order; "largest" = most nodes, then most arcs, then the
+ *                      smaller minimum id (reading Q15).
  *
  * Every function is pinned by tests/test_oracle.py against closed forms, brute force, golden
  * records (tests/golden/) or each other; see DESIGN.md "Oracle pins".
@@ -357,4 +362,69 @@ int oracle_records(int64_t n, const int64_t *row_ptr, const int32_t *col, int64_
   for (int t = 0; t < threads; ++t) pthread_join(th[t], NULL);
   free(th);
   return J.err;
+}
+
+/*
+ * Largest weakly connected component (Table 1; reading Q15 for "largest").
+ * Components of the undirected view: u ~ v iff an arc u->v or v->u exists.  Labelling: for
+ * v = 0, 1, ..., n-1 not yet labelled, a FIFO search over out- and in-arcs labels v's whole
+ * component (so each component is found at its minimum vertex id).  Then per component the node
+ * count and the arc count (arcs whose source lies in it); the chosen component has the most
+ * nodes, ties -> the most arcs, then the smaller minimum id (the earlier one found).
+ * Writes its vertices ascending into out (capacity n) and returns their number; *arcs_out gets
+ * E_wcc.  Returns -1 on allocation failure.
+ */
+int64_t oracle_largest_wcc(int64_t n, const int64_t *row_ptr, const int32_t *col, int64_t *out,
+                           uint64_t *arcs_out) {
+  const int64_t m = row_ptr[n];
+  /* reversed arcs (in-adjacency) by a counting sort */
+  int64_t *in_ptr = calloc((size_t)n + 1, sizeof(int64_t));
+  int32_t *in_src = malloc(sizeof(int32_t) * (size_t)(m > 0 ? m : 1));
+  int64_t *label = malloc(sizeof(int64_t) * (size_t)n);
+  int64_t *queue = malloc(sizeof(int64_t) * (size_t)n);
+  if (!in_ptr || !in_src || !label || !queue) {
+    free(in_ptr); free(in_src); free(label); free(queue);
+    return -1;
+  }
+  for (int64_t j = 0; j < m; ++j) in_ptr[col[j] + 1]++;
+  for (int64_t v = 0; v < n; ++v) in_ptr[v + 1] += in_ptr[v];
+  {
+    int64_t *fill = malloc(sizeof(int64_t) * (size_t)n);
+    if (!fill) { free(in_ptr); free(in_src); free(label); free(queue); return -1; }
+    for (int64_t v = 0; v < n; ++v) fill[v] = in_ptr[v];
+    for (int64_t u = 0; u < n; ++u)
+      for (int64_t j = row_ptr[u]; j < row_ptr[u + 1]; ++j) in_src[fill[col[j]]++] = (int32_t)u;
+    free(fill);
+  }
+  for (int64_t v = 0; v < n; ++v) label[v] = -1;
+  int64_t best = -1, best_nodes = 0;
+  uint64_t best_arcs = 0;
+  for (int64_t s = 0; s < n; ++s) {
+    if (label[s] >= 0) continue;
+    int64_t head = 0, tail = 0, nodes = 0;
+    uint64_t arcs = 0;
+    label[s] = s;
+    queue[tail++] = s;
+    while (head < tail) {
+      const int64_t v = queue[head++];
+      nodes++;
+      arcs += (uint64_t)(row_ptr[v + 1] - row_ptr[v]);
+      for (int64_t j = row_ptr[v]; j < row_ptr[v + 1]; ++j)
+        if (label[col[j]] < 0) { label[col[j]] = s; queue[tail++] = col[j]; }
+      for (int64_t j = in_ptr[v]; j < in_ptr[v + 1]; ++j)
+        if (label[in_src[j]] < 0) { label[in_src[j]] = s; queue[tail++] = in_src[j]; }
+    }
+    /* s is this component's minimum id; a later component wins only if strictly larger */
+    if (nodes > best_nodes || (nodes == best_nodes && arcs > best_arcs)) {
+      best = s;
+      best_nodes = nodes;
+      best_arcs = arcs;
+    }
+  }
+  int64_t k = 0;
+  for (int64_t v = 0; v < n; ++v)
+    if (label[v] == best) out[k++] = v;
+  if (arcs_out) *arcs_out = best_arcs;
+  free(in_ptr); free(in_src); free(label); free(queue);
+  return k;
 }

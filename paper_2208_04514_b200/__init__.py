@@ -17,13 +17,13 @@ import subprocess
 import numpy as np
 import torch
 
-__all__ = ["build", "Graph", "sssp", "msssp", "apsp", "apsp_shard", "DawnError", "UNREACHED",
-           "AUTO", "PUSH", "PULL", "MS_BATCH", "REC_DTYPE", "records_to_numpy", "stats_to_dict",
-           "gather_records"]
+__all__ = ["build", "Graph", "sssp", "sssp_batch", "msssp", "apsp", "apsp_shard", "largest_wcc",
+           "check", "DawnError", "UNREACHED", "AUTO", "PUSH", "PULL", "MS_BATCH", "REC_DTYPE",
+           "records_to_numpy", "stats_to_dict", "gather_records"]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _CSRC = os.path.join(_HERE, "csrc")
-_LIB = os.environ.get("DAWN_LIB") or os.path.join(_HERE, "libdawn.so")  # DAWN_LIB: A/B builds
+_LIB = os.path.join(_HERE, "libdawn.so")  # always the in-tree build (no override)
 _INCLUDE = os.path.join(os.path.dirname(_HERE), "include")
 
 UNREACHED = 0xFFFFFFFF
@@ -111,6 +111,13 @@ def lib():
         L.dawn_graph_trace.argtypes = [vp, vp, i64, ctypes.POINTER(ctypes.c_int64), vp]
         L.dawn_version.restype = ctypes.c_char_p
         L.dawn_version.argtypes = []
+        L.dawn_graph_check.restype = st
+        L.dawn_graph_check.argtypes = [vp, vp]
+        L.dawn_graph_ms_counters.restype = st
+        L.dawn_graph_ms_counters.argtypes = [vp, vp, vp]
+        L.dawn_largest_wcc.restype = st
+        L.dawn_largest_wcc.argtypes = [vp, vp, ctypes.POINTER(ctypes.c_int64),
+                                       ctypes.POINTER(ctypes.c_uint64), vp]
         _lib = L
     return _lib
 
@@ -141,7 +148,8 @@ class Graph:
     """
 
     def __init__(self, row_ptr, col, symmetric: bool, in_row_ptr=None, in_col=None,
-                 validate: bool = False, device=None, stream=None, trace: bool = False):
+                 validate: bool = False, device=None, stream=None, trace: bool = False,
+                 lean: bool = False):
         dev = torch.device(device) if device is not None else torch.device("cuda",
                                                                             torch.cuda.current_device())
         to = lambda a, dt: (a if isinstance(a, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(a))
@@ -153,7 +161,9 @@ class Graph:
         self.symmetric = bool(symmetric)
         self.in_row_ptr = to(in_row_ptr, torch.int64) if in_row_ptr is not None else None
         self.in_col = to(in_col, torch.int32) if in_col is not None else None
-        flags = (1 if symmetric else 0) | (2 if validate else 0) | (4 if trace else 0)
+        # lean: DAWN_GRAPH_LEAN (no multi-source words / degree-ordered in-rows / arc array)
+        flags = ((1 if symmetric else 0) | (2 if validate else 0) | (4 if trace else 0) |
+                 (8 if lean else 0))
         nbytes = lib().dawn_workspace_bytes(self.n, self.m, flags)
         if nbytes == 0:
             raise DawnError(4, "unsupported graph size")
@@ -184,7 +194,8 @@ class Graph:
         return buf[: min(cnt.value, len(buf) - 1)].copy()
 
     _PARAMS = {"alpha": 0, "beta": 1, "ms_alpha": 2, "bitmap_push_edges": 3, "solo_edges": 4,
-               "cluster_start": 5, "cluster_handover_edges": 6, "bitmap_push_grow_edges": 7}
+               "cluster_start": 5, "cluster_handover_edges": 6, "bitmap_push_grow_edges": 7,
+               "narrow_queue_cap": 8, "batch_lanes": 9}
 
     def set_tuning(self, **kw):
         """dawn_graph_set_param for each keyword (alpha, beta, ms_alpha, bitmap_push_edges,
@@ -214,7 +225,7 @@ def sssp(g: Graph, source: int, variant="auto", stats: bool = False, out: torch.
 
 
 def sssp_batch(g: Graph, sources: torch.Tensor, variant="auto", stats: bool = False,
-               out: torch.Tensor | None = None, stream=None):
+               out: torch.Tensor | None = None, stream=None, check: bool = False):
     """dawn_sssp_batch: k single-source searches with no host work between them (include/dawn.h:
     concurrent one-CTA searches on tiny graphs, one grid-wide launch running them one after the
     other otherwise).  `sources`: uint32/int32 CUDA tensor [k] of vertex ids in [0, n).
@@ -226,7 +237,36 @@ def sssp_batch(g: Graph, sources: torch.Tensor, variant="auto", stats: bool = Fa
     st = torch.zeros((k, 4), dtype=torch.int64, device=g.device) if stats else None
     _check(lib().dawn_sssp_batch(g.handle, _dptr(sources), k, _VARIANTS[variant], _dptr(dist),
                                  _dptr(st), _stream(stream)))
+    if check:  # synchronise and surface a device-side source-id error (DAWN_ERR_BOUNDS)
+        globals()["check"](g, stream)
     return (dist, st) if stats else dist
+
+
+def check(g: Graph, stream=None):
+    """dawn_graph_check: synchronise the stream; raise DawnError(DAWN_ERR_BOUNDS) if a
+    dawn_sssp_batch since the last check met a source id outside [0, n) (it wrote nothing)."""
+    _check(lib().dawn_graph_check(g.handle, _stream(stream)))
+
+
+def ms_counters(g: Graph, stream=None) -> dict:
+    """dawn_graph_ms_counters: executed-schedule counters of the bit-parallel kernel since the
+    last read (levels, adjacency entries gathered, word reductions, batches); resets them."""
+    out = np.zeros(4, np.uint64)
+    _check(lib().dawn_graph_ms_counters(g.handle, out.ctypes.data_as(ctypes.c_void_p),
+                                        _stream(stream)))
+    return {"levels": int(out[0]), "gathered": int(out[1]), "reductions": int(out[2]),
+            "batches": int(out[3])}
+
+
+def largest_wcc(g: Graph, stream=None):
+    """dawn_largest_wcc (device union-find): (vertices of the largest WCC ascending as int64
+    numpy array, E_wcc).  PAPER Table 1; ties per DESIGN.md reading Q15."""
+    out = np.empty(g.n, np.int64)
+    k = ctypes.c_int64(0)
+    arcs = ctypes.c_uint64(0)
+    _check(lib().dawn_largest_wcc(g.handle, out.ctypes.data_as(ctypes.c_void_p), ctypes.byref(k),
+                                  ctypes.byref(arcs), _stream(stream)))
+    return out[: k.value].copy(), int(arcs.value)
 
 
 def stats_to_dict(st: torch.Tensor) -> dict:

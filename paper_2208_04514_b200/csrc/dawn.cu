@@ -5,10 +5,11 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
-#include <string>
+#include <new>
 #include <vector>
 
 #include "../../include/dawn.h"
@@ -17,27 +18,35 @@
 #include "small_kernel.cuh"
 #include "narrow_kernel.cuh"
 #include "sssp_kernel.cuh"
+#include "wcc_kernel.cuh"
 
 using namespace dawn;
 
 namespace {
 
-thread_local std::string g_err;
+// Thread-local message buffer: formatting never allocates, so no exception can start here.
+thread_local char g_err[512];
 
-dawn_status fail(dawn_status s, const std::string &msg) {
-  g_err = msg;
+dawn_status fail(dawn_status s, const char *fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
   return s;
 }
 dawn_status cuda_fail(cudaError_t e, const char *where) {
-  return fail(DAWN_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+  return fail(DAWN_ERR_CUDA, "%s: %s", where, cudaGetErrorString(e));
 }
+void clear_err() { g_err[0] = 0; }
 
 constexpr int kNT = 512;  // threads per CTA of the persistent kernels
-
-int env_int(const char *name, int dflt) {
-  const char *e = getenv(name);
-  return (e && *e) ? atoi(e) : dflt;
-}
+// Graph-size thresholds of the kernel choice (measured on B200)
+constexpr int64_t kSsspOneMaxN = 1 << 22;  // k_sssp<kNT, 1> (1 CTA/SM, 128 regs) up to 2^22
+constexpr int64_t kOneCtaMaxNM = 1 << 15;  // n + m this small: one CTA, barriers are __syncthreads
+constexpr int kMsBlocksPerSm = 2;          // k_ms64 CTAs per SM (if they fit)
+constexpr uint32_t kNarrowQcapMax = 1u << 20;
+// dawn_sssp_batch lanes (concurrent searches) by default: measured on B200
+int kDefaultLanes(int64_t n) { return n <= (int64_t(1) << 22) ? 2 : 1; }
 
 // ---------------------------------------------------------------- graph residency kernels
 __global__ void k_offsets32(const int64_t *__restrict__ in, uint32_t *__restrict__ out, int64_t n1) {
@@ -310,8 +319,21 @@ struct dawn_graph_s {
   bool narrow_owner = false;     // owner-computes queues (ids local: most arcs stay in a CTA)
   bool narrow_ok = false;        // the visited bitmap fits 16 CTAs and the cluster launches
   uint32_t narrow_wpc = 0, narrow_qcap = 0, narrow_grid = 0;
+  uint32_t narrow_qcap_max = 0;  // load-time capacity (DAWN_PARAM_NARROW_QUEUE_CAP lowers qcap)
   size_t narrow_smem = 0;
   uint32_t seq = 0;
+  bool lean = false;             // DAWN_GRAPH_LEAN: no ms64 words / icol2 / augmented arcs
+  int lanes = 1;                 // DAWN_PARAM_BATCH_LANES (<= L.nlanes)
+  // lane streams / fork-join events of dawn_sssp_batch (created at load, host resources only)
+  cudaStream_t lane_st[kMaxLanes] = {};
+  cudaEvent_t ev_fork = nullptr, ev_join[kMaxLanes] = {};
+  ~dawn_graph_s() {
+    for (int l = 0; l < kMaxLanes; ++l) {
+      if (lane_st[l]) cudaStreamDestroy(lane_st[l]);
+      if (ev_join[l]) cudaEventDestroy(ev_join[l]);
+    }
+    if (ev_fork) cudaEventDestroy(ev_fork);
+  }
 };
 
 namespace {
@@ -321,10 +343,10 @@ T *at(dawn_graph g, size_t off) {
   return reinterpret_cast<T *>(g->ws + off);
 }
 
-int grid_for(const void *fn, int nsm, const char *env_bps) {
+int grid_for(const void *fn, int nsm) {
   int bps = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, fn, kNT, 0);
-  bps = std::max(1, std::min(bps, env_int(env_bps, 2)));
+  bps = std::max(1, std::min(bps, 2));
   return std::min<int>(nsm * bps, (int)kMaxBlocks);
 }
 
@@ -336,26 +358,29 @@ dawn_status set_device(dawn_graph g) {
 
 }  // namespace
 
-extern "C" {
+// Every exported function runs its body inside this guard: a host allocation failure (the
+// only exception the bodies can raise: std::vector) becomes DAWN_ERR_CAPACITY instead of
+// crossing the C ABI.
+#define DAWN_GUARD(body)                                                       \
+  try {                                                                        \
+    clear_err();                                                               \
+    body                                                                       \
+  } catch (...) {                                                              \
+    return fail(DAWN_ERR_CAPACITY, "host allocation failed");                  \
+  }
 
-const char *dawn_last_error(void) { return g_err.c_str(); }
-const char *dawn_version(void) { return "dawn-b200 0.2 sm_100a"; }
+namespace {
 
-size_t dawn_workspace_bytes(int64_t n, int64_t m, uint32_t flags) {
-  if (n < 1 || n >= (int64_t(1) << 31) || m < 0 || m >= (int64_t(1) << 32)) return 0;
-  return make_layout(n, m, flags).total;
-}
-
-dawn_status dawn_graph_load_csr(int64_t n, int64_t m, const int64_t *row_ptr, const int32_t *col,
-                                const int64_t *in_row_ptr, const int32_t *in_col, uint32_t flags,
-                                void *workspace, size_t ws_bytes, void *stream, dawn_graph *out) {
-  g_err.clear();
+dawn_status load_csr(int64_t n, int64_t m, const int64_t *row_ptr, const int32_t *col,
+                     const int64_t *in_row_ptr, const int32_t *in_col, uint32_t flags,
+                     void *workspace, size_t ws_bytes, void *stream, dawn_graph *out) {
   if (!out) return fail(DAWN_ERR_INVALID_ARGUMENT, "out is NULL");
   *out = nullptr;
   if (n < 1 || m < 0) return fail(DAWN_ERR_INVALID_ARGUMENT, "n must be >= 1 and m >= 0");
   if (n >= (int64_t(1) << 31) || m >= (int64_t(1) << 32))
     return fail(DAWN_ERR_CAPACITY, "n must be < 2^31 and m < 2^32 (32-bit offsets)");
-  if (flags & ~uint32_t(DAWN_GRAPH_SYMMETRIC | DAWN_GRAPH_VALIDATE | DAWN_GRAPH_TRACE))
+  if (flags & ~uint32_t(DAWN_GRAPH_SYMMETRIC | DAWN_GRAPH_VALIDATE | DAWN_GRAPH_TRACE |
+                        DAWN_GRAPH_LEAN))
     return fail(DAWN_ERR_INVALID_ARGUMENT, "unknown graph flag");
   if (!row_ptr || (!col && m > 0) || !workspace)
     return fail(DAWN_ERR_INVALID_ARGUMENT, "row_ptr/col/workspace is NULL");
@@ -367,14 +392,15 @@ dawn_status dawn_graph_load_csr(int64_t n, int64_t m, const int64_t *row_ptr, co
     return fail(DAWN_ERR_INVALID_ARGUMENT, "workspace must be 256-byte aligned");
   Layout L = make_layout(n, m, flags);
   if (ws_bytes < L.total)
-    return fail(DAWN_ERR_WORKSPACE, "workspace too small: need " + std::to_string(L.total) +
-                                        " bytes, got " + std::to_string(ws_bytes));
+    return fail(DAWN_ERR_WORKSPACE, "workspace too small: need %zu bytes, got %zu", L.total,
+                ws_bytes);
   cudaPointerAttributes pa{};
   cudaError_t e = cudaPointerGetAttributes(&pa, workspace);
   if (e != cudaSuccess) return cuda_fail(e, "cudaPointerGetAttributes(workspace)");
   if (pa.type != cudaMemoryTypeDevice)
     return fail(DAWN_ERR_INVALID_ARGUMENT, "workspace is not device memory");
-  auto *g = new dawn_graph_s;
+  auto *g = new (std::nothrow) dawn_graph_s;
+  if (!g) return fail(DAWN_ERR_CAPACITY, "host allocation failed");
   g->n = n;
   g->m = m;
   g->flags = flags;
@@ -385,37 +411,31 @@ dawn_status dawn_graph_load_csr(int64_t n, int64_t m, const int64_t *row_ptr, co
   g->has_csc = has_csc;
   g->icol = sym ? col : in_col;
   g->trace = flags & DAWN_GRAPH_TRACE;
+  g->lean = flags & DAWN_GRAPH_LEAN;
   if ((e = cudaSetDevice(g->device)) != cudaSuccess) { delete g; return cuda_fail(e, "cudaSetDevice"); }
   cudaDeviceGetAttribute(&g->nsm, cudaDevAttrMultiProcessorCount, g->device);
-  g->alpha = (float)env_int("DAWN_ALPHA", 2);
-  g->bmpush_e = (uint32_t)env_int("DAWN_BMPUSH_E", 1 << 18);
-  g->bmpush_grow = (uint32_t)env_int("DAWN_BMPUSH_GROW", 4096);
-  g->solo_e = (uint32_t)env_int("DAWN_SOLO_E", 512);
-  g->beta = (float)env_int("DAWN_BETA", 96);
-  g->ms_alpha = (float)env_int("DAWN_MS_ALPHA", 2);
   // small graphs: k_sssp<kNT, 1> (one CTA per SM, 128 registers); big ones k_sssp<kNT, 2>
-  g->sssp_one = n <= env_int("DAWN_SSSP_ONE_MAX_N", 1 << 22);
+  g->sssp_one = n <= kSsspOneMaxN;
   g->sssp_grid = g->sssp_one ? std::min<int>(g->nsm, (int)kMaxBlocks)
-                             : grid_for((const void *)k_sssp<kNT, 2>, g->nsm, "DAWN_SSSP_BPS");
+                             : grid_for((const void *)k_sssp<kNT, 2>, g->nsm);
   {
     int optin = 0;
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, g->device);
     const size_t cap = (size_t)std::max(0, optin - 1024);
     g->small_cap = 0;
-    if (env_int("DAWN_SMALL", 1) &&
-        cudaFuncSetAttribute((const void *)k_small<1024>,
+    if (cudaFuncSetAttribute((const void *)k_small<1024>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cap) == cudaSuccess)
       g->small_cap = cap;
     cudaGetLastError();
     // k_narrow: visited slice of ceil(nwords / 16) words (multiple of 4) per CTA, the rest of
     // the shared memory holds the two frontier queues
     g->narrow_ok = false;
-    if ((uint64_t)n <= kNarrowMaxN && m > 0 && env_int("DAWN_NARROW", 1)) {
+    if ((uint64_t)n <= kNarrowMaxN && m > 0) {
       const uint32_t nw = (uint32_t)((n + 31) / 32);
       const uint32_t wpc = ((nw + kNarrowCluster - 1) / kNarrowCluster + 3) & ~3u;
       const size_t fixed = narrow_smem_bytes(wpc, 0);
       uint32_t qcap = fixed < cap ? (uint32_t)((cap - fixed) / kNarrowEntryBytes) : 0u;
-      qcap = std::min<uint32_t>(qcap, (uint32_t)env_int("DAWN_NARROW_QCAP", 1 << 20));
+      qcap = std::min<uint32_t>(qcap, kNarrowQcapMax);
       const size_t bytes = narrow_smem_bytes(wpc, qcap);
       if (qcap >= 32 && bytes <= cap &&
           cudaFuncSetAttribute((const void *)k_narrow, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -438,7 +458,7 @@ dawn_status dawn_graph_load_csr(int64_t n, int64_t m, const int64_t *row_ptr, co
             ncl >= 1) {
           g->narrow_ok = true;
           g->narrow_wpc = wpc;
-          g->narrow_qcap = qcap;
+          g->narrow_qcap = g->narrow_qcap_max = qcap;
           g->narrow_smem = bytes;
           g->narrow_grid = kNarrowCluster * (uint32_t)std::min(ncl, std::max(1, g->nsm / (int)kNarrowCluster));
         }
@@ -446,20 +466,22 @@ dawn_status dawn_graph_load_csr(int64_t n, int64_t m, const int64_t *row_ptr, co
     }
     cudaGetLastError();
   }
-  cudaFuncSetAttribute((const void *)k_ms64<kNT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)ms_smem_bytes(kNT));
-  {
+  if (!g->lean) {
+    cudaFuncSetAttribute((const void *)k_ms64<kNT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)ms_smem_bytes(kNT));
     int bps = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, (const void *)k_ms64<kNT>, kNT,
                                                   ms_smem_bytes(kNT));
-    bps = std::max(1, std::min(bps, env_int("DAWN_MS_BPS", 2)));
+    bps = std::max(1, std::min(bps, kMsBlocksPerSm));
     g->ms_grid = std::min<int>(g->nsm * bps, (int)kMaxBlocks);
   }
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const uint32_t nwords = (uint32_t)((n + 31) / 32);
   const int blocks = std::max(1, std::min<int>(g->nsm * 4, (int)((n + 255) / 256)));
-  cudaMemsetAsync(g->ws + L.ctrl, 0, sizeof(Ctrl), st);
-  cudaMemsetAsync(g->ws + L.cand, 0, 4 * (size_t)nwords, st);  // invariant: zero between uses
+  for (int l = 0; l < L.nlanes; ++l) {
+    cudaMemsetAsync(g->ws + L.lane[l].ctrl, 0, sizeof(Ctrl), st);
+    cudaMemsetAsync(g->ws + L.lane[l].cand, 0, 4 * (size_t)nwords, st);  // zero between uses
+  }
   cudaMemsetAsync(g->ws + L.msctrl, 0, sizeof(MsCtrl), st);
   if (flags & DAWN_GRAPH_VALIDATE) {
     k_validate<<<blocks, 256, 0, st>>>(row_ptr, col, n, m, &at<Ctrl>(g, L.ctrl)->err);
@@ -470,10 +492,10 @@ dawn_status dawn_graph_load_csr(int64_t n, int64_t m, const int64_t *row_ptr, co
     if ((e = cudaStreamSynchronize(st)) != cudaSuccess) { delete g; return cuda_fail(e, "validate"); }
     if (err) {
       delete g;
-      return fail(DAWN_ERR_INVALID_GRAPH, std::string("CSR invariant violated:") +
-                                              ((err & 1) ? " row_ptr[0]!=0 or row_ptr[n]!=m" : "") +
-                                              ((err & 2) ? " row_ptr not monotone" : "") +
-                                              ((err & 4) ? " column id out of range" : ""));
+      return fail(DAWN_ERR_INVALID_GRAPH, "CSR invariant violated:%s%s%s",
+                  (err & 1) ? " row_ptr[0]!=0 or row_ptr[n]!=m" : "",
+                  (err & 2) ? " row_ptr not monotone" : "",
+                  (err & 4) ? " column id out of range" : "");
     }
   }
   k_offsets32<<<blocks, 256, 0, st>>>(row_ptr, at<uint32_t>(g, L.rp), n + 1);
@@ -526,7 +548,7 @@ dawn_status dawn_graph_load_csr(int64_t n, int64_t m, const int64_t *row_ptr, co
       cudaMemcpyAsync(&C->n_hp_in, &C->n_hp_out, 4, cudaMemcpyDeviceToDevice, st);
     }
   }
-  if ((sym || has_csc) && m > 0) {  // degree-ordered in-rows for the pull probes
+  if ((sym || has_csc) && m > 0 && L.icol2) {  // degree-ordered in-rows for the pull probes
     const uint32_t *irp2 = sym ? at<uint32_t>(g, L.rp) : at<uint32_t>(g, L.irp);
     k_topk_rows<<<g->nsm * 8, 256, 0, st>>>(irp2, sym ? col : in_col, at<uint32_t>(g, L.rp),
                                             (uint32_t)n, at<int32_t>(g, L.icol2));
@@ -544,7 +566,7 @@ dawn_status dawn_graph_load_csr(int64_t n, int64_t m, const int64_t *row_ptr, co
     k_arcs<<<g->nsm * 8, 256, 0, st>>>(col, at<uint32_t>(g, L.rp), m, at<uint4>(g, L.arc));
   unsigned long long loc[2] = {0, 0};
   if (g->narrow_ok) {
-    unsigned long long *dcnt = at<unsigned long long>(g, L.part);  // scratch (ms64 partials)
+    unsigned long long *dcnt = at<unsigned long long>(g, L.useg);  // scratch (pull segments)
     cudaMemsetAsync(dcnt, 0, 16, st);
     k_locality<<<g->nsm * 4, 256, 0, st>>>(at<uint32_t>(g, L.rp), col,
                                              (uint32_t)std::min<int64_t>(n, 1 << 20), dcnt);
@@ -563,18 +585,23 @@ dawn_status dawn_graph_load_csr(int64_t n, int64_t m, const int64_t *row_ptr, co
   // Other graphs start on the grid-wide kernel by default: their narrow first levels are a
   // few microseconds, less than the extra kernel boundary (measured on Kronecker-20: +6 us).
   g->cluster_start = g->narrow_owner;
+  // the other lanes' control blocks get lane 0's load-time fields (n_hasin, heavy-piece counts)
+  for (int l = 1; l < L.nlanes; ++l)
+    cudaMemcpyAsync(g->ws + L.lane[l].ctrl, g->ws + L.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToDevice, st);
+  if (L.nlanes > 1) {
+    bool ok = cudaEventCreateWithFlags(&g->ev_fork, cudaEventDisableTiming) == cudaSuccess;
+    for (int l = 1; l < L.nlanes && ok; ++l)
+      ok = cudaStreamCreateWithFlags(&g->lane_st[l], cudaStreamNonBlocking) == cudaSuccess &&
+           cudaEventCreateWithFlags(&g->ev_join[l], cudaEventDisableTiming) == cudaSuccess;
+    g->lanes = ok ? std::min(L.nlanes, kDefaultLanes(n)) : 1;
+  }
+  if ((e = cudaStreamSynchronize(st)) != cudaSuccess) { delete g; return cuda_fail(e, "graph load"); }
   if ((e = cudaGetLastError()) != cudaSuccess) { delete g; return cuda_fail(e, "graph load"); }
   *out = g;
   return DAWN_OK;
 }
 
-dawn_status dawn_graph_destroy(dawn_graph g) {
-  delete g;
-  return DAWN_OK;
-}
-
-dawn_status dawn_graph_set_param(dawn_graph g, dawn_param key, double value) {
-  g_err.clear();
+dawn_status set_param(dawn_graph g, dawn_param key, double value) {
   if (!g) return fail(DAWN_ERR_INVALID_ARGUMENT, "graph is NULL");
   if (!(value >= 0)) return fail(DAWN_ERR_INVALID_ARGUMENT, "value must be >= 0");
   switch (key) {
@@ -590,14 +617,24 @@ dawn_status dawn_graph_set_param(dawn_graph g, dawn_param key, double value) {
     case DAWN_PARAM_CLUSTER_HANDOVER_EDGES:
       g->handover_m = value >= 1.8e19 ? ~0ull : (unsigned long long)value;
       break;
+    case DAWN_PARAM_BATCH_LANES:
+      if (value < 1 || value > g->L.nlanes || (value > 1 && !g->ev_fork))
+        return fail(DAWN_ERR_INVALID_ARGUMENT, "batch lanes must be in [1, %d]", g->L.nlanes);
+      g->lanes = (int)value;
+      break;
+    case DAWN_PARAM_NARROW_QUEUE_CAP:
+      if (value < 32) return fail(DAWN_ERR_INVALID_ARGUMENT, "queue capacity must be >= 32");
+      g->narrow_qcap = (uint32_t)std::min<double>(value, g->narrow_qcap_max);
+      break;
     default: return fail(DAWN_ERR_INVALID_ARGUMENT, "unknown parameter");
   }
   return DAWN_OK;
 }
 
-static SsspParams sssp_params(dawn_graph g, uint32_t variant, uint32_t *dist,
-                              dawn_sssp_stats *stats) {
+SsspParams sssp_params(dawn_graph g, uint32_t variant, uint32_t *dist, dawn_sssp_stats *stats,
+                       int lane = 0) {
   const Layout &L = g->L;
+  const LaneLayout &Q = L.lane[lane];
   SsspParams p{};
   p.n = (uint32_t)g->n;
   p.nwords = (uint32_t)((g->n + 31) / 32);
@@ -611,20 +648,20 @@ static SsspParams sssp_params(dawn_graph g, uint32_t variant, uint32_t *dist,
   p.hin_s = at<uint32_t>(g, L.hin.s);
   p.hin_e = at<uint32_t>(g, L.hin.e);
   p.hin_bits = at<uint32_t>(g, L.hin.bits);
-  p.vis = at<uint32_t>(g, L.vis);
-  p.cand = at<uint32_t>(g, L.cand);
+  p.vis = at<uint32_t>(g, Q.vis);
+  p.cand = at<uint32_t>(g, Q.cand);
   p.hasin = at<uint32_t>(g, L.hasin);
-  p.ulist = at<uint32_t>(g, L.ulist);
-  p.useg = at<uint32_t>(g, L.useg);
+  p.ulist = at<uint32_t>(g, Q.ulist);
+  p.useg = at<uint32_t>(g, Q.useg);
   p.n_hasin = g->n_hasin;
-  for (int i = 0; i < 3; ++i) p.fb[i] = at<uint32_t>(g, L.fb[i]);
-  p.trace = g->trace ? at<TraceRec>(g, L.trace) : nullptr;
+  for (int i = 0; i < 3; ++i) p.fb[i] = at<uint32_t>(g, Q.fb[i]);
+  p.trace = (g->trace && lane == 0) ? at<TraceRec>(g, L.trace) : nullptr;
   for (int i = 0; i < 2; ++i) {
-    p.Lv[i] = at<uint32_t>(g, L.Lv[i]);
-    p.Lsd[i] = at<uint2>(g, L.Lsd[i]);
-    p.Cf[i] = at<uint32_t>(g, L.Cf[i]);
+    p.Lv[i] = at<uint32_t>(g, Q.Lv[i]);
+    p.Lsd[i] = at<uint2>(g, Q.Lsd[i]);
+    p.Cf[i] = at<uint32_t>(g, Q.Cf[i]);
   }
-  p.ctrl = at<Ctrl>(g, L.ctrl);
+  p.ctrl = at<Ctrl>(g, Q.ctrl);
   p.dist = dist;
   p.stats = stats;
   p.variant = variant;
@@ -639,10 +676,9 @@ static SsspParams sssp_params(dawn_graph g, uint32_t variant, uint32_t *dist,
   return p;
 }
 
-static dawn_status launch_sssp(dawn_graph g, SsspParams &p, cudaStream_t stream) {
-  int grid = g->sssp_grid;
-  const int small_m = env_int("DAWN_SMALL_M", 1 << 15);
-  if (g->m + g->n <= small_m) grid = 1;  // tiny graphs: one CTA, barriers are __syncthreads
+dawn_status launch_sssp(dawn_graph g, SsspParams &p, cudaStream_t stream, int lanes = 1) {
+  int grid = std::max(1, g->sssp_grid / lanes);
+  if (g->m + g->n <= kOneCtaMaxNM) grid = 1;  // tiny graphs: one CTA, barriers are __syncthreads
   void *args[] = {&p};
   const void *kfn = g->sssp_one ? (const void *)k_sssp<kNT, 1> : (const void *)k_sssp<kNT, 2>;
   cudaError_t e = cudaLaunchCooperativeKernel(kfn, dim3(grid), dim3(kNT), args, 0, stream);
@@ -650,8 +686,8 @@ static dawn_status launch_sssp(dawn_graph g, SsspParams &p, cudaStream_t stream)
   return DAWN_OK;
 }
 
-static dawn_status launch_narrow(dawn_graph g, const SsspParams &p, uint32_t source,
-                                 const uint32_t *src_dev, cudaStream_t stream) {
+dawn_status launch_narrow(dawn_graph g, const SsspParams &p, uint32_t source,
+                          const uint32_t *src_dev, cudaStream_t stream) {
   const Layout &L = g->L;
   NarrowParams np{};
   np.n = p.n;
@@ -672,6 +708,8 @@ static dawn_status launch_narrow(dawn_graph g, const SsspParams &p, uint32_t sou
   np.stats = p.stats;
   np.source = source;
   np.src_dev = src_dev;
+  np.vsrc = p.vsrc;
+  np.vn = p.vn;
   np.max_reach_base = g->n_hasin;
   np.seq = p.seq;
   np.trace = p.trace;
@@ -692,13 +730,12 @@ static dawn_status launch_narrow(dawn_graph g, const SsspParams &p, uint32_t sou
   return DAWN_OK;
 }
 
-dawn_status dawn_sssp(dawn_graph g, int64_t source, uint32_t variant, uint32_t *dist,
-                      dawn_sssp_stats *stats, void *stream) {
-  g_err.clear();
+dawn_status sssp_one(dawn_graph g, int64_t source, uint32_t variant, uint32_t *dist,
+                     dawn_sssp_stats *stats, void *stream) {
   if (!g || !dist) return fail(DAWN_ERR_INVALID_ARGUMENT, "graph or dist is NULL");
   if (variant > DAWN_PULL) return fail(DAWN_ERR_INVALID_ARGUMENT, "unknown variant");
   if (source < 0 || source >= g->n)
-    return fail(DAWN_ERR_BOUNDS, "source " + std::to_string(source) + " not in [0, n)");
+    return fail(DAWN_ERR_BOUNDS, "source %lld not in [0, n)", (long long)source);
   if (variant == DAWN_PULL && !g->has_csc)
     return fail(DAWN_ERR_CONFIG, "PULL needs CSC (in-edges) on a directed graph");
   dawn_status s = set_device(g);
@@ -708,7 +745,7 @@ dawn_status dawn_sssp(dawn_graph g, int64_t source, uint32_t variant, uint32_t *
   if (variant != DAWN_PULL && !g->trace && small_bytes <= g->small_cap) {
     // whole SSSP in one CTA's shared memory (tiny graphs, e.g. configs[0])
     SmallParams sp{(uint32_t)g->n, (uint32_t)g->m, at<uint32_t>(g, L.rp), g->col, dist, stats,
-                   (uint32_t)source, nullptr, 0u};
+                   (uint32_t)source, nullptr, 0u, &at<Ctrl>(g, L.ctrl)->bad_src};
     k_small<1024><<<1, 1024, small_bytes, static_cast<cudaStream_t>(stream)>>>(sp);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "k_small launch");
@@ -725,10 +762,8 @@ dawn_status dawn_sssp(dawn_graph g, int64_t source, uint32_t variant, uint32_t *
   return launch_sssp(g, p, static_cast<cudaStream_t>(stream));
 }
 
-
-dawn_status dawn_sssp_batch(dawn_graph g, const uint32_t *sources, int64_t k, uint32_t variant,
-                            uint32_t *dist, dawn_sssp_stats *stats, void *stream) {
-  g_err.clear();
+dawn_status sssp_batch(dawn_graph g, const uint32_t *sources, int64_t k, uint32_t variant,
+                       uint32_t *dist, dawn_sssp_stats *stats, void *stream) {
   if (!g || k < 0 || (k > 0 && (!dist || !sources)))
     return fail(DAWN_ERR_INVALID_ARGUMENT, "bad arguments");
   if (variant > DAWN_PULL) return fail(DAWN_ERR_INVALID_ARGUMENT, "unknown variant");
@@ -744,7 +779,7 @@ dawn_status dawn_sssp_batch(dawn_graph g, const uint32_t *sources, int64_t k, ui
     // tiny graphs: the searches are independent, so up to one CTA per SM, each loading the CSR
     // into its shared memory once and running searches blockIdx.x, blockIdx.x + grid, ...
     SmallParams sp{(uint32_t)g->n, (uint32_t)g->m, at<uint32_t>(g, g->L.rp), g->col, dist, stats,
-                   0u, sources, (uint32_t)k};
+                   0u, sources, (uint32_t)k, &at<Ctrl>(g, g->L.ctrl)->bad_src};
     const unsigned grid = (unsigned)std::min<int64_t>(k, g->nsm);
     k_small<1024><<<grid, 1024, small_bytes, st>>>(sp);
     cudaError_t e = cudaGetLastError();
@@ -753,11 +788,13 @@ dawn_status dawn_sssp_batch(dawn_graph g, const uint32_t *sources, int64_t k, ui
   }
   if (variant != DAWN_PULL && g->narrow_ok && g->cluster_start) {
     // cluster-start graphs: per search, k_narrow then k_sssp (resume or exit), both reading the
-    // source id from the device list
+    // source id from the device list; every launch validates the whole list first
     for (int64_t i = 0; i < k; ++i) {
       SsspParams p = sssp_params(g, variant, dist + (size_t)i * g->n, stats ? stats + i : nullptr);
       p.sources = sources + i;
       p.nsrc = 1;
+      p.vsrc = sources;
+      p.vn = (uint32_t)k;
       dawn_status sn = launch_narrow(g, p, 0u, sources + i, st);
       if (sn != DAWN_OK) return sn;
       sn = launch_sssp(g, p, st);
@@ -765,14 +802,59 @@ dawn_status dawn_sssp_batch(dawn_graph g, const uint32_t *sources, int64_t k, ui
     }
     return DAWN_OK;
   }
+  const int lanes = (g->trace || k < 2) ? 1 : (int)std::min<int64_t>(g->lanes, k);
+  if (lanes > 1) {
+    // independent searches at once: lane l (its own per-search state, its own stream, grid/lanes
+    // CTAs) runs the contiguous share [k*l/lanes, k*(l+1)/lanes) of the batch; every lane
+    // validates the whole list first, so a bad id still means nothing is written
+    cudaError_t e = cudaEventRecord(g->ev_fork, st);
+    for (int l = 1; l < lanes && e == cudaSuccess; ++l) e = cudaStreamWaitEvent(g->lane_st[l], g->ev_fork, 0);
+    if (e != cudaSuccess) return cuda_fail(e, "batch fork");
+    for (int l = 0; l < lanes; ++l) {
+      const int64_t b = k * l / lanes, c = k * (l + 1) / lanes - b;
+      SsspParams p = sssp_params(g, variant, dist + (size_t)b * g->n, stats ? stats + b : nullptr, l);
+      p.sources = sources + b;
+      p.nsrc = (uint32_t)c;
+      p.vsrc = sources;
+      p.vn = (uint32_t)k;
+      dawn_status sl = launch_sssp(g, p, l ? g->lane_st[l] : st, lanes);
+      if (sl != DAWN_OK) return sl;
+    }
+    for (int l = 1; l < lanes && e == cudaSuccess; ++l) {
+      e = cudaEventRecord(g->ev_join[l], g->lane_st[l]);
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(st, g->ev_join[l], 0);
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "batch join");
+    return DAWN_OK;
+  }
   SsspParams p = sssp_params(g, variant, dist, stats);
   p.sources = sources;
   p.nsrc = (uint32_t)k;
+  p.vsrc = sources;
+  p.vn = (uint32_t)k;
   return launch_sssp(g, p, st);
 }
 
-static dawn_status launch_ms(dawn_graph g, const std::vector<uint32_t> &src, uint32_t *dist,
-                             dawn_record *rec, cudaStream_t st) {
+dawn_status graph_check(dawn_graph g, void *stream) {
+  if (!g) return fail(DAWN_ERR_INVALID_ARGUMENT, "graph is NULL");
+  dawn_status s = set_device(g);
+  if (s != DAWN_OK) return s;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  uint32_t bad = 0;
+  uint32_t *flag = &at<Ctrl>(g, g->L.ctrl)->bad_src;
+  cudaError_t e = cudaMemcpyAsync(&bad, flag, 4, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return cuda_fail(e, "dawn_graph_check");
+  if (bad) {
+    cudaMemsetAsync(flag, 0, 4, st);
+    if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return cuda_fail(e, "dawn_graph_check");
+    return fail(DAWN_ERR_BOUNDS, "a dawn_sssp_batch source id was not in [0, n); nothing written");
+  }
+  return DAWN_OK;
+}
+
+dawn_status launch_ms(dawn_graph g, const std::vector<uint32_t> &src, uint32_t *dist,
+                      dawn_record *rec, cudaStream_t st) {
   const Layout &L = g->L;
   const size_t chunk = (L.srccap / kMsBatch) * kMsBatch;
   for (size_t off = 0; off < src.size(); off += chunk) {
@@ -813,8 +895,7 @@ static dawn_status launch_ms(dawn_graph g, const std::vector<uint32_t> &src, uin
     p.trace = g->trace ? at<TraceRec>(g, L.trace) : nullptr;
     p.trace_n = &at<Ctrl>(g, L.ctrl)->trace_n;
     int grid = g->ms_grid;
-    const int small_m = env_int("DAWN_SMALL_M", 1 << 15);
-    if (g->m + g->n <= small_m) grid = 1;
+    if (g->m + g->n <= kOneCtaMaxNM) grid = 1;
     void *args[] = {&p};
     e = cudaLaunchCooperativeKernel((const void *)k_ms64<kNT>, dim3(grid), dim3(kNT), args,
                                     ms_smem_bytes(kNT), st);
@@ -823,14 +904,14 @@ static dawn_status launch_ms(dawn_graph g, const std::vector<uint32_t> &src, uin
   return DAWN_OK;
 }
 
-dawn_status dawn_msssp(dawn_graph g, const int64_t *sources, int64_t k, uint32_t *dist,
-                       dawn_record *rec, void *stream) {
-  g_err.clear();
+dawn_status msssp(dawn_graph g, const int64_t *sources, int64_t k, uint32_t *dist,
+                  dawn_record *rec, void *stream) {
   if (!g || (!sources && k > 0) || k < 0) return fail(DAWN_ERR_INVALID_ARGUMENT, "bad arguments");
+  if (g->lean) return fail(DAWN_ERR_CONFIG, "graph loaded with DAWN_GRAPH_LEAN (no multi-source words)");
   for (int64_t i = 0; i < k; ++i)
     if (sources[i] < 0 || sources[i] >= g->n)
-      return fail(DAWN_ERR_BOUNDS, "sources[" + std::to_string(i) + "] = " +
-                                       std::to_string(sources[i]) + " not in [0, n)");
+      return fail(DAWN_ERR_BOUNDS, "sources[%lld] = %lld not in [0, n)", (long long)i,
+                  (long long)sources[i]);
   if (dist && (double)k * (double)g->n >= 1099511627776.0)
     return fail(DAWN_ERR_CAPACITY, "k*n too large for a dense output");
   if (k == 0) return DAWN_OK;
@@ -840,9 +921,8 @@ dawn_status dawn_msssp(dawn_graph g, const int64_t *sources, int64_t k, uint32_t
   return launch_ms(g, src, dist, rec, static_cast<cudaStream_t>(stream));
 }
 
-dawn_status dawn_graph_trace(dawn_graph g, dawn_trace_rec *host_out, int64_t cap, int64_t *count,
-                             void *stream) {
-  g_err.clear();
+dawn_status graph_trace(dawn_graph g, dawn_trace_rec *host_out, int64_t cap, int64_t *count,
+                        void *stream) {
   if (!g || !count || (cap > 0 && !host_out)) return fail(DAWN_ERR_INVALID_ARGUMENT, "bad arguments");
   if (!g->trace) return fail(DAWN_ERR_CONFIG, "graph loaded without DAWN_GRAPH_TRACE");
   dawn_status s = set_device(g);
@@ -868,9 +948,8 @@ dawn_status dawn_graph_trace(dawn_graph g, dawn_trace_rec *host_out, int64_t cap
   return DAWN_OK;
 }
 
-dawn_status dawn_apsp_shard(int64_t k, int32_t rank, int32_t world, int64_t *idx, int64_t cap,
-                            int64_t *count) {
-  g_err.clear();
+dawn_status apsp_shard(int64_t k, int32_t rank, int32_t world, int64_t *idx, int64_t cap,
+                       int64_t *count) {
   if (k < 0 || world < 1 || rank < 0 || rank >= world || !count)
     return fail(DAWN_ERR_INVALID_ARGUMENT, "need k >= 0, 0 <= rank < world");
   int64_t c = 0;
@@ -888,16 +967,16 @@ dawn_status dawn_apsp_shard(int64_t k, int32_t rank, int32_t world, int64_t *idx
   return DAWN_OK;
 }
 
-dawn_status dawn_apsp(dawn_graph g, const int64_t *sources, int64_t k, int32_t rank, int32_t world,
-                      dawn_record *rec, int64_t cap, int64_t *n_written, void *stream) {
-  g_err.clear();
+dawn_status apsp(dawn_graph g, const int64_t *sources, int64_t k, int32_t rank, int32_t world,
+                 dawn_record *rec, int64_t cap, int64_t *n_written, void *stream) {
   if (!g || !rec || !n_written || (!sources && k > 0) || k < 0)
     return fail(DAWN_ERR_INVALID_ARGUMENT, "bad arguments");
   if (world < 1 || rank < 0 || rank >= world)
     return fail(DAWN_ERR_INVALID_ARGUMENT, "need 0 <= rank < world");
+  if (g->lean) return fail(DAWN_ERR_CONFIG, "graph loaded with DAWN_GRAPH_LEAN (no multi-source words)");
   for (int64_t i = 0; i < k; ++i)
     if (sources[i] < 0 || sources[i] >= g->n)
-      return fail(DAWN_ERR_BOUNDS, "sources[" + std::to_string(i) + "] not in [0, n)");
+      return fail(DAWN_ERR_BOUNDS, "sources[%lld] not in [0, n)", (long long)i);
   std::vector<uint32_t> mine;
   const int64_t B = kMsBatch;
   const int64_t nb = (k + B - 1) / B;
@@ -909,6 +988,142 @@ dawn_status dawn_apsp(dawn_graph g, const int64_t *sources, int64_t k, int32_t r
   dawn_status s = set_device(g);
   if (s != DAWN_OK) return s;
   return launch_ms(g, mine, nullptr, rec, static_cast<cudaStream_t>(stream));
+}
+
+dawn_status largest_wcc(dawn_graph g, int64_t *sources_out, int64_t *k, uint64_t *arcs,
+                        void *stream) {
+  if (!g || !k) return fail(DAWN_ERR_INVALID_ARGUMENT, "graph or k is NULL");
+  dawn_status s = set_device(g);
+  if (s != DAWN_OK) return s;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const Layout &L = g->L;
+  const uint32_t n = (uint32_t)g->n;
+  // frontier scratch of the handle (no search is in flight: one call per handle at a time)
+  uint32_t *par = at<uint32_t>(g, L.Lv[0]), *cnt = at<uint32_t>(g, L.Lv[1]);
+  uint32_t *arcc = at<uint32_t>(g, L.ulist), *list = reinterpret_cast<uint32_t *>(g->ws + L.Lsd[0]);
+  Ctrl *C = at<Ctrl>(g, L.ctrl);
+  const int blocks = std::max(1, std::min<int>(g->nsm * 8, (int)((n + 255) / 256)));
+  const uint32_t nblk = (n + kScanBlock - 1) / kScanBlock;
+  cudaMemsetAsync(cnt, 0, 4 * (size_t)n, st);
+  cudaMemsetAsync(arcc, 0, 4 * (size_t)n, st);
+  cudaMemsetAsync(&C->wcc_cnt, 0, 8, st);            // wcc_cnt, wcc_arcs
+  cudaMemsetAsync(&C->wcc_root, 0xff, 4, st);
+  k_wcc_init<<<blocks, 256, 0, st>>>(par, n);
+  if (g->m > 0) {
+    k_wcc_hook_light<<<blocks, 256, 0, st>>>(at<uint32_t>(g, L.rp), g->col, n, par);
+    k_wcc_hook_pieces<<<g->nsm * 8, 256, 0, st>>>(at<uint32_t>(g, L.hout.v),
+                                                    at<uint32_t>(g, L.hout.s),
+                                                    at<uint32_t>(g, L.hout.e), &C->n_hp_out,
+                                                    g->col, par);
+  }
+  k_wcc_count<<<blocks, 256, 0, st>>>(at<uint32_t>(g, L.rp), n, par, cnt, arcc);
+  for (int pass = 0; pass < 3; ++pass)
+    k_wcc_select<<<blocks, 256, 0, st>>>(par, cnt, arcc, n, pass, C);
+  k_wcc_bcount<<<nblk, 256, 0, st>>>(par, n, C, at<uint32_t>(g, L.scan_tmp));
+  k_hscan<<<1, 32, 0, st>>>(at<uint32_t>(g, L.scan_tmp), nblk, &C->wcc_k);
+  k_wcc_bfill<<<nblk, 256, 0, st>>>(par, n, C, at<uint32_t>(g, L.scan_tmp), list);
+  uint32_t hdr[3] = {0, 0, 0};  // wcc_cnt, wcc_arcs, wcc_root
+  cudaError_t e = cudaMemcpyAsync(hdr, &C->wcc_cnt, 12, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return cuda_fail(e, "dawn_largest_wcc");
+  const uint32_t kk = hdr[0];
+  if (sources_out && kk) {
+    std::vector<uint32_t> tmp(kk);
+    e = cudaMemcpy(tmp.data(), list, 4 * (size_t)kk, cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return cuda_fail(e, "dawn_largest_wcc copy");
+    for (uint32_t i = 0; i < kk; ++i) sources_out[i] = tmp[i];
+  }
+  *k = kk;
+  if (arcs) *arcs = hdr[1];
+  return DAWN_OK;
+}
+
+dawn_status ms_counters(dawn_graph g, uint64_t *host_out, void *stream) {
+  if (!g || !host_out) return fail(DAWN_ERR_INVALID_ARGUMENT, "graph or host_out is NULL");
+  dawn_status s = set_device(g);
+  if (s != DAWN_OK) return s;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  MsCtrl *C = at<MsCtrl>(g, g->L.msctrl);
+  cudaError_t e = cudaMemcpyAsync(host_out, C->stat, sizeof(C->stat), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(C->stat, 0, sizeof(C->stat), st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return cuda_fail(e, "dawn_graph_ms_counters");
+  return DAWN_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *dawn_last_error(void) { return g_err; }
+const char *dawn_version(void) { return "dawn-b200 0.3 sm_100a"; }
+
+size_t dawn_workspace_bytes(int64_t n, int64_t m, uint32_t flags) {
+  try {
+    if (n < 1 || n >= (int64_t(1) << 31) || m < 0 || m >= (int64_t(1) << 32)) return 0;
+    return make_layout(n, m, flags).total;
+  } catch (...) {
+    return 0;
+  }
+}
+
+dawn_status dawn_graph_load_csr(int64_t n, int64_t m, const int64_t *row_ptr, const int32_t *col,
+                                const int64_t *in_row_ptr, const int32_t *in_col, uint32_t flags,
+                                void *workspace, size_t ws_bytes, void *stream, dawn_graph *out) {
+  DAWN_GUARD(return load_csr(n, m, row_ptr, col, in_row_ptr, in_col, flags, workspace, ws_bytes,
+                             stream, out);)
+}
+
+dawn_status dawn_graph_destroy(dawn_graph g) {
+  delete g;
+  return DAWN_OK;
+}
+
+dawn_status dawn_graph_set_param(dawn_graph g, dawn_param key, double value) {
+  DAWN_GUARD(return set_param(g, key, value);)
+}
+
+dawn_status dawn_sssp(dawn_graph g, int64_t source, uint32_t variant, uint32_t *dist,
+                      dawn_sssp_stats *stats, void *stream) {
+  DAWN_GUARD(return sssp_one(g, source, variant, dist, stats, stream);)
+}
+
+dawn_status dawn_sssp_batch(dawn_graph g, const uint32_t *sources, int64_t k, uint32_t variant,
+                            uint32_t *dist, dawn_sssp_stats *stats, void *stream) {
+  DAWN_GUARD(return sssp_batch(g, sources, k, variant, dist, stats, stream);)
+}
+
+dawn_status dawn_graph_check(dawn_graph g, void *stream) {
+  DAWN_GUARD(return graph_check(g, stream);)
+}
+
+dawn_status dawn_msssp(dawn_graph g, const int64_t *sources, int64_t k, uint32_t *dist,
+                       dawn_record *rec, void *stream) {
+  DAWN_GUARD(return msssp(g, sources, k, dist, rec, stream);)
+}
+
+dawn_status dawn_graph_trace(dawn_graph g, dawn_trace_rec *host_out, int64_t cap, int64_t *count,
+                             void *stream) {
+  DAWN_GUARD(return graph_trace(g, host_out, cap, count, stream);)
+}
+
+dawn_status dawn_apsp_shard(int64_t k, int32_t rank, int32_t world, int64_t *idx, int64_t cap,
+                            int64_t *count) {
+  DAWN_GUARD(return apsp_shard(k, rank, world, idx, cap, count);)
+}
+
+dawn_status dawn_apsp(dawn_graph g, const int64_t *sources, int64_t k, int32_t rank, int32_t world,
+                      dawn_record *rec, int64_t cap, int64_t *n_written, void *stream) {
+  DAWN_GUARD(return apsp(g, sources, k, rank, world, rec, cap, n_written, stream);)
+}
+
+dawn_status dawn_largest_wcc(dawn_graph g, int64_t *sources_out, int64_t *k, uint64_t *arcs,
+                             void *stream) {
+  DAWN_GUARD(return largest_wcc(g, sources_out, k, arcs, stream);)
+}
+
+dawn_status dawn_graph_ms_counters(dawn_graph g, uint64_t *host_out, void *stream) {
+  DAWN_GUARD(return ms_counters(g, host_out, stream);)
 }
 
 }  // extern "C"

@@ -112,7 +112,9 @@ struct Ctrl {
   uint32_t narrow_status;       // k_narrow -> k_sssp: 1 finished, 2 resume from the bitmap
   uint32_t narrow_seq;          // dawn_sssp call number the status belongs to
   unsigned long long narrow_fill;  // k_narrow: CTAs done with the init fill (monotonic)
-  uint32_t pad1[4];
+  uint32_t bad_src;             // sticky: a dawn_sssp_batch device source id was >= n
+  uint32_t wcc_cnt, wcc_arcs, wcc_root, wcc_k;  // dawn_largest_wcc selection / output size
+  uint32_t pad1[3];
   alignas(16) unsigned char solo_state[256];  // LevelState snapshot published with solo_epoch
 };
 
@@ -120,6 +122,10 @@ struct MsCtrl {
   GridBarrier bar;
   uint32_t pad0[12];
   unsigned long long cnt[3][4];   // per level slot: [0] n_active, [1] m_active, [2] m_full
+  // executed-schedule counters, accumulated over launches until dawn_graph_ms_counters reads
+  // them: [0] levels, [1] adjacency entries gathered (push arcs + pull probes), [2] word
+  // reductions issued (red.or.b64), [3] batches
+  unsigned long long stat[4];
   uint32_t pad1[8];
 };
 
@@ -137,8 +143,19 @@ struct HeavyList {  // static pieces of rows with degree > kHeavy
   size_t v, s, e, bits;
 };
 
+// dawn_sssp_batch lanes: the grid-wide kernel's per-search state, replicated so that up to
+// kMaxLanes cooperative launches (one per lane, each on its own share of the SMs and its own
+// stream) run independent searches of one batch at the same time (sources are
+// independent).  Lane 0 is the state every other call uses.
+constexpr int kMaxLanes = 4;
+struct LaneLayout {
+  size_t vis, cand, fb[3], Lv[2], Lsd[2], Cf[2], ctrl, ulist, useg;
+};
+
 struct Layout {
   size_t rp, irp, noin, vis, cand, fb[3], Lv[2], Lsd[2], Cf[2], ctrl, trace;
+  LaneLayout lane[kMaxLanes];
+  int nlanes;
   HeavyList hout, hin;
   size_t scan_tmp, piece_tmp, hasin, ulist, useg, icol2, arc;
   size_t seen, F0, F1, nxt, msctrl, part, srcbuf, total;
@@ -160,6 +177,7 @@ inline Layout make_layout(int64_t n, int64_t m, uint32_t flags) {
   L.capCf = (uint64_t)m / kChunk + 2;
   L.capHP = (uint64_t)m / kHPiece + (uint64_t)m / kHeavy + 1;
   L.own_irp = !(flags & DAWN_GRAPH_SYMMETRIC);
+  const bool lean = flags & DAWN_GRAPH_LEAN;  // no ms64 words, no icol2, no augmented arcs
   L.rp = take(4 * (size_t)(n + 1));
   L.irp = L.own_irp ? take(4 * (size_t)(n + 1)) : L.rp;
   L.noin = take(4 * W);
@@ -186,18 +204,40 @@ inline Layout make_layout(int64_t n, int64_t m, uint32_t flags) {
   L.hasin = take(4 * (size_t)n);
   L.ulist = take(4 * (size_t)n);
   L.useg = take(4 * (size_t)kMaxBlocks * 32);
-  L.icol2 = take(4 * (size_t)m);  // in-rows, highest-degree in-neighbours first
+  L.icol2 = (lean || m == 0) ? 0 : take(4 * (size_t)m);  // in-rows, highest-degree in-neighbours first
   // k_narrow's augmented arcs (target, target row start, target row end, 0): low-degree graphs
-  L.arc = (m > 0 && (uint64_t)n <= kNarrowMaxN && (uint64_t)m <= (uint64_t)kNarrowMaxAvgDeg * (uint64_t)n)
+  L.arc = (!lean && m > 0 && (uint64_t)n <= kNarrowMaxN &&
+           (uint64_t)m <= (uint64_t)kNarrowMaxAvgDeg * (uint64_t)n)
               ? take(16 * (size_t)m) : 0;
-  L.seen = take(8 * kMsW * (size_t)n);
-  L.F0 = take(8 * kMsW * (size_t)n);
-  L.F1 = take(8 * kMsW * (size_t)n);
-  L.nxt = take(8 * kMsW * (size_t)n);
   L.msctrl = take(sizeof(MsCtrl));
-  L.part = take(sizeof(uint32_t) * 4 * kMsBatch * 2 * kMaxBlocks);
-  L.srccap = (uint64_t)(n > 65536 ? n : 65536);
-  L.srcbuf = take(4 * L.srccap);
+  if (!lean) {
+    L.seen = take(8 * kMsW * (size_t)n);
+    L.F0 = take(8 * kMsW * (size_t)n);
+    L.F1 = take(8 * kMsW * (size_t)n);
+    L.nxt = take(8 * kMsW * (size_t)n);
+    L.part = take(sizeof(uint32_t) * 4 * kMsBatch * 2 * kMaxBlocks);
+    L.srccap = (uint64_t)(n > 65536 ? n : 65536);
+    L.srcbuf = take(4 * L.srccap);
+  }
+  // extra lanes (lane 0 = the arrays above): not in lean mode; 4 lanes up to 2^22 vertices
+  // (latency-bound searches overlap best), 2 above
+  L.nlanes = lean ? 1 : ((uint64_t)n <= (1ull << 22) ? 4 : 2);
+  L.lane[0] = LaneLayout{L.vis, L.cand, {L.fb[0], L.fb[1], L.fb[2]}, {L.Lv[0], L.Lv[1]},
+                         {L.Lsd[0], L.Lsd[1]}, {L.Cf[0], L.Cf[1]}, L.ctrl, L.ulist, L.useg};
+  for (int l = 1; l < L.nlanes; ++l) {
+    LaneLayout &q = L.lane[l];
+    q.vis = take(4 * W);
+    q.cand = take(4 * W);
+    for (int i = 0; i < 3; ++i) q.fb[i] = take(4 * W);
+    for (int i = 0; i < 2; ++i) {
+      q.Lv[i] = take(4 * (size_t)n);
+      q.Lsd[i] = take(8 * (size_t)n);
+      q.Cf[i] = take(4 * L.capCf);
+    }
+    q.ctrl = take(sizeof(Ctrl));
+    q.ulist = take(4 * (size_t)n);
+    q.useg = take(4 * (size_t)kMaxBlocks * 32);
+  }
   L.total = o;
   return L;
 }

@@ -18,9 +18,6 @@
 #pragma once
 #include "layout.h"
 
-#ifndef DAWN_MS_NOREC
-#define DAWN_MS_NOREC 0
-#endif
 #ifndef DAWN_MS_PUSH_U
 #define DAWN_MS_PUSH_U 4  // 32-arc rounds batched per warp iteration (push phases, heavy pulls)
 #endif
@@ -147,9 +144,6 @@ template <int W>
 __device__ __forceinline__ void ms_record_group(const MsParams &p, const Word<W> &nw, uint32_t u,
                                                 uint32_t L1, uint32_t batch_base,
                                                 unsigned long long *hs, MsWarpAcc &wa) {
-#if DAWN_MS_NOREC
-  return;  // experiment (WRONG RECORDS): no record accumulation, timing only
-#endif
   const bool mine = wany<W>(nw);
   if (!__any_sync(DAWN_FULL, mine)) return;
   const uint32_t lane = lane_id();
@@ -225,6 +219,7 @@ __global__ void __launch_bounds__(NT, DAWN_MS_MINB) k_ms64(MsParams p) {
   const uint32_t nbatches = (p.count + kMsBatch - 1) / kMsBatch;
   const uint32_t ngroups = (p.n + 31) / 32;
   unsigned long long bar_target = 0;
+  unsigned long long c_arcs = 0, c_reds = 0;  // executed-schedule counters (MsCtrl::stat)
 
   for (uint32_t bt = 0; bt < nbatches; ++bt) {
     const uint32_t bbase = bt * kMsBatch;
@@ -238,7 +233,7 @@ __global__ void __launch_bounds__(NT, DAWN_MS_MINB) k_ms64(MsParams p) {
     // ---- init
     // nxt is all-zero at the end of every batch (each level's vertex pass clears what it
     // consumed), so only the launch's first batch clears it
-    for (uint32_t x = gtid; x < p.n * W; x += nthreads) {
+    for (size_t x = gtid; x < (size_t)p.n * W; x += nthreads) {
       p.seen[x] = 0;
       p.F[0][x] = 0;
       if (bt == 0) p.nxt[x] = 0;
@@ -366,10 +361,11 @@ __global__ void __launch_bounds__(NT, DAWN_MS_MINB) k_ms64(MsParams p) {
 #pragma unroll
             for (uint32_t r = 0; r < kPU; ++r) {
               if (u[r] == 0xffffffffu) continue;
+              ++c_arcs;
 #pragma unroll
               for (int i = 0; i < W; ++i) {
                 const unsigned long long x = fk[r].w[i] & ~su[r].w[i];
-                if (x) red_or64(p.nxt + (size_t)u[r] * W + i, x);
+                if (x) { red_or64(p.nxt + (size_t)u[r] * W + i, x); ++c_reds; }
               }
             }
           }
@@ -409,10 +405,11 @@ __global__ void __launch_bounds__(NT, DAWN_MS_MINB) k_ms64(MsParams p) {
 #pragma unroll
             for (uint32_t r = 0; r < kPU; ++r) {
               if (u[r] == 0xffffffffu) continue;
+              ++c_arcs;
 #pragma unroll
               for (int i = 0; i < W; ++i) {
                 const unsigned long long x = fv.w[i] & ~su[r].w[i];
-                if (x) red_or64(p.nxt + (size_t)u[r] * W + i, x);
+                if (x) { red_or64(p.nxt + (size_t)u[r] * W + i, x); ++c_reds; }
               }
             }
           }
@@ -478,6 +475,7 @@ __global__ void __launch_bounds__(NT, DAWN_MS_MINB) k_ms64(MsParams p) {
 #pragma unroll
                 for (uint32_t x = 0; x < PU; ++x) {
                   if (vv[x] == 0xffffffffu) continue;
+                  ++c_arcs;
                   const Word<W> f = wload<W>(Fc, vv[x]);
 #pragma unroll
                   for (int i = 0; i < W; ++i) a.w[i] |= f.w[i];
@@ -553,6 +551,7 @@ __global__ void __launch_bounds__(NT, DAWN_MS_MINB) k_ms64(MsParams p) {
 #pragma unroll
               for (uint32_t r = 0; r < kHU; ++r) {
                 if (vv[r] == 0xffffffffu) continue;
+                ++c_arcs;
                 const Word<W> g = wload<W>(Fc, vv[r]);
 #pragma unroll
                 for (int i = 0; i < W; ++i) f.w[i] |= g.w[i];
@@ -572,7 +571,7 @@ __global__ void __launch_bounds__(NT, DAWN_MS_MINB) k_ms64(MsParams p) {
 #pragma unroll
           for (int i = 0; i < W; ++i) {
             const unsigned long long x = a.w[i] & U.w[i];
-            if (lane == (uint32_t)i && x) red_or64(p.nxt + (size_t)u * W + i, x);
+            if (lane == (uint32_t)i && x) { red_or64(p.nxt + (size_t)u * W + i, x); ++c_reds; }
           }
           }
         }
@@ -644,7 +643,11 @@ __global__ void __launch_bounds__(NT, DAWN_MS_MINB) k_ms64(MsParams p) {
         atomicAdd(&C->cnt[(st.L + 1) % 3][2], red[2]);
       }
       grid_sync(&C->bar, nblocks, bar_target);
-      if (threadIdx.x == 0) { st.cur ^= 1; st.L++; }
+      if (threadIdx.x == 0) {
+        if (blockIdx.x == 0) atomicAdd(&C->stat[0], 1ull);
+        st.cur ^= 1;
+        st.L++;
+      }
       __syncthreads();
     }
     // ---- records: per-CTA partials, reduced by CTA 0 after a barrier
@@ -697,6 +700,13 @@ __global__ void __launch_bounds__(NT, DAWN_MS_MINB) k_ms64(MsParams p) {
       }
     }
     __syncthreads();
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&C->stat[3], 1ull);
+  }
+  c_arcs = warp_sum(c_arcs);
+  c_reds = warp_sum(c_reds);
+  if (lane == 0 && (c_arcs | c_reds)) {
+    atomicAdd(&C->stat[1], c_arcs);
+    atomicAdd(&C->stat[2], c_reds);
   }
   grid_exit(&C->bar, nblocks);
 }

@@ -45,9 +45,6 @@ namespace dawn {
 #ifndef DAWN_NARROW_CG
 #define DAWN_NARROW_CG 0  // experiment: arc loads ld.global.cg instead of .nc
 #endif
-#ifndef DAWN_NARROW_NODIST
-#define DAWN_NARROW_NODIST 0  // experiment (WRONG RESULTS): skip the dist stores, timing only
-#endif
 #ifndef DAWN_NARROW_TMA
 #define DAWN_NARROW_TMA 1  // stage rows with one TMA bulk copy each (else 16-B cp.async pieces)
 #endif
@@ -80,6 +77,8 @@ struct NarrowParams {
   dawn_sssp_stats *stats;
   uint32_t source, max_reach_base, seq;  // max_reach_base = #vertices with an in-edge
   const uint32_t *src_dev;               // source id on the device (dawn_sssp_batch) or NULL
+  const uint32_t *vsrc;                  // dawn_sssp_batch: the whole device source list,
+  uint32_t vn;                           //   validated before any write (vn = 0: none)
   TraceRec *trace;                 // per-level trace (DAWN_GRAPH_TRACE) or NULL
 };
 
@@ -214,9 +213,7 @@ __device__ __forceinline__ void narrow_visit(const NarrowParams &p, NarrowCtl &S
   const uint32_t d = a.z - a.y;
   const bool put = fresh && d > 0;
   if (fresh) {
-#if !DAWN_NARROW_NODIST
     p.dist[a.x] = L1;
-#endif
     n_new += 1;
     m_new += d;
   }
@@ -278,6 +275,14 @@ __global__ void __launch_bounds__(kNarrowThreads, 1) k_narrow(NarrowParams p) {
   uint4 *qbuf0 = reinterpret_cast<uint4 *>(smraw + q0off);
   uint4 *abuf0 = qbuf0 + 2 * (size_t)p.qcap;  // row arcs of the staged entries
   Ctrl *C = p.ctrl;
+  if (p.vn) {  // every CTA checks the whole batch list first: a bad id -> nothing written
+    bool bad = false;
+    for (uint32_t i = threadIdx.x; i < p.vn; i += kNarrowThreads) bad |= ld_nc(p.vsrc + i) >= p.n;
+    if (__syncthreads_or(bad)) {
+      if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(&C->bad_src, 1u);
+      return;
+    }
+  }
   const uint32_t src = p.src_dev ? ld_nc(p.src_dev) : p.source, tid = threadIdx.x;
   const uint32_t gtid = blockIdx.x * kNarrowThreads + tid, nthreads = gridDim.x * kNarrowThreads;
 

@@ -19,6 +19,7 @@ struct SmallParams {
   uint32_t source;
   const uint32_t *sources;    // batch mode (dawn_sssp_batch): nsrc device source ids
   uint32_t nsrc;
+  uint32_t *bad_src;          // sticky flag: a batch source id was >= n (nothing written)
 };
 
 // Shared-memory bytes k_small needs for (n, m).
@@ -40,6 +41,14 @@ __global__ void __launch_bounds__(NT) k_small(SmallParams p) {
   __shared__ uint32_t nq_cnt[3];  // level L appends to nq_cnt[L % 3]
   __shared__ unsigned long long m_acc;
   const uint32_t tid = threadIdx.x, lane = lane_id();
+  if (p.nsrc) {  // the whole device source list is checked before anything is written
+    bool bad = false;
+    for (uint32_t i = tid; i < p.nsrc; i += NT) bad |= ld_nc(p.sources + i) >= n;
+    if (__syncthreads_or(bad)) {
+      if (blockIdx.x == 0 && tid == 0) atomicOr(p.bad_src, 1u);
+      return;
+    }
+  }
   // CSR -> shared memory, 4 independent loads in flight per thread
   {
     constexpr int U = 4;

@@ -24,14 +24,7 @@ namespace dawn {
 #ifndef DAWN_TRACE_MAX
 #define DAWN_TRACE_MAX 0  // experiment: trace per-phase max over warps instead of the sum
 #endif
-#ifndef DAWN_SSSP_NODIST
-#define DAWN_SSSP_NODIST 0  // experiment (WRONG RESULTS): drop the per-level dist stores, timing only
-#endif
-#if DAWN_SSSP_NODIST
-#define DIST_ST(i, v) ((void)0)
-#else
 #define DIST_ST(i, v) (st.drow[i] = (v))
-#endif
 
 struct SsspParams {
   uint32_t n, nwords;
@@ -60,7 +53,24 @@ struct SsspParams {
   // after the other in this launch; source i writes dist + i * n and stats[i]
   const uint32_t *sources;
   uint32_t nsrc;
+  // device source list validated before any write (dawn_sssp_batch; vn = 0: host-validated)
+  const uint32_t *vsrc;
+  uint32_t vn;
 };
+
+// Every CTA checks the whole device source list of a dawn_sssp_batch call before it writes
+// anything (identical inputs -> the same decision in every CTA, no communication).  A bad id
+// sets the handle's sticky flag (dawn_graph_check reports DAWN_ERR_BOUNDS) and the kernel
+// exits with every output untouched (validation before work).
+template <int NT>
+__device__ __forceinline__ bool sources_invalid(const uint32_t *vsrc, uint32_t vn, uint32_t n,
+                                                uint32_t *flag) {
+  bool bad = false;
+  for (uint32_t i = threadIdx.x; i < vn; i += NT) bad |= ld_nc(vsrc + i) >= n;
+  bad = __syncthreads_or(bad);
+  if (bad && blockIdx.x == 0 && threadIdx.x == 0) atomicOr(flag, 1u);
+  return bad;
+}
 
 struct __align__(16) LevelState {
   uint32_t L, nf, prev_nf, dir, rep, q, b, stop, ecc, solo, bm, deep, ul;
@@ -778,6 +788,7 @@ __global__ void __launch_bounds__(NT, MINB) k_sssp(SsspParams p) {
   WarpStage &stg = stage[threadIdx.x / 32];
   Ctrl *C = p.ctrl;
   unsigned long long bar_target = 0;
+  if (p.vn && sources_invalid<NT>(p.vsrc, p.vn, p.n, &C->bad_src)) return;
   const uint32_t nsrc = p.nsrc ? p.nsrc : 1u;
   // batch mode: the searches run back to back in this launch, a grid barrier apart (no kernel
   // boundary or launch ramp between them)

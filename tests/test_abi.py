@@ -63,6 +63,18 @@ def test_host_validation_errors_before_device_work():
     assert L.dawn_sssp_batch(None, None, 4, 0, None, None, None) == 1
     assert L.dawn_sssp_batch(None, None, -1, 0, None, None, None) == 1
     assert L.dawn_graph_destroy(None) == 0
+    assert L.dawn_graph_check(None, None) == 1
+    assert L.dawn_largest_wcc(None, None, None, None, None) == 1
+    assert L.dawn_msssp(None, None, 1, None, None, None) == 1
+
+
+def test_lean_workspace_is_smaller():
+    # DAWN_GRAPH_LEAN (PAPER L312-323 memory frugality): C4-sized graph
+    L = dawn.lib()
+    n, m = 1 << 24, 520_745_006
+    full, lean = L.dawn_workspace_bytes(n, m, 1), L.dawn_workspace_bytes(n, m, 1 | 8)
+    assert lean < full / 3, (full, lean)
+    assert lean < 1.3e9, lean
 
 
 @pytest.mark.parametrize("k,world", [(0, 1), (1, 1), (64, 2), (130, 2), (173778, 8), (200, 3)])

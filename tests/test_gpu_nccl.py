@@ -1,0 +1,61 @@
+"""The APSP path through a real NCCL process group (PAPER E11-E12 L303-308: the
+sources are independent, so they shard; NCCL carries only the 32-byte records).  One process
+per visible GPU (world = torch.cuda.device_count(): 1 on the single-GPU test box, N on an
+N-GPU box): every rank runs dawn_apsp on its shard on its own GPU and the binding's
+gather_records does the one all-gather over NCCL; rank 0 compares the gathered records with the
+oracle byte for byte, and the gathered set is identical for every world size (determinism
+across W, the SPEC S:L456 idea applied to GPU count)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import graphgen
+import oracle
+import paper_2208_04514_b200 as dawn
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, out_dir):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(rank)
+    dev = torch.device("cuda", rank)
+    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
+    g = graphgen.kron(13, 16, 13)
+    G = dawn.Graph(g.row_ptr, g.col, True)
+    verts, _ = dawn.largest_wcc(G)
+    for k in (len(verts), 700, 256, 1):
+        srcs = verts[:k]
+        full = dawn.apsp(G, srcs, rank, world)             # shard + NCCL all-gather
+        torch.cuda.synchronize()
+        if rank == 0:
+            np.save(os.path.join(out_dir, f"nccl_{k}.npy"), full.cpu().numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_apsp_nccl_all_visible_gpus(tmp_path):
+    world = torch.cuda.device_count()
+    assert world >= 1
+    mp.start_processes(_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world,
+                       join=True, start_method="spawn")
+    g = graphgen.kron(13, 16, 13)
+    verts, _ = oracle.largest_wcc(g.n, g.row_ptr, g.col)
+    for k in (len(verts), 700, 256, 1):
+        full = np.load(tmp_path / f"nccl_{k}.npy")
+        exp = oracle.records(g.n, g.row_ptr, g.col, verts[:k])
+        assert full.tobytes() == exp.tobytes(), (world, k)

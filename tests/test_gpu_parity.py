@@ -280,17 +280,17 @@ def test_narrow_kernel_and_handover():
         check_sssp(g, G, srcs[:2], variants=("auto",))
 
 
-def test_narrow_forced_handover(monkeypatch):
-    # tiny shared-memory queues (DAWN_NARROW_QCAP, read at load) make every wide-enough level
+def test_narrow_forced_handover():
+    # tiny shared-memory queues (DAWN_PARAM_NARROW_QUEUE_CAP) make every wide-enough level
     # overflow: hand-over to k_sssp from the frontier bitmap at many different levels
-    monkeypatch.setenv("DAWN_NARROW_QCAP", "40")
     rng = np.random.default_rng(12)
     n = 50_000
     rand = graphgen.from_edges(n, rng.integers(0, n, size=(n, 2)), symmetric=True)
     dirg = graphgen.from_edges(n, rng.integers(0, n, size=(3 * n, 2)))
     for g in (graphgen.grid(300, 200), rand, dirg):
         G = dev_graph(g)
-        G.set_tuning(cluster_start=1, cluster_handover_edges=2e19)  # only overflow hands over
+        G.set_tuning(cluster_start=1, cluster_handover_edges=2e19,  # only overflow hands over
+                     narrow_queue_cap=40)
         srcs = [0, g.n // 3, g.n - 1] + list(g.sample_sources(3, seed=3))
         check_sssp(g, G, srcs, variants=("auto", "push"))
 
@@ -422,3 +422,30 @@ def test_push_from_pull_bitmap_frontier():
         D = D.cpu().numpy().view(np.uint32)
         assert np.array_equal(D[0], exp) and np.array_equal(D[1], exp)
         assert np.array_equal(D[2], oracle.bfs_fifo(g.n, g.row_ptr, g.col, 1)[0])
+
+
+def test_sssp_batch_lanes():
+    # DAWN_PARAM_BATCH_LANES: 1/2/4 concurrent grid-wide searches (own state, own stream) give
+    # the oracle's rows and statistics for every source, incl. k not a multiple of the lanes,
+    # repeated sources, and every direction variant
+    g = graphgen.kron(15, 16, 15)
+    G = dev_graph(g)
+    srcs = np.concatenate([g.sample_sources(9, seed=11), [0]]).astype(np.int32)
+    srcs[3] = srcs[1]                                               # a repeated source
+    exp = [oracle.bfs_fifo(g.n, g.row_ptr, g.col, int(s))[0] for s in srcs]
+    for lanes in (1, 2, 4):
+        G.set_tuning(batch_lanes=lanes)
+        for v in VARIANTS:
+            d, st = dawn.sssp_batch(G, torch.from_numpy(srcs).cuda(), v, stats=True, check=True)
+            d = d.cpu().numpy().view(np.uint32)
+            for i, s in enumerate(srcs):
+                assert np.array_equal(d[i], exp[i]), (lanes, v, int(s))
+                rec, er = oracle.record(g.n, g.row_ptr, int(s), exp[i])
+                sd = dawn.stats_to_dict(st[i])
+                assert sd["levels"] == int(rec["ecc"]) and sd["edges_reach"] == er, (lanes, v)
+    with pytest.raises(dawn.DawnError):
+        G.set_tuning(batch_lanes=5)
+    # the lanes share nothing across calls: a single dawn_sssp between batches still matches
+    G.set_tuning(batch_lanes=4)
+    dawn.sssp_batch(G, torch.from_numpy(srcs).cuda())
+    assert np.array_equal(gpu_dist(G, int(srcs[2])), exp[2])

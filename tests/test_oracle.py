@@ -259,3 +259,61 @@ def test_wcc_spec_example():
     g = graphgen.from_edges(5, [[0, 1], [1, 2], [3, 4]])
     v, e = g.largest_wcc()
     assert v.tolist() == [0, 1, 2] and e == 2
+
+
+# ------------------------------------------------------------------ largest WCC (Table 1, Q15)
+def _fw_components(g):
+    """Weak components by brute force: Floyd-Warshall reachability on the symmetrised graph."""
+    edges = [(u, int(v)) for u in range(g.n) for v in g.col[g.row_ptr[u]:g.row_ptr[u + 1]]]
+    sym = graphgen.from_edges(g.n, edges + [(v, u) for u, v in edges], symmetric=False)
+    D = oracle.floyd_warshall(sym.n, sym.row_ptr, sym.col)
+    comps = {tuple(np.nonzero(D[v] != UNR)[0].tolist()) for v in range(g.n)}
+    return [list(c) for c in comps]
+
+
+def test_largest_wcc_hand_fixtures():
+    # PAPER Table 1 (L95-98): S_wcc / E_wcc; reading Q15: most nodes, then most arcs, then the
+    # smaller minimum id.  SPEC S:L98-101 example first.
+    cases = [
+        (5, [[0, 1], [1, 2], [3, 4]], [0, 1, 2], 2),
+        (6, [[0, 1], [1, 2], [3, 4], [4, 5], [5, 3]], [3, 4, 5], 3),   # tie on nodes -> arcs
+        (4, [[0, 1], [2, 3]], [0, 1], 1),                               # full tie -> min id 0
+        (6, [[5, 0], [1, 2]], [0, 5], 1),                               # min id of {0,5} wins
+        (6, [[1, 0], [2, 0], [4, 3]], [0, 1, 2], 2),                    # weak: no directed path 1~>2
+        (5, [], [0], 0),                                                # all isolated
+        (1, [], [0], 0),
+    ]
+    for n, edges, exp_v, exp_e in cases:
+        g = graphgen.from_edges(n, edges, symmetric=False)
+        v, e = oracle.largest_wcc(g.n, g.row_ptr, g.col)
+        assert v.tolist() == exp_v and e == exp_e, (n, edges, v, e)
+
+
+def test_largest_wcc_brute_force_corpus():
+    # every ER digraph of the corpus: the oracle's component equals the one chosen from the
+    # Floyd-Warshall components by the Q15 rule, with E_wcc = its out-degree sum
+    rng = np.random.default_rng(2208)
+    for t in range(60):
+        n = int(rng.integers(1, 40))
+        p = float(rng.choice([0.0, 0.02, 0.05, 0.1, 0.3]))
+        g = graphgen.er_prob(n, p, 1000 + t)
+        deg = np.diff(g.row_ptr)
+        best = None
+        for c in _fw_components(g):
+            key = (len(c), int(deg[c].sum()), -min(c))
+            if best is None or key > best[0]:
+                best = (key, sorted(c))
+        v, e = oracle.largest_wcc(g.n, g.row_ptr, g.col)
+        assert v.tolist() == best[1] and e == best[0][1], (t, n, p)
+
+
+def test_largest_wcc_e10_identity():
+    # PAPER E10/E11 (L299-307): on a symmetric graph every source of the component reaches
+    # S_wcc - 1 others and its E10 count equals E_wcc (FIFO BFS, Algorithm 3, independent)
+    g = graphgen.kron(12, 16, 12)
+    v, e = oracle.largest_wcc(g.n, g.row_ptr, g.col)
+    for s in v[:: max(1, len(v) // 8)]:
+        d, _ = oracle.bfs_fifo(g.n, g.row_ptr, g.col, int(s))
+        rec, er = oracle.record(g.n, g.row_ptr, int(s), d)
+        assert int(rec["reached"]) == len(v) - 1 and er == e
+        assert np.array_equal(np.nonzero(d != UNR)[0], v)
