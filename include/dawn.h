@@ -173,12 +173,17 @@ typedef enum {
   DAWN_PARAM_NARROW_QUEUE_CAP = 8, /* lowers k_narrow's per-CTA queue capacity (entries, >= 32;
                                       capped at the load-time capacity).  Only for tests that
                                       force queue-overflow hand-overs; speed only.            */
-  DAWN_PARAM_BATCH_LANES = 9       /* dawn_sssp_batch on the grid-wide kernel runs this many
+  DAWN_PARAM_BATCH_LANES = 9,      /* dawn_sssp_batch on the grid-wide kernel runs this many
                                       searches at once, each on 1/lanes of the SMs with its own
                                       per-search state and stream (the sources are
                                       independent).  1 .. 4 (n <= 2^22) or
                                       1 .. 2 (larger n; 1 with DAWN_GRAPH_LEAN).  Default set at
                                       load from B200 measurements.              */
+  DAWN_PARAM_DENSE_MAX_ENTRIES = 10 /* dense distance outputs (dawn_msssp dist, one piece of
+                                      dawn_apsp_rows) are refused with DAWN_ERR_CAPACITY when
+                                      rows * n >= this ("dense-matrix mode refused
+                                      above a configurable threshold").  Default and maximum
+                                      2^40 entries.  Changes admission only, never results.    */
 } dawn_param;
 
 /* Set one tunable (INVALID_ARGUMENT for an unknown key or a negative value). */
@@ -223,7 +228,9 @@ dawn_status dawn_sssp_batch(dawn_graph g, const uint32_t *sources, int64_t k, ui
  * processed DAWN_MS_BATCH (256) at a time by the bit-parallel kernel: each vertex holds four
  * 64-bit words, bit j of the batch's word w = source DAWN_MS_BATCH*b + 64w + j, so one adjacency
  * pass serves 256 BFS trees (a 32-byte word = one L2 sector).
- *   dist   device uint32[k][n] (source-major) or NULL.  k*n must be < 2^40 else CAPACITY.
+ *   dist   device uint32[k][n] (source-major) or NULL.  k*n must be below
+ *          DAWN_PARAM_DENSE_MAX_ENTRIES (default 2^40) else CAPACITY: stream the rows with
+ *          dawn_apsp_rows instead.
  *   rec    device dawn_record[k] or NULL (record i belongs to sources[i]).
  * Repeated sources give identical rows and records.
  */
@@ -249,6 +256,30 @@ dawn_status dawn_apsp_shard(int64_t k, int32_t rank, int32_t world, int64_t *idx
  */
 dawn_status dawn_apsp(dawn_graph g, const int64_t *sources, int64_t k, int32_t rank, int32_t world,
                       dawn_record *rec, int64_t cap, int64_t *n_written, void *stream);
+
+/*
+ * All-pairs distance ROWS streamed to host memory through a caller sink ("for
+ * large n a streaming per-row sink must be supplied"; the dense k x n matrix of dawn_msssp is
+ * refused above DAWN_PARAM_DENSE_MAX_ENTRIES).  Row i = the distances from sources[i] (the
+ * bit-parallel kernel, 256 sources per pass), delivered in order in pieces of `chunk` rows:
+ *   piece p is computed on `stream` into dev_stage[p % 2], copied on an internal stream into
+ *   host_stage[p % 2], and handed to sink(user, first_row, rows, host_rows) on the CALLING
+ *   thread while piece p + 1 computes.  host_rows (rows x n uint32, row-major) is valid only
+ *   during the sink call.  The sink returns 0 to continue; a nonzero return stops the call
+ *   (DAWN_ERR_INVALID_ARGUMENT, rows already delivered stay delivered).
+ *   sources     HOST int64[k], all in [0, n) (validated before any work -> DAWN_ERR_BOUNDS)
+ *   chunk       rows per piece, >= 1 (a multiple of DAWN_MS_BATCH avoids partial passes);
+ *               chunk * n >= DAWN_PARAM_DENSE_MAX_ENTRIES -> DAWN_ERR_CAPACITY
+ *   dev_stage   DEVICE uint32[2 * chunk * n], caller-owned scratch
+ *   host_stage  HOST uint32[2 * chunk * n], caller-owned; pinned (page-locked) memory makes the
+ *               copies asynchronous
+ * Returns when every row was delivered (synchronous in the host sense).  CONFIG on a
+ * DAWN_GRAPH_LEAN handle.  Not concurrent with other calls on g.
+ */
+typedef int (*dawn_row_sink)(void *user, int64_t first_row, int64_t rows, const uint32_t *host_rows);
+dawn_status dawn_apsp_rows(dawn_graph g, const int64_t *sources, int64_t k, int64_t chunk,
+                           uint32_t *dev_stage, uint32_t *host_stage, dawn_row_sink sink,
+                           void *user, void *stream);
 
 /* Copy the per-level trace of the last dawn_sssp call (graph loaded with DAWN_GRAPH_TRACE)
  * into host_out[0 .. min(cap, levels+1)); *count receives the number of records.  With

@@ -17,7 +17,7 @@ import subprocess
 import numpy as np
 import torch
 
-__all__ = ["build", "Graph", "sssp", "sssp_batch", "msssp", "apsp", "apsp_shard", "largest_wcc",
+__all__ = ["build", "Graph", "sssp", "sssp_batch", "msssp", "apsp", "apsp_rows", "apsp_shard", "largest_wcc",
            "check", "DawnError", "UNREACHED", "AUTO", "PUSH", "PULL", "MS_BATCH", "REC_DTYPE",
            "records_to_numpy", "stats_to_dict", "gather_records"]
 
@@ -69,6 +69,9 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None,
 
 
 _lib = None
+# dawn_row_sink: int (*)(void *user, int64_t first_row, int64_t rows, const uint32_t *host_rows)
+_ROW_SINK = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64,
+                             ctypes.c_void_p)
 
 
 class _SsspStats(ctypes.Structure):
@@ -115,6 +118,8 @@ def lib():
         L.dawn_graph_check.argtypes = [vp, vp]
         L.dawn_graph_ms_counters.restype = st
         L.dawn_graph_ms_counters.argtypes = [vp, vp, vp]
+        L.dawn_apsp_rows.restype = st
+        L.dawn_apsp_rows.argtypes = [vp, vp, i64, i64, vp, vp, _ROW_SINK, vp, vp]
         L.dawn_largest_wcc.restype = st
         L.dawn_largest_wcc.argtypes = [vp, vp, ctypes.POINTER(ctypes.c_int64),
                                        ctypes.POINTER(ctypes.c_uint64), vp]
@@ -195,7 +200,7 @@ class Graph:
 
     _PARAMS = {"alpha": 0, "beta": 1, "ms_alpha": 2, "bitmap_push_edges": 3, "solo_edges": 4,
                "cluster_start": 5, "cluster_handover_edges": 6, "bitmap_push_grow_edges": 7,
-               "narrow_queue_cap": 8, "batch_lanes": 9}
+               "narrow_queue_cap": 8, "batch_lanes": 9, "dense_max_entries": 10}
 
     def set_tuning(self, **kw):
         """dawn_graph_set_param for each keyword (alpha, beta, ms_alpha, bitmap_push_edges,
@@ -294,6 +299,37 @@ def msssp(g: Graph, sources, dist: bool = True, records: bool = True, stream=Non
     _check(lib().dawn_msssp(g.handle, src.ctypes.data_as(ctypes.c_void_p), k, _dptr(d), _dptr(r),
                             _stream(stream)))
     return d, r
+
+
+def apsp_rows(g: Graph, sources, sink, chunk: int = MS_BATCH, stream=None):
+    """dawn_apsp_rows: the distance rows of every source streamed to host memory.  `sink(first,
+    rows)` is called in order with `rows` a uint32 numpy array [r, n] (rows first .. first+r-1),
+    valid only during the call (copy what you keep); return False to stop early.  Uses two
+    device pieces of chunk x n and two pinned host pieces (allocated here, torch)."""
+    src = np.ascontiguousarray(np.asarray(sources, dtype=np.int64).reshape(-1))
+    k = len(src)
+    c = max(1, min(int(chunk), max(1, k)))
+    dev = torch.empty(2 * c * g.n, dtype=torch.int32, device=g.device)
+    host = torch.empty(2 * c * g.n, dtype=torch.int32, pin_memory=True)
+    base = host.data_ptr()
+    hv = host.numpy().view(np.uint32)
+    err = []
+
+    def _cb(_user, first, rows, ptr):
+        try:
+            off = (ptr - base) // 4
+            r = sink(int(first), hv[off: off + rows * g.n].reshape(rows, g.n))
+            return 1 if r is False else 0
+        except BaseException as ex:  # noqa: BLE001 - surfaced after the C call returns
+            err.append(ex)
+            return 1
+
+    cb = _ROW_SINK(_cb)
+    st = lib().dawn_apsp_rows(g.handle, src.ctypes.data_as(ctypes.c_void_p), k, c, _dptr(dev),
+                              base, cb, None, _stream(stream))
+    if err:
+        raise err[0]
+    _check(st)
 
 
 def apsp_shard(k: int, rank: int, world: int) -> np.ndarray:

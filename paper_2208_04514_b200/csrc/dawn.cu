@@ -324,6 +324,7 @@ struct dawn_graph_s {
   uint32_t seq = 0;
   bool lean = false;             // DAWN_GRAPH_LEAN: no ms64 words / icol2 / augmented arcs
   int lanes = 1;                 // DAWN_PARAM_BATCH_LANES (<= L.nlanes)
+  double dense_max = 1099511627776.0;  // DAWN_PARAM_DENSE_MAX_ENTRIES (k*n of a dense output)
   // lane streams / fork-join events of dawn_sssp_batch (created at load, host resources only)
   cudaStream_t lane_st[kMaxLanes] = {};
   cudaEvent_t ev_fork = nullptr, ev_join[kMaxLanes] = {};
@@ -622,6 +623,10 @@ dawn_status set_param(dawn_graph g, dawn_param key, double value) {
         return fail(DAWN_ERR_INVALID_ARGUMENT, "batch lanes must be in [1, %d]", g->L.nlanes);
       g->lanes = (int)value;
       break;
+    case DAWN_PARAM_DENSE_MAX_ENTRIES:
+      if (value < 1) return fail(DAWN_ERR_INVALID_ARGUMENT, "dense limit must be >= 1");
+      g->dense_max = std::min(value, 1099511627776.0);
+      break;
     case DAWN_PARAM_NARROW_QUEUE_CAP:
       if (value < 32) return fail(DAWN_ERR_INVALID_ARGUMENT, "queue capacity must be >= 32");
       g->narrow_qcap = (uint32_t)std::min<double>(value, g->narrow_qcap_max);
@@ -912,8 +917,8 @@ dawn_status msssp(dawn_graph g, const int64_t *sources, int64_t k, uint32_t *dis
     if (sources[i] < 0 || sources[i] >= g->n)
       return fail(DAWN_ERR_BOUNDS, "sources[%lld] = %lld not in [0, n)", (long long)i,
                   (long long)sources[i]);
-  if (dist && (double)k * (double)g->n >= 1099511627776.0)
-    return fail(DAWN_ERR_CAPACITY, "k*n too large for a dense output");
+  if (dist && (double)k * (double)g->n >= g->dense_max)
+    return fail(DAWN_ERR_CAPACITY, "k*n above the dense-output limit (use dawn_apsp_rows)");
   if (k == 0) return DAWN_OK;
   dawn_status s = set_device(g);
   if (s != DAWN_OK) return s;
@@ -988,6 +993,86 @@ dawn_status apsp(dawn_graph g, const int64_t *sources, int64_t k, int32_t rank, 
   dawn_status s = set_device(g);
   if (s != DAWN_OK) return s;
   return launch_ms(g, mine, nullptr, rec, static_cast<cudaStream_t>(stream));
+}
+
+// Owns the host-side resources of one dawn_apsp_rows call (no device memory).
+struct RowsRes {
+  cudaStream_t copy = nullptr;
+  cudaEvent_t done[2] = {}, landed[2] = {};
+  ~RowsRes() {
+    for (int i = 0; i < 2; ++i) {
+      if (done[i]) cudaEventDestroy(done[i]);
+      if (landed[i]) cudaEventDestroy(landed[i]);
+    }
+    if (copy) cudaStreamDestroy(copy);
+  }
+};
+
+dawn_status apsp_rows(dawn_graph g, const int64_t *sources, int64_t k, int64_t chunk,
+                      uint32_t *dev_stage, uint32_t *host_stage, dawn_row_sink sink, void *user,
+                      void *stream) {
+  if (!g || !sink || k < 0 || (k > 0 && (!sources || !dev_stage || !host_stage)) || chunk < 1)
+    return fail(DAWN_ERR_INVALID_ARGUMENT, "bad arguments");
+  if (g->lean) return fail(DAWN_ERR_CONFIG, "graph loaded with DAWN_GRAPH_LEAN (no multi-source words)");
+  for (int64_t i = 0; i < k; ++i)
+    if (sources[i] < 0 || sources[i] >= g->n)
+      return fail(DAWN_ERR_BOUNDS, "sources[%lld] = %lld not in [0, n)", (long long)i,
+                  (long long)sources[i]);
+  if ((double)chunk * (double)g->n >= g->dense_max)
+    return fail(DAWN_ERR_CAPACITY, "chunk*n above the dense-output limit");
+  if (k == 0) return DAWN_OK;
+  dawn_status s = set_device(g);
+  if (s != DAWN_OK) return s;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  RowsRes R;
+  cudaError_t e = cudaStreamCreateWithFlags(&R.copy, cudaStreamNonBlocking);
+  for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
+    e = cudaEventCreateWithFlags(&R.done[i], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&R.landed[i], cudaEventDisableTiming);
+  }
+  if (e != cudaSuccess) return cuda_fail(e, "dawn_apsp_rows resources");
+  const size_t n = (size_t)g->n;
+  const int64_t np = (k + chunk - 1) / chunk;
+  std::vector<uint32_t> src;
+  src.reserve((size_t)std::min(k, chunk));
+  // piece p: compute into dev_stage[p % 2] on `stream`, D2H into host_stage[p % 2] on the copy
+  // stream, sink(p) on this thread once it landed; piece p + 1 computes meanwhile
+  for (int64_t p = 0; p <= np; ++p) {
+    if (p < np) {
+      const int64_t b = p * chunk, c = std::min(k, b + chunk) - b;
+      const int slot = (int)(p & 1);
+      uint32_t *d = dev_stage + (size_t)slot * (size_t)chunk * n;
+      src.assign(sources + b, sources + b + c);
+      // dev_stage[slot] is free once piece p - 2's copy has left it
+      if (p >= 2 && (e = cudaStreamWaitEvent(st, R.landed[slot], 0)) != cudaSuccess)
+        return cuda_fail(e, "dawn_apsp_rows");
+      if ((s = launch_ms(g, src, d, nullptr, st)) != DAWN_OK) return s;
+      if ((e = cudaEventRecord(R.done[slot], st)) != cudaSuccess) return cuda_fail(e, "dawn_apsp_rows");
+    }
+    if (p >= 1) {  // hand piece p - 1 to the sink (host_stage[slot] was enqueued last iteration)
+      const int slot = (int)((p - 1) & 1);
+      if ((e = cudaEventSynchronize(R.landed[slot])) != cudaSuccess) return cuda_fail(e, "dawn_apsp_rows copy");
+      const int64_t b = (p - 1) * chunk, c = std::min(k, b + chunk) - b;
+      if (sink(user, b, c, host_stage + (size_t)slot * (size_t)chunk * n) != 0)
+        return fail(DAWN_ERR_INVALID_ARGUMENT, "the row sink aborted at row %lld", (long long)b);
+    }
+    if (p < np) {  // host_stage[slot] is free: its previous piece (p - 2) went to the sink
+      const int slot = (int)(p & 1);
+      const int64_t b = p * chunk, c = std::min(k, b + chunk) - b;
+      e = cudaStreamWaitEvent(R.copy, R.done[slot], 0);
+      if (e == cudaSuccess)
+        e = cudaMemcpyAsync(host_stage + (size_t)slot * (size_t)chunk * n,
+                            dev_stage + (size_t)slot * (size_t)chunk * n, 4 * (size_t)c * n,
+                            cudaMemcpyDeviceToHost, R.copy);
+      if (e == cudaSuccess) e = cudaEventRecord(R.landed[slot], R.copy);
+      if (e != cudaSuccess) return cuda_fail(e, "dawn_apsp_rows copy");
+    }
+  }
+  // `stream` must not run past the rows' copies (the caller may reuse dev_stage)
+  if ((e = cudaStreamWaitEvent(st, R.landed[(np - 1) & 1], 0)) != cudaSuccess)
+    return cuda_fail(e, "dawn_apsp_rows");
+  if ((e = cudaStreamSynchronize(R.copy)) != cudaSuccess) return cuda_fail(e, "dawn_apsp_rows");
+  return DAWN_OK;
 }
 
 dawn_status largest_wcc(dawn_graph g, int64_t *sources_out, int64_t *k, uint64_t *arcs,
@@ -1115,6 +1200,12 @@ dawn_status dawn_apsp_shard(int64_t k, int32_t rank, int32_t world, int64_t *idx
 dawn_status dawn_apsp(dawn_graph g, const int64_t *sources, int64_t k, int32_t rank, int32_t world,
                       dawn_record *rec, int64_t cap, int64_t *n_written, void *stream) {
   DAWN_GUARD(return apsp(g, sources, k, rank, world, rec, cap, n_written, stream);)
+}
+
+dawn_status dawn_apsp_rows(dawn_graph g, const int64_t *sources, int64_t k, int64_t chunk,
+                           uint32_t *dev_stage, uint32_t *host_stage, dawn_row_sink sink,
+                           void *user, void *stream) {
+  DAWN_GUARD(return apsp_rows(g, sources, k, chunk, dev_stage, host_stage, sink, user, stream);)
 }
 
 dawn_status dawn_largest_wcc(dawn_graph g, int64_t *sources_out, int64_t *k, uint64_t *arcs,
