@@ -319,6 +319,68 @@ dawn_status dawn_largest_wcc(dawn_graph g, int64_t *sources_out, int64_t *k, uin
  * (bench.py derives the executed bytes B_exec of SURVEY §8(d) from them).                   */
 dawn_status dawn_graph_ms_counters(dawn_graph g, uint64_t *host_out, void *stream);
 
+/* ------------------------------------------------------------------------------------------
+ * Partitioned single-source SSSP over W GPUs: the graph is cut by
+ * vertex ranges so each GPU holds ~2m/W arcs — the paper's memory-frugality motivation
+ * (E13; L554: graphs a GPU cannot hold).  Rank r owns the ids
+ * [lo, hi) = [r*B, min(n, (r+1)*B)), B = ceil(n/W) rounded up to a multiple of 32, and keeps
+ * the arcs whose TARGET it owns, grouped twice: by source (the "out-slice", for push = SOVM,
+ * Algorithm 2) and by target (the in-rows, for pull = BOVM, Algorithm 1).
+ * Every discovery is then local; one level needs only the global frontier F_L, exchanged as an
+ * all-gather of per-rank bitmap slices between two dawn_part_step calls (the caller's NCCL
+ * all_gather: recv <- concat over ranks of send).  Distances equal dawn_sssp's bit for bit.
+ *
+ *   dawn_part_begin(p, s, variant, dist_own)     level-0 slice into `send`
+ *   loop: all_gather(recv <- send); dawn_part_step(p)   until dawn_part_done() reports 1
+ *   dawn_part_finish(p, stats)                   dist_own[t] = d(s, lo + t); statistics
+ * Extra steps after convergence are no-ops, so the caller may test dawn_part_done every few
+ * levels.  Every rank must call begin/step/finish the same number of times.
+ * ------------------------------------------------------------------------------------------ */
+typedef struct dawn_part_s *dawn_part;
+
+/* The owned range [lo, hi) of `rank` (empty when rank * B >= n).  Host only. */
+dawn_status dawn_part_range(int64_t n, int32_t world, int32_t rank, int64_t *lo, int64_t *hi);
+
+/* Host-side partition builder from the global CSR (host arrays).  With all outputs NULL it only
+ * counts *m_r = arcs whose target lies in [lo, hi).  Otherwise (caller-allocated host arrays):
+ *   out_rp  int64[n+1], out_col int32[m_r]: the out-slice (row v = v's arcs into the range, in
+ *           input order, targets as local ids t = u - lo)
+ *   in_rp   int64[hi-lo+1], in_col int32[m_r]: the same arcs by target (sources ascending)
+ *   own_deg uint32[hi-lo]: global out-degree of lo + t (the E10 counts)
+ * Errors: INVALID_ARGUMENT, INVALID_GRAPH (row_ptr not a CSR, col out of range),
+ * CAPACITY (m_r >= 2^32). */
+dawn_status dawn_part_build(int64_t n, int64_t m, const int64_t *row_ptr, const int32_t *col,
+                            int32_t world, int32_t rank, int64_t *m_r, int64_t *out_rp,
+                            int32_t *out_col, int64_t *in_rp, int32_t *in_col, uint32_t *own_deg);
+
+/* Device workspace bytes of one rank's handle (0 if the sizes are unsupported). */
+size_t dawn_part_workspace_bytes(int64_t n, int64_t m_r, int32_t world, int32_t rank);
+
+/* Make rank `rank`'s partition resident: the dawn_part_build arrays as DEVICE copies
+ * (caller-owned, must outlive the handle), m = arcs of the whole graph.  Synchronises `stream`.
+ * Errors: INVALID_ARGUMENT, CAPACITY, WORKSPACE, CUDA. */
+dawn_status dawn_part_load(int64_t n, int64_t m, int32_t world, int32_t rank, int64_t m_r,
+                           const int64_t *out_rp, const int32_t *out_col, const int64_t *in_rp,
+                           const int32_t *in_col, const uint32_t *own_deg, void *workspace,
+                           size_t ws_bytes, void *stream, dawn_part *out);
+dawn_status dawn_part_destroy(dawn_part p);
+
+/* The exchange buffers inside the workspace: send = this rank's slice (slice_words uint32:
+ * 4 header words + B/32 bitmap words), recv = world slices in rank order. */
+dawn_status dawn_part_exchange(dawn_part p, uint32_t **send, uint32_t **recv, int64_t *slice_words);
+
+/* Start a search from global `source` (BOUNDS if not in [0, n)); dist_own = DEVICE
+ * uint32[hi-lo], fully written by dawn_part_finish. */
+dawn_status dawn_part_begin(dawn_part p, int64_t source, uint32_t variant, uint32_t *dist_own,
+                            void *stream);
+/* One level (reads recv, writes send).  Enqueue only. */
+dawn_status dawn_part_step(dawn_part p, void *stream);
+/* *done = 1 once the search converged (the frontier is empty on every rank).  Synchronises. */
+dawn_status dawn_part_done(dawn_part p, int32_t *done, void *stream);
+/* Write dist_own and (DEVICE, or NULL) the search's statistics: levels, reached, edges_reach
+ * are global (identical on every rank), edges_examined counts this rank's reads. */
+dawn_status dawn_part_finish(dawn_part p, dawn_sssp_stats *stats, void *stream);
+
 /* Thread-local description of the last error of this thread ("" if none). */
 const char *dawn_last_error(void);
 

@@ -17,7 +17,8 @@ import subprocess
 import numpy as np
 import torch
 
-__all__ = ["build", "Graph", "sssp", "sssp_batch", "msssp", "apsp", "apsp_rows", "apsp_shard", "largest_wcc",
+__all__ = ["build", "Graph", "sssp", "sssp_batch", "msssp", "apsp", "apsp_rows", "apsp_shard",
+           "part_range", "part_build", "PartGraph", "part_exchange", "part_sssp", "part_sssp_local", "largest_wcc",
            "check", "DawnError", "UNREACHED", "AUTO", "PUSH", "PULL", "MS_BATCH", "REC_DTYPE",
            "records_to_numpy", "stats_to_dict", "gather_records"]
 
@@ -120,6 +121,30 @@ def lib():
         L.dawn_graph_ms_counters.argtypes = [vp, vp, vp]
         L.dawn_apsp_rows.restype = st
         L.dawn_apsp_rows.argtypes = [vp, vp, i64, i64, vp, vp, _ROW_SINK, vp, vp]
+        L.dawn_part_range.restype = st
+        L.dawn_part_range.argtypes = [i64, i32, i32, ctypes.POINTER(ctypes.c_int64),
+                                      ctypes.POINTER(ctypes.c_int64)]
+        L.dawn_part_build.restype = st
+        L.dawn_part_build.argtypes = [i64, i64, vp, vp, i32, i32, ctypes.POINTER(ctypes.c_int64),
+                                      vp, vp, vp, vp, vp]
+        L.dawn_part_workspace_bytes.restype = ctypes.c_size_t
+        L.dawn_part_workspace_bytes.argtypes = [i64, i64, i32, i32]
+        L.dawn_part_load.restype = st
+        L.dawn_part_load.argtypes = [i64, i64, i32, i32, i64, vp, vp, vp, vp, vp, vp,
+                                     ctypes.c_size_t, vp, ctypes.POINTER(vp)]
+        L.dawn_part_destroy.restype = st
+        L.dawn_part_destroy.argtypes = [vp]
+        L.dawn_part_exchange.restype = st
+        L.dawn_part_exchange.argtypes = [vp, ctypes.POINTER(vp), ctypes.POINTER(vp),
+                                         ctypes.POINTER(ctypes.c_int64)]
+        L.dawn_part_begin.restype = st
+        L.dawn_part_begin.argtypes = [vp, i64, u32, vp, vp]
+        L.dawn_part_step.restype = st
+        L.dawn_part_step.argtypes = [vp, vp]
+        L.dawn_part_done.restype = st
+        L.dawn_part_done.argtypes = [vp, ctypes.POINTER(ctypes.c_int32), vp]
+        L.dawn_part_finish.restype = st
+        L.dawn_part_finish.argtypes = [vp, vp, vp]
         L.dawn_largest_wcc.restype = st
         L.dawn_largest_wcc.argtypes = [vp, vp, ctypes.POINTER(ctypes.c_int64),
                                        ctypes.POINTER(ctypes.c_uint64), vp]
@@ -377,6 +402,152 @@ def gather_records(local: torch.Tensor, k: int, world: int, group=None) -> torch
         if len(idx):
             full[torch.from_numpy(idx).to(local.device)] = parts[r][: len(idx)]
     return full
+
+
+# ----------------------------------------------------------- partitioned SSSP (NEXT-3)
+def part_range(n: int, world: int, rank: int) -> tuple[int, int]:
+    """dawn_part_range: the vertex ids [lo, hi) rank `rank` owns (host only)."""
+    lo, hi = ctypes.c_int64(0), ctypes.c_int64(0)
+    _check(lib().dawn_part_range(n, world, rank, ctypes.byref(lo), ctypes.byref(hi)))
+    return lo.value, hi.value
+
+
+def part_build(row_ptr, col, world: int, rank: int) -> dict:
+    """dawn_part_build (host C++): rank's out-slice (out_rp, out_col: targets local), in-rows
+    (in_rp, in_col: sources global) and own out-degrees, from the global host CSR."""
+    rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
+    cl = np.ascontiguousarray(col, dtype=np.int32)
+    n, m = len(rp) - 1, len(cl)
+    lo, hi = part_range(n, world, rank)
+    mr = ctypes.c_int64(0)
+    P = lambda a: a.ctypes.data_as(ctypes.c_void_p)
+    _check(lib().dawn_part_build(n, m, P(rp), P(cl), world, rank, ctypes.byref(mr),
+                                 None, None, None, None, None))
+    out = {"n": n, "m": m, "lo": lo, "hi": hi, "m_r": mr.value,
+           "out_rp": np.empty(n + 1, np.int64), "out_col": np.empty(max(1, mr.value), np.int32),
+           "in_rp": np.empty(hi - lo + 1, np.int64), "in_col": np.empty(max(1, mr.value), np.int32),
+           "deg": np.empty(max(1, hi - lo), np.uint32)}
+    _check(lib().dawn_part_build(n, m, P(rp), P(cl), world, rank, ctypes.byref(mr),
+                                 P(out["out_rp"]), P(out["out_col"]), P(out["in_rp"]),
+                                 P(out["in_col"]), P(out["deg"])))
+    out["out_col"] = out["out_col"][: mr.value]
+    out["in_col"] = out["in_col"][: mr.value]
+    out["deg"] = out["deg"][: hi - lo]
+    return out
+
+
+class PartGraph:
+    """One rank's share of a vertex-partitioned graph on its device (dawn_part_load)."""
+
+    def __init__(self, part: dict, world: int, rank: int, device=None, stream=None):
+        dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        t = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a)).to(device=dev, dtype=dt)
+        self.n, self.m, self.world, self.rank = part["n"], part["m"], world, rank
+        self.lo, self.hi, self.m_r = part["lo"], part["hi"], part["m_r"]
+        self.R = self.hi - self.lo
+        self.out_rp = t(part["out_rp"], torch.int64)
+        self.out_col = t(part["out_col"] if self.m_r else np.zeros(1, np.int32), torch.int32)
+        self.in_rp = t(part["in_rp"], torch.int64)
+        self.in_col = t(part["in_col"] if self.m_r else np.zeros(1, np.int32), torch.int32)
+        self.deg = t(part["deg"].view(np.int32) if self.R else np.zeros(1, np.int32), torch.int32)
+        nb = lib().dawn_part_workspace_bytes(self.n, self.m_r, world, rank)
+        if nb == 0:
+            raise DawnError(4, "unsupported partition size")
+        self.workspace = torch.empty(nb, dtype=torch.uint8, device=dev)
+        self.device = dev
+        h = ctypes.c_void_p()
+        with torch.cuda.device(dev):
+            _check(lib().dawn_part_load(self.n, self.m, world, rank, self.m_r, _dptr(self.out_rp),
+                                        _dptr(self.out_col), _dptr(self.in_rp), _dptr(self.in_col),
+                                        _dptr(self.deg), _dptr(self.workspace), nb, _stream(stream),
+                                        ctypes.byref(h)))
+        self._h = h
+        sp, rp, sw = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_int64(0)
+        _check(lib().dawn_part_exchange(h, ctypes.byref(sp), ctypes.byref(rp), ctypes.byref(sw)))
+        self.slice_words = sw.value
+        off_s = sp.value - self.workspace.data_ptr()
+        off_r = rp.value - self.workspace.data_ptr()
+        # views of the workspace's exchange buffers (what the all-gather moves)
+        self.send = self.workspace[off_s: off_s + 4 * sw.value].view(torch.int32)
+        self.recv = self.workspace[off_r: off_r + 4 * sw.value * world].view(torch.int32)
+
+    @property
+    def handle(self):
+        return self._h
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h and _lib is not None:
+            _lib.dawn_part_destroy(h)
+            self._h = None
+
+
+def part_exchange(pg: PartGraph, group=None):
+    """recv <- concatenation over ranks of send: one all-gather (NCCL over NVLink for CUDA
+    tensors; gloo for CPU tensors in the host tests); a device copy at world 1."""
+    import torch.distributed as dist
+    if pg.world == 1 and not (dist.is_available() and dist.is_initialized()):
+        pg.recv.copy_(pg.send)
+        return
+    if pg.send.is_cuda:
+        dist.all_gather_into_tensor(pg.recv, pg.send, group=group)
+    else:
+        parts = list(pg.recv.view(pg.world, -1).unbind(0))
+        dist.all_gather(parts, pg.send, group=group)
+
+
+def part_sssp(pg: PartGraph, source: int, variant="auto", group=None, out=None,
+              stats: bool = False, check_every: int = 4, exchange=None, stream=None):
+    """Partitioned SSSP on this rank (every rank calls it with the same arguments): returns the
+    distances of the owned vertices [lo, hi) as int32 [hi - lo] (and the statistics)."""
+    dist_t = out if out is not None else torch.empty(max(1, pg.R), dtype=torch.int32, device=pg.device)
+    st = torch.zeros(4, dtype=torch.int64, device=pg.device) if stats else None
+    s = _stream(stream)
+    ex = exchange or (lambda: part_exchange(pg, group))
+    _check(lib().dawn_part_begin(pg.handle, int(source), _VARIANTS[variant], _dptr(dist_t), s))
+    steps = 0
+    done = ctypes.c_int32(0)
+    while True:
+        ex()
+        _check(lib().dawn_part_step(pg.handle, s))
+        steps += 1
+        if steps % check_every == 0:
+            _check(lib().dawn_part_done(pg.handle, ctypes.byref(done), s))
+            if done.value:
+                break
+    _check(lib().dawn_part_finish(pg.handle, _dptr(st), s))
+    d = dist_t[: pg.R]
+    return (d, st) if stats else d
+
+
+def part_sssp_local(parts: list, source: int, variant="auto", stats: bool = False,
+                    check_every: int = 4):
+    """All W ranks' partitions on ONE device, the all-gather done by device copies: the same
+    kernels and exchange layout as part_sssp under torch.distributed (used by the tests to
+    check W > 1 on a single GPU).  Returns the global distance vector (int32 [n])."""
+    W = len(parts)
+    outs = [torch.empty(max(1, p.R), dtype=torch.int32, device=p.device) for p in parts]
+    sts = [torch.zeros(4, dtype=torch.int64, device=p.device) for p in parts] if stats else None
+    s = _stream(None)
+    for i, p in enumerate(parts):
+        _check(lib().dawn_part_begin(p.handle, int(source), _VARIANTS[variant], _dptr(outs[i]), s))
+    steps = 0
+    done = ctypes.c_int32(0)
+    while True:
+        full = torch.cat([p.send for p in parts])
+        for p in parts:
+            p.recv.copy_(full)
+        for p in parts:
+            _check(lib().dawn_part_step(p.handle, s))
+        steps += 1
+        if steps % check_every == 0:
+            _check(lib().dawn_part_done(parts[0].handle, ctypes.byref(done), s))
+            if done.value:
+                break
+    for i, p in enumerate(parts):
+        _check(lib().dawn_part_finish(p.handle, _dptr(sts[i]) if stats else None, s))
+    d = torch.cat([o[: p.R] for o, p in zip(outs, parts)])
+    return (d, sts) if stats else d
 
 
 def version() -> str:

@@ -19,6 +19,7 @@
 #include "narrow_kernel.cuh"
 #include "sssp_kernel.cuh"
 #include "wcc_kernel.cuh"
+#include "part_kernel.cuh"
 
 using namespace dawn;
 
@@ -1136,6 +1137,314 @@ dawn_status ms_counters(dawn_graph g, uint64_t *host_out, void *stream) {
   return DAWN_OK;
 }
 
+// ---------------------------------------------------------------- partitioned SSSP (NEXT-3)
+int64_t part_block(int64_t n, int32_t world) {  // Rmax: ceil(n / world) rounded up to 32
+  const int64_t q = (n + world - 1) / world;
+  return (q + 31) / 32 * 32;
+}
+
+dawn_status part_range(int64_t n, int32_t world, int32_t rank, int64_t *lo, int64_t *hi) {
+  if (n < 1 || world < 1 || rank < 0 || rank >= world || !lo || !hi)
+    return fail(DAWN_ERR_INVALID_ARGUMENT, "need n >= 1, 0 <= rank < world, lo/hi");
+  const int64_t B = part_block(n, world);
+  *lo = std::min<int64_t>(n, (int64_t)rank * B);
+  *hi = std::min<int64_t>(n, *lo + B);
+  return DAWN_OK;
+}
+
+dawn_status part_build(int64_t n, int64_t m, const int64_t *row_ptr, const int32_t *col,
+                       int32_t world, int32_t rank, int64_t *m_r, int64_t *out_rp,
+                       int32_t *out_col, int64_t *in_rp, int32_t *in_col, uint32_t *own_deg) {
+  int64_t lo = 0, hi = 0;
+  dawn_status s = part_range(n, world, rank, &lo, &hi);
+  if (s != DAWN_OK) return s;
+  if (m < 0 || !row_ptr || (m > 0 && !col) || !m_r)
+    return fail(DAWN_ERR_INVALID_ARGUMENT, "bad arguments");
+  if (row_ptr[0] != 0 || row_ptr[n] != m)
+    return fail(DAWN_ERR_INVALID_GRAPH, "row_ptr[0] must be 0 and row_ptr[n] = m");
+  const int64_t R = hi - lo;
+  // pass 1: arcs into the owned range, per source (out-slice) and per target (in-rows)
+  int64_t cnt = 0;
+  for (int64_t v = 0; v < n; ++v) {
+    if (row_ptr[v + 1] < row_ptr[v]) return fail(DAWN_ERR_INVALID_GRAPH, "row_ptr not monotone");
+    for (int64_t j = row_ptr[v]; j < row_ptr[v + 1]; ++j) {
+      const int64_t u = col[j];
+      if (u < 0 || u >= n) return fail(DAWN_ERR_INVALID_GRAPH, "col[%lld] out of range", (long long)j);
+      cnt += (u >= lo && u < hi);
+    }
+  }
+  *m_r = cnt;
+  if (!out_rp && !out_col && !in_rp && !in_col && !own_deg) return DAWN_OK;  // count only
+  if (!out_rp || !in_rp || !own_deg || (cnt > 0 && (!out_col || !in_col)))
+    return fail(DAWN_ERR_INVALID_ARGUMENT, "outputs must all be given (or all NULL to count)");
+  if (cnt >= (int64_t(1) << 32)) return fail(DAWN_ERR_CAPACITY, "partition holds >= 2^32 arcs");
+  // out-slice: rows in global source order, targets local (row order of the input kept)
+  int64_t o = 0;
+  for (int64_t v = 0; v < n; ++v) {
+    out_rp[v] = o;
+    for (int64_t j = row_ptr[v]; j < row_ptr[v + 1]; ++j) {
+      const int64_t u = col[j];
+      if (u >= lo && u < hi) out_col[o++] = (int32_t)(u - lo);
+    }
+  }
+  out_rp[n] = o;
+  // in-rows: counting sort of the same arcs by target (sources ascending within a row)
+  for (int64_t t = 0; t <= R; ++t) in_rp[t] = 0;
+  for (int64_t j = 0; j < cnt; ++j) in_rp[out_col[j] + 1]++;
+  for (int64_t t = 0; t < R; ++t) in_rp[t + 1] += in_rp[t];
+  std::vector<int64_t> cur(in_rp, in_rp + R + 1);
+  for (int64_t v = 0; v < n; ++v)
+    for (int64_t j = out_rp[v]; j < out_rp[v + 1]; ++j) in_col[cur[out_col[j]]++] = (int32_t)v;
+  for (int64_t t = 0; t < R; ++t) {
+    const int64_t d = row_ptr[lo + t + 1] - row_ptr[lo + t];
+    own_deg[t] = (uint32_t)std::min<int64_t>(d, 0xffffffffll);
+  }
+  return DAWN_OK;
+}
+
+struct PartLayout {
+  size_t rp, irp, hout_bits, hout_v, hout_s, hout_e, hin_bits, hin_v, hin_s, hin_e;
+  size_t scan_tmp, piece_tmp, vis, lev, send, recv, ctrl, total;
+  uint64_t capHP;
+};
+
+PartLayout part_layout(int64_t n, int64_t m_r, int32_t world, int64_t R, int64_t Rmax) {
+  PartLayout L{};
+  size_t o = 0;
+  auto take = [&](size_t bytes) {
+    size_t at = o;
+    o = align_up(o + (bytes ? bytes : 1));
+    return at;
+  };
+  const size_t S = kPartHdr + (size_t)Rmax / 32;
+  L.capHP = (uint64_t)m_r / kHPiece + (uint64_t)m_r / kHeavy + 1;
+  L.rp = take(4 * (size_t)(n + 1));
+  L.irp = take(4 * (size_t)(R + 1));
+  L.hout_bits = take(4 * (size_t)((n + 31) / 32));
+  L.hout_v = take(4 * L.capHP);
+  L.hout_s = take(4 * L.capHP);
+  L.hout_e = take(4 * L.capHP);
+  L.hin_bits = take(4 * (size_t)((R + 31) / 32 + 1));
+  L.hin_v = take(4 * L.capHP);
+  L.hin_s = take(4 * L.capHP);
+  L.hin_e = take(4 * L.capHP);
+  L.scan_tmp = take(4 * ((size_t)std::max(n, R) / kScanBlock + 2));
+  L.piece_tmp = take(4 * (3 * ((size_t)m_r / kHPiece + 3) + 1));
+  L.vis = take(4 * (size_t)((R + 31) / 32 + 1));
+  L.lev = take((size_t)R + 8);
+  L.send = take(4 * S);
+  L.recv = take(4 * S * (size_t)world);
+  L.ctrl = take(sizeof(PartCtrl));
+  L.total = o;
+  return L;
+}
+
+}  // namespace
+
+struct dawn_part_s {
+  int64_t n = 0, m = 0, lo = 0, R = 0, Rmax = 0, m_r = 0;
+  int32_t world = 1, rank = 0;
+  int device = 0, nsm = 0, grid = 0;
+  char *ws = nullptr;
+  PartLayout L{};
+  const int32_t *col = nullptr, *icol = nullptr;
+  const uint32_t *deg = nullptr;
+  uint32_t *dist = nullptr;
+  uint32_t steps = 0, src_local = 0xffffffffu, variant = 0;
+  float alpha = 2.f, beta = 96.f;
+};
+
+namespace {
+
+PartParams part_params(dawn_part p) {
+  PartParams q{};
+  q.n = (uint32_t)p->n;
+  q.R = (uint32_t)p->R;
+  q.Rmax = (uint32_t)p->Rmax;
+  q.lo = (uint32_t)p->lo;
+  q.world = (uint32_t)p->world;
+  q.S = (uint32_t)(kPartHdr + p->Rmax / 32);
+  q.nwg = (uint32_t)((p->n + 31) / 32);
+  q.src_local = p->src_local;
+  auto u32 = [&](size_t off) { return reinterpret_cast<uint32_t *>(p->ws + off); };
+  q.rp = u32(p->L.rp);
+  q.col = p->col;
+  q.irp = u32(p->L.irp);
+  q.icol = p->icol;
+  q.deg = p->deg;
+  q.hout_v = u32(p->L.hout_v);
+  q.hout_s = u32(p->L.hout_s);
+  q.hout_e = u32(p->L.hout_e);
+  q.hout_bits = u32(p->L.hout_bits);
+  q.hin_v = u32(p->L.hin_v);
+  q.hin_s = u32(p->L.hin_s);
+  q.hin_e = u32(p->L.hin_e);
+  q.hin_bits = u32(p->L.hin_bits);
+  q.vis = u32(p->L.vis);
+  q.lev = reinterpret_cast<uint8_t *>(p->ws + p->L.lev);
+  q.dist = p->dist;
+  q.recv = u32(p->L.recv);
+  q.send = u32(p->L.send);
+  q.ctrl = reinterpret_cast<PartCtrl *>(p->ws + p->L.ctrl);
+  q.variant = p->variant;
+  q.can_pull = 1;
+  q.alpha = p->alpha;
+  q.beta = p->beta;
+  q.m_total = (unsigned long long)p->m;
+  return q;
+}
+
+dawn_status part_load(int64_t n, int64_t m, int32_t world, int32_t rank, int64_t m_r,
+                      const int64_t *out_rp, const int32_t *out_col, const int64_t *in_rp,
+                      const int32_t *in_col, const uint32_t *own_deg, void *workspace,
+                      size_t ws_bytes, void *stream, dawn_part *out) {
+  if (!out) return fail(DAWN_ERR_INVALID_ARGUMENT, "out is NULL");
+  *out = nullptr;
+  int64_t lo = 0, hi = 0;
+  dawn_status s = part_range(n, world, rank, &lo, &hi);
+  if (s != DAWN_OK) return s;
+  if (n >= (int64_t(1) << 31) || m < 0 || m >= (int64_t(1) << 32) || m_r < 0 || m_r > m)
+    return fail(DAWN_ERR_CAPACITY, "n < 2^31 and m_r <= m < 2^32 required");
+  const int64_t R = hi - lo;
+  if (!out_rp || !in_rp || (R > 0 && !own_deg) || (m_r > 0 && (!out_col || !in_col)) || !workspace)
+    return fail(DAWN_ERR_INVALID_ARGUMENT, "NULL array");
+  if (reinterpret_cast<uintptr_t>(workspace) & 255)
+    return fail(DAWN_ERR_INVALID_ARGUMENT, "workspace must be 256-byte aligned");
+  const int64_t Rmax = part_block(n, world);
+  PartLayout L = part_layout(n, m_r, world, R, Rmax);
+  if (ws_bytes < L.total)
+    return fail(DAWN_ERR_WORKSPACE, "workspace too small: need %zu bytes, got %zu", L.total, ws_bytes);
+  cudaPointerAttributes pa{};
+  cudaError_t e = cudaPointerGetAttributes(&pa, workspace);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaPointerGetAttributes(workspace)");
+  if (pa.type != cudaMemoryTypeDevice) return fail(DAWN_ERR_INVALID_ARGUMENT, "workspace is not device memory");
+  if ((e = cudaSetDevice(pa.device)) != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+  auto *p = new (std::nothrow) dawn_part_s;
+  if (!p) return fail(DAWN_ERR_CAPACITY, "host allocation failed");
+  p->n = n;
+  p->m = m;
+  p->lo = lo;
+  p->R = R;
+  p->Rmax = Rmax;
+  p->m_r = m_r;
+  p->world = world;
+  p->rank = rank;
+  p->device = pa.device;
+  p->ws = static_cast<char *>(workspace);
+  p->L = L;
+  p->col = out_col;
+  p->icol = in_col;
+  p->deg = own_deg;
+  cudaDeviceGetAttribute(&p->nsm, cudaDevAttrMultiProcessorCount, pa.device);
+  int bps = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_part_level<kNT>, kNT, 0);
+  p->grid = std::max(1, p->nsm * std::max(1, std::min(bps, 2)));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int blocks = std::max(1, std::min<int>(p->nsm * 8, (int)((n + 255) / 256)));
+  auto u32 = [&](size_t off) { return reinterpret_cast<uint32_t *>(p->ws + off); };
+  k_offsets32<<<blocks, 256, 0, st>>>(out_rp, u32(L.rp), n + 1);
+  k_offsets32<<<blocks, 256, 0, st>>>(in_rp, u32(L.irp), R + 1);
+  PartCtrl *C = reinterpret_cast<PartCtrl *>(p->ws + L.ctrl);
+  cudaMemsetAsync(C, 0, sizeof(PartCtrl), st);
+  // static heavy pieces of the out-slice rows (over n sources) and of the in-rows (over R)
+  auto build_list = [&](const uint32_t *rows, uint32_t nrows, size_t bits, size_t hv, size_t hs,
+                        size_t he, uint32_t *count) {
+    const uint32_t nblk = (uint32_t)((nrows + kScanBlock - 1) / kScanBlock);
+    if (nrows == 0 || m_r == 0) {
+      cudaMemsetAsync(p->ws + bits, 0, 4 * (size_t)((nrows + 31) / 32 + 1), st);
+      cudaMemsetAsync(count, 0, 4, st);
+      return;
+    }
+    k_hcount<<<nblk, 256, 0, st>>>(rows, nrows, u32(bits), u32(L.scan_tmp));
+    k_hscan<<<1, 32, 0, st>>>(u32(L.scan_tmp), nblk, count);
+    const size_t cap = (size_t)m_r / kHPiece + 3;
+    uint32_t *hc = u32(L.piece_tmp), *base = hc + cap, *cursor = base + cap, *maxc = cursor + cap;
+    cudaMemsetAsync(hc, 0, 4 * cap, st);
+    cudaMemsetAsync(maxc, 0, 4, st);
+    const int hb = std::max(1, std::min<int>(p->nsm * 8, (int)((nrows + 255) / 256)));
+    k_hhist<<<hb, 256, 0, st>>>(rows, nrows, hc, maxc);
+    k_hbase<<<1, 32, 0, st>>>(hc, base, cursor, maxc);
+    k_hfill<<<hb, 256, 0, st>>>(rows, nrows, base, cursor, u32(hv), u32(hs), u32(he));
+  };
+  build_list(u32(L.rp), (uint32_t)n, L.hout_bits, L.hout_v, L.hout_s, L.hout_e, &C->n_hp[0]);
+  build_list(u32(L.irp), (uint32_t)R, L.hin_bits, L.hin_v, L.hin_s, L.hin_e, &C->n_hp[1]);
+  if ((e = cudaStreamSynchronize(st)) != cudaSuccess || (e = cudaGetLastError()) != cudaSuccess) {
+    delete p;
+    return cuda_fail(e, "dawn_part_load");
+  }
+  *out = p;
+  return DAWN_OK;
+}
+
+dawn_status part_exchange(dawn_part p, uint32_t **send, uint32_t **recv, int64_t *slice_words) {
+  if (!p || !send || !recv || !slice_words) return fail(DAWN_ERR_INVALID_ARGUMENT, "NULL argument");
+  *send = reinterpret_cast<uint32_t *>(p->ws + p->L.send);
+  *recv = reinterpret_cast<uint32_t *>(p->ws + p->L.recv);
+  *slice_words = (int64_t)(kPartHdr + p->Rmax / 32);
+  return DAWN_OK;
+}
+
+dawn_status part_begin(dawn_part p, int64_t source, uint32_t variant, uint32_t *dist, void *stream) {
+  if (!p || (p->R > 0 && !dist)) return fail(DAWN_ERR_INVALID_ARGUMENT, "part or dist is NULL");
+  if (variant > DAWN_PULL) return fail(DAWN_ERR_INVALID_ARGUMENT, "unknown variant");
+  if (source < 0 || source >= p->n)
+    return fail(DAWN_ERR_BOUNDS, "source %lld not in [0, n)", (long long)source);
+  cudaError_t e = cudaSetDevice(p->device);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  p->dist = dist;
+  p->variant = variant;
+  p->steps = 0;
+  p->src_local = (source >= p->lo && source < p->lo + p->R) ? (uint32_t)(source - p->lo) : 0xffffffffu;
+  PartParams q = part_params(p);
+  e = cudaMemsetAsync(q.send, 0, 4 * (size_t)q.S, st);
+  if (e != cudaSuccess) return cuda_fail(e, "dawn_part_begin");
+  const int blocks = std::max(1, std::min<int>(p->nsm * 4, (int)((p->R / 32 + 255) / 256)));
+  k_part_begin<<<blocks, 256, 0, st>>>(q);
+  if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "k_part_begin launch");
+  return DAWN_OK;
+}
+
+dawn_status part_step(dawn_part p, void *stream) {
+  if (!p) return fail(DAWN_ERR_INVALID_ARGUMENT, "part is NULL");
+  cudaError_t e = cudaSetDevice(p->device);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  PartParams q = part_params(p);
+  // the slice of F_{L+1} is built from zero (the previous one was already gathered)
+  if ((e = cudaMemsetAsync(q.send, 0, 4 * (size_t)q.S, st)) != cudaSuccess) return cuda_fail(e, "dawn_part_step");
+  k_part_level<kNT><<<p->grid, kNT, 0, st>>>(q, p->steps);
+  if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "k_part_level launch");
+  p->steps++;
+  return DAWN_OK;
+}
+
+dawn_status part_done(dawn_part p, int32_t *done, void *stream) {
+  if (!p || !done) return fail(DAWN_ERR_INVALID_ARGUMENT, "NULL argument");
+  cudaError_t e = cudaSetDevice(p->device);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  PartCtrl *C = reinterpret_cast<PartCtrl *>(p->ws + p->L.ctrl);
+  uint32_t d = 0;
+  e = cudaMemcpyAsync(&d, &C->st[p->steps & 1].done, 4, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return cuda_fail(e, "dawn_part_done");
+  *done = (int32_t)d;
+  return DAWN_OK;
+}
+
+dawn_status part_finish(dawn_part p, dawn_sssp_stats *stats, void *stream) {
+  if (!p) return fail(DAWN_ERR_INVALID_ARGUMENT, "part is NULL");
+  cudaError_t e = cudaSetDevice(p->device);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  PartParams q = part_params(p);
+  const int blocks = std::max(1, std::min<int>(p->nsm * 8, (int)((p->R + 255) / 256)));
+  k_part_finish<<<blocks, 256, 0, st>>>(q, p->steps & 1, stats);
+  if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "k_part_finish launch");
+  return DAWN_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -1215,6 +1524,61 @@ dawn_status dawn_largest_wcc(dawn_graph g, int64_t *sources_out, int64_t *k, uin
 
 dawn_status dawn_graph_ms_counters(dawn_graph g, uint64_t *host_out, void *stream) {
   DAWN_GUARD(return ms_counters(g, host_out, stream);)
+}
+
+dawn_status dawn_part_range(int64_t n, int32_t world, int32_t rank, int64_t *lo, int64_t *hi) {
+  DAWN_GUARD(return part_range(n, world, rank, lo, hi);)
+}
+
+dawn_status dawn_part_build(int64_t n, int64_t m, const int64_t *row_ptr, const int32_t *col,
+                            int32_t world, int32_t rank, int64_t *m_r, int64_t *out_rp,
+                            int32_t *out_col, int64_t *in_rp, int32_t *in_col, uint32_t *own_deg) {
+  DAWN_GUARD(return part_build(n, m, row_ptr, col, world, rank, m_r, out_rp, out_col, in_rp, in_col,
+                               own_deg);)
+}
+
+size_t dawn_part_workspace_bytes(int64_t n, int64_t m_r, int32_t world, int32_t rank) {
+  try {
+    int64_t lo = 0, hi = 0;
+    if (n < 1 || n >= (int64_t(1) << 31) || m_r < 0 || m_r >= (int64_t(1) << 32) ||
+        part_range(n, world, rank, &lo, &hi) != DAWN_OK)
+      return 0;
+    return part_layout(n, m_r, world, hi - lo, part_block(n, world)).total;
+  } catch (...) {
+    return 0;
+  }
+}
+
+dawn_status dawn_part_load(int64_t n, int64_t m, int32_t world, int32_t rank, int64_t m_r,
+                           const int64_t *out_rp, const int32_t *out_col, const int64_t *in_rp,
+                           const int32_t *in_col, const uint32_t *own_deg, void *workspace,
+                           size_t ws_bytes, void *stream, dawn_part *out) {
+  DAWN_GUARD(return part_load(n, m, world, rank, m_r, out_rp, out_col, in_rp, in_col, own_deg,
+                              workspace, ws_bytes, stream, out);)
+}
+
+dawn_status dawn_part_destroy(dawn_part p) {
+  delete p;
+  return DAWN_OK;
+}
+
+dawn_status dawn_part_exchange(dawn_part p, uint32_t **send, uint32_t **recv, int64_t *slice_words) {
+  DAWN_GUARD(return part_exchange(p, send, recv, slice_words);)
+}
+
+dawn_status dawn_part_begin(dawn_part p, int64_t source, uint32_t variant, uint32_t *dist_own,
+                            void *stream) {
+  DAWN_GUARD(return part_begin(p, source, variant, dist_own, stream);)
+}
+
+dawn_status dawn_part_step(dawn_part p, void *stream) { DAWN_GUARD(return part_step(p, stream);) }
+
+dawn_status dawn_part_done(dawn_part p, int32_t *done, void *stream) {
+  DAWN_GUARD(return part_done(p, done, stream);)
+}
+
+dawn_status dawn_part_finish(dawn_part p, dawn_sssp_stats *stats, void *stream) {
+  DAWN_GUARD(return part_finish(p, stats, stream);)
 }
 
 }  // extern "C"

@@ -1,0 +1,322 @@
+// part_kernel.cuh — partitioned single-source DAWN over W GPUs (the
+// paper's memory-frugality motivation, PAPER.md L312-323 (E13) and L554 — graphs one device
+// cannot hold).
+//
+// 1D vertex partition: rank r owns the ids [lo_r, lo_r + R_r) (blocks of Rmax, a multiple of 32).
+// It holds only the arcs whose TARGET it owns, twice grouped:
+//   out-slice  CSR over every global source v: the arcs v -> u with u owned (targets local)
+//   in-rows    CSR over the owned u: the same arcs grouped by target (sources global)
+// so a level needs the global frontier F_L and nothing else: push expands the out-slice rows of
+// F_L's vertices (Algorithm 2), pull scans the in-rows of the owned unreached
+// vertices until the first in-neighbour in F_L (Algorithm 1, Eq. 4) — every discovery
+// is local, no remote write.  The only exchange per level is an all-gather of the ranks' slices
+// of the next frontier bitmap (Rmax / 8 bytes each) with a 16-byte header (|F|, sum of
+// out-degrees) from which every rank takes the same direction / stop decision.  The caller runs
+// that all-gather (NCCL over NVLink, torch.distributed) between two dawn_part_step calls.
+#pragma once
+#include "layout.h"
+
+namespace dawn {
+
+constexpr uint32_t kPartHdr = 4;  // exchange slice header words: [0] |F_{L+1}| here, [2..3] m_f
+
+struct PartState {
+  uint32_t done, dir, prev_nf, ecc;
+  uint32_t push_levels, pull_levels, reached, pad;
+  unsigned long long explored, pad2;
+};
+static_assert(sizeof(PartState) % 16 == 0, "PartState");
+
+struct PartCtrl {
+  PartState st[2];               // level L reads st[L & 1], CTA 0 writes st[(L + 1) & 1]
+  unsigned long long examined;   // adjacency entries read on this rank
+  uint32_t n_hp[2];              // static heavy pieces: [0] out-slice rows, [1] in-rows
+  uint32_t pad[12];
+};
+
+struct PartParams {
+  uint32_t n, R, Rmax, lo, world, S;  // S = exchange slice words = kPartHdr + Rmax / 32
+  uint32_t nwg;                       // words of the global frontier bitmap = ceil(n / 32)
+  uint32_t src_local;                 // dawn_part_begin: source - lo if owned, else ~0
+  const uint32_t *rp;                 // out-slice offsets over the n global sources
+  const int32_t *col;                 // out-slice targets (local ids)
+  const uint32_t *irp;                // in-row offsets over the R owned vertices
+  const int32_t *icol;                // in-row sources (global ids)
+  const uint32_t *deg;                // global out-degree of the owned vertices (E10 counts)
+  const uint32_t *hout_v, *hout_s, *hout_e, *hout_bits;  // out-slice rows > kHeavy: pieces
+  const uint32_t *hin_v, *hin_s, *hin_e, *hin_bits;      // in-rows > kHeavy: pieces
+  uint32_t *vis;                      // owned vertices reached so far (bitmap)
+  uint8_t *lev;                       // deferred distances (as k_sssp: byte L+1, 255 = direct)
+  uint32_t *dist;                     // caller's distance slice [R]
+  const uint32_t *recv;               // gathered slices of F_L: world x S words
+  uint32_t *send;                     // this rank's slice of F_{L+1} (zeroed before the step)
+  PartCtrl *ctrl;
+  uint32_t variant, can_pull;
+  float alpha, beta;
+  unsigned long long m_total;         // arcs of the whole graph
+};
+
+// Is global vertex v in the frontier held by the gathered slices?
+__device__ __forceinline__ bool part_ftest(const PartParams &p, uint32_t v) {
+  const uint32_t q = v / p.Rmax, r = v - q * p.Rmax;
+  return (ld_nc(p.recv + (size_t)q * p.S + kPartHdr + (r >> 5)) >> (r & 31)) & 1u;
+}
+
+__device__ __forceinline__ void part_discover(const PartParams &p, uint32_t t, uint32_t L1,
+                                              uint32_t &n_new, unsigned long long &m_new) {
+  if (L1 < 255u) {
+    p.lev[t] = (uint8_t)L1;
+  } else {
+    p.dist[t] = L1;
+    p.lev[t] = 255u;
+  }
+  red_or(p.send + kPartHdr + (t >> 5), 1u << (t & 31));
+  n_new += 1;
+  m_new += ld_nc(p.deg + t);
+}
+
+// Claim owned vertex t for level L+1 (test-and-set on vis; each vertex is discovered once).
+__device__ __forceinline__ void part_claim(const PartParams &p, uint32_t t, uint32_t L1,
+                                           uint32_t &n_new, unsigned long long &m_new) {
+  const uint32_t w = t >> 5, bit = 1u << (t & 31);
+  if (!(p.vis[w] & bit) && !(atomicOr(p.vis + w, bit) & bit)) part_discover(p, t, L1, n_new, m_new);
+}
+
+// dawn_part_begin: vis <- {s} on the owner, level-0 slice (the caller zeroed `send`), state.
+__global__ void k_part_begin(PartParams p) {
+  const uint32_t gtid = blockIdx.x * blockDim.x + threadIdx.x, nth = gridDim.x * blockDim.x;
+  const uint32_t nwo = (p.R + 31) / 32;
+  for (uint32_t w = gtid; w < nwo; w += nth)
+    p.vis[w] = (p.src_local != 0xffffffffu && w == (p.src_local >> 5)) ? 1u << (p.src_local & 31) : 0u;
+  if (gtid == 0) {
+    if (p.src_local != 0xffffffffu) {
+      p.send[kPartHdr + (p.src_local >> 5)] = 1u << (p.src_local & 31);
+      p.send[0] = 1;
+      const unsigned long long d = ld_nc(p.deg + p.src_local);
+      p.send[2] = (uint32_t)d;
+      p.send[3] = (uint32_t)(d >> 32);
+    }
+    PartState s{};
+    s.dir = (p.variant == DAWN_PULL) ? kPull : kPush;
+    p.ctrl->st[0] = s;
+    p.ctrl->examined = 0;
+  }
+}
+
+// One level: F_L (gathered) -> this rank's slice of F_{L+1}.  Every CTA takes the same decision
+// from the identical headers; CTA 0 records the next state.
+template <int NT>
+__global__ void __launch_bounds__(NT, 2) k_part_level(PartParams p, uint32_t L) {
+  __shared__ PartState st;
+  __shared__ unsigned long long red[3];
+  const uint32_t lane = lane_id();
+  const uint32_t gwarp = blockIdx.x * (NT / 32) + threadIdx.x / 32;
+  const uint32_t nwarps = gridDim.x * (NT / 32);
+  const uint32_t L1 = L + 1;
+  if (threadIdx.x == 0) {
+    const uint4 *s4 = reinterpret_cast<const uint4 *>(&p.ctrl->st[L & 1]);
+    uint4 *d4 = reinterpret_cast<uint4 *>(&st);
+    for (int i = 0; i < (int)(sizeof(PartState) / 16); ++i) d4[i] = __ldcg(s4 + i);
+    if (!st.done) {
+      uint32_t nf = 0;
+      unsigned long long mf = 0;
+      for (uint32_t q = 0; q < p.world; ++q) {
+        const uint32_t *h = p.recv + (size_t)q * p.S;
+        nf += h[0];
+        mf += ((unsigned long long)h[3] << 32) | h[2];
+      }
+      if (nf == 0) {  // condition 2: F_L is empty
+        st.done = 1;
+        st.ecc = L ? L - 1 : 0;
+      } else {
+        if (L > 0) st.reached += nf;
+        st.explored += mf;
+        if (st.reached + 1 >= p.n || L1 >= p.n) {  // condition 1 (L177) / the n-1 round bound
+          st.done = 1;
+          st.ecc = L;
+        } else {
+          if (p.variant == DAWN_PUSH || !p.can_pull) {
+            st.dir = kPush;
+          } else if (p.variant == DAWN_PULL) {
+            st.dir = kPull;
+          } else {  // the k_sssp rule (level_header), on the global counters
+            const double mu = (double)(p.m_total - min(st.explored, p.m_total));
+            const double nu = (double)(p.n - 1 - min(st.reached, p.n - 1));
+            if (st.dir == kPush) {
+              if ((double)mf * (double)mf * p.alpha > nu * mu && nf > st.prev_nf) st.dir = kPull;
+            } else {
+              if ((double)nf * p.beta < (double)p.n && nf < st.prev_nf) st.dir = kPush;
+            }
+          }
+          st.prev_nf = nf;
+          if (st.dir == kPush) st.push_levels++; else st.pull_levels++;
+        }
+      }
+    }
+    if (blockIdx.x == 0) p.ctrl->st[L1 & 1] = st;
+    red[0] = red[1] = red[2] = 0;
+  }
+  __syncthreads();
+  if (st.done) return;
+  uint32_t n_new = 0;
+  unsigned long long m_new = 0, exam = 0;
+  if (st.dir == kPush) {
+    // (a) light out-slice rows (<= kHeavy arcs): 32 words of F_L per warp, each round every lane
+    //     contributes its word's next vertex; the round's rows are dealt 32 arcs at a time
+    const uint32_t wpr = p.Rmax / 32;
+    for (uint32_t base = gwarp * 32; base < p.nwg; base += nwarps * 32) {
+      const uint32_t gw = base + lane;
+      uint32_t bits = 0;
+      if (gw < p.nwg) {
+        const uint32_t q = gw / wpr;
+        bits = ld_nc(p.recv + (size_t)q * p.S + kPartHdr + (gw - q * wpr)) & ~ld_nc(p.hout_bits + gw);
+      }
+      while (__ballot_sync(DAWN_FULL, bits != 0)) {
+        uint32_t rs = 0, d = 0;
+        if (bits) {
+          const uint32_t v = gw * 32 + (__ffs(bits) - 1);
+          bits &= bits - 1;
+          rs = ld_nc(p.rp + v);
+          d = ld_nc(p.rp + v + 1) - rs;
+        }
+        const uint32_t incl = warp_incl_scan(d);
+        const uint32_t total = __shfl_sync(DAWN_FULL, incl, 31);
+        const uint32_t excl = incl - d;
+        for (uint32_t r0 = 0; r0 < total; r0 += 32) {
+          const uint32_t t = r0 + lane;
+          uint32_t k = 0;
+#pragma unroll
+          for (uint32_t step = 16; step; step >>= 1) {
+            const uint32_t e = __shfl_sync(DAWN_FULL, excl, k + step);
+            if (e <= t) k += step;
+          }
+          const uint32_t ek = __shfl_sync(DAWN_FULL, excl, k);
+          const uint32_t sk = __shfl_sync(DAWN_FULL, rs, k);
+          if (t < total) {
+            part_claim(p, (uint32_t)ld_nc(p.col + sk + (t - ek)), L1, n_new, m_new);
+            ++exam;
+          }
+        }
+      }
+    }
+    // (b) heavy out-slice rows: static pieces; warp w takes pieces w + k * nwarps, 32 tested at
+    //     once against F_L, then each live piece is expanded 32 arcs per round
+    const uint32_t hend = p.ctrl->n_hp[0];
+    for (uint32_t pb = gwarp; pb < hend; pb += 32 * nwarps) {
+      const uint32_t pcl = pb + lane * nwarps;
+      const bool live = pcl < hend && part_ftest(p, ld_nc(p.hout_v + pcl));
+      uint32_t lm = __ballot_sync(DAWN_FULL, live);
+      while (lm) {
+        const uint32_t kk = __ffs(lm) - 1;
+        lm &= lm - 1;
+        const uint32_t pc = pb + kk * nwarps;
+        const uint32_t s = ld_nc(p.hout_s + pc), e = ld_nc(p.hout_e + pc);
+        for (uint32_t j = s + lane; j < e; j += 32) {
+          part_claim(p, (uint32_t)ld_nc(p.col + j), L1, n_new, m_new);
+          ++exam;
+        }
+      }
+    }
+  } else {
+    // (a) light in-rows: a warp takes one vis word (32 owned vertices, one lane each) and scans
+    //     each unreached vertex's in-row until the first in-neighbour in F_L (early exit, Eq. 4)
+    const uint32_t nwo = (p.R + 31) / 32;
+    for (uint32_t w = gwarp; w < nwo; w += nwarps) {
+      const uint32_t t = w * 32 + lane;
+      const uint32_t vw = ld_cg(p.vis + w), hw = ld_nc(p.hin_bits + w);
+      bool found = false;
+      if (t < p.R && !((vw >> lane) & 1u) && !((hw >> lane) & 1u)) {
+        const uint32_t s = ld_nc(p.irp + t), e = ld_nc(p.irp + t + 1);
+        for (uint32_t j = s; j < e && !found; j += 4) {
+          uint32_t v[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) v[i] = (j + i < e) ? (uint32_t)ld_nc(p.icol + j + i) : 0xffffffffu;
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            if (!found && v[i] != 0xffffffffu) {
+              ++exam;
+              found = part_ftest(p, v[i]);
+            }
+          }
+        }
+      }
+      if (found) {
+        red_or(p.vis + w, 1u << lane);  // light rows: this lane alone settles t
+        part_discover(p, t, L1, n_new, m_new);
+      }
+    }
+    // (b) heavy in-rows: static pieces, 32 in-edges per round, stop at the first hit or once
+    //     another piece settled the vertex
+    const uint32_t hend = p.ctrl->n_hp[1];
+    for (uint32_t pb = gwarp; pb < hend; pb += 32 * nwarps) {
+      const uint32_t pcl = pb + lane * nwarps;
+      uint32_t tl = 0;
+      bool need = false;
+      if (pcl < hend) {
+        tl = ld_nc(p.hin_v + pcl);
+        need = !((ld_cg(p.vis + (tl >> 5)) >> (tl & 31)) & 1u);
+      }
+      uint32_t nm = __ballot_sync(DAWN_FULL, need);
+      while (nm) {
+        const uint32_t kk = __ffs(nm) - 1;
+        nm &= nm - 1;
+        const uint32_t pc = pb + kk * nwarps;
+        const uint32_t t = __shfl_sync(DAWN_FULL, tl, kk);
+        const uint32_t s = ld_nc(p.hin_s + pc), e = ld_nc(p.hin_e + pc);
+        for (uint32_t j = s; j < e; j += 32) {
+          const uint32_t jj = j + lane;
+          const bool hit = jj < e && part_ftest(p, (uint32_t)ld_nc(p.icol + jj));
+          const uint32_t hm = __ballot_sync(DAWN_FULL, hit);
+          if (hm) {
+            if (lane == 0) {
+              exam += __ffs(hm);
+              const uint32_t w = t >> 5, bit = 1u << (t & 31);
+              if (!(atomicOr(p.vis + w, bit) & bit)) part_discover(p, t, L1, n_new, m_new);
+            }
+            break;
+          }
+          if (lane == 0) exam += min(32u, e - j);
+          if ((ld_cg(p.vis + (t >> 5)) >> (t & 31)) & 1u) break;
+        }
+      }
+    }
+  }
+  // counters of F_{L+1} (this rank) and the examined entries
+  n_new = warp_sum(n_new);
+  m_new = warp_sum(m_new);
+  exam = warp_sum(exam);
+  if (lane == 0) {
+    if (n_new) atomicAdd(&red[0], (unsigned long long)n_new);
+    if (m_new) atomicAdd(&red[1], m_new);
+    if (exam) atomicAdd(&red[2], exam);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (red[0]) atomicAdd(p.send, (uint32_t)red[0]);
+    if (red[1]) atomicAdd(reinterpret_cast<unsigned long long *>(p.send + 2), red[1]);
+    if (red[2]) atomicAdd(&p.ctrl->examined, red[2]);
+  }
+}
+
+// dawn_part_finish: the distance slice from the deferred bytes (as dist_final), statistics.
+__global__ void k_part_finish(PartParams p, uint32_t parity, dawn_sssp_stats *stats) {
+  const uint32_t gtid = blockIdx.x * blockDim.x + threadIdx.x, nth = gridDim.x * blockDim.x;
+  for (uint32_t t = gtid; t < p.R; t += nth) {
+    const uint32_t reached = (ld_cg(p.vis + (t >> 5)) >> (t & 31)) & 1u;
+    const uint32_t d = (t == p.src_local) ? 0u : (reached ? (uint32_t)ld_cg(reinterpret_cast<const uint32_t *>(p.lev) + (t >> 2)) >> (8 * (t & 3)) & 0xffu : kUnreached);
+    if (d != 255u) p.dist[t] = d;
+  }
+  if (gtid == 0 && stats) {
+    const PartState s = p.ctrl->st[parity];
+    dawn_sssp_stats o;
+    o.levels = s.ecc;
+    o.reached = s.reached;
+    o.edges_reach = s.explored;
+    o.edges_examined = p.ctrl->examined;
+    o.push_levels = s.push_levels;
+    o.pull_levels = s.pull_levels;
+    *stats = o;
+  }
+}
+
+}  // namespace dawn
