@@ -561,6 +561,59 @@ def run_apsp(args, rank, world, dev, steps, warmup, with_cpu=False):
     return res
 
 
+def run_part(args, rank, world, dev, cfg="C4", nsrc=8, steps=3):
+    """NEXT-3: single-source searches over the vertex-partitioned graph (each rank holds only the
+    arcs into its vertex range; one frontier-slice all-gather per level, NCCL at N > 1).  A step =
+    `nsrc` searches one after the other; time = max over ranks; strong scaling (the same search
+    on more GPUs)."""
+    import torch
+    import torch.distributed as tdist
+    import paper_2208_04514_b200 as dawn
+
+    g = graphgen.config_graph(cfg)
+    t0 = time.time()
+    pg = dawn.PartGraph(dawn.part_build(g.row_ptr, g.col, world, rank), world, rank, device=dev)
+    t_build = time.time() - t0
+    srcs = sources_for(g, cfg, 0, nsrc)  # the same sources on every rank
+    out = torch.empty(max(1, pg.R), dtype=torch.int32, device=dev)
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(int(2.2 * L2_BYTES) // 4, dtype=torch.int32, device=dev)
+    er = []
+    for s in srcs:  # E10 counts (global, identical on every rank) + warm-up
+        _, st = dawn.part_sssp(pg, int(s), args.variant, out=out, stats=True)
+        er.append(dawn.stats_to_dict(st)["edges_reach"])
+    ms = []
+    for _ in range(steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        if world > 1:
+            tdist.barrier()
+        a, b = _events()
+        a.record(stream)
+        for s in srcs:
+            dawn.part_sssp(pg, int(s), args.variant, out=out)
+        b.record(stream)
+        torch.cuda.synchronize()
+        ms.append(a.elapsed_time(b))
+    tot = sum(ms)
+    if world > 1:
+        t = torch.tensor([tot], dtype=torch.float64, device=dev)
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+        tot = float(t.item())
+    part_bytes = (pg.workspace.numel() + 8 * (pg.out_rp.numel() + pg.in_rp.numel()) +
+                  4 * (pg.out_col.numel() + pg.in_col.numel() + pg.deg.numel()))
+    res = {"value": float(sum(er)) * steps / (tot * 1e-3) / 1e9, "unit": "GTEPS",
+           "workload": f"{cfg}: {CONFIG_TEXT[cfg]}, {len(srcs)} sources, vertex-partitioned over "
+                       f"{world} rank(s)",
+           "ms_per_search": tot / (steps * len(srcs)), "ranks": world, "scaling": "strong",
+           "device_bytes_per_rank": int(part_bytes), "partition_build_s": t_build,
+           "how": "dawn_part_begin / (all-gather + dawn_part_step) per level / dawn_part_finish; "
+                  "the host tests convergence every 4 levels; L2 flushed between steps"}
+    del pg, out, flush
+    torch.cuda.empty_cache()
+    return res
+
+
 def run_dawn(args):
     import torch
     rank, world, local = dist_setup(args.gpus)
@@ -614,6 +667,9 @@ def run_dawn(args):
             ex["C5"] = run_apsp(args, rank, world, dev, max(2, min(args.steps, 5)), 2,
                                 with_cpu=not args.no_cpu)
             res["configs"] = ex
+    if args.extra and world >= 1:
+        # NEXT-3: the same C4 searches over the vertex-partitioned graph (W = N ranks)
+        res["partitioned_sssp"] = run_part(args, rank, world, dev)
     if world > 1:
         import torch.distributed as tdist
         tdist.barrier()

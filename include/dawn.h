@@ -179,6 +179,11 @@ typedef enum {
                                       independent).  1 .. 4 (n <= 2^22) or
                                       1 .. 2 (larger n; 1 with DAWN_GRAPH_LEAN).  Default set at
                                       load from B200 measurements.              */
+  DAWN_PARAM_MS_LANES = 11,        /* dawn_msssp / dawn_apsp / dawn_apsp_rows run this many
+                                      256-source batches at once, each on 1/lanes of the SMs with
+                                      its own bit-parallel state and stream (independent sources,
+                                      PAPER L303-308).  1 .. 3 for n <= 2^22, else 1.  Default
+                                      set at load from B200 measurements.      */
   DAWN_PARAM_DENSE_MAX_ENTRIES = 10 /* dense distance outputs (dawn_msssp dist, one piece of
                                       dawn_apsp_rows) are refused with DAWN_ERR_CAPACITY when
                                       rows * n >= this ("dense-matrix mode refused

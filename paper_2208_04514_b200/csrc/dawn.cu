@@ -47,6 +47,7 @@ constexpr int64_t kOneCtaMaxNM = 1 << 15;  // n + m this small: one CTA, barrier
 constexpr int kMsBlocksPerSm = 2;          // k_ms64 CTAs per SM (if they fit)
 constexpr uint32_t kNarrowQcapMax = 1u << 20;
 // dawn_sssp_batch lanes (concurrent searches) by default: measured on B200
+constexpr int kDefaultMsLanes = DAWN_MS_LANES;  // multi-source lanes (B200 measurement)
 int kDefaultLanes(int64_t n) { return n <= (int64_t(1) << 22) ? 2 : 1; }
 
 // ---------------------------------------------------------------- graph residency kernels
@@ -325,6 +326,7 @@ struct dawn_graph_s {
   uint32_t seq = 0;
   bool lean = false;             // DAWN_GRAPH_LEAN: no ms64 words / icol2 / augmented arcs
   int lanes = 1;                 // DAWN_PARAM_BATCH_LANES (<= L.nlanes)
+  int ms_lanes = 1;               // DAWN_PARAM_MS_LANES (<= L.ms_nlanes)
   double dense_max = 1099511627776.0;  // DAWN_PARAM_DENSE_MAX_ENTRIES (k*n of a dense output)
   // lane streams / fork-join events of dawn_sssp_batch (created at load, host resources only)
   cudaStream_t lane_st[kMaxLanes] = {};
@@ -484,7 +486,7 @@ dawn_status load_csr(int64_t n, int64_t m, const int64_t *row_ptr, const int32_t
     cudaMemsetAsync(g->ws + L.lane[l].ctrl, 0, sizeof(Ctrl), st);
     cudaMemsetAsync(g->ws + L.lane[l].cand, 0, 4 * (size_t)nwords, st);  // zero between uses
   }
-  cudaMemsetAsync(g->ws + L.msctrl, 0, sizeof(MsCtrl), st);
+  for (int l = 0; l < L.ms_nlanes; ++l) cudaMemsetAsync(g->ws + L.ms[l].msctrl, 0, sizeof(MsCtrl), st);
   if (flags & DAWN_GRAPH_VALIDATE) {
     k_validate<<<blocks, 256, 0, st>>>(row_ptr, col, n, m, &at<Ctrl>(g, L.ctrl)->err);
     if (!sym && has_csc && m > 0)
@@ -596,6 +598,7 @@ dawn_status load_csr(int64_t n, int64_t m, const int64_t *row_ptr, const int32_t
       ok = cudaStreamCreateWithFlags(&g->lane_st[l], cudaStreamNonBlocking) == cudaSuccess &&
            cudaEventCreateWithFlags(&g->ev_join[l], cudaEventDisableTiming) == cudaSuccess;
     g->lanes = ok ? std::min(L.nlanes, kDefaultLanes(n)) : 1;
+    g->ms_lanes = ok ? std::min(L.ms_nlanes, kDefaultMsLanes) : 1;
   }
   if ((e = cudaStreamSynchronize(st)) != cudaSuccess) { delete g; return cuda_fail(e, "graph load"); }
   if ((e = cudaGetLastError()) != cudaSuccess) { delete g; return cuda_fail(e, "graph load"); }
@@ -623,6 +626,11 @@ dawn_status set_param(dawn_graph g, dawn_param key, double value) {
       if (value < 1 || value > g->L.nlanes || (value > 1 && !g->ev_fork))
         return fail(DAWN_ERR_INVALID_ARGUMENT, "batch lanes must be in [1, %d]", g->L.nlanes);
       g->lanes = (int)value;
+      break;
+    case DAWN_PARAM_MS_LANES:
+      if (value < 1 || value > g->L.ms_nlanes || (value > 1 && !g->ev_fork))
+        return fail(DAWN_ERR_INVALID_ARGUMENT, "multi-source lanes must be in [1, %d]", g->L.ms_nlanes);
+      g->ms_lanes = (int)value;
       break;
     case DAWN_PARAM_DENSE_MAX_ENTRIES:
       if (value < 1) return fail(DAWN_ERR_INVALID_ARGUMENT, "dense limit must be >= 1");
@@ -859,53 +867,84 @@ dawn_status graph_check(dawn_graph g, void *stream) {
   return DAWN_OK;
 }
 
+// One k_ms64 launch of lane `l` over cnt sources (its own state; grid = its share of the SMs).
+dawn_status launch_ms_lane(dawn_graph g, int l, const uint32_t *src, size_t cnt, size_t off,
+                           uint32_t *dist, dawn_record *rec, int grid, cudaStream_t st) {
+  const Layout &L = g->L;
+  const MsLaneLayout &Q = L.ms[l];
+  cudaError_t e = cudaMemcpyAsync(g->ws + Q.srcbuf, src, 4 * cnt, cudaMemcpyHostToDevice, st);
+  if (e != cudaSuccess) return cuda_fail(e, "source upload");
+  MsParams p{};
+  p.n = (uint32_t)g->n;
+  p.nwords = (uint32_t)((g->n + 31) / 32);
+  p.m = (unsigned long long)g->m;
+  p.rp = at<uint32_t>(g, L.rp);
+  p.irp = at<uint32_t>(g, L.irp);
+  p.col = g->col;
+  p.icol = g->icol;
+  p.hout_v = at<uint32_t>(g, L.hout.v);
+  p.hout_s = at<uint32_t>(g, L.hout.s);
+  p.hout_e = at<uint32_t>(g, L.hout.e);
+  p.hout_bits = at<uint32_t>(g, L.hout.bits);
+  p.hin_v = at<uint32_t>(g, L.hin.v);
+  p.hin_s = at<uint32_t>(g, L.hin.s);
+  p.hin_e = at<uint32_t>(g, L.hin.e);
+  p.hin_bits = at<uint32_t>(g, L.hin.bits);
+  p.sctrl = at<Ctrl>(g, L.ctrl);
+  p.seen = at<unsigned long long>(g, Q.seen);
+  p.F[0] = at<unsigned long long>(g, Q.F0);
+  p.F[1] = at<unsigned long long>(g, Q.F1);
+  p.nxt = at<unsigned long long>(g, Q.nxt);
+  p.ctrl = at<MsCtrl>(g, Q.msctrl);
+  p.sources = at<uint32_t>(g, Q.srcbuf);
+  p.count = (uint32_t)cnt;
+  p.rec = rec ? rec + off : nullptr;
+  p.dist = dist ? dist + off * (size_t)g->n : nullptr;
+  p.can_pull = g->has_csc ? 1u : 0u;
+  p.sym = (g->flags & DAWN_GRAPH_SYMMETRIC) ? 1u : 0u;
+  p.ms_alpha = g->ms_alpha;
+  p.part = at<uint4>(g, Q.part);
+  p.trace = (g->trace && l == 0) ? at<TraceRec>(g, L.trace) : nullptr;
+  p.trace_n = &at<Ctrl>(g, L.ctrl)->trace_n;
+  void *args[] = {&p};
+  e = cudaLaunchCooperativeKernel((const void *)k_ms64<kNT>, dim3(grid), dim3(kNT), args,
+                                  ms_smem_bytes(kNT), st);
+  if (e != cudaSuccess) return cuda_fail(e, "k_ms64 launch");
+  return DAWN_OK;
+}
+
 dawn_status launch_ms(dawn_graph g, const std::vector<uint32_t> &src, uint32_t *dist,
                       dawn_record *rec, cudaStream_t st) {
   const Layout &L = g->L;
   const size_t chunk = (L.srccap / kMsBatch) * kMsBatch;
   for (size_t off = 0; off < src.size(); off += chunk) {
     const size_t cnt = std::min(src.size() - off, chunk);
-    cudaError_t e = cudaMemcpyAsync(g->ws + L.srcbuf, src.data() + off, 4 * cnt,
-                                    cudaMemcpyHostToDevice, st);
-    if (e != cudaSuccess) return cuda_fail(e, "source upload");
-    MsParams p{};
-    p.n = (uint32_t)g->n;
-    p.nwords = (uint32_t)((g->n + 31) / 32);
-    p.m = (unsigned long long)g->m;
-    p.rp = at<uint32_t>(g, L.rp);
-    p.irp = at<uint32_t>(g, L.irp);
-    p.col = g->col;
-    p.icol = g->icol;
-    p.hout_v = at<uint32_t>(g, L.hout.v);
-    p.hout_s = at<uint32_t>(g, L.hout.s);
-    p.hout_e = at<uint32_t>(g, L.hout.e);
-    p.hout_bits = at<uint32_t>(g, L.hout.bits);
-    p.hin_v = at<uint32_t>(g, L.hin.v);
-    p.hin_s = at<uint32_t>(g, L.hin.s);
-    p.hin_e = at<uint32_t>(g, L.hin.e);
-    p.hin_bits = at<uint32_t>(g, L.hin.bits);
-    p.sctrl = at<Ctrl>(g, L.ctrl);
-    p.seen = at<unsigned long long>(g, L.seen);
-    p.F[0] = at<unsigned long long>(g, L.F0);
-    p.F[1] = at<unsigned long long>(g, L.F1);
-    p.nxt = at<unsigned long long>(g, L.nxt);
-    p.ctrl = at<MsCtrl>(g, L.msctrl);
-    p.sources = at<uint32_t>(g, L.srcbuf);
-    p.count = (uint32_t)cnt;
-    p.rec = rec ? rec + off : nullptr;
-    p.dist = dist ? dist + off * (size_t)g->n : nullptr;
-    p.can_pull = g->has_csc ? 1u : 0u;
-    p.sym = (g->flags & DAWN_GRAPH_SYMMETRIC) ? 1u : 0u;
-    p.ms_alpha = g->ms_alpha;
-    p.part = at<uint4>(g, L.part);
-    p.trace = g->trace ? at<TraceRec>(g, L.trace) : nullptr;
-    p.trace_n = &at<Ctrl>(g, L.ctrl)->trace_n;
-    int grid = g->ms_grid;
-    if (g->m + g->n <= kOneCtaMaxNM) grid = 1;
-    void *args[] = {&p};
-    e = cudaLaunchCooperativeKernel((const void *)k_ms64<kNT>, dim3(grid), dim3(kNT), args,
-                                    ms_smem_bytes(kNT), st);
-    if (e != cudaSuccess) return cuda_fail(e, "k_ms64 launch");
+    const size_t nb = (cnt + kMsBatch - 1) / kMsBatch;
+    int lanes = (g->trace || g->m + g->n <= kOneCtaMaxNM) ? 1 : (int)std::min<size_t>(g->ms_lanes, nb);
+    if (lanes > 1 && !g->ev_fork) lanes = 1;
+    if (lanes == 1) {
+      int grid = g->ms_grid;
+      if (g->m + g->n <= kOneCtaMaxNM) grid = 1;
+      dawn_status s = launch_ms_lane(g, 0, src.data() + off, cnt, off, dist, rec, grid, st);
+      if (s != DAWN_OK) return s;
+      continue;
+    }
+    // independent batches at once: lane l runs the contiguous batch share
+    // [nb*l/lanes, nb*(l+1)/lanes) on grid/lanes CTAs with its own state and stream
+    cudaError_t e = cudaEventRecord(g->ev_fork, st);
+    for (int l = 1; l < lanes && e == cudaSuccess; ++l) e = cudaStreamWaitEvent(g->lane_st[l], g->ev_fork, 0);
+    if (e != cudaSuccess) return cuda_fail(e, "ms fork");
+    for (int l = 0; l < lanes; ++l) {
+      const size_t b0 = nb * l / lanes * kMsBatch, b1 = std::min(cnt, nb * (l + 1) / lanes * kMsBatch);
+      dawn_status s = launch_ms_lane(g, l, src.data() + off + b0, b1 - b0, off + b0, dist, rec,
+                                     std::max(1, g->ms_grid / lanes), l ? g->lane_st[l] : st);
+      if (s != DAWN_OK) return s;
+    }
+    for (int l = 1; l < lanes && e == cudaSuccess; ++l) {
+      e = cudaEventRecord(g->ev_join[l], g->lane_st[l]);
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(st, g->ev_join[l], 0);
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "ms join");
   }
   return DAWN_OK;
 }
@@ -1129,11 +1168,16 @@ dawn_status ms_counters(dawn_graph g, uint64_t *host_out, void *stream) {
   dawn_status s = set_device(g);
   if (s != DAWN_OK) return s;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  MsCtrl *C = at<MsCtrl>(g, g->L.msctrl);
-  cudaError_t e = cudaMemcpyAsync(host_out, C->stat, sizeof(C->stat), cudaMemcpyDeviceToHost, st);
-  if (e == cudaSuccess) e = cudaMemsetAsync(C->stat, 0, sizeof(C->stat), st);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-  if (e != cudaSuccess) return cuda_fail(e, "dawn_graph_ms_counters");
+  for (int i = 0; i < 4; ++i) host_out[i] = 0;
+  for (int l = 0; l < g->L.ms_nlanes; ++l) {  // summed over the multi-source lanes
+    MsCtrl *C = at<MsCtrl>(g, g->L.ms[l].msctrl);
+    uint64_t part[4] = {0, 0, 0, 0};
+    cudaError_t e = cudaMemcpyAsync(part, C->stat, sizeof(C->stat), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(C->stat, 0, sizeof(C->stat), st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return cuda_fail(e, "dawn_graph_ms_counters");
+    for (int i = 0; i < 4; ++i) host_out[i] += part[i];
+  }
   return DAWN_OK;
 }
 

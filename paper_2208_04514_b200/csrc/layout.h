@@ -148,14 +148,27 @@ struct HeavyList {  // static pieces of rows with degree > kHeavy
 // stream) run independent searches of one batch at the same time (sources are
 // independent).  Lane 0 is the state every other call uses.
 constexpr int kMaxLanes = 4;
+constexpr int kMsMaxLanes = 3;
+#ifndef DAWN_MS_LANES
+#define DAWN_MS_LANES 3  // default multi-source lanes (C5: 1 -> 707K, 2 -> 815K, 3 -> 829K sources/s)
+#endif  // multi-source lanes allocated (<= kMaxLanes)
 struct LaneLayout {
   size_t vis, cand, fb[3], Lv[2], Lsd[2], Cf[2], ctrl, ulist, useg;
+};
+
+// Multi-source lanes: the bit-parallel kernel's per-batch state, replicated so that several
+// k_ms64 launches (one per lane, each on its own share of the SMs and its own stream) run
+// different 256-source batches of one msssp / apsp call at the same time.
+struct MsLaneLayout {
+  size_t seen, F0, F1, nxt, msctrl, part, srcbuf;
 };
 
 struct Layout {
   size_t rp, irp, noin, vis, cand, fb[3], Lv[2], Lsd[2], Cf[2], ctrl, trace;
   LaneLayout lane[kMaxLanes];
   int nlanes;
+  MsLaneLayout ms[kMaxLanes];
+  int ms_nlanes;
   HeavyList hout, hin;
   size_t scan_tmp, piece_tmp, hasin, ulist, useg, icol2, arc;
   size_t seen, F0, F1, nxt, msctrl, part, srcbuf, total;
@@ -210,14 +223,28 @@ inline Layout make_layout(int64_t n, int64_t m, uint32_t flags) {
            (uint64_t)m <= (uint64_t)kNarrowMaxAvgDeg * (uint64_t)n)
               ? take(16 * (size_t)m) : 0;
   L.msctrl = take(sizeof(MsCtrl));
+  L.srccap = (uint64_t)(n > 65536 ? n : 65536);
   if (!lean) {
     L.seen = take(8 * kMsW * (size_t)n);
     L.F0 = take(8 * kMsW * (size_t)n);
     L.F1 = take(8 * kMsW * (size_t)n);
     L.nxt = take(8 * kMsW * (size_t)n);
     L.part = take(sizeof(uint32_t) * 4 * kMsBatch * 2 * kMaxBlocks);
-    L.srccap = (uint64_t)(n > 65536 ? n : 65536);
     L.srcbuf = take(4 * L.srccap);
+  }
+  L.ms[0] = MsLaneLayout{L.seen, L.F0, L.F1, L.nxt, L.msctrl, L.part, L.srcbuf};
+  // extra multi-source lanes up to 2^22 vertices (their 4 x 32-byte words per vertex stay
+  // L2-resident next to the graph), none in lean mode
+  L.ms_nlanes = lean ? 1 : ((uint64_t)n <= (1ull << 22) ? kMsMaxLanes : 1);
+  for (int l = 1; l < L.ms_nlanes; ++l) {
+    MsLaneLayout &q = L.ms[l];
+    q.seen = take(8 * kMsW * (size_t)n);
+    q.F0 = take(8 * kMsW * (size_t)n);
+    q.F1 = take(8 * kMsW * (size_t)n);
+    q.nxt = take(8 * kMsW * (size_t)n);
+    q.msctrl = take(sizeof(MsCtrl));
+    q.part = take(sizeof(uint32_t) * 4 * kMsBatch * 2 * kMaxBlocks);
+    q.srcbuf = take(4 * L.srccap);
   }
   // extra lanes (lane 0 = the arrays above): not in lean mode; 4 lanes up to 2^22 vertices
   // (latency-bound searches overlap best), 2 above
