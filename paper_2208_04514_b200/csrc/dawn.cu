@@ -1141,12 +1141,13 @@ dawn_status largest_wcc(dawn_graph g, int64_t *sources_out, int64_t *k, uint64_t
                                                     at<uint32_t>(g, L.hout.e), &C->n_hp_out,
                                                     g->col, par);
   }
-  k_wcc_count<<<blocks, 256, 0, st>>>(at<uint32_t>(g, L.rp), n, par, cnt, arcc);
+  uint32_t *lab = reinterpret_cast<uint32_t *>(g->ws + L.Lsd[1]);  // final component labels
+  k_wcc_count<<<blocks, 256, 0, st>>>(at<uint32_t>(g, L.rp), n, par, lab, cnt, arcc);
   for (int pass = 0; pass < 3; ++pass)
-    k_wcc_select<<<blocks, 256, 0, st>>>(par, cnt, arcc, n, pass, C);
-  k_wcc_bcount<<<nblk, 256, 0, st>>>(par, n, C, at<uint32_t>(g, L.scan_tmp));
+    k_wcc_select<<<blocks, 256, 0, st>>>(lab, cnt, arcc, n, pass, C);
+  k_wcc_bcount<<<nblk, 256, 0, st>>>(lab, n, C, at<uint32_t>(g, L.scan_tmp));
   k_hscan<<<1, 32, 0, st>>>(at<uint32_t>(g, L.scan_tmp), nblk, &C->wcc_k);
-  k_wcc_bfill<<<nblk, 256, 0, st>>>(par, n, C, at<uint32_t>(g, L.scan_tmp), list);
+  k_wcc_bfill<<<nblk, 256, 0, st>>>(lab, n, C, at<uint32_t>(g, L.scan_tmp), list);
   uint32_t hdr[3] = {0, 0, 0};  // wcc_cnt, wcc_arcs, wcc_root
   cudaError_t e = cudaMemcpyAsync(hdr, &C->wcc_cnt, 12, cudaMemcpyDeviceToHost, st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);

@@ -85,6 +85,12 @@ constexpr uint32_t kDirectRow = 256;
 #ifndef DAWN_HEAVY_ILP
 #define DAWN_HEAVY_ILP 1     // in-edges per lane in flight when a warp scans a heavy pull piece
 #endif
+#ifndef DAWN_NOVIS
+#define DAWN_NOVIS 1       // candidate push levels skip the visited read while few are settled
+#endif
+#ifndef DAWN_NOVIS_FRAC
+#define DAWN_NOVIS_FRAC 32  // ... while (reached + 1) * FRAC < reachable vertices (C4 1325 -> 1350 GTEPS; 8: forced push C2 -9%)
+#endif
 #ifndef DAWN_PULL_J
 #define DAWN_PULL_J 2  // vis words per warp iteration of the pull sweep (independent scans)
 #endif
@@ -148,9 +154,9 @@ struct HeavyList {  // static pieces of rows with degree > kHeavy
 // stream) run independent searches of one batch at the same time (sources are
 // independent).  Lane 0 is the state every other call uses.
 constexpr int kMaxLanes = 4;
-constexpr int kMsMaxLanes = 3;
+constexpr int kMsMaxLanes = 4;
 #ifndef DAWN_MS_LANES
-#define DAWN_MS_LANES 3  // default multi-source lanes (C5: 1 -> 707K, 2 -> 815K, 3 -> 829K sources/s)
+#define DAWN_MS_LANES 4  // default multi-source lanes (C5: 1 -> 707K, 2 -> 815K, 3 -> 829K, 4 -> 847K sources/s)
 #endif  // multi-source lanes allocated (<= kMaxLanes)
 struct LaneLayout {
   size_t vis, cand, fb[3], Lv[2], Lsd[2], Cf[2], ctrl, ulist, useg;

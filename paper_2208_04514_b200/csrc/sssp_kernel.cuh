@@ -78,6 +78,7 @@ struct __align__(16) LevelState {
   uint32_t qn, n_hp;            // queue entries of frontier L; static heavy pieces
   uint32_t qe;                  // queue edges of frontier L
   uint32_t big;                 // frontier L (bitmap form) has a row of > kDirectRow arcs
+  uint32_t novis;               // candidate push without the visited-word read (see push_item)
   unsigned long long mf, explored, push_edges, pad;
   uint32_t *drow;               // this search's distance row
 };
@@ -219,7 +220,7 @@ __device__ __forceinline__ void enqueue_frontier(const SsspParams &p, Slot *s, i
 // else 1), processed with all J chains' loads in flight together (memory-level parallelism):
 // Cf[c] -> 32-entry window of (row start, edge offset) -> owner by 5-step shfl search -> col ->
 // vis test-and-set -> rp of the discovered vertex.
-template <int J, bool CAND>
+template <int J, bool CAND, bool NOVIS = false>
 __device__ __forceinline__ void push_item(const SsspParams &p, const LevelState &st, Slot *ns,
                                           uint32_t item, uint32_t &n_new,
                                           unsigned long long &m_new, WarpStage &stg,
@@ -256,8 +257,11 @@ __device__ __forceinline__ void push_item(const SsspParams &p, const LevelState 
     u[j] = act[j] ? (uint32_t)ld_nc(p.col + sk + (t - ok)) : 0u;
   }
   uint32_t cur[J];
+  // candidate levels while few vertices are settled (st.novis): most targets are unvisited, so
+  // the visited-word read (one random L2 sector per arc) is skipped; cand_filter drops the rest
 #pragma unroll
-  for (int j = 0; j < J; ++j) cur[j] = act[j] ? p.vis[u[j] >> 5] : ~0u;  // weak: stale 0 = atomic
+  for (int j = 0; j < J; ++j)
+    cur[j] = (act[j] && !NOVIS) ? p.vis[u[j] >> 5] : (act[j] ? 0u : ~0u);  // weak: stale 0 = atomic
   if constexpr (CAND) {
     // bitmap push: mark the candidate, settle later in cand_filter (no returning atomic)
 #if DAWN_CAND_FILTER
@@ -315,8 +319,13 @@ __device__ void push_level(const SsspParams &p, const LevelState &st, Slot *ns, 
     if (nchunks >= nwarps * DAWN_ILP_CAND) {
       constexpr int JB = DAWN_ILP_CAND;
       const uint32_t items = (nchunks + JB - 1) / JB;
-      for (uint32_t it = gwarp; it < items; it += nwarps)
-        push_item<JB, true>(p, st, ns, it, n_new, m_new, stg, cnt);
+      if (DAWN_NOVIS && st.novis) {
+        for (uint32_t it = gwarp; it < items; it += nwarps)
+          push_item<JB, true, true>(p, st, ns, it, n_new, m_new, stg, cnt);
+      } else {
+        for (uint32_t it = gwarp; it < items; it += nwarps)
+          push_item<JB, true>(p, st, ns, it, n_new, m_new, stg, cnt);
+      }
     } else {
       constexpr int JB = DAWN_ILP_CAND / 2;
       const uint32_t items = (nchunks + JB - 1) / JB;
@@ -704,6 +713,7 @@ __device__ __forceinline__ void level_header(const SsspParams &p, Ctrl *C, Level
     st.bm = (st.dir == kPush && !st.solo &&
              st.mf >= (grows ? (unsigned long long)p.bmpush_grow : (unsigned long long)p.bmpush_e))
                 ? 1u : 0u;
+    st.novis = (st.bm && (unsigned long long)(st.reached + 1) * DAWN_NOVIS_FRAC < max_reach) ? 1u : 0u;
     // sparse frontier (a probe hits with probability ~ m_f / (m_f + m_u) < 1/6): probe 8
     // in-edges per round trip instead of 4
     st.deep = (st.dir == kPull && 6.0 * (double)st.mf < (double)(p.m - st.explored) + (double)st.mf)

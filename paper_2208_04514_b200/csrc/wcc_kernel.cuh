@@ -72,15 +72,25 @@ __global__ void k_wcc_hook_pieces(const uint32_t *__restrict__ hv, const uint32_
   }
 }
 
-// Final labels (root = component minimum) and per-root node / arc counts.  cnt, arcs zeroed.
-__global__ void k_wcc_count(const uint32_t *__restrict__ rp, uint32_t n, uint32_t *par,
-                            uint32_t *cnt, uint32_t *arcs) {
+// Root of x without path compression (the forest is final: no writes, so concurrent readers
+// never see an entry move).
+__device__ __forceinline__ uint32_t wcc_root(const uint32_t *par, uint32_t x) {
+  uint32_t cur = x, next;
+  while ((next = ld_cg(par + cur)) != cur) cur = next;
+  return cur;
+}
+
+// Final labels lab[v] = root (= component minimum) and per-root node / arc counts (cnt, arcs
+// zeroed).  The labels go to a separate array: rewriting par[v] here raced with concurrent
+// path-halving stores of the same entry (a stale ancestor could overwrite the root).
+__global__ void k_wcc_count(const uint32_t *__restrict__ rp, uint32_t n, const uint32_t *par,
+                            uint32_t *__restrict__ lab, uint32_t *cnt, uint32_t *arcs) {
   const uint32_t stride = gridDim.x * blockDim.x;
   for (uint32_t base = blockIdx.x * blockDim.x; base < n; base += stride) {
     const uint32_t v = base + threadIdx.x;
     const bool in = v < n;
-    const uint32_t r = in ? wcc_find(par, v) : 0xffffffffu;
-    if (in) par[v] = r;
+    const uint32_t r = in ? wcc_root(par, v) : 0xffffffffu;
+    if (in) lab[v] = r;
     const uint32_t d = in ? rp[v + 1] - rp[v] : 0u;
     // warp aggregation: one atomic pair per distinct root in the warp (the giant component's
     // root would otherwise take one same-address atomic per vertex).  The __match_any groups
@@ -94,15 +104,15 @@ __global__ void k_wcc_count(const uint32_t *__restrict__ rp, uint32_t n, uint32_
   }
 }
 
-// Selection passes over the roots (par[v] == v).  pass 0: max nodes; pass 1: max arcs among
+// Selection passes over the roots (lab[v] == v).  pass 0: max nodes; pass 1: max arcs among
 // max-node roots; pass 2: min root among those.
-__global__ void k_wcc_select(const uint32_t *__restrict__ par, const uint32_t *__restrict__ cnt,
+__global__ void k_wcc_select(const uint32_t *__restrict__ lab, const uint32_t *__restrict__ cnt,
                              const uint32_t *__restrict__ arcs, uint32_t n, int pass, Ctrl *C) {
   const uint32_t bc = pass > 0 ? ld_cg(&C->wcc_cnt) : 0u;
   const uint32_t ba = pass > 1 ? ld_cg(&C->wcc_arcs) : 0u;
   uint32_t best = pass == 2 ? 0xffffffffu : 0u;
   for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
-    if (par[v] != v) continue;
+    if (lab[v] != v) continue;
     if (pass == 0) best = max(best, cnt[v]);
     else if (pass == 1) { if (cnt[v] == bc) best = max(best, arcs[v]); }
     else if (cnt[v] == bc && arcs[v] == ba) best = min(best, v);
@@ -118,9 +128,9 @@ __global__ void k_wcc_select(const uint32_t *__restrict__ par, const uint32_t *_
   }
 }
 
-// Order-preserving compaction of {v : par[v] == root}: per-block counts, a serial scan of the
+// Order-preserving compaction of {v : lab[v] == root}: per-block counts, a serial scan of the
 // block counts (k_hscan), then each block writes its vertices ascending.
-__global__ void k_wcc_bcount(const uint32_t *__restrict__ par, uint32_t n, const Ctrl *C,
+__global__ void k_wcc_bcount(const uint32_t *__restrict__ lab, uint32_t n, const Ctrl *C,
                              uint32_t *__restrict__ tmp) {
   __shared__ uint32_t sm[32];
   const uint32_t root = ld_cg(&C->wcc_root);
@@ -128,7 +138,7 @@ __global__ void k_wcc_bcount(const uint32_t *__restrict__ par, uint32_t n, const
   uint32_t c = 0;
   for (uint32_t i = threadIdx.x; i < kScanBlock; i += blockDim.x) {
     const uint32_t v = base + i;
-    if (v < n && par[v] == root) ++c;
+    if (v < n && lab[v] == root) ++c;
   }
   c = warp_sum(c);
   if ((threadIdx.x & 31) == 0) sm[threadIdx.x / 32] = c;
@@ -140,7 +150,7 @@ __global__ void k_wcc_bcount(const uint32_t *__restrict__ par, uint32_t n, const
   }
 }
 
-__global__ void k_wcc_bfill(const uint32_t *__restrict__ par, uint32_t n, const Ctrl *C,
+__global__ void k_wcc_bfill(const uint32_t *__restrict__ lab, uint32_t n, const Ctrl *C,
                             const uint32_t *__restrict__ tmp, uint32_t *__restrict__ out) {
   __shared__ uint32_t sm[256];
   constexpr uint32_t kPer = kScanBlock / 256;  // blockDim.x == 256
@@ -148,7 +158,7 @@ __global__ void k_wcc_bfill(const uint32_t *__restrict__ par, uint32_t n, const 
   const uint32_t v0 = blockIdx.x * kScanBlock + threadIdx.x * kPer;
   uint32_t c = 0;
   for (uint32_t i = 0; i < kPer; ++i)
-    if (v0 + i < n && par[v0 + i] == root) ++c;
+    if (v0 + i < n && lab[v0 + i] == root) ++c;
   sm[threadIdx.x] = c;
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -163,7 +173,7 @@ __global__ void k_wcc_bfill(const uint32_t *__restrict__ par, uint32_t n, const 
   uint32_t o = sm[threadIdx.x];
   for (uint32_t i = 0; i < kPer; ++i) {
     const uint32_t v = v0 + i;
-    if (v < n && par[v] == root) out[o++] = v;
+    if (v < n && lab[v] == root) out[o++] = v;
   }
 }
 
