@@ -51,6 +51,9 @@ def _load():
         L.gg_transpose.argtypes = [i64, i64, i64p, i32p, i64p, i32p]
         L.gg_wcc_largest.restype = i64
         L.gg_wcc_largest.argtypes = [i64, i64p, i32p, i32p, ctypes.POINTER(ctypes.c_int64)]
+        L.gg_weights.restype = None
+        L.gg_weights.argtypes = [i64, i64p, i32p, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_int,
+                                 vp]
         L.gg_sample_sources.restype = i64
         L.gg_sample_sources.argtypes = [i64, i64p, i64, ctypes.c_uint64, i32p]
         _lib = L
@@ -95,6 +98,14 @@ class Graph:
         k = L.gg_wcc_largest(self.n, _ptr(self.row_ptr), _ptr(self.col), _ptr(out),
                              ctypes.byref(e))
         return out[:k].copy(), int(e.value)
+
+    def weights(self, seed: int = 1, wmax: int = 255) -> np.ndarray:
+        """Seeded integer arc weights in [1, wmax] aligned with col (uint32[m]); both arcs of a
+        symmetric graph's edge get the same weight."""
+        w = np.empty(self.m, np.uint32)
+        _load().gg_weights(self.n, _ptr(self.row_ptr), _ptr(self.col), seed, wmax,
+                           1 if self.symmetric else 0, _ptr(w))
+        return w
 
     def sample_sources(self, k: int, seed: int = 1) -> np.ndarray:
         """k seeded sources, uniform over vertices with out-degree > 0."""

@@ -326,4 +326,21 @@ int64_t gg_sample_sources(int64_t n, const int64_t *row_ptr, int64_t k, uint64_t
   return k;
 }
 
+// Arc weights for the weighted (min,+) extension: w = 1 + mix64(seed ^ key) % wmax, key = the
+// arc (u << 32 | v), or the unordered pair (min << 32 | max) when `symmetric` so both arcs of an
+// undirected edge carry the same weight (Graph500 SSSP: one weight per edge).  Counter-based:
+// independent of the thread count.
+void gg_weights(int64_t n, const int64_t *row_ptr, const int32_t *col, uint64_t seed,
+                uint32_t wmax, int symmetric, uint32_t *w) {
+  parallel_for(n, [&](int64_t lo, int64_t hi, int) {
+    for (int64_t u = lo; u < hi; ++u)
+      for (int64_t j = row_ptr[u]; j < row_ptr[u + 1]; ++j) {
+        const uint64_t v = (uint64_t)col[j];
+        const uint64_t a = symmetric ? std::min<uint64_t>(u, v) : (uint64_t)u;
+        const uint64_t b = symmetric ? std::max<uint64_t>(u, v) : v;
+        w[j] = 1u + (uint32_t)(mix64(seed ^ ((a << 32) | b)) % (uint64_t)(wmax ? wmax : 1));
+      }
+  });
+}
+
 }  // extern "C"

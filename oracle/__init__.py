@@ -62,6 +62,14 @@ def _load():
         L.oracle_records.argtypes = [i64, vp, vp, i64, vp, ctypes.c_int, vp]
         L.oracle_largest_wcc.restype = ctypes.c_int64
         L.oracle_largest_wcc.argtypes = [i64, vp, vp, vp, ctypes.POINTER(ctypes.c_uint64)]
+        L.oracle_minplus.restype = ctypes.c_int
+        L.oracle_minplus.argtypes = [i64, vp, vp, vp, i64, vp, ctypes.POINTER(_Stats)]
+        L.oracle_dijkstra.restype = ctypes.c_int
+        L.oracle_dijkstra.argtypes = [i64, vp, vp, vp, i64, vp]
+        L.oracle_floyd_warshall_w.restype = ctypes.c_int
+        L.oracle_floyd_warshall_w.argtypes = [i64, vp, vp, vp, vp]
+        L.oracle_certify_w.restype = ctypes.c_int
+        L.oracle_certify_w.argtypes = [i64, vp, vp, vp, i64, vp, ctypes.POINTER(ctypes.c_int64)]
         L.oracle_hash_term.restype = ctypes.c_uint64
         L.oracle_hash_term.argtypes = [ctypes.c_uint32, ctypes.c_uint32]
         _lib = L
@@ -170,3 +178,51 @@ def largest_wcc(n, row_ptr, col):
 
 def hash_term(v: int, d: int) -> int:
     return int(_load().oracle_hash_term(v, d))
+
+
+# ------------------------------------------------------------------ weighted (min,+), NEXT-4
+UNREACHED64 = 0xFFFFFFFFFFFFFFFF
+
+
+def _wcsr(row_ptr, col, w):
+    rp, c = _csr(row_ptr, col)
+    return rp, c, np.ascontiguousarray(w, dtype=np.uint32)
+
+
+def minplus(n, row_ptr, col, w, s):
+    """(min,+) SOVM with synchronous rounds (oracle.c oracle_minplus; reading Q26).
+    Returns (uint64 distances, stats dict)."""
+    rp, c, ww = _wcsr(row_ptr, col, w)
+    d = np.empty(n, np.uint64)
+    st = _Stats()
+    rc = _load().oracle_minplus(n, _p(rp), _p(c), _p(ww), int(s), _p(d), ctypes.byref(st))
+    if rc:
+        raise ValueError(f"oracle_minplus rc={rc}")
+    return d, {f: getattr(st, f) for f, _ in _Stats._fields_}
+
+
+def dijkstra(n, row_ptr, col, w, s):
+    rp, c, ww = _wcsr(row_ptr, col, w)
+    d = np.empty(n, np.uint64)
+    rc = _load().oracle_dijkstra(n, _p(rp), _p(c), _p(ww), int(s), _p(d))
+    if rc:
+        raise ValueError(f"oracle_dijkstra rc={rc}")
+    return d
+
+
+def floyd_warshall_w(n, row_ptr, col, w):
+    rp, c, ww = _wcsr(row_ptr, col, w)
+    D = np.empty((n, n), np.uint64)
+    rc = _load().oracle_floyd_warshall_w(n, _p(rp), _p(c), _p(ww), _p(D))
+    if rc:
+        raise ValueError(f"oracle_floyd_warshall_w rc={rc}")
+    return D
+
+
+def certify_w(n, row_ptr, col, w, s, dist):
+    """0 if dist (uint64) is the exact weighted distance vector from s (weights >= 1)."""
+    rp, c, ww = _wcsr(row_ptr, col, w)
+    d = np.ascontiguousarray(dist, dtype=np.uint64)
+    bad = ctypes.c_int64(-1)
+    rc = _load().oracle_certify_w(n, _p(rp), _p(c), _p(ww), int(s), _p(d), ctypes.byref(bad))
+    return rc, bad.value

@@ -28,6 +28,19 @@
  *                      taken in ascending order; "largest" = most nodes, then most arcs, then the
  *                      smaller minimum id (reading Q15).
  *
+ * Weighted (min,+) extension ("(min,+) operations ... to
+ * expand the applicability of DAWN on weighted graphs"; reading Q26 in DESIGN.md):
+ *   oracle_minplus     Algorithm 2's round structure over the (min,+) semiring with synchronous
+ *                      rounds: alpha = vertices whose distance dropped in the previous round;
+ *                      each round relaxes alpha's out-arcs from the round-start distances and
+ *                      beta = {u : d(u) dropped}; stop when beta is empty (<= n-1 rounds).
+ *   oracle_dijkstra    textbook Dijkstra with a binary heap (independent check).
+ *   oracle_floyd_warshall_w  brute-force weighted all pairs, n <= 512.
+ *   oracle_certify_w   d(s) = 0, d(v) <= d(u) + w(u,v) on every arc, every reached v != s has a
+ *                      tight in-arc, UNREACHED exactly where no in-arc comes from a reached
+ *                      vertex: with weights >= 1 this proves d = delta.
+ *   Distances are uint64 (ORACLE_UNREACHED64 = UINT64_MAX), weights uint32 aligned with col.
+ *
  * Every function is pinned by tests/test_oracle.py against closed forms, brute force, golden
  * records (tests/golden/) or each other; see DESIGN.md "Oracle pins".
  */
@@ -427,4 +440,163 @@ int64_t oracle_largest_wcc(int64_t n, const int64_t *row_ptr, const int32_t *col
   if (arcs_out) *arcs_out = best_arcs;
   free(in_ptr); free(in_src); free(label); free(queue);
   return k;
+}
+
+
+/* ------------------------------------------------------------------ weighted (min,+) */
+#define ORACLE_UNREACHED64 0xFFFFFFFFFFFFFFFFull
+
+/*
+ * (min,+) SOVM, synchronous rounds (reading Q26):
+ *   d_0 = e_s (0 at s, infinity elsewhere); alpha_0 = {s}
+ *   round k: for every v in alpha_k, every arc v -> u:  cand(u) <- min(cand(u), d_k(v) + w)
+ *            d_{k+1}(u) = min(d_k(u), cand(u));  alpha_{k+1} = {u : d_{k+1}(u) < d_k(u)}
+ *   stop when alpha_{k+1} is empty.  st->iterations = rounds that improved >= 1 vertex,
+ *   st->edge_inspections = arcs relaxed.
+ */
+int oracle_minplus(int64_t n, const int64_t *row_ptr, const int32_t *col, const uint32_t *w,
+                   int64_t s, uint64_t *dist, oracle_stats *st) {
+  if (n < 1 || s < 0 || s >= n) return 2;
+  unsigned char *alpha = (unsigned char *)calloc((size_t)n, 1);
+  unsigned char *beta = (unsigned char *)calloc((size_t)n, 1);
+  uint64_t *cand = (uint64_t *)malloc((size_t)n * sizeof(uint64_t));
+  if (!alpha || !beta || !cand) { free(alpha); free(beta); free(cand); return 3; }
+  for (int64_t i = 0; i < n; ++i) dist[i] = ORACLE_UNREACHED64;
+  dist[s] = 0;
+  alpha[s] = 1;
+  oracle_stats S = {0, 0, 0, 0};
+  for (int64_t round = 0; round < n; ++round) {
+    S.rounds++;
+    for (int64_t i = 0; i < n; ++i) cand[i] = ORACLE_UNREACHED64;
+    for (int64_t v = 0; v < n; ++v) {
+      S.node_inspections++;
+      if (!alpha[v]) continue;
+      for (int64_t j = row_ptr[v]; j < row_ptr[v + 1]; ++j) {
+        S.edge_inspections++;
+        const uint64_t c = dist[v] + (uint64_t)w[j];
+        if (c < cand[col[j]]) cand[col[j]] = c;
+      }
+    }
+    int improved = 0;
+    for (int64_t u = 0; u < n; ++u) {
+      beta[u] = 0;
+      if (cand[u] < dist[u]) {
+        dist[u] = cand[u];
+        beta[u] = 1;
+        improved = 1;
+      }
+    }
+    unsigned char *t = alpha;
+    alpha = beta;
+    beta = t;
+    if (!improved) break;
+    S.iterations++;
+  }
+  if (st) *st = S;
+  free(alpha);
+  free(beta);
+  free(cand);
+  return 0;
+}
+
+/* Dijkstra with a binary heap of (distance, vertex); lazy deletion. */
+int oracle_dijkstra(int64_t n, const int64_t *row_ptr, const int32_t *col, const uint32_t *w,
+                    int64_t s, uint64_t *dist) {
+  if (n < 1 || s < 0 || s >= n) return 2;
+  const int64_t cap = row_ptr[n] + 1;
+  uint64_t *hk = (uint64_t *)malloc((size_t)cap * sizeof(uint64_t));
+  int64_t *hv = (int64_t *)malloc((size_t)cap * sizeof(int64_t));
+  unsigned char *done = (unsigned char *)calloc((size_t)n, 1);
+  if (!hk || !hv || !done) { free(hk); free(hv); free(done); return 3; }
+  for (int64_t i = 0; i < n; ++i) dist[i] = ORACLE_UNREACHED64;
+  dist[s] = 0;
+  int64_t hn = 0;
+  hk[0] = 0; hv[0] = s; hn = 1;
+  while (hn > 0) {
+    const uint64_t k = hk[0];
+    const int64_t v = hv[0];
+    hn--;  /* pop: move the last entry to the root and sift down */
+    hk[0] = hk[hn]; hv[0] = hv[hn];
+    for (int64_t i = 0;;) {
+      int64_t l = 2 * i + 1, r = l + 1, m = i;
+      if (l < hn && hk[l] < hk[m]) m = l;
+      if (r < hn && hk[r] < hk[m]) m = r;
+      if (m == i) break;
+      uint64_t tk = hk[i]; hk[i] = hk[m]; hk[m] = tk;
+      int64_t tv = hv[i]; hv[i] = hv[m]; hv[m] = tv;
+      i = m;
+    }
+    if (done[v] || k != dist[v]) continue;
+    done[v] = 1;
+    for (int64_t j = row_ptr[v]; j < row_ptr[v + 1]; ++j) {
+      const int64_t u = col[j];
+      const uint64_t c = k + (uint64_t)w[j];
+      if (c < dist[u]) {
+        dist[u] = c;
+        int64_t i = hn++;  /* push and sift up */
+        hk[i] = c; hv[i] = u;
+        while (i > 0) {
+          int64_t p = (i - 1) / 2;
+          if (hk[p] <= hk[i]) break;
+          uint64_t tk = hk[i]; hk[i] = hk[p]; hk[p] = tk;
+          int64_t tv = hv[i]; hv[i] = hv[p]; hv[p] = tv;
+          i = p;
+        }
+      }
+    }
+  }
+  free(hk);
+  free(hv);
+  free(done);
+  return 0;
+}
+
+/* Weighted Floyd-Warshall, n <= 512: D[i*n + j]; parallel arcs take the lightest. */
+int oracle_floyd_warshall_w(int64_t n, const int64_t *row_ptr, const int32_t *col,
+                            const uint32_t *w, uint64_t *D) {
+  if (n < 1 || n > 512) return 2;
+  for (int64_t i = 0; i < n * n; ++i) D[i] = ORACLE_UNREACHED64;
+  for (int64_t i = 0; i < n; ++i) {
+    D[i * n + i] = 0;
+    for (int64_t j = row_ptr[i]; j < row_ptr[i + 1]; ++j)
+      if (col[j] != i && (uint64_t)w[j] < D[i * n + col[j]]) D[i * n + col[j]] = w[j];
+  }
+  for (int64_t k = 0; k < n; ++k)
+    for (int64_t i = 0; i < n; ++i) {
+      if (D[i * n + k] == ORACLE_UNREACHED64) continue;
+      for (int64_t j = 0; j < n; ++j)
+        if (D[k * n + j] != ORACLE_UNREACHED64 && D[i * n + k] + D[k * n + j] < D[i * n + j])
+          D[i * n + j] = D[i * n + k] + D[k * n + j];
+    }
+  return 0;
+}
+
+/* Certificate of a weighted distance vector (weights >= 1).  Returns 0 if valid, else the
+ * number of the first failing condition; *bad = the offending vertex. */
+int oracle_certify_w(int64_t n, const int64_t *row_ptr, const int32_t *col, const uint32_t *w,
+                     int64_t s, const uint64_t *dist, int64_t *bad) {
+  *bad = -1;
+  if (dist[s] != 0) { *bad = s; return 1; }
+  unsigned char *tight = (unsigned char *)calloc((size_t)n, 1);
+  unsigned char *fed = (unsigned char *)calloc((size_t)n, 1);
+  if (!tight || !fed) { free(tight); free(fed); return 9; }
+  int rc = 0;
+  for (int64_t u = 0; u < n && !rc; ++u) {
+    if (dist[u] == ORACLE_UNREACHED64) continue;
+    for (int64_t j = row_ptr[u]; j < row_ptr[u + 1]; ++j) {
+      const int64_t v = col[j];
+      const uint64_t c = dist[u] + (uint64_t)w[j];
+      fed[v] = 1;
+      if (dist[v] > c) { *bad = v; rc = 2; break; }        /* (ii) relaxed arc violated */
+      if (dist[v] == c && v != s) tight[v] = 1;
+    }
+  }
+  for (int64_t v = 0; v < n && !rc; ++v) {
+    if (v == s) continue;
+    if (dist[v] != ORACLE_UNREACHED64 && !tight[v]) { *bad = v; rc = 3; }   /* (iii) */
+    else if (dist[v] == ORACLE_UNREACHED64 && fed[v]) { *bad = v; rc = 4; } /* (iv) */
+  }
+  free(tight);
+  free(fed);
+  return rc;
 }
