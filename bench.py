@@ -603,13 +603,52 @@ def run_part(args, rank, world, dev, cfg="C4", nsrc=8, steps=3):
     part_bytes = (pg.workspace.numel() + 8 * (pg.out_rp.numel() + pg.in_rp.numel()) +
                   4 * (pg.out_col.numel() + pg.in_col.numel() + pg.deg.numel()))
     res = {"value": float(sum(er)) * steps / (tot * 1e-3) / 1e9, "unit": "GTEPS",
-           "workload": f"{cfg}: {CONFIG_TEXT[cfg]}, {len(srcs)} sources, vertex-partitioned over "
-                       f"{world} rank(s)",
+           "workload": f"{cfg} graph ({CONFIG_TEXT[cfg].split(', 64')[0]}), {len(srcs)} sources, "
+                       f"vertex-partitioned over {world} rank(s)",
            "ms_per_search": tot / (steps * len(srcs)), "ranks": world, "scaling": "strong",
            "device_bytes_per_rank": int(part_bytes), "partition_build_s": t_build,
            "how": "dawn_part_begin / (all-gather + dawn_part_step) per level / dawn_part_finish; "
                   "the host tests convergence every 4 levels; L2 flushed between steps"}
     del pg, out, flush
+    torch.cuda.empty_cache()
+    return res
+
+
+def run_weighted(args, dev, cfg="C4", nsrc=4, steps=3):
+    """NEXT-4: weighted SSSP by (min,+) DAWN rounds (dawn_wsssp) on the config's graph with seeded
+    integer arc weights in [1, 255] (one per undirected edge).  GTEPS over E10 counts of the
+    reached set (the Graph500 SSSP convention counts the component's edges likewise)."""
+    import torch
+    import paper_2208_04514_b200 as dawn
+
+    g = graphgen.config_graph(cfg)
+    G = dawn.Graph(g.row_ptr, g.col, True)
+    wt = torch.from_numpy(g.weights(seed=int(cfg[1:]), wmax=255).view(np.int32)).to(dev)
+    srcs = sources_for(g, cfg, 0, nsrc)
+    out = torch.empty(g.n, dtype=torch.int32, device=dev)
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(int(2.2 * L2_BYTES) // 4, dtype=torch.int32, device=dev)
+    er, rounds, relaxed = [], [], []
+    for s in srcs:
+        _, st = dawn.wsssp(G, int(s), wt, stats=True, out=out)
+        x = dawn.stats_to_dict(st)
+        er.append(x["edges_reach"]); rounds.append(x["levels"]); relaxed.append(x["edges_examined"])
+    ms = timed(lambda: [dawn.wsssp(G, int(s), wt, out=out) for s in srcs], steps, flush, stream)
+    t = float(np.median(ms))
+    peak, _ = peaks()
+    # executed bytes: per relaxed arc a 4-B target, a 4-B weight and a 4-B distance read
+    b_exec = 12 * float(np.sum(relaxed)) + 4 * g.n * len(srcs)
+    res = {"value": float(np.sum(er)) / (t * 1e-3) / 1e9, "unit": "GTEPS",
+           "workload": f"{cfg} graph ({CONFIG_TEXT[cfg].split(', 64')[0]}), {len(srcs)} sources, "
+                       "uint32 weights in [1, 255]",
+           "ms_per_search": t / len(srcs), "rounds_mean": float(np.mean(rounds)),
+           "arcs_relaxed_per_search": float(np.mean(relaxed)),
+           "roofline": {"bound": "hbm", "achieved": b_exec / (t * 1e-3) / 1e9, "peak": peak,
+                        "unit": "GB/s", "frac": b_exec / (t * 1e-3) / 1e9 / peak,
+                        "bytes_model": "12 B per relaxed arc (target, weight, distance) + 4n"},
+           "how": "dawn_wsssp per source (one persistent k_wsssp launch each), L2 flushed between "
+                  "steps"}
+    del G, wt, out, flush
     torch.cuda.empty_cache()
     return res
 
@@ -666,6 +705,7 @@ def run_dawn(args):
                                  e2e=False)
             ex["C5"] = run_apsp(args, rank, world, dev, max(2, min(args.steps, 5)), 2,
                                 with_cpu=not args.no_cpu)
+            ex["C4_weighted"] = run_weighted(args, dev)
             res["configs"] = ex
     if args.extra and world >= 1:
         # NEXT-3: the same C4 searches over the vertex-partitioned graph (W = N ranks)

@@ -324,6 +324,23 @@ dawn_status dawn_largest_wcc(dawn_graph g, int64_t *sources_out, int64_t *k, uin
  * (bench.py derives the executed bytes B_exec of SURVEY §8(d) from them).                   */
 dawn_status dawn_graph_ms_counters(dawn_graph g, uint64_t *host_out, void *stream);
 
+/*
+ * Weighted single-source shortest paths: DAWN's SOVM round over the
+ * (min,+) semiring, the extension PAPER.md L596 names as future work (reading Q26 of
+ * DESIGN.md): the frontier holds the vertices whose distance dropped in the previous round;
+ * a round relaxes their out-arcs, d(u) <- min(d(u), d(v) + w(v,u)); stop when a round improves
+ * nothing (<= n-1 rounds).  One persistent kernel, frontier-empty test on the device.
+ *   weights  DEVICE uint32[m] aligned with the CSR col array, >= 0 (non-negative weights:
+ *            the fixpoint is the shortest-path distance; a zero-weight arc is allowed)
+ *   dist     DEVICE uint32[n]: d(s) = 0, DAWN_UNREACHED if no path; path weights saturate at
+ *            0xFFFFFFFE (exact while every shortest path weighs < 2^32 - 1)
+ *   stats    DEVICE or NULL: levels = rounds that lowered >= 1 distance, reached, edges_reach
+ *            (E10 over the reached set), edges_examined = arcs relaxed
+ * Errors: INVALID_ARGUMENT, BOUNDS, CUDA.  Uses the handle's frontier state.
+ */
+dawn_status dawn_wsssp(dawn_graph g, int64_t source, const uint32_t *weights, uint32_t *dist,
+                       dawn_sssp_stats *stats, void *stream);
+
 /* ------------------------------------------------------------------------------------------
  * Partitioned single-source SSSP over W GPUs: the graph is cut by
  * vertex ranges so each GPU holds ~2m/W arcs — the paper's memory-frugality motivation

@@ -18,7 +18,7 @@ import numpy as np
 import torch
 
 __all__ = ["build", "Graph", "sssp", "sssp_batch", "msssp", "apsp", "apsp_rows", "apsp_shard",
-           "part_range", "part_build", "PartGraph", "part_exchange", "part_sssp", "part_sssp_local", "largest_wcc",
+           "wsssp", "part_range", "part_build", "PartGraph", "part_exchange", "part_sssp", "part_sssp_local", "largest_wcc",
            "check", "DawnError", "UNREACHED", "AUTO", "PUSH", "PULL", "MS_BATCH", "REC_DTYPE",
            "records_to_numpy", "stats_to_dict", "gather_records"]
 
@@ -121,6 +121,8 @@ def lib():
         L.dawn_graph_ms_counters.argtypes = [vp, vp, vp]
         L.dawn_apsp_rows.restype = st
         L.dawn_apsp_rows.argtypes = [vp, vp, i64, i64, vp, vp, _ROW_SINK, vp, vp]
+        L.dawn_wsssp.restype = st
+        L.dawn_wsssp.argtypes = [vp, i64, vp, vp, vp, vp]
         L.dawn_part_range.restype = st
         L.dawn_part_range.argtypes = [i64, i32, i32, ctypes.POINTER(ctypes.c_int64),
                                       ctypes.POINTER(ctypes.c_int64)]
@@ -402,6 +404,18 @@ def gather_records(local: torch.Tensor, k: int, world: int, group=None) -> torch
         if len(idx):
             full[torch.from_numpy(idx).to(local.device)] = parts[r][: len(idx)]
     return full
+
+
+def wsssp(g: Graph, source: int, weights: torch.Tensor, stats: bool = False,
+          out: torch.Tensor | None = None, stream=None):
+    """dawn_wsssp: weighted SSSP by (min,+) DAWN rounds (NEXT-4).  `weights`: uint32/int32 CUDA
+    tensor [m] aligned with the CSR col array.  Returns int32 [n] (uint32 bits, UNREACHED = -1)."""
+    assert weights.is_cuda and weights.dtype in (torch.int32, torch.uint32) and weights.numel() == g.m
+    dist = out if out is not None else torch.empty(g.n, dtype=torch.int32, device=g.device)
+    st = torch.zeros(4, dtype=torch.int64, device=g.device) if stats else None
+    _check(lib().dawn_wsssp(g.handle, int(source), _dptr(weights), _dptr(dist), _dptr(st),
+                            _stream(stream)))
+    return (dist, st) if stats else dist
 
 
 # ----------------------------------------------------------- partitioned SSSP (NEXT-3)

@@ -20,6 +20,7 @@
 #include "sssp_kernel.cuh"
 #include "wcc_kernel.cuh"
 #include "part_kernel.cuh"
+#include "wsssp_kernel.cuh"
 
 using namespace dawn;
 
@@ -310,7 +311,7 @@ struct dawn_graph_s {
   const int32_t *col, *icol;
   bool has_csc;
   float alpha = 2.f, beta = 96.f, ms_alpha = 2.f;
-  int sssp_grid, ms_grid;
+  int sssp_grid, ms_grid, wsssp_grid = 1;
   bool sssp_one = false;  // the 1-CTA-per-SM instantiation of k_sssp (small graphs)
   bool trace;
   size_t small_cap;  // max dynamic smem for k_small (0 = disabled)
@@ -470,6 +471,7 @@ dawn_status load_csr(int64_t n, int64_t m, const int64_t *row_ptr, const int32_t
     }
     cudaGetLastError();
   }
+  g->wsssp_grid = grid_for((const void *)k_wsssp<kNT>, g->nsm);
   if (!g->lean) {
     cudaFuncSetAttribute((const void *)k_ms64<kNT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)ms_smem_bytes(kNT));
@@ -1182,6 +1184,39 @@ dawn_status ms_counters(dawn_graph g, uint64_t *host_out, void *stream) {
   return DAWN_OK;
 }
 
+// ---------------------------------------------------------------- weighted (min,+) (NEXT-4)
+dawn_status wsssp(dawn_graph g, int64_t source, const uint32_t *weights, uint32_t *dist,
+                  dawn_sssp_stats *stats, void *stream) {
+  if (!g || !dist || (g->m > 0 && !weights)) return fail(DAWN_ERR_INVALID_ARGUMENT, "NULL argument");
+  if (source < 0 || source >= g->n)
+    return fail(DAWN_ERR_BOUNDS, "source %lld not in [0, n)", (long long)source);
+  dawn_status s = set_device(g);
+  if (s != DAWN_OK) return s;
+  const Layout &L = g->L;
+  WParams p{};
+  p.n = (uint32_t)g->n;
+  p.nwords = (uint32_t)((g->n + 31) / 32);
+  p.source = (uint32_t)source;
+  p.rp = at<uint32_t>(g, L.rp);
+  p.col = g->col;
+  p.w = weights;
+  p.hout_v = at<uint32_t>(g, L.hout.v);
+  p.hout_s = at<uint32_t>(g, L.hout.s);
+  p.hout_e = at<uint32_t>(g, L.hout.e);
+  p.hout_bits = at<uint32_t>(g, L.hout.bits);
+  for (int i = 0; i < 3; ++i) p.fb[i] = at<uint32_t>(g, L.fb[i]);
+  p.ctrl = at<Ctrl>(g, L.ctrl);
+  p.dist = dist;
+  p.stats = stats;
+  int grid = g->wsssp_grid;
+  if (g->m + g->n <= kOneCtaMaxNM) grid = 1;
+  void *args[] = {&p};
+  cudaError_t e = cudaLaunchCooperativeKernel((const void *)k_wsssp<kNT>, dim3(grid), dim3(kNT), args,
+                                              0, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "k_wsssp launch");
+  return DAWN_OK;
+}
+
 // ---------------------------------------------------------------- partitioned SSSP (NEXT-3)
 int64_t part_block(int64_t n, int32_t world) {  // Rmax: ceil(n / world) rounded up to 32
   const int64_t q = (n + world - 1) / world;
@@ -1569,6 +1604,11 @@ dawn_status dawn_largest_wcc(dawn_graph g, int64_t *sources_out, int64_t *k, uin
 
 dawn_status dawn_graph_ms_counters(dawn_graph g, uint64_t *host_out, void *stream) {
   DAWN_GUARD(return ms_counters(g, host_out, stream);)
+}
+
+dawn_status dawn_wsssp(dawn_graph g, int64_t source, const uint32_t *weights, uint32_t *dist,
+                       dawn_sssp_stats *stats, void *stream) {
+  DAWN_GUARD(return wsssp(g, source, weights, dist, stats, stream);)
 }
 
 dawn_status dawn_part_range(int64_t n, int32_t world, int32_t rank, int64_t *lo, int64_t *hi) {
