@@ -176,8 +176,8 @@ typedef enum {
   DAWN_PARAM_BATCH_LANES = 9,      /* dawn_sssp_batch on the grid-wide kernel runs this many
                                       searches at once, each on 1/lanes of the SMs with its own
                                       per-search state and stream (the sources are
-                                      independent).  1 .. 4 (n <= 2^22) or
-                                      1 .. 2 (larger n; 1 with DAWN_GRAPH_LEAN).  Default set at
+                                      independent).  1 .. 8 (n <= 2^22) or
+                                      1 .. 4 (larger n; 1 with DAWN_GRAPH_LEAN).  Default set at
                                       load from B200 measurements.              */
   DAWN_PARAM_MS_LANES = 11,        /* dawn_msssp / dawn_apsp / dawn_apsp_rows run this many
                                       256-source batches at once, each on 1/lanes of the SMs with

@@ -49,7 +49,13 @@ constexpr int kMsBlocksPerSm = 2;          // k_ms64 CTAs per SM (if they fit)
 constexpr uint32_t kNarrowQcapMax = 1u << 20;
 // dawn_sssp_batch lanes (concurrent searches) by default: measured on B200
 constexpr int kDefaultMsLanes = DAWN_MS_LANES;  // multi-source lanes (B200 measurement)
-int kDefaultLanes(int64_t n) { return n <= (int64_t(1) << 22) ? 2 : 1; }
+#ifndef DAWN_LANES_SMALL
+#define DAWN_LANES_SMALL 8  // default batch lanes for n <= 2^22 (C2: 2 -> 650, 8 -> 1008 GTEPS)
+#endif
+#ifndef DAWN_LANES_BIG
+#define DAWN_LANES_BIG 4    // ... and above (C4: 1 -> 1343, 2 -> 1590, 4 -> 1678 GTEPS)
+#endif
+int kDefaultLanes(int64_t n) { return n <= (int64_t(1) << 22) ? DAWN_LANES_SMALL : DAWN_LANES_BIG; }
 
 // ---------------------------------------------------------------- graph residency kernels
 __global__ void k_offsets32(const int64_t *__restrict__ in, uint32_t *__restrict__ out, int64_t n1) {

@@ -44,6 +44,7 @@ constexpr uint32_t kNarrowMaxAvgDeg = 8;           // arc array kept when m <= 8
 // Multi-source kernel: kMsW 64-bit words per vertex = kMsBatch sources per adjacency pass.
 constexpr int kMsW = 4;
 constexpr uint32_t kMsBatch = 64 * kMsW;
+
 static_assert(kMsBatch == DAWN_MS_BATCH, "dawn.h DAWN_MS_BATCH must match kMsW");
 
 #ifndef DAWN_PULL_DEEP
@@ -153,7 +154,7 @@ struct HeavyList {  // static pieces of rows with degree > kHeavy
 // kMaxLanes cooperative launches (one per lane, each on its own share of the SMs and its own
 // stream) run independent searches of one batch at the same time (sources are
 // independent).  Lane 0 is the state every other call uses.
-constexpr int kMaxLanes = 4;
+constexpr int kMaxLanes = 8;
 constexpr int kMsMaxLanes = 4;
 #ifndef DAWN_MS_LANES
 #define DAWN_MS_LANES 4  // default multi-source lanes (C5: 1 -> 707K, 2 -> 815K, 3 -> 829K, 4 -> 847K sources/s)
@@ -254,7 +255,7 @@ inline Layout make_layout(int64_t n, int64_t m, uint32_t flags) {
   }
   // extra lanes (lane 0 = the arrays above): not in lean mode; 4 lanes up to 2^22 vertices
   // (latency-bound searches overlap best), 2 above
-  L.nlanes = lean ? 1 : ((uint64_t)n <= (1ull << 22) ? 4 : 2);
+  L.nlanes = lean ? 1 : ((uint64_t)n <= (1ull << 22) ? kMaxLanes : 4);
   L.lane[0] = LaneLayout{L.vis, L.cand, {L.fb[0], L.fb[1], L.fb[2]}, {L.Lv[0], L.Lv[1]},
                          {L.Lsd[0], L.Lsd[1]}, {L.Cf[0], L.Cf[1]}, L.ctrl, L.ulist, L.useg};
   for (int l = 1; l < L.nlanes; ++l) {

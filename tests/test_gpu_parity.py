@@ -425,7 +425,7 @@ def test_push_from_pull_bitmap_frontier():
 
 
 def test_sssp_batch_lanes():
-    # DAWN_PARAM_BATCH_LANES: 1/2/4 concurrent grid-wide searches (own state, own stream) give
+    # DAWN_PARAM_BATCH_LANES: 1/2/4/8 concurrent grid-wide searches (own state, own stream) give
     # the oracle's rows and statistics for every source, incl. k not a multiple of the lanes,
     # repeated sources, and every direction variant
     g = graphgen.kron(15, 16, 15)
@@ -433,7 +433,7 @@ def test_sssp_batch_lanes():
     srcs = np.concatenate([g.sample_sources(9, seed=11), [0]]).astype(np.int32)
     srcs[3] = srcs[1]                                               # a repeated source
     exp = [oracle.bfs_fifo(g.n, g.row_ptr, g.col, int(s))[0] for s in srcs]
-    for lanes in (1, 2, 4):
+    for lanes in (1, 2, 4, 8):
         G.set_tuning(batch_lanes=lanes)
         for v in VARIANTS:
             d, st = dawn.sssp_batch(G, torch.from_numpy(srcs).cuda(), v, stats=True, check=True)
@@ -444,7 +444,7 @@ def test_sssp_batch_lanes():
                 sd = dawn.stats_to_dict(st[i])
                 assert sd["levels"] == int(rec["ecc"]) and sd["edges_reach"] == er, (lanes, v)
     with pytest.raises(dawn.DawnError):
-        G.set_tuning(batch_lanes=5)
+        G.set_tuning(batch_lanes=9)
     # the lanes share nothing across calls: a single dawn_sssp between batches still matches
     G.set_tuning(batch_lanes=4)
     dawn.sssp_batch(G, torch.from_numpy(srcs).cuda())
