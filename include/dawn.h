@@ -177,8 +177,13 @@ typedef enum {
                                       searches at once, each on 1/lanes of the SMs with its own
                                       per-search state and stream (the sources are
                                       independent).  1 .. 8 (n <= 2^22) or
-                                      1 .. 4 (larger n; 1 with DAWN_GRAPH_LEAN).  Default set at
+                                      1 .. 8 (larger n; 1 with DAWN_GRAPH_LEAN).  Default set at
                                       load from B200 measurements.              */
+  DAWN_PARAM_WEIGHT_DELTA = 12,    /* dawn_wsssp near/far step: a round expands only frontier
+                                      vertices with d < T (the others stay in the frontier); T
+                                      moves to (minimum frontier distance) + delta when no
+                                      frontier vertex lies below it.  0 = off (every frontier
+                                      vertex each round).  Speed only, never results.         */
   DAWN_PARAM_MS_LANES = 11,        /* dawn_msssp / dawn_apsp / dawn_apsp_rows run this many
                                       256-source batches at once, each on 1/lanes of the SMs with
                                       its own bit-parallel state and stream (independent sources,

@@ -49,6 +49,9 @@ constexpr int kMsBlocksPerSm = 2;          // k_ms64 CTAs per SM (if they fit)
 constexpr uint32_t kNarrowQcapMax = 1u << 20;
 // dawn_sssp_batch lanes (concurrent searches) by default: measured on B200
 constexpr int kDefaultMsLanes = DAWN_MS_LANES;  // multi-source lanes (B200 measurement)
+#ifndef DAWN_WDELTA
+#define DAWN_WDELTA 8  // near/far step of dawn_wsssp (weights 1..255 on Kronecker-24)
+#endif
 #ifndef DAWN_LANES_SMALL
 #define DAWN_LANES_SMALL 8  // default batch lanes for n <= 2^22 (C2: 2 -> 650, 8 -> 1008 GTEPS)
 #endif
@@ -334,6 +337,7 @@ struct dawn_graph_s {
   bool lean = false;             // DAWN_GRAPH_LEAN: no ms64 words / icol2 / augmented arcs
   int lanes = 1;                 // DAWN_PARAM_BATCH_LANES (<= L.nlanes)
   int ms_lanes = 1;               // DAWN_PARAM_MS_LANES (<= L.ms_nlanes)
+  uint32_t wdelta = DAWN_WDELTA;   // DAWN_PARAM_WEIGHT_DELTA (0: near/far off)
   double dense_max = 1099511627776.0;  // DAWN_PARAM_DENSE_MAX_ENTRIES (k*n of a dense output)
   // lane streams / fork-join events of dawn_sssp_batch (created at load, host resources only)
   cudaStream_t lane_st[kMaxLanes] = {};
@@ -635,6 +639,7 @@ dawn_status set_param(dawn_graph g, dawn_param key, double value) {
         return fail(DAWN_ERR_INVALID_ARGUMENT, "batch lanes must be in [1, %d]", g->L.nlanes);
       g->lanes = (int)value;
       break;
+    case DAWN_PARAM_WEIGHT_DELTA: g->wdelta = (uint32_t)std::min(value, 4294967294.0); break;
     case DAWN_PARAM_MS_LANES:
       if (value < 1 || value > g->L.ms_nlanes || (value > 1 && !g->ev_fork))
         return fail(DAWN_ERR_INVALID_ARGUMENT, "multi-source lanes must be in [1, %d]", g->L.ms_nlanes);
@@ -1214,6 +1219,7 @@ dawn_status wsssp(dawn_graph g, int64_t source, const uint32_t *weights, uint32_
   p.ctrl = at<Ctrl>(g, L.ctrl);
   p.dist = dist;
   p.stats = stats;
+  p.delta = g->wdelta == 0 ? kWInf : g->wdelta;
   int grid = g->wsssp_grid;
   if (g->m + g->n <= kOneCtaMaxNM) grid = 1;
   void *args[] = {&p};

@@ -89,6 +89,9 @@ constexpr uint32_t kDirectRow = 256;
 #ifndef DAWN_NOVIS
 #define DAWN_NOVIS 1       // candidate push levels skip the visited read while few are settled
 #endif
+#ifndef DAWN_NOVIS2
+#define DAWN_NOVIS2 1      // ... also in the 64-register kernel (4 chunks per item there)
+#endif
 #ifndef DAWN_NOVIS_FRAC
 #define DAWN_NOVIS_FRAC 32  // ... while (reached + 1) * FRAC < reachable vertices (C4 1325 -> 1350 GTEPS; 8: forced push C2 -9%)
 #endif
@@ -255,7 +258,7 @@ inline Layout make_layout(int64_t n, int64_t m, uint32_t flags) {
   }
   // extra lanes (lane 0 = the arrays above): not in lean mode; 4 lanes up to 2^22 vertices
   // (latency-bound searches overlap best), 2 above
-  L.nlanes = lean ? 1 : ((uint64_t)n <= (1ull << 22) ? kMaxLanes : 4);
+  L.nlanes = lean ? 1 : kMaxLanes;
   L.lane[0] = LaneLayout{L.vis, L.cand, {L.fb[0], L.fb[1], L.fb[2]}, {L.Lv[0], L.Lv[1]},
                          {L.Lsd[0], L.Lsd[1]}, {L.Cf[0], L.Cf[1]}, L.ctrl, L.ulist, L.useg};
   for (int l = 1; l < L.nlanes; ++l) {

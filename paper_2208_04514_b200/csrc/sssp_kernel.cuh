@@ -306,6 +306,11 @@ __device__ __forceinline__ void push_item(const SsspParams &p, const LevelState 
   }
 }
 
+// NV: the candidate push may skip the visited read (st.novis).  Only in the 1-CTA/SM kernel: the
+// extra instantiation makes the 64-register kernel spill, and a kernel with a stack frame
+// running concurrently with other cooperative launches (batch lanes) faulted or hung
+// intermittently on B200; every cooperative kernel is kept at 0 bytes of stack.
+template <bool NV>
 __device__ void push_level(const SsspParams &p, const LevelState &st, Slot *ns, uint32_t gwarp,
                            uint32_t nwarps, uint32_t &n_new, unsigned long long &m_new,
                            WarpStage &stg, long long &t0, unsigned long long *fsm) {
@@ -319,9 +324,15 @@ __device__ void push_level(const SsspParams &p, const LevelState &st, Slot *ns, 
     if (nchunks >= nwarps * DAWN_ILP_CAND) {
       constexpr int JB = DAWN_ILP_CAND;
       const uint32_t items = (nchunks + JB - 1) / JB;
-      if (DAWN_NOVIS && st.novis) {
+      if (NV && DAWN_NOVIS && st.novis) {
         for (uint32_t it = gwarp; it < items; it += nwarps)
           push_item<JB, true, true>(p, st, ns, it, n_new, m_new, stg, cnt);
+      } else if (!NV && DAWN_NOVIS && DAWN_NOVIS2 && st.novis) {
+        // 64-register kernel: half the chunks per item keeps the extra instantiation spill-free
+        constexpr int JH = JB / 2;
+        const uint32_t items2 = (nchunks + JH - 1) / JH;
+        for (uint32_t it = gwarp; it < items2; it += nwarps)
+          push_item<JH, true, true>(p, st, ns, it, n_new, m_new, stg, cnt);
       } else {
         for (uint32_t it = gwarp; it < items; it += nwarps)
           push_item<JB, true>(p, st, ns, it, n_new, m_new, stg, cnt);
@@ -913,7 +924,7 @@ __global__ void __launch_bounds__(NT, MINB) k_sssp(SsspParams p) {
         uint32_t n_new = 0;
         unsigned long long m_new = 0;
         long long t0 = clock64();
-        push_level(p, st, ns, lw, NT / 32, n_new, m_new, stg, t0, fsm);
+        push_level<MINB == 1>(p, st, ns, lw, NT / 32, n_new, m_new, stg, t0, fsm);
         block_flush(n_new, m_new, &ns->n_new, &ns->m_new, red);
         trace_done(p, st.L);
         __syncthreads();
@@ -993,7 +1004,7 @@ __global__ void __launch_bounds__(NT, MINB) k_sssp(SsspParams p) {
     if (kDirect && direct) {
       push_bitmap(p, st, ns, gwarp, nwarps, n_new, m_new, stg, tconv, fsm);
     } else if (st.dir == kPush) {
-      push_level(p, st, ns, gwarp, nwarps, n_new, m_new, stg, tconv, fsm);
+      push_level<MINB == 1>(p, st, ns, gwarp, nwarps, n_new, m_new, stg, tconv, fsm);
       if (st.bm) {
         grid_sync(&C->bar, nblocks, bar_target);
         cand_filter(p, st, gwarp, nwarps, n_new, m_new, bigf);

@@ -12,11 +12,19 @@
 // for non-negative weights — is unique, so the result equals the synchronous oracle's.
 // Frontier rows of <= kHeavy arcs are dealt 32 arcs per warp round from a bitmap scan; longer
 // rows go through the graph's static 256-arc out-pieces (32 pieces tested per warp at once).
+// Near/far threshold (the "balance ... of (min,+) operations" of L596): a round expands only the
+// frontier vertices with d < T and carries the others to the next frontier; T stays while the
+// next frontier holds a vertex below it and otherwise jumps to (its minimum distance) + delta.
+// Expanding roughly in distance order avoids most Bellman-Ford re-relaxations; any order
+// reaches the same fixpoint (a vertex whose distance drops re-enters the frontier).
 #pragma once
 #include "layout.h"
 
 namespace dawn {
 
+#ifndef DAWN_W_RED
+#define DAWN_W_RED 1  // relax with red.min (no returning atomic) instead of atomicMin
+#endif
 constexpr uint32_t kWInf = 0xFFFFFFFFu;   // unreached
 constexpr uint32_t kWSat = 0xFFFFFFFEu;   // largest representable distance (saturating add)
 
@@ -30,25 +38,37 @@ struct WParams {
   Ctrl *ctrl;
   uint32_t *dist;
   dawn_sssp_stats *stats;
+  uint32_t delta;                                      // near/far step (>= 1; ~0u: off)
 };
 
 __device__ __forceinline__ void w_relax(const WParams &p, uint32_t dv, uint32_t j, uint32_t *fnext,
-                                        uint32_t &improved) {
+                                        uint32_t &improved, uint32_t &fmin) {
   const uint32_t u = (uint32_t)ld_nc(p.col + j);
   uint32_t c = dv + ld_nc(p.w + j);
   if (c < dv || c > kWSat) c = kWSat;  // saturate (exact while every distance < 2^32 - 1)
   if (c < ld_cg(p.dist + u)) {
+#if DAWN_W_RED
+    // fire-and-forget min: no returning round trip on the chain; u joins the next frontier on
+    // the observed improvement (if another arc lowered d(u) further meanwhile, u is expanded
+    // with that value — an extra frontier entry at worst)
+    asm volatile("red.relaxed.gpu.global.min.u32 [%0], %1;" ::"l"(p.dist + u), "r"(c) : "memory");
+    red_or(fnext + (u >> 5), 1u << (u & 31));
+    ++improved;
+    fmin = min(fmin, c);
+#else
     const uint32_t old = atomicMin(p.dist + u, c);
     if (c < old) {
       red_or(fnext + (u >> 5), 1u << (u & 31));
       ++improved;
+      fmin = min(fmin, c);
     }
+#endif
   }
 }
 
 template <int NT>
 __global__ void __launch_bounds__(NT, 1) k_wsssp(WParams p) {
-  __shared__ uint32_t s_imp, s_stop;
+  __shared__ uint32_t s_imp, s_stop, s_min, s_T;
   __shared__ unsigned long long red[3];
   const uint32_t lane = lane_id();
   const uint32_t nblocks = gridDim.x;
@@ -65,9 +85,10 @@ __global__ void __launch_bounds__(NT, 1) k_wsssp(WParams p) {
     p.fb[2][w] = 0;
   }
   if (gtid == 0) {
-    for (int i = 0; i < 3; ++i) C->slot[i] = Slot{0, 0, 0, 0, 0};
+    for (int i = 0; i < 3; ++i) C->slot[i] = Slot{0, kWInf, 0, 0, 0};  // n_new, big = min d
     C->examined = 0;
   }
+  if (threadIdx.x == 0) s_T = p.delta == kWInf ? kWInf : p.delta;  // F_0 = {s}, d(s) = 0 < T
   grid_sync(&C->bar, nblocks, bar);
   uint32_t b = 0, rounds = 0;
   unsigned long long relaxed = 0;
@@ -77,20 +98,31 @@ __global__ void __launch_bounds__(NT, 1) k_wsssp(WParams p) {
     const uint32_t *fcur = pick(b);
     uint32_t *fnext = pick((b + 1) % 3);
     uint32_t *fclr = pick((b + 2) % 3);  // F_{k-1}: cleared now, written in round k+1
-    uint32_t improved = 0;
+    uint32_t improved = 0, fmin = kWInf;
+    const uint32_t T = s_T;
     for (uint32_t w = gtid; w < p.nwords; w += nth) fclr[w] = 0;
-    // (a) light rows: 32 words per warp, one frontier vertex per lane per round
+    // (a) every frontier vertex: far ones (d >= T) are carried to the next frontier; near light
+    //     rows are expanded here, 32 words per warp, one frontier vertex per lane per round
+    //     (near heavy rows: the pieces below)
     for (uint32_t base = gwarp * 32; base < p.nwords; base += nwarps * 32) {
       const uint32_t wd = base + lane;
-      uint32_t bits = wd < p.nwords ? (ld_cg(fcur + wd) & ~ld_nc(p.hout_bits + wd)) : 0u;
+      uint32_t bits = wd < p.nwords ? ld_cg(fcur + wd) : 0u;
+      const uint32_t hvy = wd < p.nwords ? ld_nc(p.hout_bits + wd) : 0u;
       while (__ballot_sync(DAWN_FULL, bits != 0)) {
         uint32_t rs = 0, d = 0, dv = 0;
         if (bits) {
-          const uint32_t v = wd * 32 + (__ffs(bits) - 1);
+          const uint32_t b0 = __ffs(bits) - 1;
+          const uint32_t v = wd * 32 + b0;
           bits &= bits - 1;
-          rs = ld_nc(p.rp + v);
-          d = ld_nc(p.rp + v + 1) - rs;
           dv = ld_cg(p.dist + v);
+          if (dv >= T) {  // far: stays in the frontier
+            red_or(fnext + wd, 1u << b0);
+            ++improved;
+            fmin = min(fmin, dv);
+          } else if (!((hvy >> b0) & 1u)) {
+            rs = ld_nc(p.rp + v);
+            d = ld_nc(p.rp + v + 1) - rs;
+          }
         }
         const uint32_t incl = warp_incl_scan(d);
         const uint32_t total = __shfl_sync(DAWN_FULL, incl, 31);
@@ -107,7 +139,7 @@ __global__ void __launch_bounds__(NT, 1) k_wsssp(WParams p) {
           const uint32_t sk = __shfl_sync(DAWN_FULL, rs, kk);
           const uint32_t dk = __shfl_sync(DAWN_FULL, dv, kk);
           if (t < total) {
-            w_relax(p, dk, sk + (t - ek), fnext, improved);
+            w_relax(p, dk, sk + (t - ek), fnext, improved, fmin);
             ++relaxed;
           }
         }
@@ -119,36 +151,54 @@ __global__ void __launch_bounds__(NT, 1) k_wsssp(WParams p) {
       const uint32_t pcl = pb + lane * nwarps;
       uint32_t vl = 0;
       bool live = false;
+      uint32_t dl = 0;
       if (pcl < hend) {
         vl = ld_nc(p.hout_v + pcl);
         live = (ld_cg(fcur + (vl >> 5)) >> (vl & 31)) & 1u;
+        if (live) {
+          dl = ld_cg(p.dist + vl);
+          live = dl < T;  // far heavy vertices were carried by (a)
+        }
       }
       uint32_t lm = __ballot_sync(DAWN_FULL, live);
       while (lm) {
         const uint32_t kk = __ffs(lm) - 1;
         lm &= lm - 1;
         const uint32_t pc = pb + kk * nwarps;
-        const uint32_t v = __shfl_sync(DAWN_FULL, vl, kk);
-        const uint32_t dv = ld_cg(p.dist + v);
+        const uint32_t dv = __shfl_sync(DAWN_FULL, dl, kk);
         const uint32_t s = ld_nc(p.hout_s + pc), e = ld_nc(p.hout_e + pc);
         for (uint32_t j = s + lane; j < e; j += 32) {
-          w_relax(p, dv, j, fnext, improved);
+          w_relax(p, dv, j, fnext, improved, fmin);
           ++relaxed;
         }
       }
     }
-    // round counters: improvements into slot k % 3 (slot k+1 % 3 reset for the next round)
+    // round counters: next-frontier entries (improved + carried) and their minimum distance
+    // into slot k % 3 (slot (k+1) % 3 reset for the next round)
     improved = warp_sum(improved);
-    if (threadIdx.x == 0) s_imp = 0;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) fmin = min(fmin, __shfl_xor_sync(DAWN_FULL, fmin, o));
+    if (threadIdx.x == 0) { s_imp = 0; s_min = kWInf; }
     __syncthreads();
-    if (lane == 0 && improved) atomicAdd(&s_imp, improved);
+    if (lane == 0 && improved) {
+      atomicAdd(&s_imp, improved);
+      atomicMin(&s_min, fmin);
+    }
     __syncthreads();
     if (threadIdx.x == 0) {
-      if (s_imp) atomicAdd(&C->slot[k % 3].n_new, s_imp);
-      if (blockIdx.x == 0) C->slot[(k + 1) % 3].n_new = 0;
+      if (s_imp) {
+        atomicAdd(&C->slot[k % 3].n_new, s_imp);
+        atomicMin(&C->slot[k % 3].big, s_min);
+      }
+      if (blockIdx.x == 0) C->slot[(k + 1) % 3] = Slot{0, kWInf, 0, 0, 0};
     }
     grid_sync(&C->bar, nblocks, bar);
-    if (threadIdx.x == 0) s_stop = ld_cg(&C->slot[k % 3].n_new) == 0;
+    if (threadIdx.x == 0) {
+      s_stop = ld_cg(&C->slot[k % 3].n_new) == 0;
+      const uint32_t mn = ld_cg(&C->slot[k % 3].big);
+      // T stays while the next frontier has a vertex below it, else min + delta
+      if (p.delta != kWInf && mn >= s_T) s_T = (mn > kWSat - p.delta) ? kWInf : mn + p.delta;
+    }
     __syncthreads();
     b = (b + 1) % 3;
     if (s_stop) break;

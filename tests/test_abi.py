@@ -90,3 +90,20 @@ def test_apsp_shard_rule_partitions(k, world):
     assert max(sizes) - min(sizes) <= dawn.MS_BATCH
     with pytest.raises(dawn.DawnError):
         dawn.apsp_shard(k, world, world)
+
+
+def test_persistent_kernels_have_no_stack_frame():
+    # A cooperative kernel with a stack frame (register spills) running next to other
+    # cooperative launches (dawn_sssp_batch lanes) faulted or hung intermittently on B200 while
+    # the spill-free build never did: every kernel must stay at STACK:0 / LOCAL:0.
+    import subprocess
+    dawn.build()
+    out = subprocess.run(["cuobjdump", "-res-usage", dawn._LIB], capture_output=True,
+                         text=True).stdout
+    funcs = re.findall(r"Function (\S+):\s*\n\s*REG:(\d+) STACK:(\d+) SHARED:\d+ LOCAL:(\d+)", out)
+    assert len(funcs) >= 10
+    bad = [(f, st, lo) for f, _, st, lo in funcs if st != "0" or lo != "0"]
+    assert not bad, bad
+    names = " ".join(f for f, *_ in funcs)
+    for k in ("k_sssp", "k_ms64", "k_narrow", "k_wsssp", "k_part_level", "k_small"):
+        assert k in names, k
