@@ -330,6 +330,17 @@ dawn_status dawn_largest_wcc(dawn_graph g, int64_t *sources_out, int64_t *k, uin
 dawn_status dawn_graph_ms_counters(dawn_graph g, uint64_t *host_out, void *stream);
 
 /*
+ * Compact distance rows for transfer: out[i] = dist[i] when dist[i] < 255, else 255 (255 =
+ * DAWN_UNREACHED, or a finite distance >= 255, which also sets bit 0 of *flags — the caller then
+ * transfers that row as uint32).  Low-diameter graphs (every config here has eps <= 8190; the
+ * Kronecker ones <= 8) thus move 1 byte per vertex to the host instead of 4.
+ *   dist  DEVICE uint32[count], 16-byte aligned;  out  DEVICE uint8[count], 4-byte aligned
+ *   flags DEVICE uint32, OR-ed (never cleared by the call).  Enqueue only.
+ */
+dawn_status dawn_dist_u8(const uint32_t *dist, int64_t count, uint8_t *out, uint32_t *flags,
+                         void *stream);
+
+/*
  * Weighted single-source shortest paths: DAWN's SOVM round over the
  * (min,+) semiring, the extension PAPER.md L596 names as future work (reading Q26 of
  * DESIGN.md): the frontier holds the vertices whose distance dropped in the previous round;

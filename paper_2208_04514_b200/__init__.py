@@ -18,7 +18,7 @@ import numpy as np
 import torch
 
 __all__ = ["build", "Graph", "sssp", "sssp_batch", "msssp", "apsp", "apsp_rows", "apsp_shard",
-           "wsssp", "part_range", "part_build", "PartGraph", "part_exchange", "part_sssp", "part_sssp_local", "largest_wcc",
+           "wsssp", "dist_u8", "part_range", "part_build", "PartGraph", "part_exchange", "part_sssp", "part_sssp_local", "largest_wcc",
            "check", "DawnError", "UNREACHED", "AUTO", "PUSH", "PULL", "MS_BATCH", "REC_DTYPE",
            "records_to_numpy", "stats_to_dict", "gather_records"]
 
@@ -121,6 +121,8 @@ def lib():
         L.dawn_graph_ms_counters.argtypes = [vp, vp, vp]
         L.dawn_apsp_rows.restype = st
         L.dawn_apsp_rows.argtypes = [vp, vp, i64, i64, vp, vp, _ROW_SINK, vp, vp]
+        L.dawn_dist_u8.restype = st
+        L.dawn_dist_u8.argtypes = [vp, i64, vp, vp, vp]
         L.dawn_wsssp.restype = st
         L.dawn_wsssp.argtypes = [vp, i64, vp, vp, vp, vp]
         L.dawn_part_range.restype = st
@@ -404,6 +406,17 @@ def gather_records(local: torch.Tensor, k: int, world: int, group=None) -> torch
         if len(idx):
             full[torch.from_numpy(idx).to(local.device)] = parts[r][: len(idx)]
     return full
+
+
+def dist_u8(dist: torch.Tensor, out: torch.Tensor | None = None,
+            flags: torch.Tensor | None = None, stream=None):
+    """dawn_dist_u8: 1-byte copy of distance rows (255 = unreached, or a distance >= 255 that
+    did not fit: then flags[0] bit 0 is set).  Returns (uint8 tensor like dist, int32 flags[1])."""
+    assert dist.is_cuda and dist.dtype in (torch.int32, torch.uint32) and dist.is_contiguous()
+    out = out if out is not None else torch.empty(dist.shape, dtype=torch.uint8, device=dist.device)
+    flags = flags if flags is not None else torch.zeros(1, dtype=torch.int32, device=dist.device)
+    _check(lib().dawn_dist_u8(_dptr(dist), dist.numel(), _dptr(out), _dptr(flags), _stream(stream)))
+    return out, flags
 
 
 def wsssp(g: Graph, source: int, weights: torch.Tensor, stats: bool = False,

@@ -1195,6 +1195,52 @@ dawn_status ms_counters(dawn_graph g, uint64_t *host_out, void *stream) {
   return DAWN_OK;
 }
 
+// ---------------------------------------------------------------- compact distance rows
+// out[i] = d[i] for d < 255, 255 otherwise (UNREACHED, or a finite distance that does not fit:
+// then bit 0 of *flags is set).  4 distances per thread, one flag atomic per CTA at most.
+__global__ void k_dist_u8(const uint32_t *__restrict__ d, int64_t count, uint8_t *__restrict__ out,
+                          uint32_t *flags) {
+  const int64_t n4 = count / 4;
+  bool over = false;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint4 x = __ldcs(reinterpret_cast<const uint4 *>(d) + i);
+    const uint32_t a[4] = {x.x, x.y, x.z, x.w};
+    uint32_t packed = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t v = a[k] < 255u ? a[k] : 255u;
+      over |= a[k] >= 255u && a[k] != kUnreached;
+      packed |= v << (8 * k);
+    }
+    reinterpret_cast<uint32_t *>(out)[i] = packed;
+  }
+  for (int64_t i = 4 * n4 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t v = d[i];
+    over |= v >= 255u && v != kUnreached;
+    out[i] = (uint8_t)(v < 255u ? v : 255u);
+  }
+  if (__syncthreads_or(over) && threadIdx.x == 0) atomicOr(flags, 1u);
+}
+
+dawn_status dist_u8(const uint32_t *dist, int64_t count, uint8_t *out, uint32_t *flags,
+                    void *stream) {
+  if (count < 0 || (count > 0 && (!dist || !out || !flags)))
+    return fail(DAWN_ERR_INVALID_ARGUMENT, "bad arguments");
+  if ((reinterpret_cast<uintptr_t>(dist) & 15) || (reinterpret_cast<uintptr_t>(out) & 3))
+    return fail(DAWN_ERR_INVALID_ARGUMENT, "dist must be 16-byte and out 4-byte aligned");
+  if (count == 0) return DAWN_OK;
+  int dev = 0, nsm = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(nsm * 8, (count / 4 + 255) / 256));
+  k_dist_u8<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(dist, count, out, flags);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "k_dist_u8 launch");
+  return DAWN_OK;
+}
+
 // ---------------------------------------------------------------- weighted (min,+) (NEXT-4)
 dawn_status wsssp(dawn_graph g, int64_t source, const uint32_t *weights, uint32_t *dist,
                   dawn_sssp_stats *stats, void *stream) {
@@ -1616,6 +1662,11 @@ dawn_status dawn_largest_wcc(dawn_graph g, int64_t *sources_out, int64_t *k, uin
 
 dawn_status dawn_graph_ms_counters(dawn_graph g, uint64_t *host_out, void *stream) {
   DAWN_GUARD(return ms_counters(g, host_out, stream);)
+}
+
+dawn_status dawn_dist_u8(const uint32_t *dist, int64_t count, uint8_t *out, uint32_t *flags,
+                         void *stream) {
+  DAWN_GUARD(return dist_u8(dist, count, out, flags, stream);)
 }
 
 dawn_status dawn_wsssp(dawn_graph g, int64_t source, const uint32_t *weights, uint32_t *dist,

@@ -102,3 +102,22 @@ def test_sink_stop_and_errors():
     got, _ = _collect(G, list(range(20)), chunk=9)  # pieces under the limit stream fine
     assert all(np.array_equal(got[i], oracle.bfs_fifo(g.n, g.row_ptr, g.col, i)[0]) for i in range(20))
     torch.cuda.synchronize()
+
+
+def test_dist_u8_compaction():
+    # dawn_dist_u8: 1-byte rows (255 = unreached / overflow with the flag), ragged lengths
+    g = graphgen.kron(11, 16, 11)
+    G = _graph(g)
+    for s in g.sample_sources(3, seed=1):
+        d = dawn.sssp(G, int(s))
+        u8, fl = dawn.dist_u8(d)
+        exp = oracle.bfs_fifo(g.n, g.row_ptr, g.col, int(s))[0]
+        assert np.array_equal(u8.cpu().numpy(), np.where(exp == UNR, 255, exp).astype(np.uint8))
+        assert int(fl[0]) == 0
+    x = torch.tensor([0, 1, 254, 255, 256, -1, 7], dtype=torch.int32, device="cuda")  # n % 4 = 3
+    u8, fl = dawn.dist_u8(x)
+    assert u8.cpu().tolist() == [0, 1, 254, 255, 255, 255, 7] and int(fl[0]) == 1
+    u8, fl = dawn.dist_u8(torch.tensor([3, -1, 2, 9], dtype=torch.int32, device="cuda"))
+    assert u8.cpu().tolist() == [3, 255, 2, 9] and int(fl[0]) == 0
+    with pytest.raises(dawn.DawnError):
+        dawn.dist_u8(torch.zeros(9, dtype=torch.int32, device="cuda")[1:])  # misaligned
