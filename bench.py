@@ -597,26 +597,36 @@ def run_part(args, rank, world, dev, cfg="C4", nsrc=8, steps=3):
     flush = torch.empty(int(2.2 * L2_BYTES) // 4, dtype=torch.int32, device=dev)
     er = []
     for s in srcs:  # E10 counts (global, identical on every rank) + warm-up
-        _, st = dawn.part_sssp(pg, int(s), args.variant, out=out, stats=True)
+        _, st = dawn.part_sssp_fused(pg, int(s), args.variant, out=out, stats=True)
         er.append(dawn.stats_to_dict(st)["edges_reach"])
-    ms = []
-    for _ in range(steps):
-        flush.zero_()
-        torch.cuda.synchronize()
+        dawn.part_sssp(pg, int(s), args.variant, out=out)
+
+    def run(fused):
+        ms = []
+        for _ in range(steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            if world > 1:
+                tdist.barrier()
+            a, b = _events()
+            a.record(stream)
+            for s in srcs:
+                if fused:
+                    dawn.part_sssp_fused(pg, int(s), args.variant, out=out)
+                else:
+                    dawn.part_sssp(pg, int(s), args.variant, out=out)
+            b.record(stream)
+            torch.cuda.synchronize()
+            ms.append(a.elapsed_time(b))
+        tot = sum(ms)
         if world > 1:
-            tdist.barrier()
-        a, b = _events()
-        a.record(stream)
-        for s in srcs:
-            dawn.part_sssp(pg, int(s), args.variant, out=out)
-        b.record(stream)
-        torch.cuda.synchronize()
-        ms.append(a.elapsed_time(b))
-    tot = sum(ms)
-    if world > 1:
-        t = torch.tensor([tot], dtype=torch.float64, device=dev)
-        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
-        tot = float(t.item())
+            t = torch.tensor([tot], dtype=torch.float64, device=dev)
+            tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+            tot = float(t.item())
+        return tot
+
+    tot = run(True)
+    tot_nccl = run(False)
     part_bytes = (pg.workspace.numel() + 8 * (pg.out_rp.numel() + pg.in_rp.numel()) +
                   4 * (pg.out_col.numel() + pg.in_col.numel() + pg.deg.numel()))
     res = {"value": float(sum(er)) * steps / (tot * 1e-3) / 1e9, "unit": "GTEPS",
@@ -624,8 +634,13 @@ def run_part(args, rank, world, dev, cfg="C4", nsrc=8, steps=3):
                        f"vertex-partitioned over {world} rank(s)",
            "ms_per_search": tot / (steps * len(srcs)), "ranks": world, "scaling": "strong",
            "device_bytes_per_rank": int(part_bytes), "partition_build_s": t_build,
-           "how": "dawn_part_begin / (all-gather + dawn_part_step) per level / dawn_part_finish; "
-                  "the host tests convergence every 4 levels; L2 flushed between steps"}
+           "how": "dawn_part_fused_sssp: one persistent kernel per rank and search, frontier "
+                  "slices stored into every rank's receive buffer (CUDA IPC mappings over NVLink "
+                  "at N > 1) with system-scope arrival counters; L2 flushed between steps",
+           "nccl_per_level": {"value": float(sum(er)) * steps / (tot_nccl * 1e-3) / 1e9,
+                              "unit": "GTEPS", "ms_per_search": tot_nccl / (steps * len(srcs)),
+                              "how": "dawn_part_begin / (NCCL all-gather + dawn_part_step) per "
+                                     "level / dawn_part_finish, convergence tested every 4 levels"}}
     del pg, out, flush
     torch.cuda.empty_cache()
     return res

@@ -419,6 +419,29 @@ dawn_status dawn_part_done(dawn_part p, int32_t *done, void *stream);
  * are global (identical on every rank), edges_examined counts this rank's reads. */
 dawn_status dawn_part_finish(dawn_part p, dawn_sssp_stats *stats, void *stream);
 
+/*
+ * Fused exchange (the whole partitioned search in ONE persistent kernel per rank): each level
+ * the rank writes its slice of the next frontier straight into every rank's receive buffer —
+ * plain stores into peer memory over NVLink / NVSwitch, or local memory when ranks share a
+ * device — and then adds 1 to every rank's arrival counter (system-scope release); a rank starts
+ * the next level once all W slices of it landed.  No NCCL call, host round trip or kernel
+ * boundary per level.  All ranks must run dawn_part_fused_sssp concurrently (the kernels wait
+ * for each other): on one device, give each rank a share of the SMs with `grid`.
+ *   dawn_part_fused_peers  every rank's exchange buffer as mapped in this process (rank order,
+ *                          this rank's own included; e.g. CUDA IPC mappings of the peers'
+ *                          buffers): peer_recv[q] = DEVICE uint32[2 * world * slice_words]
+ *                          (dawn_part_exchange's slice_words), zero-initialised;
+ *                          peer_flag[q] = DEVICE uint64 arrival counter, zero-initialised.  The
+ *                          buffers are bound to this handle for its lifetime (the counters are
+ *                          monotonic across searches).
+ *   dawn_part_fused_sssp   one search; dist_own / stats as dawn_part_finish.  grid = CTAs of the
+ *                          cooperative launch (0 = the whole device).  Enqueue only.
+ * Errors: INVALID_ARGUMENT, BOUNDS, CONFIG (peers not set), CUDA. */
+dawn_status dawn_part_fused_peers(dawn_part p, int32_t world, void *const *peer_recv,
+                                  void *const *peer_flag);
+dawn_status dawn_part_fused_sssp(dawn_part p, int64_t source, uint32_t variant, uint32_t *dist_own,
+                                 dawn_sssp_stats *stats, int32_t grid, void *stream);
+
 /* Thread-local description of the last error of this thread ("" if none). */
 const char *dawn_last_error(void);
 

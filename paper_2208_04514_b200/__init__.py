@@ -18,7 +18,8 @@ import numpy as np
 import torch
 
 __all__ = ["build", "Graph", "sssp", "sssp_batch", "msssp", "apsp", "apsp_rows", "apsp_shard",
-           "wsssp", "dist_u8", "part_range", "part_build", "PartGraph", "part_exchange", "part_sssp", "part_sssp_local", "largest_wcc",
+           "wsssp", "dist_u8", "part_range", "part_build", "PartGraph", "part_exchange", "part_sssp", "part_sssp_local",
+           "part_fused_local", "part_sssp_fused", "largest_wcc",
            "check", "DawnError", "UNREACHED", "AUTO", "PUSH", "PULL", "MS_BATCH", "REC_DTYPE",
            "records_to_numpy", "stats_to_dict", "gather_records"]
 
@@ -147,6 +148,10 @@ def lib():
         L.dawn_part_step.argtypes = [vp, vp]
         L.dawn_part_done.restype = st
         L.dawn_part_done.argtypes = [vp, ctypes.POINTER(ctypes.c_int32), vp]
+        L.dawn_part_fused_peers.restype = st
+        L.dawn_part_fused_peers.argtypes = [vp, i32, vp, vp]
+        L.dawn_part_fused_sssp.restype = st
+        L.dawn_part_fused_sssp.argtypes = [vp, i64, u32, vp, vp, i32, vp]
         L.dawn_part_finish.restype = st
         L.dawn_part_finish.argtypes = [vp, vp, vp]
         L.dawn_largest_wcc.restype = st
@@ -502,11 +507,84 @@ class PartGraph:
     def handle(self):
         return self._h
 
+    def xbuffer(self) -> torch.Tensor:
+        """This rank's exchange buffer of the fused path (int32: two receive slots of
+        world x slice_words words, then the 64-bit arrival counter), zero-initialised once."""
+        if getattr(self, "_xbuf", None) is None:
+            self._xbuf = torch.zeros(2 * self.world * self.slice_words + 2, dtype=torch.int32,
+                                     device=self.device)
+        return self._xbuf
+
+    def set_peers(self, bufs: list):
+        """dawn_part_fused_peers from every rank's exchange buffer (as mapped in this process)."""
+        assert len(bufs) == self.world
+        recv = (ctypes.c_void_p * self.world)(*[b.data_ptr() for b in bufs])
+        flag = (ctypes.c_void_p * self.world)(
+            *[b.data_ptr() + 4 * 2 * self.world * self.slice_words for b in bufs])
+        _check(lib().dawn_part_fused_peers(self._h, self.world, recv, flag))
+        self._peers = bufs  # keep the mappings alive
+
     def __del__(self):
         h = getattr(self, "_h", None)
         if h and _lib is not None:
             _lib.dawn_part_destroy(h)
             self._h = None
+
+
+def part_fused_local(parts: list, source: int, variant="auto", stats: bool = False):
+    """The fused exchange with all W ranks on ONE device (each rank's persistent kernel on its
+    own stream and 1/W of the SMs; the slices go through device memory instead of NVLink): the
+    same kernel and protocol as part_sssp_fused across processes.  Returns the global distance
+    vector (int32 [n]) (and the per-rank statistics)."""
+    W = len(parts)
+    key = tuple(id(p) for p in parts)
+    if getattr(parts[0], "_local_peers", None) != key:
+        bufs = [p.xbuffer() for p in parts]
+        for p in parts:
+            p.set_peers(bufs)
+            p._local_peers = key
+    outs = [torch.empty(max(1, p.R), dtype=torch.int32, device=p.device) for p in parts]
+    sts = [torch.zeros(4, dtype=torch.int64, device=p.device) for p in parts] if stats else None
+    nsm = torch.cuda.get_device_properties(parts[0].device).multi_processor_count
+    grid = max(1, 2 * nsm // W)
+    cur = torch.cuda.current_stream()
+    streams = [torch.cuda.Stream(device=parts[0].device) for _ in parts]
+    for i, p in enumerate(parts):
+        streams[i].wait_stream(cur)
+        _check(lib().dawn_part_fused_sssp(p.handle, int(source), _VARIANTS[variant], _dptr(outs[i]),
+                                          _dptr(sts[i]) if stats else None, grid,
+                                          streams[i].cuda_stream))
+    for st_ in streams:
+        cur.wait_stream(st_)
+    d = torch.cat([o[: p.R] for o, p in zip(outs, parts)])
+    return (d, sts) if stats else d
+
+
+def part_sssp_fused(pg: PartGraph, source: int, variant="auto", group=None, out=None,
+                    stats: bool = False, stream=None):
+    """Partitioned SSSP with the fused exchange across processes (one GPU per rank): the first
+    call maps every rank's exchange buffer into this process (CUDA IPC through
+    torch.multiprocessing's tensor sharing, handles exchanged with one all_gather_object), then
+    each search is ONE persistent kernel per rank.  Every rank calls it with the same
+    arguments; returns this rank's distance slice."""
+    if getattr(pg, "_peers", None) is None:
+        if pg.world == 1:
+            pg.set_peers([pg.xbuffer()])
+        else:
+            import torch.distributed as dist
+            from torch.multiprocessing.reductions import reduce_tensor
+            mine = pg.xbuffer()
+            objs = [None] * pg.world
+            dist.all_gather_object(objs, reduce_tensor(mine), group=group)
+            bufs = [mine if q == pg.rank else fn(*args) for q, (fn, args) in enumerate(objs)]
+            pg.set_peers(bufs)
+            dist.barrier(group=group)
+    dist_t = out if out is not None else torch.empty(max(1, pg.R), dtype=torch.int32, device=pg.device)
+    st = torch.zeros(4, dtype=torch.int64, device=pg.device) if stats else None
+    _check(lib().dawn_part_fused_sssp(pg.handle, int(source), _VARIANTS[variant], _dptr(dist_t),
+                                      _dptr(st), 0, _stream(stream)))
+    d = dist_t[: pg.R]
+    return (d, st) if stats else d
 
 
 def part_exchange(pg: PartGraph, group=None):

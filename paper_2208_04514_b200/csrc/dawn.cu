@@ -1342,7 +1342,7 @@ dawn_status part_build(int64_t n, int64_t m, const int64_t *row_ptr, const int32
 
 struct PartLayout {
   size_t rp, irp, hout_bits, hout_v, hout_s, hout_e, hin_bits, hin_v, hin_s, hin_e;
-  size_t scan_tmp, piece_tmp, vis, lev, send, recv, ctrl, total;
+  size_t scan_tmp, piece_tmp, vis, cand, lev, send, recv, ctrl, icol2, total;
   uint64_t capHP;
 };
 
@@ -1369,6 +1369,8 @@ PartLayout part_layout(int64_t n, int64_t m_r, int32_t world, int64_t R, int64_t
   L.scan_tmp = take(4 * ((size_t)std::max(n, R) / kScanBlock + 2));
   L.piece_tmp = take(4 * (3 * ((size_t)m_r / kHPiece + 3) + 1));
   L.vis = take(4 * (size_t)((R + 31) / 32 + 1));
+  L.cand = take(4 * (size_t)((R + 31) / 32 + 1));
+  L.icol2 = take(4 * (size_t)m_r);  // in-rows with their highest-degree sources first
   L.lev = take((size_t)R + 8);
   L.send = take(4 * S);
   L.recv = take(4 * S * (size_t)world);
@@ -1390,6 +1392,10 @@ struct dawn_part_s {
   uint32_t *dist = nullptr;
   uint32_t steps = 0, src_local = 0xffffffffu, variant = 0;
   float alpha = 2.f, beta = 96.f;
+  int fused_grid = 0;                   // full-device cooperative grid of k_part_fused
+  bool have_peers = false;
+  uint32_t *peer_recv[kPartMaxW] = {};
+  unsigned long long *peer_flag[kPartMaxW] = {};
 };
 
 namespace {
@@ -1404,6 +1410,7 @@ PartParams part_params(dawn_part p) {
   q.S = (uint32_t)(kPartHdr + p->Rmax / 32);
   q.nwg = (uint32_t)((p->n + 31) / 32);
   q.src_local = p->src_local;
+  q.rank = (uint32_t)p->rank;
   auto u32 = [&](size_t off) { return reinterpret_cast<uint32_t *>(p->ws + off); };
   q.rp = u32(p->L.rp);
   q.col = p->col;
@@ -1419,6 +1426,7 @@ PartParams part_params(dawn_part p) {
   q.hin_e = u32(p->L.hin_e);
   q.hin_bits = u32(p->L.hin_bits);
   q.vis = u32(p->L.vis);
+  q.cand = u32(p->L.cand);
   q.lev = reinterpret_cast<uint8_t *>(p->ws + p->L.lev);
   q.dist = p->dist;
   q.recv = u32(p->L.recv);
@@ -1471,7 +1479,7 @@ dawn_status part_load(int64_t n, int64_t m, int32_t world, int32_t rank, int64_t
   p->ws = static_cast<char *>(workspace);
   p->L = L;
   p->col = out_col;
-  p->icol = in_col;
+  p->icol = m_r ? reinterpret_cast<int32_t *>(p->ws + L.icol2) : in_col;
   p->deg = own_deg;
   cudaDeviceGetAttribute(&p->nsm, cudaDevAttrMultiProcessorCount, pa.device);
   int bps = 0;
@@ -1484,6 +1492,12 @@ dawn_status part_load(int64_t n, int64_t m, int32_t world, int32_t rank, int64_t
   k_offsets32<<<blocks, 256, 0, st>>>(in_rp, u32(L.irp), R + 1);
   PartCtrl *C = reinterpret_cast<PartCtrl *>(p->ws + L.ctrl);
   cudaMemsetAsync(C, 0, sizeof(PartCtrl), st);
+  cudaMemsetAsync(p->ws + L.cand, 0, 4 * (size_t)((R + 31) / 32 + 1), st);
+  {
+    int fb = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fb, k_part_fused<kNT>, kNT, 0);
+    p->fused_grid = std::max(1, p->nsm * std::max(1, std::min(fb, 2)));
+  }
   // static heavy pieces of the out-slice rows (over n sources) and of the in-rows (over R)
   auto build_list = [&](const uint32_t *rows, uint32_t nrows, size_t bits, size_t hv, size_t hs,
                         size_t he, uint32_t *count) {
@@ -1504,6 +1518,12 @@ dawn_status part_load(int64_t n, int64_t m, int32_t world, int32_t rank, int64_t
     k_hbase<<<1, 32, 0, st>>>(hc, base, cursor, maxc);
     k_hfill<<<hb, 256, 0, st>>>(rows, nrows, base, cursor, u32(hv), u32(hs), u32(he));
   };
+  // pull probes meet hubs first: each in-row with its 8 sources of largest out-slice degree (a
+  // proxy of the global out-degree: labels are random, so a vertex sends ~1/W of its arcs
+  // to every range) moved to the front, as k_sssp's degree-ordered in-rows
+  if (m_r > 0 && R > 0)
+    k_topk_rows<<<p->nsm * 8, 256, 0, st>>>(u32(L.irp), in_col, u32(L.rp), (uint32_t)R,
+                                            reinterpret_cast<int32_t *>(p->ws + L.icol2));
   build_list(u32(L.rp), (uint32_t)n, L.hout_bits, L.hout_v, L.hout_s, L.hout_e, &C->n_hp[0]);
   build_list(u32(L.irp), (uint32_t)R, L.hin_bits, L.hin_v, L.hin_s, L.hin_e, &C->n_hp[1]);
   if ((e = cudaStreamSynchronize(st)) != cudaSuccess || (e = cudaGetLastError()) != cudaSuccess) {
@@ -1568,6 +1588,47 @@ dawn_status part_done(dawn_part p, int32_t *done, void *stream) {
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) return cuda_fail(e, "dawn_part_done");
   *done = (int32_t)d;
+  return DAWN_OK;
+}
+
+dawn_status part_fused_peers(dawn_part p, int32_t world, void *const *peer_recv,
+                             void *const *peer_flag) {
+  if (!p || !peer_recv || !peer_flag) return fail(DAWN_ERR_INVALID_ARGUMENT, "NULL argument");
+  if (world != p->world || world > kPartMaxW)
+    return fail(DAWN_ERR_INVALID_ARGUMENT, "world must equal the partition's (<= %d)", kPartMaxW);
+  for (int q = 0; q < world; ++q) {
+    if (!peer_recv[q] || !peer_flag[q]) return fail(DAWN_ERR_INVALID_ARGUMENT, "NULL peer pointer");
+    p->peer_recv[q] = static_cast<uint32_t *>(peer_recv[q]);
+    p->peer_flag[q] = static_cast<unsigned long long *>(peer_flag[q]);
+  }
+  p->have_peers = true;
+  return DAWN_OK;
+}
+
+dawn_status part_fused_sssp(dawn_part p, int64_t source, uint32_t variant, uint32_t *dist,
+                            dawn_sssp_stats *stats, int32_t grid, void *stream) {
+  if (!p || (p->R > 0 && !dist)) return fail(DAWN_ERR_INVALID_ARGUMENT, "part or dist is NULL");
+  if (!p->have_peers) return fail(DAWN_ERR_CONFIG, "dawn_part_fused_peers was not called");
+  if (variant > DAWN_PULL) return fail(DAWN_ERR_INVALID_ARGUMENT, "unknown variant");
+  if (source < 0 || source >= p->n)
+    return fail(DAWN_ERR_BOUNDS, "source %lld not in [0, n)", (long long)source);
+  if (grid < 0 || grid > p->fused_grid)
+    return fail(DAWN_ERR_INVALID_ARGUMENT, "grid must be in [0, %d]", p->fused_grid);
+  cudaError_t e = cudaSetDevice(p->device);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+  p->dist = dist;
+  p->variant = variant;
+  p->src_local = (source >= p->lo && source < p->lo + p->R) ? (uint32_t)(source - p->lo) : 0xffffffffu;
+  PartParams q = part_params(p);
+  PartPeers peers{};
+  for (int r = 0; r < p->world; ++r) {
+    peers.recv[r] = p->peer_recv[r];
+    peers.flag[r] = p->peer_flag[r];
+  }
+  void *args[] = {&q, &peers, &stats};
+  e = cudaLaunchCooperativeKernel((const void *)k_part_fused<kNT>, dim3(grid ? grid : p->fused_grid),
+                                  dim3(kNT), args, 0, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "k_part_fused launch");
   return DAWN_OK;
 }
 
@@ -1723,6 +1784,16 @@ dawn_status dawn_part_step(dawn_part p, void *stream) { DAWN_GUARD(return part_s
 
 dawn_status dawn_part_done(dawn_part p, int32_t *done, void *stream) {
   DAWN_GUARD(return part_done(p, done, stream);)
+}
+
+dawn_status dawn_part_fused_peers(dawn_part p, int32_t world, void *const *peer_recv,
+                                  void *const *peer_flag) {
+  DAWN_GUARD(return part_fused_peers(p, world, peer_recv, peer_flag);)
+}
+
+dawn_status dawn_part_fused_sssp(dawn_part p, int64_t source, uint32_t variant, uint32_t *dist_own,
+                                 dawn_sssp_stats *stats, int32_t grid, void *stream) {
+  DAWN_GUARD(return part_fused_sssp(p, source, variant, dist_own, stats, grid, stream);)
 }
 
 dawn_status dawn_part_finish(dawn_part p, dawn_sssp_stats *stats, void *stream) {

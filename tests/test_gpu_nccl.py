@@ -74,6 +74,9 @@ def _part_worker(rank, world, port, out_dir):
             d = dawn.part_sssp(pg, int(s), v)              # one NCCL all-gather per level
             torch.cuda.synchronize()
             np.save(os.path.join(out_dir, f"part_{rank}_{i}_{v}.npy"), d.cpu().numpy())
+            f = dawn.part_sssp_fused(pg, int(s), v)        # fused: peer stores over IPC mappings
+            torch.cuda.synchronize()
+            np.save(os.path.join(out_dir, f"fused_{rank}_{i}_{v}.npy"), f.cpu().numpy())
     dist.barrier()
     dist.destroy_process_group()
 
@@ -88,6 +91,7 @@ def test_partitioned_sssp_nccl_all_visible_gpus(tmp_path):
     for i, s in enumerate(g.sample_sources(3, seed=5)):
         exp, _ = oracle.bfs_fifo(g.n, g.row_ptr, g.col, int(s))
         for v in ("auto", "push", "pull"):
-            got = np.concatenate([np.load(tmp_path / f"part_{r}_{i}_{v}.npy")[: dawn.part_range(g.n, world, r)[1] - dawn.part_range(g.n, world, r)[0]]
-                                  for r in range(world)]).view(np.uint32)
-            assert np.array_equal(got, exp), (world, s, v)
+            for tag in ("part", "fused"):
+                got = np.concatenate([np.load(tmp_path / f"{tag}_{r}_{i}_{v}.npy")[: dawn.part_range(g.n, world, r)[1] - dawn.part_range(g.n, world, r)[0]]
+                                      for r in range(world)]).view(np.uint32)
+                assert np.array_equal(got, exp), (tag, world, s, v)

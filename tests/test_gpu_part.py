@@ -96,3 +96,55 @@ def test_matches_single_gpu_path_c2_sampled():
         b = dawn.sssp(G, int(s))
         assert torch.equal(a, b), s
     torch.cuda.synchronize()
+
+
+# ---- fused exchange: the whole search in one persistent kernel per rank, slices written into
+# ---- every rank's receive buffer, system-scope arrival counters (no host work per level)
+def _check_fused(g, parts, sources, variants=VARIANTS):
+    for s in sources:
+        exp, _ = oracle.bfs_fifo(g.n, g.row_ptr, g.col, int(s))
+        rec, er = oracle.record(g.n, g.row_ptr, int(s), exp)
+        for v in variants:
+            d, sts = dawn.part_fused_local(parts, int(s), v, stats=True)
+            torch.cuda.synchronize()
+            d = d.cpu().numpy().view(np.uint32)
+            bad = np.nonzero(d != exp)[0]
+            assert len(bad) == 0, (g.name, len(parts), s, v, bad[:5], d[bad[:5]], exp[bad[:5]])
+            for st in sts:
+                x = dawn.stats_to_dict(st)
+                assert x["levels"] == int(rec["ecc"]) and x["reached"] == int(rec["reached"])
+                assert x["edges_reach"] == er, (s, v, x, er)
+
+
+@pytest.mark.parametrize("W", [1, 2, 3, 4])
+def test_fused_kron(W):
+    g = graphgen.kron(12, 16, 12)
+    _check_fused(g, _parts(g, W), g.sample_sources(4, seed=W))  # 12 searches on one set of
+                                                                # counters (monotonic across)
+
+
+def test_fused_directed_hubs_deep_edges():
+    g = graphgen.er(1000, 8000, 1)
+    _check_fused(g, _parts(g, 3), [0, 999])
+    rng = np.random.default_rng(3)
+    n = 5000
+    e = [(0, v) for v in range(1, n)] + [(v, 0) for v in range(1, n)]
+    e += [(int(a), int(b)) for a, b in rng.integers(0, n, size=(20000, 2)) if a != b]
+    h = graphgen.from_edges(n, e)
+    _check_fused(h, _parts(h, 2), [0, 123])
+    p = graphgen.from_edges(600, [(i, i + 1) for i in range(599)])  # 599 levels, 255+ direct
+    _check_fused(p, _parts(p, 3), [0], variants=("auto", "push"))
+    g40 = graphgen.from_edges(40, [(i, (i * 7 + 3) % 40) for i in range(40)] + [(3, 4), (4, 3)])
+    _check_fused(g40, _parts(g40, 4), [0, 39])  # two ranks own nothing
+    g1 = graphgen.from_edges(1, [])
+    assert dawn.part_fused_local(_parts(g1, 2), 0).cpu().numpy().view(np.uint32).tolist() == [0]
+
+
+def test_fused_c2_matches_single_gpu():
+    g = graphgen.config_graph("C2")
+    G = dawn.Graph(g.row_ptr, g.col, True)
+    parts = _parts(g, 2)
+    for s in g.sample_sources(3, seed=9):
+        a = dawn.part_fused_local(parts, int(s))
+        assert torch.equal(a, dawn.sssp(G, int(s))), s
+    torch.cuda.synchronize()
