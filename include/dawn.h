@@ -33,7 +33,9 @@ extern "C" {
 #define DAWN_UNREACHED 0xFFFFFFFFu
 /* Sources per pass of the bit-parallel multi-source kernel (4 x 64-bit words per vertex) and the
  * unit of the APSP shard rule. */
+#ifndef DAWN_MS_BATCH
 #define DAWN_MS_BATCH 256
+#endif
 
 typedef enum {
   DAWN_OK = 0,

@@ -483,11 +483,11 @@ dawn_status load_csr(int64_t n, int64_t m, const int64_t *row_ptr, const int32_t
   }
   g->wsssp_grid = grid_for((const void *)k_wsssp<kNT>, g->nsm);
   if (!g->lean) {
-    cudaFuncSetAttribute((const void *)k_ms64<kNT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)ms_smem_bytes(kNT));
+    cudaFuncSetAttribute((const void *)k_ms64<kMsNT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)ms_smem_bytes(kMsNT));
     int bps = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, (const void *)k_ms64<kNT>, kNT,
-                                                  ms_smem_bytes(kNT));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, (const void *)k_ms64<kMsNT>, kMsNT,
+                                                  ms_smem_bytes(kMsNT));
     bps = std::max(1, std::min(bps, kMsBlocksPerSm));
     g->ms_grid = std::min<int>(g->nsm * bps, (int)kMaxBlocks);
   }
@@ -920,8 +920,8 @@ dawn_status launch_ms_lane(dawn_graph g, int l, const uint32_t *src, size_t cnt,
   p.trace = (g->trace && l == 0) ? at<TraceRec>(g, L.trace) : nullptr;
   p.trace_n = &at<Ctrl>(g, L.ctrl)->trace_n;
   void *args[] = {&p};
-  e = cudaLaunchCooperativeKernel((const void *)k_ms64<kNT>, dim3(grid), dim3(kNT), args,
-                                  ms_smem_bytes(kNT), st);
+  e = cudaLaunchCooperativeKernel((const void *)k_ms64<kMsNT>, dim3(grid), dim3(kMsNT), args,
+                                  ms_smem_bytes(kMsNT), st);
   if (e != cudaSuccess) return cuda_fail(e, "k_ms64 launch");
   return DAWN_OK;
 }

@@ -42,7 +42,14 @@ constexpr uint32_t kNarrowVisBytes = 160 * 1024;   // max visited-slice bytes pe
 constexpr uint64_t kNarrowMaxN = (uint64_t)kNarrowCluster * kNarrowVisBytes * 8;  // 20,971,520
 constexpr uint32_t kNarrowMaxAvgDeg = 8;           // arc array kept when m <= 8 n
 // Multi-source kernel: kMsW 64-bit words per vertex = kMsBatch sources per adjacency pass.
-constexpr int kMsW = 4;
+#ifndef DAWN_MS_W
+#define DAWN_MS_W 4  // 64-bit words per vertex of the multi-source kernel
+#endif
+#ifndef DAWN_MS_NT
+#define DAWN_MS_NT 512  // threads per CTA of k_ms64
+#endif
+constexpr int kMsW = DAWN_MS_W;
+constexpr int kMsNT = DAWN_MS_NT;
 constexpr uint32_t kMsBatch = 64 * kMsW;
 
 static_assert(kMsBatch == DAWN_MS_BATCH, "dawn.h DAWN_MS_BATCH must match kMsW");
