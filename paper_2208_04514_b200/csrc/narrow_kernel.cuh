@@ -97,7 +97,8 @@ struct NarrowCtl {
   // slot [b][r] = (CTA r's discoveries | overflow << 31, their out-degree sum)
   uint2 x[2][kNarrowCluster];
   unsigned long long mbar[2];     // level barrier b = L & 1 (phase parity (L >> 1) & 1)
-  uint32_t nbig;                  // rows of > 16 arcs this level (expanded by the whole CTA)
+  uint32_t nbig[2];               // rows of > 16 arcs of level L in nbig[L & 1] (expanded by the
+                                  // whole CTA); level L resets nbig[(L+1) & 1], last read at L-1
   uint4 big[kNarrowBig];          // (vertex, row start, row end, discoverer)
 };
 constexpr size_t kNarrowCtlBytes = (sizeof(NarrowCtl) + 255) & ~size_t(255);
@@ -333,7 +334,7 @@ __global__ void __launch_bounds__(kNarrowThreads, 1) k_narrow(NarrowParams p) {
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     S.qn[0] = S.qn[1] = 0;
     S.n_new = S.m_new = S.ovf = 0;
-    S.nbig = 0;
+    S.nbig[0] = S.nbig[1] = 0;
     if (((src >> 5) % kNarrowCluster) == rank && re0 > rs0) {  // the source's owner queues it
       qbuf0[0] = make_uint4(src, rs0, re0, 0x7fffffffu);
       S.qn[0] = 1;
@@ -425,7 +426,7 @@ __global__ void __launch_bounds__(kNarrowThreads, 1) k_narrow(NarrowParams p) {
         const uint4 eb = make_uint4(__shfl_sync(DAWN_FULL, e.x, k), __shfl_sync(DAWN_FULL, e.y, k),
                                     __shfl_sync(DAWN_FULL, e.z, k), __shfl_sync(DAWN_FULL, skip, k));
         uint32_t slot = 0;
-        if (lane == 0) slot = atomicAdd(&S.nbig, 1u);
+        if (lane == 0) slot = atomicAdd(&S.nbig[L & 1], 1u);
         slot = __shfl_sync(DAWN_FULL, slot, 0);
         if (slot < kNarrowBig) {
           if (lane == 0) S.big[slot] = eb;
@@ -451,8 +452,8 @@ __global__ void __launch_bounds__(kNarrowThreads, 1) k_narrow(NarrowParams p) {
     };
     fold();
     __syncthreads();
-    if (S.nbig) {  // uniform after the barrier: listed long rows, one arc per thread per round
-      const uint32_t nb = min(S.nbig, kNarrowBig);
+    if (S.nbig[L & 1]) {  // uniform after the barrier: listed long rows, one arc per thread per round
+      const uint32_t nb = min(S.nbig[L & 1], kNarrowBig);
       for (uint32_t b = 0; b < nb; ++b) {
         const uint4 eb = S.big[b];
         for (uint32_t j0 = eb.y + warp * 32; j0 < eb.z; j0 += kNarrowThreads) {
@@ -484,7 +485,7 @@ __global__ void __launch_bounds__(kNarrowThreads, 1) k_narrow(NarrowParams p) {
       // (peers append to it only after this level's barrier, which needs this CTA's slot)
       if (lane == 31) {
         S.n_new = S.m_new = S.ovf = 0;  // this level's local totals are sent below
-        S.nbig = 0;
+        S.nbig[(L + 1) & 1] = 0;  // read for the last time at level L-1 (before its barrier)
         S.qn[cur] = 0;
       }
       __syncwarp();

@@ -897,6 +897,7 @@ __global__ void __launch_bounds__(NT, MINB) k_sssp(SsspParams p) {
     if (st.solo) {
       // ---- solo stretch: narrow push levels on CTA 0 with __syncthreads only
       if (blockIdx.x != 0) {
+        __syncthreads();  // every thread has read st.stop / st.solo before thread 0 rewrites st
         if ((MINB == 1 || DAWN_MINB2_EXTRAS) && si + 1 < nsrc && !prefilled) {
           // idle while CTA 0 runs the narrow levels: initialise this CTA's share of the next
           // search's distance row (independent memory; its source entry is set at its init)
