@@ -1596,8 +1596,25 @@ dawn_status part_fused_peers(dawn_part p, int32_t world, void *const *peer_recv,
   if (!p || !peer_recv || !peer_flag) return fail(DAWN_ERR_INVALID_ARGUMENT, "NULL argument");
   if (world != p->world || world > kPartMaxW)
     return fail(DAWN_ERR_INVALID_ARGUMENT, "world must equal the partition's (<= %d)", kPartMaxW);
+  cudaError_t e = cudaSetDevice(p->device);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
   for (int q = 0; q < world; ++q) {
     if (!peer_recv[q] || !peer_flag[q]) return fail(DAWN_ERR_INVALID_ARGUMENT, "NULL peer pointer");
+    // a buffer on another device (a CUDA-IPC mapping of a peer's buffer) needs peer access
+    cudaPointerAttributes pa{};
+    if ((e = cudaPointerGetAttributes(&pa, peer_recv[q])) != cudaSuccess)
+      return cuda_fail(e, "cudaPointerGetAttributes(peer buffer)");
+    if (pa.type == cudaMemoryTypeDevice && pa.device != p->device) {
+      int can = 0;
+      cudaDeviceCanAccessPeer(&can, p->device, pa.device);
+      if (!can) return fail(DAWN_ERR_CONFIG, "device %d cannot access peer device %d", p->device, pa.device);
+      e = cudaDeviceEnablePeerAccess(pa.device, 0);
+      if (e == cudaErrorPeerAccessAlreadyEnabled) {
+        cudaGetLastError();
+      } else if (e != cudaSuccess) {
+        return cuda_fail(e, "cudaDeviceEnablePeerAccess");
+      }
+    }
     p->peer_recv[q] = static_cast<uint32_t *>(peer_recv[q]);
     p->peer_flag[q] = static_cast<unsigned long long *>(peer_flag[q]);
   }
