@@ -209,6 +209,20 @@ def search_stats(G, srcs, variant, out):
     return rows
 
 
+def memory_footprint(g):
+    """Device bytes of the graph residency (PAPER L312-323 memory frugality): the caller's CSR
+    (+ CSC for directed graphs) and dawn_workspace_bytes for the default and the lean handle."""
+    import paper_2208_04514_b200 as dawn
+    L = dawn.lib()
+    flags = 1 if g.symmetric else 0
+    csr = 8 * (g.n + 1) + 4 * g.m
+    return {"csr_bytes": int(csr if g.symmetric else 2 * csr),
+            "workspace_bytes": int(L.dawn_workspace_bytes(g.n, g.m, flags)),
+            "lean_workspace_bytes": int(L.dawn_workspace_bytes(g.n, g.m, flags | 8)),
+            "note": "default = degree-ordered in-rows, bit-parallel words, 8 batch lanes' state; "
+                    "lean (DAWN_GRAPH_LEAN) = one search's state, same distances"}
+
+
 def level_floor(dev, flush, stream, levels: int):
     """C3's latency floor, measured in the same run through the same kernels: one SSSP on a
     directed path with `levels` + 1 vertices (one vertex and one arc per level: nothing but the
@@ -323,7 +337,8 @@ def run_sssp(args, rank, world, dev, cfg, steps, warmup, e2e=True, with_cpu=Fals
         "single_search": {"median_us": lat_med * 1e3, "calls": len(lat),
                           "gteps": float(np.mean(er[:len(lat)])) / (lat_med * 1e-3) / 1e9},
         "clocks": clk.summary(),
-        "gpu_launches_per_step": 2 * k if cfg == "C3" else 1,
+        "gpu_launches_per_step": 2 * k if cfg == "C3" else (min(k, int(G.get_tuning("batch_lanes"))) if k > 1 else 1),
+        "memory": memory_footprint(g),
     }
     if cfg == "C1":
         # context only: 64 concurrent copies of the search on 64 CTAs (k_small per CTA)
@@ -541,7 +556,7 @@ def run_apsp(args, rank, world, dev, steps, warmup, with_cpu=False):
         "check": {"all_reached_S_wcc_minus_1":
                   bool(np.all(dawn.records_to_numpy(rec)["reached"] == k - 1))},
         "clocks": clk.summary(),
-        "gpu_launches_per_step": 1,
+        "gpu_launches_per_step": min(-(-k // dawn.MS_BATCH), int(G.get_tuning("ms_lanes"))),
     }
     # e2e: host source list in, records out to host (the API a user calls)
     host_rec = torch.empty((k if world > 1 else mine, 4), dtype=torch.int64, pin_memory=True)

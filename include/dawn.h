@@ -200,6 +200,8 @@ typedef enum {
 
 /* Set one tunable (INVALID_ARGUMENT for an unknown key or a negative value). */
 dawn_status dawn_graph_set_param(dawn_graph g, dawn_param key, double value);
+/* Read one tunable's current value (the load-time default until set). */
+dawn_status dawn_graph_get_param(dawn_graph g, dawn_param key, double *value);
 
 /*
  * Single-source shortest paths (SSSP), one enqueue: initialisation, every level (push or

@@ -98,6 +98,8 @@ def lib():
                                           ctypes.POINTER(vp)]
         L.dawn_graph_destroy.restype = st
         L.dawn_graph_destroy.argtypes = [vp]
+        L.dawn_graph_get_param.restype = st
+        L.dawn_graph_get_param.argtypes = [vp, ctypes.c_int, ctypes.POINTER(ctypes.c_double)]
         L.dawn_graph_set_param.restype = st
         L.dawn_graph_set_param.argtypes = [vp, ctypes.c_int, ctypes.c_double]
         L.dawn_sssp.restype = st
@@ -235,6 +237,12 @@ class Graph:
     _PARAMS = {"alpha": 0, "beta": 1, "ms_alpha": 2, "bitmap_push_edges": 3, "solo_edges": 4,
                "cluster_start": 5, "cluster_handover_edges": 6, "bitmap_push_grow_edges": 7,
                "narrow_queue_cap": 8, "batch_lanes": 9, "dense_max_entries": 10, "ms_lanes": 11, "weight_delta": 12}
+
+    def get_tuning(self, key: str) -> float:
+        """dawn_graph_get_param (e.g. "batch_lanes", "ms_lanes")."""
+        v = ctypes.c_double(0)
+        _check(lib().dawn_graph_get_param(self._h, self._PARAMS[key], ctypes.byref(v)))
+        return v.value
 
     def set_tuning(self, **kw):
         """dawn_graph_set_param for each keyword (alpha, beta, ms_alpha, bitmap_push_edges,

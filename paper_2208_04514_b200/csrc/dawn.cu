@@ -1689,6 +1689,28 @@ dawn_status dawn_graph_destroy(dawn_graph g) {
   return DAWN_OK;
 }
 
+dawn_status dawn_graph_get_param(dawn_graph g, dawn_param key, double *value) {
+  DAWN_GUARD(
+    if (!g || !value) return fail(DAWN_ERR_INVALID_ARGUMENT, "graph or value is NULL");
+    switch (key) {
+      case DAWN_PARAM_ALPHA: *value = g->alpha; break;
+      case DAWN_PARAM_BETA: *value = g->beta; break;
+      case DAWN_PARAM_MS_ALPHA: *value = g->ms_alpha; break;
+      case DAWN_PARAM_BITMAP_PUSH_EDGES: *value = g->bmpush_e; break;
+      case DAWN_PARAM_SOLO_EDGES: *value = g->solo_e; break;
+      case DAWN_PARAM_CLUSTER_START: *value = g->cluster_start; break;
+      case DAWN_PARAM_CLUSTER_HANDOVER_EDGES: *value = (double)g->handover_m; break;
+      case DAWN_PARAM_BITMAP_PUSH_GROW_EDGES: *value = g->bmpush_grow; break;
+      case DAWN_PARAM_NARROW_QUEUE_CAP: *value = g->narrow_qcap; break;
+      case DAWN_PARAM_BATCH_LANES: *value = g->lanes; break;
+      case DAWN_PARAM_DENSE_MAX_ENTRIES: *value = g->dense_max; break;
+      case DAWN_PARAM_MS_LANES: *value = g->ms_lanes; break;
+      case DAWN_PARAM_WEIGHT_DELTA: *value = g->wdelta; break;
+      default: return fail(DAWN_ERR_INVALID_ARGUMENT, "unknown parameter");
+    }
+    return DAWN_OK;)
+}
+
 dawn_status dawn_graph_set_param(dawn_graph g, dawn_param key, double value) {
   DAWN_GUARD(return set_param(g, key, value);)
 }
