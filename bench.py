@@ -539,7 +539,7 @@ def run_apsp(args, rank, world, dev, steps, warmup, with_cpu=False):
         "batch": dawn.MS_BATCH, "per_rank": per_rank,
         "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
                      "frac": ach / peak, "peak_kind": peak_kind,
-                     "kernel": "k_ms64 (one persistent launch per rank per step)",
+                     "kernel": "k_ms64 (one persistent launch per multi-source lane per rank and step)",
                      "bytes_model": "B_exec = 96*n*levels + 36*gathered + 8*reductions "
                                     "(executed word traffic, kernel counters)",
                      "exec_bytes_per_step": b_exec / steps,
