@@ -1342,7 +1342,7 @@ dawn_status part_build(int64_t n, int64_t m, const int64_t *row_ptr, const int32
 
 struct PartLayout {
   size_t rp, irp, hout_bits, hout_v, hout_s, hout_e, hin_bits, hin_v, hin_s, hin_e;
-  size_t scan_tmp, piece_tmp, vis, cand, lev, send, recv, ctrl, icol2, total;
+  size_t scan_tmp, piece_tmp, vis, cand, lev, send, recv, ctrl, icol2, hasin, ulist, useg, total;
   uint64_t capHP;
 };
 
@@ -1371,6 +1371,9 @@ PartLayout part_layout(int64_t n, int64_t m_r, int32_t world, int64_t R, int64_t
   L.vis = take(4 * (size_t)((R + 31) / 32 + 1));
   L.cand = take(4 * (size_t)((R + 31) / 32 + 1));
   L.icol2 = take(4 * (size_t)m_r);  // in-rows with their highest-degree sources first
+  L.hasin = take(4 * (size_t)R + 4);  // owned vertices with an in-edge (the first pull's list)
+  L.ulist = take(4 * (size_t)R + 4);  // unreached survivors, per-warp segments
+  L.useg = take(4 * (size_t)kMaxBlocks * 32);
   L.lev = take((size_t)R + 8);
   L.send = take(4 * S);
   L.recv = take(4 * S * (size_t)world);
@@ -1391,6 +1394,7 @@ struct dawn_part_s {
   const uint32_t *deg = nullptr;
   uint32_t *dist = nullptr;
   uint32_t steps = 0, src_local = 0xffffffffu, variant = 0;
+  uint32_t n_has = 0;
   float alpha = 2.f, beta = 96.f;
   int fused_grid = 0;                   // full-device cooperative grid of k_part_fused
   bool have_peers = false;
@@ -1427,6 +1431,10 @@ PartParams part_params(dawn_part p) {
   q.hin_bits = u32(p->L.hin_bits);
   q.vis = u32(p->L.vis);
   q.cand = u32(p->L.cand);
+  q.hasin = u32(p->L.hasin);
+  q.ulist = u32(p->L.ulist);
+  q.useg = u32(p->L.useg);
+  q.n_has = p->n_has;
   q.lev = reinterpret_cast<uint8_t *>(p->ws + p->L.lev);
   q.dist = p->dist;
   q.recv = u32(p->L.recv);
@@ -1524,6 +1532,13 @@ dawn_status part_load(int64_t n, int64_t m, int32_t world, int32_t rank, int64_t
   if (m_r > 0 && R > 0)
     k_topk_rows<<<p->nsm * 8, 256, 0, st>>>(u32(L.irp), in_col, u32(L.rp), (uint32_t)R,
                                             reinterpret_cast<int32_t *>(p->ws + L.icol2));
+  if (R > 0) {  // static ascending list of the owned vertices with an in-edge
+    const uint32_t nblk = (uint32_t)((R + kScanBlock - 1) / kScanBlock);
+    k_lcount<<<nblk, 256, 0, st>>>(u32(L.irp), (uint32_t)R, u32(L.scan_tmp));
+    k_hscan<<<1, 32, 0, st>>>(u32(L.scan_tmp), nblk, u32(L.useg));  // total -> useg[0]
+    k_lfill<<<nblk, 256, 0, st>>>(u32(L.irp), (uint32_t)R, u32(L.scan_tmp), u32(L.hasin));
+    cudaMemcpyAsync(&p->n_has, u32(L.useg), 4, cudaMemcpyDeviceToHost, st);
+  }
   build_list(u32(L.rp), (uint32_t)n, L.hout_bits, L.hout_v, L.hout_s, L.hout_e, &C->n_hp[0]);
   build_list(u32(L.irp), (uint32_t)R, L.hin_bits, L.hin_v, L.hin_s, L.hin_e, &C->n_hp[1]);
   if ((e = cudaStreamSynchronize(st)) != cudaSuccess || (e = cudaGetLastError()) != cudaSuccess) {

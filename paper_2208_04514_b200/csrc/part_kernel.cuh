@@ -50,6 +50,9 @@ struct PartParams {
   const uint32_t *hin_v, *hin_s, *hin_e, *hin_bits;      // in-rows > kHeavy: pieces
   uint32_t *vis;                      // owned vertices reached so far (bitmap)
   uint32_t *cand;                     // candidate bitmap of wide push levels (zero between uses)
+  const uint32_t *hasin;              // owned vertices with an in-edge, ascending (n_has)
+  uint32_t *ulist, *useg;             // unreached list in per-warp segments, segment counts
+  uint32_t n_has;
   uint8_t *lev;                       // deferred distances (as k_sssp: byte L+1, 255 = direct)
   uint32_t *dist;                     // caller's distance slice [R]
   const uint32_t *recv;               // gathered slices of F_L: world x S words
@@ -147,6 +150,7 @@ __device__ __forceinline__ void part_settle(const PartParams &p, uint32_t *sd, u
 __device__ __forceinline__ void part_header(const PartParams &p, const uint32_t *rv, uint32_t L,
                                             PartState &st) {
   if (st.done) return;
+  if (L > 0 && st.dir == kPull) st.pad2 = 1;  // a pull level ran: the unreached list is compacted
   uint32_t nf = 0;
   unsigned long long mf = 0;
   for (uint32_t q = 0; q < p.world; ++q) {
@@ -250,25 +254,33 @@ __device__ void part_work(const PartParams &p, const PartState &st, uint32_t L, 
       }
     }
   } else {
-    // (a) light in-rows: a warp takes two vis words (2 x 32 owned vertices, two per lane, both
-    //     chains in flight) and scans each unreached vertex's in-row until the first in-neighbour
-    //     in F_L (early exit, Eq. 4), 4 independent probes per round trip
+    // (a) light in-rows over the warp's segment of the unreached list (the static list of owned
+    //     vertices with an in-edge at the first pull level, the warp's compacted survivors after;
+    //     as k_sssp's pull): two vertices per lane in flight, each scanning its in-row until the
+    //     first in-neighbour in F_L (early exit, Eq. 4), 4 independent probes per round trip.
+    //     Vertices with heavy in-rows are left to the pieces but stay in the list while unreached.
     constexpr int PJ = 2;
-    const uint32_t nwo = (p.R + 31) / 32;
-    for (uint32_t w0 = gwarp * PJ; w0 < nwo; w0 += nwarps * PJ) {
-      uint32_t t[PJ], s[PJ], e[PJ], dg[PJ], vw[PJ];
-      bool need[PJ], found[PJ];
+    const uint32_t cap = (p.n_has + nwarps - 1) / nwarps;
+    const uint32_t seg0 = gwarp * cap;
+    const uint32_t *srcl = (st.pad2 ? p.ulist : p.hasin) + seg0;
+    uint32_t *dstl = p.ulist + seg0;
+    const uint32_t cnt = st.pad2 ? ld_cg(p.useg + gwarp)
+                                 : (seg0 < p.n_has ? min(cap, p.n_has - seg0) : 0u);
+    uint32_t wr = 0;
+    for (uint32_t ib = 0; ib < cnt; ib += 32 * PJ) {
+      uint32_t t[PJ], s[PJ], e[PJ], dg[PJ];
+      bool need[PJ], keep[PJ], found[PJ];
 #pragma unroll
       for (int k = 0; k < PJ; ++k) {
-        const uint32_t w = w0 + k;
-        t[k] = w * 32 + lane;
-        vw[k] = w < nwo ? ld_cg(p.vis + w) : ~0u;
-        const uint32_t hw = w < nwo ? ld_nc(p.hin_bits + w) : ~0u;
-        need[k] = t[k] < p.R && !((vw[k] >> lane) & 1u) && !((hw >> lane) & 1u);
-        found[k] = false;
+        const uint32_t i2 = ib + k * 32 + lane;
+        t[k] = i2 < cnt ? ld_cg(srcl + i2) : 0xffffffffu;
+        need[k] = keep[k] = found[k] = false;
         s[k] = e[k] = dg[k] = 0;
-        if (need[k]) {  // row bounds and the E10 degree in the same round trip
-          s[k] = ld_nc(p.irp + t[k]);
+        if (t[k] != 0xffffffffu) {
+          const uint32_t bit = 1u << (t[k] & 31);
+          keep[k] = !(ld_cg(p.vis + (t[k] >> 5)) & bit);
+          need[k] = keep[k] && !(ld_nc(p.hin_bits + (t[k] >> 5)) & bit);
+          s[k] = ld_nc(p.irp + t[k]);  // speculative, same round trip
           e[k] = ld_nc(p.irp + t[k] + 1);
           dg[k] = ld_nc(p.deg + t[k]);
         }
@@ -301,19 +313,25 @@ __device__ void part_work(const PartParams &p, const PartState &st, uint32_t L, 
 #pragma unroll
       for (int k = 0; k < PJ; ++k) {
         if (found[k]) {
-          red_or(p.vis + (t[k] >> 5), 1u << lane);  // light rows: this lane alone settles t
+          red_or(p.vis + (t[k] >> 5), 1u << (t[k] & 31));  // light rows: this lane alone settles t
           if (L1 < 255u) {
             p.lev[t[k]] = (uint8_t)L1;
           } else {
             p.dist[t[k]] = L1;
             p.lev[t[k]] = 255u;
           }
-          red_or(sd + kPartHdr + (t[k] >> 5), 1u << lane);
+          red_or(sd + kPartHdr + (t[k] >> 5), 1u << (t[k] & 31));
           n_new += 1;
           m_new += dg[k];
         }
+        // survivors (still unreached) stay in the warp's segment, order preserved
+        const bool kp = keep[k] && !found[k];
+        const uint32_t km = __ballot_sync(DAWN_FULL, kp);
+        if (kp) dstl[wr + __popc(km & lanemask_lt())] = t[k];
+        wr += __popc(km);
       }
     }
+    if (lane == 0) p.useg[gwarp] = wr;
     // (b) heavy in-rows: static pieces, 32 in-edges per round, stop at the first hit or once
     //     another piece settled the vertex
     const uint32_t hend = ld_cg(&p.ctrl->n_hp[1]);
