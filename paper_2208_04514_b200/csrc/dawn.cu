@@ -1099,15 +1099,22 @@ dawn_status apsp_rows(dawn_graph g, const int64_t *sources, int64_t k, int64_t c
       // dev_stage[slot] is free once piece p - 2's copy has left it
       if (p >= 2 && (e = cudaStreamWaitEvent(st, R.landed[slot], 0)) != cudaSuccess)
         return cuda_fail(e, "dawn_apsp_rows");
-      if ((s = launch_ms(g, src, d, nullptr, st)) != DAWN_OK) return s;
+      if ((s = launch_ms(g, src, d, nullptr, st)) != DAWN_OK) {
+        cudaStreamSynchronize(R.copy);
+        return s;
+      }
       if ((e = cudaEventRecord(R.done[slot], st)) != cudaSuccess) return cuda_fail(e, "dawn_apsp_rows");
     }
     if (p >= 1) {  // hand piece p - 1 to the sink (host_stage[slot] was enqueued last iteration)
       const int slot = (int)((p - 1) & 1);
       if ((e = cudaEventSynchronize(R.landed[slot])) != cudaSuccess) return cuda_fail(e, "dawn_apsp_rows copy");
       const int64_t b = (p - 1) * chunk, c = std::min(k, b + chunk) - b;
-      if (sink(user, b, c, host_stage + (size_t)slot * (size_t)chunk * n) != 0)
+      if (sink(user, b, c, host_stage + (size_t)slot * (size_t)chunk * n) != 0) {
+        // nothing may still write the caller's buffers once we return
+        cudaStreamSynchronize(st);
+        cudaStreamSynchronize(R.copy);
         return fail(DAWN_ERR_INVALID_ARGUMENT, "the row sink aborted at row %lld", (long long)b);
+      }
     }
     if (p < np) {  // host_stage[slot] is free: its previous piece (p - 2) went to the sink
       const int slot = (int)(p & 1);
