@@ -385,7 +385,9 @@ def run_sssp(args, rank, world, dev, cfg, steps, warmup, e2e=True, with_cpu=Fals
         host_src = torch.from_numpy(srcs.astype(np.int32)).pin_memory()
         dev_src = torch.empty_like(host_src, device=dev)
         host_u8 = torch.empty((k, g.n), dtype=torch.uint8, pin_memory=True)
-        CH = min(8, k)  # sources per dawn_sssp_batch call (runs on the batch lanes)
+        # sources per dawn_sssp_batch call: two searches per batch lane, so a chunk keeps every
+        # lane busy while the previous chunk's rows travel
+        CH = max(1, min(k, 2 * int(G.get_tuning("batch_lanes"))))
         dev_u8 = torch.empty((2, CH, g.n), dtype=torch.uint8, device=dev)
         flags = torch.zeros(1, dtype=torch.int32, device=dev)
         host_flags = torch.zeros(1, dtype=torch.int32, pin_memory=True)
@@ -426,10 +428,10 @@ def run_sssp(args, rank, world, dev, cfg, steps, warmup, e2e=True, with_cpu=Fals
                       "unit": "GTEPS", "h2d_bytes_per_step": int(host_src.numel() * 4),
                       "d2h_bytes_per_step": int(host_u8.numel() + 4),
                       "ms_per_step": e_tot / len(e_ms),
-                      "how": "source list H2D from pinned memory, dawn_sssp_batch per 8 sources, "
+                      "how": f"source list H2D from pinned memory, dawn_sssp_batch per {CH} sources, "
                              "dawn_dist_u8 (1 byte per vertex, exact while eps < 255; its flag is "
                              "read back and checked), the rows D2H into pinned memory on a second "
-                             "stream overlapping the next 8 searches"}
+                             "stream overlapping the next chunk's searches"}
         del host_u8
     if with_cpu:
         cores = len(os.sched_getaffinity(0))
