@@ -1688,7 +1688,7 @@ dawn_status part_finish(dawn_part p, dawn_sssp_stats *stats, void *stream) {
 extern "C" {
 
 const char *dawn_last_error(void) { return g_err; }
-const char *dawn_version(void) { return "dawn-b200 0.3 sm_100a"; }
+const char *dawn_version(void) { return "dawn-b200 0.4 sm_100a"; }
 
 size_t dawn_workspace_bytes(int64_t n, int64_t m, uint32_t flags) {
   try {
