@@ -180,3 +180,30 @@ def test_c5_apsp_sharded_matches():
             part = dawn.records_to_numpy(dawn.apsp(G, verts, r, W, gather=False))
             full[idx] = part
         assert full.tobytes() == exp.tobytes(), W
+
+
+def test_c4_weighted_certificate():
+    # NEXT-4 at full size: the bench's weighted searches on Kronecker-24 (weights 1..255, the
+    # bench seed) certified exactly (weighted certificate, weights >= 1) for 2 bench sources
+    g = graphgen.config_graph("C4")
+    G = dawn.Graph(g.row_ptr, g.col, True)
+    w = g.weights(seed=24, wmax=255)
+    wt = torch.from_numpy(w.view(np.int32)).cuda()
+    for s in g.sample_sources(2, seed=1):
+        d = dawn.wsssp(G, int(s), wt).cpu().numpy().view(np.uint32).astype(np.uint64)
+        d[d == 0xFFFFFFFF] = oracle.UNREACHED64
+        rc, bad = oracle.certify_w(g.n, g.row_ptr, g.col, w, int(s), d)
+        assert rc == 0, (int(s), rc, bad)
+
+
+def test_c4_partitioned_matches_single_gpu_path():
+    # NEXT-3 at full size: the fused partitioned search over 2 ranks (on one device) equals the
+    # certified single-GPU rows of the bench sources
+    g = graphgen.config_graph("C4")
+    G = dawn.Graph(g.row_ptr, g.col, True)
+    parts = [dawn.PartGraph(dawn.part_build(g.row_ptr, g.col, 2, r), 2, r) for r in range(2)]
+    for s in g.sample_sources(3, seed=1):
+        a = dawn.part_fused_local(parts, int(s))
+        b = dawn.sssp(G, int(s))
+        assert torch.equal(a, b), int(s)
+    torch.cuda.synchronize()
