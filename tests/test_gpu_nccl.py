@@ -95,3 +95,42 @@ def test_partitioned_sssp_nccl_all_visible_gpus(tmp_path):
                 got = np.concatenate([np.load(tmp_path / f"{tag}_{r}_{i}_{v}.npy")[: dawn.part_range(g.n, world, r)[1] - dawn.part_range(g.n, world, r)[0]]
                                       for r in range(world)]).view(np.uint32)
                 assert np.array_equal(got, exp), (tag, world, s, v)
+
+
+def _fused_ipc_worker(rank, world, port, out_dir):
+    # two processes on ONE device: the exchange buffers are shared through CUDA IPC
+    # (torch.multiprocessing's tensor sharing, handles over a gloo group) exactly as across GPUs,
+    # and the two persistent kernels signal each other with system-scope atomics; the device
+    # time-slices the two contexts, so this checks the protocol, not the speed
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    g = graphgen.kron(10, 8, 10)
+    pg = dawn.PartGraph(dawn.part_build(g.row_ptr, g.col, world, rank), world, rank,
+                        device=torch.device("cuda", 0))
+    for i, s in enumerate(g.sample_sources(2, seed=3)):
+        d = dawn.part_sssp_fused(pg, int(s))
+        torch.cuda.synchronize()
+        np.save(os.path.join(out_dir, f"ipc_{rank}_{i}.npy"), d.cpu().numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_fused_exchange_across_processes_ipc(tmp_path):
+    world = 2
+    ctx = mp.start_processes(_fused_ipc_worker, args=(world, _free_port(), str(tmp_path)),
+                             nprocs=world, join=False, start_method="spawn")
+    import time
+    deadline = time.time() + 240
+    while not ctx.join(timeout=5):
+        if time.time() > deadline:
+            for p in ctx.processes:
+                p.kill()
+            pytest.fail("fused exchange across processes did not finish in 240 s")
+    g = graphgen.kron(10, 8, 10)
+    for i, s in enumerate(g.sample_sources(2, seed=3)):
+        exp, _ = oracle.bfs_fifo(g.n, g.row_ptr, g.col, int(s))
+        got = np.concatenate([np.load(tmp_path / f"ipc_{r}_{i}.npy")[: dawn.part_range(g.n, world, r)[1] - dawn.part_range(g.n, world, r)[0]]
+                              for r in range(world)]).view(np.uint32)
+        assert np.array_equal(got, exp), (i, int(s))
