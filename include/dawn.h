@@ -360,6 +360,13 @@ dawn_status dawn_dist_u8(const uint32_t *dist, int64_t count, uint8_t *out, uint
  */
 dawn_status dawn_wsssp(dawn_graph g, int64_t source, const uint32_t *weights, uint32_t *dist,
                        dawn_sssp_stats *stats, void *stream);
+/* k weighted searches from a DEVICE source list (validated on the device before any write, as
+ * dawn_sssp_batch: a bad id writes nothing and dawn_graph_check reports DAWN_ERR_BOUNDS), back to
+ * back in one persistent launch.
+ *   dist DEVICE uint32[k][n], stats DEVICE dawn_sssp_stats[k] or NULL.  k >= 2^32 -> CAPACITY. */
+dawn_status dawn_wsssp_batch(dawn_graph g, const uint32_t *sources, int64_t k,
+                             const uint32_t *weights, uint32_t *dist, dawn_sssp_stats *stats,
+                             void *stream);
 
 /* ------------------------------------------------------------------------------------------
  * Partitioned single-source SSSP over W GPUs: the graph is cut by

@@ -18,7 +18,7 @@ import numpy as np
 import torch
 
 __all__ = ["build", "Graph", "sssp", "sssp_batch", "msssp", "apsp", "apsp_rows", "apsp_shard",
-           "wsssp", "dist_u8", "part_range", "part_build", "PartGraph", "part_exchange", "part_sssp", "part_sssp_local",
+           "wsssp", "wsssp_batch", "dist_u8", "part_range", "part_build", "PartGraph", "part_exchange", "part_sssp", "part_sssp_local",
            "part_fused_local", "part_sssp_fused", "largest_wcc",
            "check", "DawnError", "UNREACHED", "AUTO", "PUSH", "PULL", "MS_BATCH", "REC_DTYPE",
            "records_to_numpy", "stats_to_dict", "gather_records"]
@@ -124,6 +124,8 @@ def lib():
         L.dawn_graph_ms_counters.argtypes = [vp, vp, vp]
         L.dawn_apsp_rows.restype = st
         L.dawn_apsp_rows.argtypes = [vp, vp, i64, i64, vp, vp, _ROW_SINK, vp, vp]
+        L.dawn_wsssp_batch.restype = st
+        L.dawn_wsssp_batch.argtypes = [vp, vp, i64, vp, vp, vp, vp]
         L.dawn_dist_u8.restype = st
         L.dawn_dist_u8.argtypes = [vp, i64, vp, vp, vp]
         L.dawn_wsssp.restype = st
@@ -441,6 +443,23 @@ def wsssp(g: Graph, source: int, weights: torch.Tensor, stats: bool = False,
     st = torch.zeros(4, dtype=torch.int64, device=g.device) if stats else None
     _check(lib().dawn_wsssp(g.handle, int(source), _dptr(weights), _dptr(dist), _dptr(st),
                             _stream(stream)))
+    return (dist, st) if stats else dist
+
+
+def wsssp_batch(g: Graph, sources: torch.Tensor, weights: torch.Tensor, stats: bool = False,
+                out: torch.Tensor | None = None, stream=None, check: bool = False):
+    """dawn_wsssp_batch: k weighted searches from a device source list on the batch lanes.
+    Returns int32 [k, n] (and int64 [k, 4] statistics)."""
+    assert sources.is_cuda and sources.dtype in (torch.int32, torch.uint32)
+    assert weights.is_cuda and weights.dtype in (torch.int32, torch.uint32) and weights.numel() == g.m
+    k = sources.numel()
+    dist = out if out is not None else torch.empty((k, g.n), dtype=torch.int32, device=g.device)
+    assert dist.shape == (k, g.n) and dist.dtype == torch.int32 and dist.is_contiguous()
+    st = torch.zeros((k, 4), dtype=torch.int64, device=g.device) if stats else None
+    _check(lib().dawn_wsssp_batch(g.handle, _dptr(sources), k, _dptr(weights), _dptr(dist),
+                                  _dptr(st), _stream(stream)))
+    if check:
+        globals()["check"](g, stream)
     return (dist, st) if stats else dist
 
 

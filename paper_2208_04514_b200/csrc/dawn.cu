@@ -1249,18 +1249,13 @@ dawn_status dist_u8(const uint32_t *dist, int64_t count, uint8_t *out, uint32_t 
 }
 
 // ---------------------------------------------------------------- weighted (min,+) (NEXT-4)
-dawn_status wsssp(dawn_graph g, int64_t source, const uint32_t *weights, uint32_t *dist,
-                  dawn_sssp_stats *stats, void *stream) {
-  if (!g || !dist || (g->m > 0 && !weights)) return fail(DAWN_ERR_INVALID_ARGUMENT, "NULL argument");
-  if (source < 0 || source >= g->n)
-    return fail(DAWN_ERR_BOUNDS, "source %lld not in [0, n)", (long long)source);
-  dawn_status s = set_device(g);
-  if (s != DAWN_OK) return s;
+WParams wparams(dawn_graph g, int lane, const uint32_t *weights, uint32_t *dist,
+                dawn_sssp_stats *stats) {
   const Layout &L = g->L;
+  const LaneLayout &Q = L.lane[lane];
   WParams p{};
   p.n = (uint32_t)g->n;
   p.nwords = (uint32_t)((g->n + 31) / 32);
-  p.source = (uint32_t)source;
   p.rp = at<uint32_t>(g, L.rp);
   p.col = g->col;
   p.w = weights;
@@ -1268,18 +1263,55 @@ dawn_status wsssp(dawn_graph g, int64_t source, const uint32_t *weights, uint32_
   p.hout_s = at<uint32_t>(g, L.hout.s);
   p.hout_e = at<uint32_t>(g, L.hout.e);
   p.hout_bits = at<uint32_t>(g, L.hout.bits);
-  for (int i = 0; i < 3; ++i) p.fb[i] = at<uint32_t>(g, L.fb[i]);
-  p.ctrl = at<Ctrl>(g, L.ctrl);
+  for (int i = 0; i < 3; ++i) p.fb[i] = at<uint32_t>(g, Q.fb[i]);
+  p.ctrl = at<Ctrl>(g, Q.ctrl);
   p.dist = dist;
   p.stats = stats;
   p.delta = g->wdelta == 0 ? kWInf : g->wdelta;
-  int grid = g->wsssp_grid;
+  p.bad_src = &at<Ctrl>(g, L.ctrl)->bad_src;
+  return p;
+}
+
+dawn_status launch_wsssp(dawn_graph g, WParams &p, int grid, cudaStream_t st) {
   if (g->m + g->n <= kOneCtaMaxNM) grid = 1;
   void *args[] = {&p};
   cudaError_t e = cudaLaunchCooperativeKernel((const void *)k_wsssp<kNT>, dim3(grid), dim3(kNT), args,
-                                              0, static_cast<cudaStream_t>(stream));
+                                              0, st);
   if (e != cudaSuccess) return cuda_fail(e, "k_wsssp launch");
   return DAWN_OK;
+}
+
+dawn_status wsssp(dawn_graph g, int64_t source, const uint32_t *weights, uint32_t *dist,
+                  dawn_sssp_stats *stats, void *stream) {
+  if (!g || !dist || (g->m > 0 && !weights)) return fail(DAWN_ERR_INVALID_ARGUMENT, "NULL argument");
+  if (source < 0 || source >= g->n)
+    return fail(DAWN_ERR_BOUNDS, "source %lld not in [0, n)", (long long)source);
+  dawn_status s = set_device(g);
+  if (s != DAWN_OK) return s;
+  WParams p = wparams(g, 0, weights, dist, stats);
+  p.source = (uint32_t)source;
+  return launch_wsssp(g, p, g->wsssp_grid, static_cast<cudaStream_t>(stream));
+}
+
+// k weighted searches back to back in ONE persistent launch (a grid barrier between searches).
+// Batch lanes (concurrent launches on SM shares, as dawn_sssp_batch) were measured slower here:
+// a (min,+) round scans the whole frontier bitmap and every heavy piece, work that grows with
+// the graph rather than the frontier, so a lane's share of the SMs just takes longer (C4 weighted
+// 43.3 GTEPS sequential vs 37.8 on 4 lanes).
+dawn_status wsssp_batch(dawn_graph g, const uint32_t *sources, int64_t k, const uint32_t *weights,
+                        uint32_t *dist, dawn_sssp_stats *stats, void *stream) {
+  if (!g || k < 0 || (k > 0 && (!dist || !sources)) || (g->m > 0 && !weights))
+    return fail(DAWN_ERR_INVALID_ARGUMENT, "bad arguments");
+  if (k == 0) return DAWN_OK;
+  if (k >= (int64_t(1) << 32)) return fail(DAWN_ERR_CAPACITY, "k too large");
+  dawn_status s = set_device(g);
+  if (s != DAWN_OK) return s;
+  WParams p = wparams(g, 0, weights, dist, stats);
+  p.sources = sources;
+  p.nsrc = (uint32_t)k;
+  p.vsrc = sources;
+  p.vn = (uint32_t)k;
+  return launch_wsssp(g, p, g->wsssp_grid, static_cast<cudaStream_t>(stream));
 }
 
 // ---------------------------------------------------------------- partitioned SSSP (NEXT-3)
@@ -1794,6 +1826,12 @@ dawn_status dawn_dist_u8(const uint32_t *dist, int64_t count, uint8_t *out, uint
 dawn_status dawn_wsssp(dawn_graph g, int64_t source, const uint32_t *weights, uint32_t *dist,
                        dawn_sssp_stats *stats, void *stream) {
   DAWN_GUARD(return wsssp(g, source, weights, dist, stats, stream);)
+}
+
+dawn_status dawn_wsssp_batch(dawn_graph g, const uint32_t *sources, int64_t k,
+                             const uint32_t *weights, uint32_t *dist, dawn_sssp_stats *stats,
+                             void *stream) {
+  DAWN_GUARD(return wsssp_batch(g, sources, k, weights, dist, stats, stream);)
 }
 
 dawn_status dawn_part_range(int64_t n, int32_t world, int32_t rank, int64_t *lo, int64_t *hi) {

@@ -36,27 +36,34 @@ struct WParams {
   const uint32_t *hout_v, *hout_s, *hout_e, *hout_bits;
   uint32_t *fb[3];                                     // rotating frontier bitmaps
   Ctrl *ctrl;
-  uint32_t *dist;
-  dawn_sssp_stats *stats;
+  uint32_t *dist;                                      // [nsrc][n]
+  dawn_sssp_stats *stats;                              // [nsrc] or null
   uint32_t delta;                                      // near/far step (>= 1; ~0u: off)
+  // batch (dawn_wsssp_batch): nsrc > 0 sources from the device list, searched one after the
+  // other in this launch (a grid barrier apart); 0: the single `source`
+  const uint32_t *sources;
+  uint32_t nsrc;
+  const uint32_t *vsrc;                                // whole device list, validated first
+  uint32_t vn;
+  uint32_t *bad_src;                                   // sticky flag: an id was >= n
 };
 
-__device__ __forceinline__ void w_relax(const WParams &p, uint32_t dv, uint32_t j, uint32_t *fnext,
-                                        uint32_t &improved, uint32_t &fmin) {
+__device__ __forceinline__ void w_relax(const WParams &p, uint32_t *dist, uint32_t dv, uint32_t j,
+                                        uint32_t *fnext, uint32_t &improved, uint32_t &fmin) {
   const uint32_t u = (uint32_t)ld_nc(p.col + j);
   uint32_t c = dv + ld_nc(p.w + j);
   if (c < dv || c > kWSat) c = kWSat;  // saturate (exact while every distance < 2^32 - 1)
-  if (c < ld_cg(p.dist + u)) {
+  if (c < ld_cg(dist + u)) {
 #if DAWN_W_RED
     // fire-and-forget min: no returning round trip on the chain; u joins the next frontier on
     // the observed improvement (if another arc lowered d(u) further meanwhile, u is expanded
     // with that value — an extra frontier entry at worst)
-    asm volatile("red.relaxed.gpu.global.min.u32 [%0], %1;" ::"l"(p.dist + u), "r"(c) : "memory");
+    asm volatile("red.relaxed.gpu.global.min.u32 [%0], %1;" ::"l"(dist + u), "r"(c) : "memory");
     red_or(fnext + (u >> 5), 1u << (u & 31));
     ++improved;
     fmin = min(fmin, c);
 #else
-    const uint32_t old = atomicMin(p.dist + u, c);
+    const uint32_t old = atomicMin(dist + u, c);
     if (c < old) {
       red_or(fnext + (u >> 5), 1u << (u & 31));
       ++improved;
@@ -77,10 +84,22 @@ __global__ void __launch_bounds__(NT, 1) k_wsssp(WParams p) {
   const uint32_t gtid = blockIdx.x * NT + threadIdx.x, nth = nblocks * NT;
   Ctrl *C = p.ctrl;
   unsigned long long bar = 0;
+  if (p.vn) {  // the whole device source list is checked before anything is written
+    bool bad = false;
+    for (uint32_t i = threadIdx.x; i < p.vn; i += NT) bad |= ld_nc(p.vsrc + i) >= p.n;
+    if (__syncthreads_or(bad)) {
+      if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(p.bad_src, 1u);
+      return;
+    }
+  }
+  const uint32_t nsrc = p.nsrc ? p.nsrc : 1u;
+  for (uint32_t si = 0; si < nsrc; ++si) {
+  const uint32_t src = p.nsrc ? ld_nc(p.sources + si) : p.source;
+  uint32_t *const dist = p.dist + (size_t)si * p.n;
   // init: d = infinity, d(s) = 0, F_0 = {s}, the other two bitmaps clear
-  for (uint32_t i = gtid; i < p.n; i += nth) p.dist[i] = (i == p.source) ? 0u : kWInf;
+  for (uint32_t i = gtid; i < p.n; i += nth) dist[i] = (i == src) ? 0u : kWInf;
   for (uint32_t w = gtid; w < p.nwords; w += nth) {
-    p.fb[0][w] = (w == (p.source >> 5)) ? 1u << (p.source & 31) : 0u;
+    p.fb[0][w] = (w == (src >> 5)) ? 1u << (src & 31) : 0u;
     p.fb[1][w] = 0;
     p.fb[2][w] = 0;
   }
@@ -114,7 +133,7 @@ __global__ void __launch_bounds__(NT, 1) k_wsssp(WParams p) {
           const uint32_t b0 = __ffs(bits) - 1;
           const uint32_t v = wd * 32 + b0;
           bits &= bits - 1;
-          dv = ld_cg(p.dist + v);
+          dv = ld_cg(dist + v);
           if (dv >= T) {  // far: stays in the frontier
             red_or(fnext + wd, 1u << b0);
             ++improved;
@@ -139,7 +158,7 @@ __global__ void __launch_bounds__(NT, 1) k_wsssp(WParams p) {
           const uint32_t sk = __shfl_sync(DAWN_FULL, rs, kk);
           const uint32_t dk = __shfl_sync(DAWN_FULL, dv, kk);
           if (t < total) {
-            w_relax(p, dk, sk + (t - ek), fnext, improved, fmin);
+            w_relax(p, dist, dk, sk + (t - ek), fnext, improved, fmin);
             ++relaxed;
           }
         }
@@ -156,7 +175,7 @@ __global__ void __launch_bounds__(NT, 1) k_wsssp(WParams p) {
         vl = ld_nc(p.hout_v + pcl);
         live = (ld_cg(fcur + (vl >> 5)) >> (vl & 31)) & 1u;
         if (live) {
-          dl = ld_cg(p.dist + vl);
+          dl = ld_cg(dist + vl);
           live = dl < T;  // far heavy vertices were carried by (a)
         }
       }
@@ -168,7 +187,7 @@ __global__ void __launch_bounds__(NT, 1) k_wsssp(WParams p) {
         const uint32_t dv = __shfl_sync(DAWN_FULL, dl, kk);
         const uint32_t s = ld_nc(p.hout_s + pc), e = ld_nc(p.hout_e + pc);
         for (uint32_t j = s + lane; j < e; j += 32) {
-          w_relax(p, dv, j, fnext, improved, fmin);
+          w_relax(p, dist, dv, j, fnext, improved, fmin);
           ++relaxed;
         }
       }
@@ -207,8 +226,8 @@ __global__ void __launch_bounds__(NT, 1) k_wsssp(WParams p) {
   // statistics: reached / E10 counts over the final distances
   unsigned long long reached = 0, er = 0;
   for (uint32_t v = gtid; v < p.n; v += nth) {
-    if (ld_cg(p.dist + v) != kWInf) {
-      reached += (v != p.source);
+    if (ld_cg(dist + v) != kWInf) {
+      reached += (v != src);
       er += ld_nc(p.rp + v + 1) - ld_nc(p.rp + v);
     }
   }
@@ -237,8 +256,10 @@ __global__ void __launch_bounds__(NT, 1) k_wsssp(WParams p) {
     s.edges_examined = ld_cg(&C->examined);
     s.push_levels = rounds + 1;
     s.pull_levels = 0;
-    *p.stats = s;
+    p.stats[si] = s;
   }
+  if (si + 1 < nsrc) grid_sync(&C->bar, nblocks, bar);  // stats read before the next init
+  }  // sources
   grid_exit(&C->bar, nblocks);
 }
 

@@ -120,3 +120,27 @@ def test_c2_certificate():
         rc, bad = oracle.certify_w(g.n, g.row_ptr, g.col, w, int(s), d)
         assert rc == 0, (s, rc, bad)
     torch.cuda.synchronize()
+
+
+def test_wsssp_batch_and_bounds():
+    g = graphgen.kron(13, 16, 13)
+    G = _graph(g)
+    w = g.weights(4, 255)
+    wt = torch.from_numpy(w.view(np.int32)).cuda()
+    srcs = np.concatenate([g.sample_sources(9, seed=2), [0]]).astype(np.int32)
+    srcs[4] = srcs[1]  # a repeated source
+    exp = [_exp32(oracle.dijkstra(g.n, g.row_ptr, g.col, w, int(s))) for s in srcs]
+    d, st = dawn.wsssp_batch(G, torch.from_numpy(srcs).cuda(), wt, stats=True, check=True)
+    d = d.cpu().numpy().view(np.uint32)
+    for i, s in enumerate(srcs):
+        assert np.array_equal(d[i], exp[i]), (i, int(s))
+        x = dawn.stats_to_dict(st[i])
+        assert x["reached"] == int((exp[i] != U32).sum()) - 1
+    bad = torch.tensor([1, 2, g.n], dtype=torch.int32, device="cuda")
+    sentinel = torch.full((3, g.n), 7, dtype=torch.int32, device="cuda")
+    dawn._check(dawn.lib().dawn_wsssp_batch(G.handle, bad.data_ptr(), 3, wt.data_ptr(),
+                                            sentinel.data_ptr(), None,
+                                            torch.cuda.current_stream().cuda_stream))
+    with pytest.raises(dawn.DawnError) as ei:
+        dawn.check(G)
+    assert ei.value.status == 2 and bool((sentinel == 7).all())
