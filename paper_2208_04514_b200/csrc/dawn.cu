@@ -44,6 +44,7 @@ void clear_err() { g_err[0] = 0; }
 constexpr int kNT = 512;  // threads per CTA of the persistent kernels
 // Graph-size thresholds of the kernel choice (measured on B200)
 constexpr int64_t kSsspOneMaxN = 1 << 22;  // k_sssp<kNT, 1> (1 CTA/SM, 128 regs) up to 2^22
+constexpr uint32_t kHubWordsOne = 49152;   // bitmap cache words of k_sssp<kNT, 1> (192 KB)
 constexpr int64_t kOneCtaMaxNM = 1 << 15;  // n + m this small: one CTA, barriers are __syncthreads
 constexpr int kMsBlocksPerSm = 2;          // k_ms64 CTAs per SM (if they fit)
 constexpr uint32_t kNarrowQcapMax = 1u << 20;
@@ -339,6 +340,8 @@ struct dawn_graph_s {
   int ms_lanes = 1;               // DAWN_PARAM_MS_LANES (<= L.ms_nlanes)
   uint32_t wdelta = DAWN_WDELTA;   // DAWN_PARAM_WEIGHT_DELTA (0: near/far off)
   double dense_max = 1099511627776.0;  // DAWN_PARAM_DENSE_MAX_ENTRIES (k*n of a dense output)
+  uint32_t hub_cap = 0, hub_w = 0;     // DAWN_PARAM_HUB_WORDS: load-time capacity / current
+  unsigned long long hub_min = 0;      // DAWN_PARAM_HUB_MIN_EDGES (0: automatic)
   // lane streams / fork-join events of dawn_sssp_batch (created at load, host resources only)
   cudaStream_t lane_st[kMaxLanes] = {};
   cudaEvent_t ev_fork = nullptr, ev_join[kMaxLanes] = {};
@@ -431,6 +434,23 @@ dawn_status load_csr(int64_t n, int64_t m, const int64_t *row_ptr, const int32_t
   cudaDeviceGetAttribute(&g->nsm, cudaDevAttrMultiProcessorCount, g->device);
   // small graphs: k_sssp<kNT, 1> (one CTA per SM, 128 registers); big ones k_sssp<kNT, 2>
   g->sssp_one = n <= kSsspOneMaxN;
+  if (g->sssp_one) {
+    // bitmap cache capacity: the dynamic shared memory next to k_sssp<kNT, 1>'s static state
+    // (192 KB), never more than the bitmap.  On by default when the whole bitmap fits (ids in any
+    // order: n <= 1,572,864); a prefix of it only helps when low ids are the hubs.  The 2-CTA/SM
+    // variant has none: 2 x 96 KB of shared memory leaves its loads ~36 KB of L1, and a 96 KB
+    // prefix of Kronecker-24 (4.7% of the vertices, or 85% of the arc targets after a hub-first
+    // relabelling, which concentrates the claim atomics on a few words) measured slower either
+    // way.
+    const uint32_t nw4 = (uint32_t)(((n + 31) / 32 + 3) & ~int64_t(3));
+    g->hub_cap = std::min(kHubWordsOne, nw4);
+    if (cudaFuncSetAttribute((const void *)k_sssp<kNT, 1>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)(4 * g->hub_cap)) != cudaSuccess)
+      g->hub_cap = 0;
+    cudaGetLastError();
+    g->hub_w = (g->hub_cap == nw4) ? g->hub_cap : 0u;
+  }
   g->sssp_grid = g->sssp_one ? std::min<int>(g->nsm, (int)kMaxBlocks)
                              : grid_for((const void *)k_sssp<kNT, 2>, g->nsm);
   {
@@ -649,6 +669,10 @@ dawn_status set_param(dawn_graph g, dawn_param key, double value) {
       if (value < 1) return fail(DAWN_ERR_INVALID_ARGUMENT, "dense limit must be >= 1");
       g->dense_max = std::min(value, 1099511627776.0);
       break;
+    case DAWN_PARAM_HUB_WORDS:
+      g->hub_w = (uint32_t)std::min<double>(value, g->hub_cap) & ~3u;
+      break;
+    case DAWN_PARAM_HUB_MIN_EDGES: g->hub_min = (unsigned long long)std::min(value, 1.8e19); break;
     case DAWN_PARAM_NARROW_QUEUE_CAP:
       if (value < 32) return fail(DAWN_ERR_INVALID_ARGUMENT, "queue capacity must be >= 32");
       g->narrow_qcap = (uint32_t)std::min<double>(value, g->narrow_qcap_max);
@@ -706,9 +730,12 @@ SsspParams sssp_params(dawn_graph g, uint32_t variant, uint32_t *dist, dawn_sssp
 dawn_status launch_sssp(dawn_graph g, SsspParams &p, cudaStream_t stream, int lanes = 1) {
   int grid = std::max(1, g->sssp_grid / lanes);
   if (g->m + g->n <= kOneCtaMaxNM) grid = 1;  // tiny graphs: one CTA, barriers are __syncthreads
+  p.hw = g->hub_w;
+  p.hub_min = g->hub_min ? g->hub_min : (unsigned long long)grid * g->hub_w / 8;
   void *args[] = {&p};
   const void *kfn = g->sssp_one ? (const void *)k_sssp<kNT, 1> : (const void *)k_sssp<kNT, 2>;
-  cudaError_t e = cudaLaunchCooperativeKernel(kfn, dim3(grid), dim3(kNT), args, 0, stream);
+  cudaError_t e = cudaLaunchCooperativeKernel(kfn, dim3(grid), dim3(kNT), args,
+                                              4 * (size_t)p.hw, stream);
   if (e != cudaSuccess) return cuda_fail(e, "k_sssp launch");
   return DAWN_OK;
 }
@@ -1760,6 +1787,8 @@ dawn_status dawn_graph_get_param(dawn_graph g, dawn_param key, double *value) {
       case DAWN_PARAM_DENSE_MAX_ENTRIES: *value = g->dense_max; break;
       case DAWN_PARAM_MS_LANES: *value = g->ms_lanes; break;
       case DAWN_PARAM_WEIGHT_DELTA: *value = g->wdelta; break;
+      case DAWN_PARAM_HUB_WORDS: *value = g->hub_w; break;
+      case DAWN_PARAM_HUB_MIN_EDGES: *value = (double)g->hub_min; break;
       default: return fail(DAWN_ERR_INVALID_ARGUMENT, "unknown parameter");
     }
     return DAWN_OK;)

@@ -56,6 +56,11 @@ struct SsspParams {
   // device source list validated before any write (dawn_sssp_batch; vn = 0: host-validated)
   const uint32_t *vsrc;
   uint32_t vn;
+  // hub cache (dynamic shared memory): words [0, hw) of the visited bitmap (push levels) or of
+  // the frontier bitmap (pull levels) are copied into each CTA at the level start; hub_min: push
+  // levels with fewer frontier arcs skip the copy
+  uint32_t hw;
+  unsigned long long hub_min;
 };
 
 // Every CTA checks the whole device source list of a dawn_sssp_batch call before it writes
@@ -79,6 +84,7 @@ struct __align__(16) LevelState {
   uint32_t qe;                  // queue edges of frontier L
   uint32_t big;                 // frontier L (bitmap form) has a row of > kDirectRow arcs
   uint32_t novis;               // candidate push without the visited-word read (see push_item)
+  uint32_t hb;                  // vertices [0, hb) are tested in the CTA's hub cache this level
   unsigned long long mf, explored, push_edges, pad;
   uint32_t *drow;               // this search's distance row
 };
@@ -87,6 +93,28 @@ static_assert(sizeof(LevelState) % 16 == 0, "LevelState is copied as uint4");
 struct WarpStage {
   uint32_t u[64], rs[64], d[64];
 };
+
+// Hub cache: the first hw words of a bitmap in the CTA's dynamic shared memory.  With the
+// graph in hub order (DAWN_GRAPH_HUB_ORDER: the highest-degree vertices take ids 0, 1, ...),
+// those words hold the vertices most arcs point to (Kronecker-24: the first 786K ids are the
+// targets of 85% of the arcs), so most visited tests of a push level and most frontier probes of
+// a pull level are shared-memory reads instead of random L2 sectors.  Push levels cache a
+// level-start snapshot of `vis` (a set bit is final: the arc is skipped; a clear one falls
+// through to the global test, and the CTA sets the bit once it has claimed or marked the
+// vertex); pull levels cache the level-L frontier, which is read-only during the level.
+__device__ __forceinline__ uint32_t *hub_smem() {
+  extern __shared__ __align__(16) uint32_t dawn_hubw[];
+  return dawn_hubw;
+}
+
+// CTA-collective: copy words [0, hw) of src (hw a multiple of 4; the 256-B aligned workspace
+// arrays are readable up to the next multiple of 4 words) into the hub cache
+__device__ __forceinline__ void hub_load(const uint32_t *src, uint32_t hw) {
+  const uint4 *s4 = reinterpret_cast<const uint4 *>(src);
+  uint4 *d4 = reinterpret_cast<uint4 *>(hub_smem());
+  for (uint32_t i = threadIdx.x; i < hw / 4; i += blockDim.x) d4[i] = __ldcg(s4 + i);
+  __syncthreads();
+}
 
 __device__ __forceinline__ unsigned long long globaltimer() {
   unsigned long long t;
@@ -258,10 +286,15 @@ __device__ __forceinline__ void push_item(const SsspParams &p, const LevelState 
   }
   uint32_t cur[J];
   // candidate levels while few vertices are settled (st.novis): most targets are unvisited, so
-  // the visited-word read (one random L2 sector per arc) is skipped; cand_filter drops the rest
+  // the visited-word read (one random L2 sector per arc) is skipped; cand_filter drops the rest.
+  // Hub targets (u < st.hb) are tested in the CTA's hub cache instead.
+  const uint32_t hb = st.hb;
+  uint32_t *const hubw = hub_smem();
 #pragma unroll
   for (int j = 0; j < J; ++j)
-    cur[j] = (act[j] && !NOVIS) ? p.vis[u[j] >> 5] : (act[j] ? 0u : ~0u);  // weak: stale 0 = atomic
+    cur[j] = !act[j] ? ~0u
+                     : (u[j] < hb ? hubw[u[j] >> 5]
+                                  : (NOVIS ? 0u : p.vis[u[j] >> 5]));  // weak: stale 0 = atomic
   if constexpr (CAND) {
     // bitmap push: mark the candidate, settle later in cand_filter (no returning atomic)
 #if DAWN_CAND_FILTER
@@ -275,14 +308,21 @@ __device__ __forceinline__ void push_item(const SsspParams &p, const LevelState 
 #pragma unroll
     for (int j = 0; j < J; ++j) {
       const uint32_t bit = 1u << (u[j] & 31);
-      if (!(cur[j] & bit)) red_or(p.cand + (u[j] >> 5), bit);
+      if (!(cur[j] & bit)) {
+        red_or(p.cand + (u[j] >> 5), bit);
+        if (u[j] < hb) atomicOr(hubw + (u[j] >> 5), bit);  // marked: later arcs of this CTA skip
+      }
     }
   } else {
 #pragma unroll
     for (int j = 0; j < J; ++j) {
       const uint32_t bit = 1u << (u[j] & 31);
       disc[j] = false;
-      if (!(cur[j] & bit)) disc[j] = !(atomicOr(p.vis + (u[j] >> 5), bit) & bit);
+      if (!(cur[j] & bit)) {
+        const uint32_t old = atomicOr(p.vis + (u[j] >> 5), bit);
+        disc[j] = !(old & bit);
+        if (u[j] < hb) atomicOr(hubw + (u[j] >> 5), old | bit);
+      }
     }
 #pragma unroll
     for (int j = 0; j < J; ++j) {
@@ -404,7 +444,12 @@ __device__ void push_bitmap(const SsspParams &p, const LevelState &st, Slot *ns,
         bool disc = false;
         if (act) {
           const uint32_t bit = 1u << (u & 31);
-          if (!(p.vis[u >> 5] & bit)) disc = !(atomicOr(p.vis + (u >> 5), bit) & bit);
+          const bool hub = u < st.hb;
+          if (!((hub ? hub_smem()[u >> 5] : p.vis[u >> 5]) & bit)) {
+            const uint32_t old = atomicOr(p.vis + (u >> 5), bit);
+            disc = !(old & bit);
+            if (hub) atomicOr(hub_smem() + (u >> 5), old | bit);
+          }
         }
         uint32_t urs = 0, ud = 0;
         if (disc) {
@@ -425,6 +470,11 @@ __device__ void push_bitmap(const SsspParams &p, const LevelState &st, Slot *ns,
 
 __device__ __forceinline__ bool fb_test(const uint32_t *fb, uint32_t v) {
   return (fb[v >> 5] >> (v & 31)) & 1u;
+}
+
+// frontier test of a pull probe: hubs (v < hb) from the CTA's copy of the level-L frontier
+__device__ __forceinline__ bool fb_test_hub(const uint32_t *fb, uint32_t v, uint32_t hb) {
+  return ((v < hb ? hub_smem()[v >> 5] : fb[v >> 5]) >> (v & 31)) & 1u;
 }
 
 template <int PR, int J>  // in-edges probed per lane per round trip (8 when the frontier is
@@ -498,7 +548,7 @@ __device__ void pull_level(const SsspParams &p, const LevelState &st, uint32_t g
         uint32_t hit = PR;
 #pragma unroll
         for (int i = PR - 1; i >= 0; --i)
-          if (v[j][i] != 0xffffffffu && fb_test(fcur, v[j][i])) hit = i;
+          if (v[j][i] != 0xffffffffu && fb_test_hub(fcur, v[j][i], st.hb)) hit = i;
         if (hit < PR) {
           found[j] = true;
           j0[j] += hit + 1;
@@ -573,7 +623,7 @@ __device__ void pull_level(const SsspParams &p, const LevelState &st, uint32_t g
         uint32_t first = 0xffffffffu;  // first round (i) with a hit in this lane
 #pragma unroll
         for (int i = (int)kHW - 1; i >= 0; --i)
-          if (v[i] != 0xffffffffu && fb_test(fcur, v[i])) first = (uint32_t)i;
+          if (v[i] != 0xffffffffu && fb_test_hub(fcur, v[i], st.hb)) first = (uint32_t)i;
         const uint32_t hm = __ballot_sync(DAWN_FULL, first != 0xffffffffu);
         if (hm) {
           const uint32_t fmin = __reduce_min_sync(DAWN_FULL, first);
@@ -729,6 +779,8 @@ __device__ __forceinline__ void level_header(const SsspParams &p, Ctrl *C, Level
     // in-edges per round trip instead of 4
     st.deep = (st.dir == kPull && 6.0 * (double)st.mf < (double)(p.m - st.explored) + (double)st.mf)
                   ? 1u : 0u;
+    // hub cache for this level: every pull level; push levels with enough arcs to repay the copy
+    st.hb = (p.hw && !st.solo && (st.dir == kPull || st.mf >= p.hub_min)) ? p.hw * 32u : 0u;
   }
   if (p.trace && blockIdx.x == 0 && st.L < kTraceCap) {
     TraceRec r;
@@ -808,7 +860,8 @@ __global__ void __launch_bounds__(NT, MINB) k_sssp(SsspParams p) {
   const uint32_t nthreads = nblocks * NT;
   WarpStage &stg = stage[threadIdx.x / 32];
   Ctrl *C = p.ctrl;
-  unsigned long long bar_target = 0;
+  __shared__ unsigned long long bar_target;  // grid_sync's arrival target (thread 0's)
+  if (threadIdx.x == 0) bar_target = 0;
   if (p.vn && sources_invalid<NT>(p.vsrc, p.vn, p.n, &C->bad_src)) return;
   const uint32_t nsrc = p.nsrc ? p.nsrc : 1u;
   // batch mode: the searches run back to back in this launch, a grid barrier apart (no kernel
@@ -818,9 +871,14 @@ __global__ void __launch_bounds__(NT, MINB) k_sssp(SsspParams p) {
   const uint32_t src = p.nsrc ? ld_nc(p.sources + si) : p.source;
   uint32_t *const drow = p.dist + (size_t)si * p.n;
   dawn_sssp_stats *const stats_out = p.stats ? p.stats + si : nullptr;
-  uint32_t solo_epoch = 0;
-  // condition 1 bound: only vertices with an in-edge (plus s itself) can ever be reached
-  const uint32_t max_reach = ld_cg(&C->n_hasin) + ((p.noin[src >> 5] >> (src & 31)) & 1u);
+  // per-search scalars live in shared memory (thread 0 uses them): registers stay free for the
+  // level loops of the 64-register variant
+  __shared__ uint32_t solo_epoch, max_reach;
+  if (threadIdx.x == 0) {
+    solo_epoch = 0;
+    // condition 1 bound: only vertices with an in-edge (plus s itself) can ever be reached
+    max_reach = ld_cg(&C->n_hasin) + ((p.noin[src >> 5] >> (src & 31)) & 1u);
+  }
 
   if (p.trace && gtid == 0) p.trace[kTraceCap - 1].t_ns = globaltimer();  // kernel timeline
   // ---- k_narrow ran first for this call: finished (nothing to do) or hand-over (resume)
@@ -997,6 +1055,8 @@ __global__ void __launch_bounds__(NT, MINB) k_sssp(SsspParams p) {
       __syncthreads();
     }
 
+    // level-start copy of the hub words: the frontier L bitmap (pull) or the visited bitmap (push)
+    if (st.hb) hub_load(st.dir == kPull ? p.fb[st.b] : p.vis, p.hw);
     Slot *ns = &C->slot[(st.L + 1) % 3];
     uint32_t n_new = 0;
     unsigned long long m_new = 0;
