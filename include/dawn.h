@@ -203,6 +203,13 @@ typedef enum {
   DAWN_PARAM_HUB_MIN_EDGES = 14,   /* push levels whose frontier has fewer arcs skip the copy
                                       (0 = automatic: CTAs x HUB_WORDS / 8, the arcs whose saved
                                       L2 sectors pay for the copy).  Speed only.              */
+  DAWN_PARAM_PULL_TOP2 = 15,       /* 1: on graphs with n <= 2^22, pull sweeps of the grid-wide
+                                      SSSP kernel test the first two in-neighbours of each
+                                      unreached vertex from a per-vertex pair (built at load, 8
+                                      bytes per vertex; not in DAWN_GRAPH_LEAN) read beside its
+                                      visited word, so a vertex they settle never reads its
+                                      in-row.  0: off.  Default 1 (no effect above 2^22).
+                                      Speed only.                                             */
   DAWN_PARAM_DENSE_MAX_ENTRIES = 10 /* dense distance outputs (dawn_msssp dist, one piece of
                                       dawn_apsp_rows) are refused with DAWN_ERR_CAPACITY when
                                       rows * n >= this ("dense-matrix mode refused

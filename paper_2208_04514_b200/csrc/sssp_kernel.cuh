@@ -34,6 +34,7 @@ struct SsspParams {
   const uint32_t *noin;
   const uint32_t *hin_v, *hin_s, *hin_e, *hin_bits;  // static heavy in-row pieces
   const uint32_t *hasin;  // static ascending list of vertices with an in-edge (n_hasin)
+  const uint32_t *top2;   // [2n]: first two entries of each degree-ordered in-row, or null
   uint32_t *ulist, *useg;  // unreached list (per-warp segments) and segment counts
   uint32_t n_hasin;
   uint32_t *vis, *cand, *fb[3];  // cand: candidate bitmap of bitmap-push levels (zero between uses)
@@ -251,7 +252,7 @@ __device__ __forceinline__ void enqueue_frontier(const SsspParams &p, Slot *s, i
 template <int J, bool CAND, bool NOVIS = false>
 __device__ __forceinline__ void push_item(const SsspParams &p, const LevelState &st, Slot *ns,
                                           uint32_t item, uint32_t &n_new,
-                                          unsigned long long &m_new, WarpStage &stg,
+                                          uint32_t &m_new, WarpStage &stg,
                                           uint32_t &cnt) {
   const int q = st.q, qn = q ^ 1;
   const uint32_t lane = lane_id();
@@ -352,7 +353,7 @@ __device__ __forceinline__ void push_item(const SsspParams &p, const LevelState 
 // intermittently on B200; every cooperative kernel is kept at 0 bytes of stack.
 template <bool NV>
 __device__ void push_level(const SsspParams &p, const LevelState &st, Slot *ns, uint32_t gwarp,
-                           uint32_t nwarps, uint32_t &n_new, unsigned long long &m_new,
+                           uint32_t nwarps, uint32_t &n_new, uint32_t &m_new,
                            WarpStage &stg, long long &t0, unsigned long long *fsm) {
   const uint32_t E = st.qe;
   const uint32_t nchunks = (E + kChunk - 1) / kChunk;
@@ -406,7 +407,7 @@ __device__ void push_level(const SsspParams &p, const LevelState &st, Slot *ns, 
 // frontier vertex of its word and the round's rows are dealt 32 arcs at a time by the owner
 // search of push_item.
 __device__ void push_bitmap(const SsspParams &p, const LevelState &st, Slot *ns, uint32_t gwarp,
-                            uint32_t nwarps, uint32_t &n_new, unsigned long long &m_new,
+                            uint32_t nwarps, uint32_t &n_new, uint32_t &m_new,
                             WarpStage &stg, long long &t0, unsigned long long *fsm) {
   const uint32_t lane = lane_id();
   const uint32_t L1 = st.L + 1;
@@ -477,11 +478,12 @@ __device__ __forceinline__ bool fb_test_hub(const uint32_t *fb, uint32_t v, uint
   return ((v < hb ? hub_smem()[v >> 5] : fb[v >> 5]) >> (v & 31)) & 1u;
 }
 
-template <int PR, int J>  // in-edges probed per lane per round trip (8 when the frontier is
-                          // sparse); J unreached vertices per lane in flight
+template <int PR, int J, bool TOP2>  // in-edges probed per lane per round trip (8 when the
+                                     // frontier is sparse); J unreached vertices per lane in
+                                     // flight; TOP2: the pair path (p.top2 set)
 __device__ void pull_level(const SsspParams &p, const LevelState &st, uint32_t gwarp,
-                           uint32_t nwarps, uint32_t &n_new, unsigned long long &m_new,
-                           unsigned long long &examined, long long &t0, bool &bigf) {
+                           uint32_t nwarps, uint32_t &n_new, uint32_t &m_new,
+                           uint32_t &examined, long long &t0, bool &bigf) {
   const uint32_t lane = lane_id();
   const uint32_t L1 = st.L + 1;
   const uint32_t *fcur = p.fb[st.b];
@@ -502,6 +504,7 @@ __device__ void pull_level(const SsspParams &p, const LevelState &st, uint32_t g
   uint32_t wr = 0;
   for (uint32_t ib = 0; ib < cnt; ib += 32 * J) {
     uint32_t u[J], s[J], e[J], j0[J], ef[J];
+    uint2 t2[J];
     bool need[J], found[J], hvy[J];
 #pragma unroll
     for (int j = 0; j < J; ++j) {
@@ -518,14 +521,43 @@ __device__ void pull_level(const SsspParams &p, const LevelState &st, uint32_t g
         const uint32_t bit = 1u << (u[j] & 31);
         need[j] = !(ld_cg(p.vis + (u[j] >> 5)) & bit);   // settled by a push level since
         hvy[j] = ld_nc(p.hin_bits + (u[j] >> 5)) & bit;
-        s[j] = ld_nc(p.irp + u[j]);                       // speculative, same round trip
-        e[j] = ld_nc(p.irp + u[j] + 1);
+        if constexpr (!TOP2) {
+          s[j] = ld_nc(p.irp + u[j]);                     // speculative, same round trip
+          e[j] = ld_nc(p.irp + u[j] + 1);
+        } else {
+          t2[j] = ld_nc2(p.top2 + 2 * (size_t)u[j]);      // speculative, same round trip
+        }
+      }
+    }
+    // pair path: the first two in-neighbours come from the per-vertex pair, read in parallel
+    // with the visited word (no dependence on the row offset); a hit settles the vertex without
+    // its in-row, and only the others read their row offsets.  The skip counts as the probes it
+    // replaces (1 or 2, for edges_examined).
+    uint32_t skip[J];
+    if constexpr (TOP2) {
+#pragma unroll
+      for (int j = 0; j < J; ++j) {
+        skip[j] = 0;
+        if (need[j] && t2[j].x != ~0u) {
+          const bool h0 = fb_test_hub(fcur, t2[j].x, st.hb);
+          const bool h1 = t2[j].y != ~0u && fb_test_hub(fcur, t2[j].y, st.hb);
+          found[j] = h0 || h1;
+          skip[j] = h0 ? 1u : (t2[j].y != ~0u ? 2u : 1u);
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < J; ++j) {
+        if (need[j]) {  // the settled ones too: their degree feeds m_f
+          s[j] = ld_nc(p.irp + u[j]);
+          e[j] = ld_nc(p.irp + u[j] + 1);
+        }
       }
     }
 #pragma unroll
     for (int j = 0; j < J; ++j) {
       if (!need[j]) e[j] = s[j];
       j0[j] = s[j];
+      if constexpr (TOP2) j0[j] += skip[j];
       // heavy rows (in-degree > kHeavy): only the first kHeavyProbe in-edges here; the
       // static pieces finish the rows still unsettled
       ef[j] = hvy[j] ? min(e[j], s[j] + kHeavyProbe) : e[j];
@@ -655,7 +687,7 @@ __device__ void pull_level(const SsspParams &p, const LevelState &st, uint32_t g
 // write the frontier bitmap fb[b+1] (every word), clear fb[b+2] and cand, set dist = L+1.
 // 32 words per warp iteration (one lane each), then lane-per-vertex for words with news.
 __device__ void cand_filter(const SsspParams &p, const LevelState &st, uint32_t gwarp,
-                            uint32_t nwarps, uint32_t &n_new, unsigned long long &m_new,
+                            uint32_t nwarps, uint32_t &n_new, uint32_t &m_new,
                             bool &bigf) {
   const uint32_t lane = lane_id();
   const uint32_t L1 = st.L + 1;
@@ -863,14 +895,18 @@ __global__ void __launch_bounds__(NT, MINB) k_sssp(SsspParams p) {
   __shared__ unsigned long long bar_target;  // grid_sync's arrival target (thread 0's)
   if (threadIdx.x == 0) bar_target = 0;
   if (p.vn && sources_invalid<NT>(p.vsrc, p.vn, p.n, &C->bad_src)) return;
-  const uint32_t nsrc = p.nsrc ? p.nsrc : 1u;
+#define NSRC (p.nsrc ? p.nsrc : 1u)
+  // the search index lives in shared memory (re-read where used): the 64-register variant keeps
+  // no per-search value in a register across the level loop
+  __shared__ uint32_t si_sh;
+  if (threadIdx.x == 0) si_sh = 0;
+  __syncthreads();
   // batch mode: the searches run back to back in this launch, a grid barrier apart (no kernel
   // boundary or launch ramp between them)
   bool prefilled = false;  // this CTA's share of row si already holds UNREACHED
-  for (uint32_t si = 0; si < nsrc; ++si) {
-  const uint32_t src = p.nsrc ? ld_nc(p.sources + si) : p.source;
-  uint32_t *const drow = p.dist + (size_t)si * p.n;
-  dawn_sssp_stats *const stats_out = p.stats ? p.stats + si : nullptr;
+  for (;;) {
+  const uint32_t src = p.nsrc ? ld_nc(p.sources + *(volatile uint32_t *)&si_sh) : p.source;
+  uint32_t *const drow = p.dist + (size_t)(*(volatile uint32_t *)&si_sh) * p.n;
   // per-search scalars live in shared memory (thread 0 uses them): registers stay free for the
   // level loops of the 64-register variant
   __shared__ uint32_t solo_epoch, max_reach;
@@ -942,7 +978,8 @@ __global__ void __launch_bounds__(NT, MINB) k_sssp(SsspParams p) {
   grid_sync(&C->bar, nblocks, bar_target);
   if (p.trace && gtid == 0) p.trace[kTraceCap - 1].t_first = globaltimer();
 
-  unsigned long long examined = 0;
+  __shared__ unsigned long long examined;  // this CTA's pull probes of the search
+  if (threadIdx.x == 0) examined = 0;
   bool have_header = false;
   for (;;) {
     if (!have_header) {
@@ -956,7 +993,8 @@ __global__ void __launch_bounds__(NT, MINB) k_sssp(SsspParams p) {
       // ---- solo stretch: narrow push levels on CTA 0 with __syncthreads only
       if (blockIdx.x != 0) {
         __syncthreads();  // every thread has read st.stop / st.solo before thread 0 rewrites st
-        if ((MINB == 1 || DAWN_MINB2_EXTRAS) && si + 1 < nsrc && !prefilled) {
+        const uint32_t si = *(volatile uint32_t *)&si_sh;
+        if ((MINB == 1 || DAWN_MINB2_EXTRAS) && si + 1 < NSRC && !prefilled) {
           // idle while CTA 0 runs the narrow levels: initialise this CTA's share of the next
           // search's distance row (independent memory; its source entry is set at its init)
           uint32_t *nrow = p.dist + (size_t)(si + 1) * p.n;
@@ -981,7 +1019,7 @@ __global__ void __launch_bounds__(NT, MINB) k_sssp(SsspParams p) {
       for (;;) {
         Slot *ns = &C->slot[(st.L + 1) % 3];
         uint32_t n_new = 0;
-        unsigned long long m_new = 0;
+        uint32_t m_new = 0;  // per thread and level: <= m < 2^32
         long long t0 = clock64();
         push_level<MINB == 1>(p, st, ns, lw, NT / 32, n_new, m_new, stg, t0, fsm);
         block_flush(n_new, m_new, &ns->n_new, &ns->m_new, red);
@@ -1059,7 +1097,8 @@ __global__ void __launch_bounds__(NT, MINB) k_sssp(SsspParams p) {
     if (st.hb) hub_load(st.dir == kPull ? p.fb[st.b] : p.vis, p.hw);
     Slot *ns = &C->slot[(st.L + 1) % 3];
     uint32_t n_new = 0;
-    unsigned long long m_new = 0;
+    uint32_t m_new = 0;   // per thread and level: <= m < 2^32
+    uint32_t exam = 0;    // pull probes of this thread in this level (<= m)
     bool bigf = false;  // a bitmap frontier being built has a row of > kDirectRow arcs
     phase_add(p, st.L, 3, tconv);
     if (kDirect && direct) {
@@ -1072,16 +1111,26 @@ __global__ void __launch_bounds__(NT, MINB) k_sssp(SsspParams p) {
         phase_add(p, st.L, 1, tconv);
       }
     } else {
-#if DAWN_PULL_DEEP
-      if (st.deep)
-        pull_level<MINB == 1 ? DAWN_PULL_DEEP_PR : DAWN_PULL_DEEP_PR2, MINB == 1 ? DAWN_PULL_J : DAWN_PULL_J2>(p, st, gwarp, nwarps, n_new, m_new,
-                                                                      examined, tconv, bigf);
-      else
-#endif
-        pull_level<MINB == 1 ? DAWN_PULL_PR : DAWN_PULL_PR2, MINB == 1 ? DAWN_PULL_J : DAWN_PULL_J2>(p, st, gwarp, nwarps, n_new, m_new, examined,
-                                                            tconv, bigf);
+      constexpr int kPrD = MINB == 1 ? DAWN_PULL_DEEP_PR : DAWN_PULL_DEEP_PR2;
+      constexpr int kPr = MINB == 1 ? DAWN_PULL_PR : DAWN_PULL_PR2;
+      constexpr int kJ = MINB == 1 ? DAWN_PULL_J : DAWN_PULL_J2;
+      // pair path: 1-CTA/SM variant only (in 64 registers it fits only with one vertex per lane
+      // in flight, which measured 12% slower on Kronecker-24 than the plain sweep with two)
+      if (MINB == 1 && p.top2) {
+        if (DAWN_PULL_DEEP && st.deep)
+          pull_level<kPrD, kJ, MINB == 1>(p, st, gwarp, nwarps, n_new, m_new, exam, tconv, bigf);
+        else
+          pull_level<kPr, kJ, MINB == 1>(p, st, gwarp, nwarps, n_new, m_new, exam, tconv, bigf);
+      } else {
+        if (DAWN_PULL_DEEP && st.deep)
+          pull_level<kPrD, kJ, false>(p, st, gwarp, nwarps, n_new, m_new, exam, tconv, bigf);
+        else
+          pull_level<kPr, kJ, false>(p, st, gwarp, nwarps, n_new, m_new, exam, tconv, bigf);
+      }
     }
     block_flush(n_new, m_new, &ns->n_new, &ns->m_new, red);
+    exam = warp_sum(exam);
+    if (lane_id() == 0 && exam) atomicAdd(&examined, (unsigned long long)exam);
     if constexpr (kDirect) {
       if (__syncthreads_or(bigf) && threadIdx.x == 0) ns->big = 1;  // one store per CTA at most
     }
@@ -1094,8 +1143,11 @@ __global__ void __launch_bounds__(NT, MINB) k_sssp(SsspParams p) {
 
   if (p.trace && gtid == 0) p.trace[kTraceCap - 1].t_last = globaltimer();
   // ---- a7 statistics
-  if (stats_out) {
-    block_flush(0u, examined, nullptr, &C->examined, red);
+  const uint32_t si = *(volatile uint32_t *)&si_sh;
+  if (p.stats) {
+    dawn_sssp_stats *const stats_out = p.stats + si;
+    __syncthreads();
+    if (threadIdx.x == 0 && examined) atomicAdd(&C->examined, examined);
     grid_sync(&C->bar, nblocks, bar_target);
     if (blockIdx.x == 0 && threadIdx.x == 0) {
       dawn_sssp_stats s;
@@ -1108,9 +1160,13 @@ __global__ void __launch_bounds__(NT, MINB) k_sssp(SsspParams p) {
       *stats_out = s;
     }
   }
-  if (si + 1 < nsrc) grid_sync(&C->bar, nblocks, bar_target);  // before the next init
+  if (si + 1 >= NSRC) break;
+  grid_sync(&C->bar, nblocks, bar_target);  // before the next init (every thread has read si_sh)
+  if (threadIdx.x == 0) si_sh = si + 1;
+  __syncthreads();
   }  // sources
   grid_exit(&C->bar, nblocks);
+#undef NSRC
 }
 
 }  // namespace dawn
