@@ -191,25 +191,6 @@ typedef enum {
                                       its own bit-parallel state and stream (independent sources,
                                       PAPER L303-308).  1 .. 3 for n <= 2^22, else 1.  Default
                                       set at load from B200 measurements.      */
-  DAWN_PARAM_HUB_WORDS = 13,       /* bitmap cache of the grid-wide SSSP kernel on graphs with
-                                      n <= 2^22: each CTA copies the first HUB_WORDS 32-bit words
-                                      of the visited bitmap (push levels) or of the frontier
-                                      bitmap (pull levels) into its shared memory at the level
-                                      start and tests vertices [0, 32 * HUB_WORDS) there.  0 =
-                                      off; capped at the load-time capacity (49152 words, or the
-                                      whole bitmap if smaller).  Default: the whole bitmap when
-                                      it fits (n <= 1,572,864), else 0 (a prefix only pays off
-                                      when the caller numbers its hubs first).  Speed only.    */
-  DAWN_PARAM_HUB_MIN_EDGES = 14,   /* push levels whose frontier has fewer arcs skip the copy
-                                      (0 = automatic: CTAs x HUB_WORDS / 8, the arcs whose saved
-                                      L2 sectors pay for the copy).  Speed only.              */
-  DAWN_PARAM_PULL_TOP2 = 15,       /* 1: on graphs with n <= 2^22, pull sweeps of the grid-wide
-                                      SSSP kernel test the first two in-neighbours of each
-                                      unreached vertex from a per-vertex pair (built at load, 8
-                                      bytes per vertex; not in DAWN_GRAPH_LEAN) read beside its
-                                      visited word, so a vertex they settle never reads its
-                                      in-row.  0: off.  Default 1 (no effect above 2^22).
-                                      Speed only.                                             */
   DAWN_PARAM_DENSE_MAX_ENTRIES = 10 /* dense distance outputs (dawn_msssp dist, one piece of
                                       dawn_apsp_rows) are refused with DAWN_ERR_CAPACITY when
                                       rows * n >= this ("dense-matrix mode refused

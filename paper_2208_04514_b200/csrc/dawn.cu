@@ -43,7 +43,7 @@ void clear_err() { g_err[0] = 0; }
 
 constexpr int kNT = 512;  // threads per CTA of the persistent kernels
 // Graph-size thresholds of the kernel choice (measured on B200)
-constexpr uint32_t kHubWordsOne = 49152;   // bitmap cache words of k_sssp<kNT, 1> (192 KB)
+constexpr int64_t kSsspOneMaxN = 1 << 22;  // k_sssp<kNT, 1> (1 CTA/SM, 128 regs) up to 2^22
 constexpr int64_t kOneCtaMaxNM = 1 << 15;  // n + m this small: one CTA, barriers are __syncthreads
 constexpr int kMsBlocksPerSm = 2;          // k_ms64 CTAs per SM (if they fit)
 constexpr uint32_t kNarrowQcapMax = 1u << 20;
@@ -227,16 +227,6 @@ __global__ void k_topk_rows(const uint32_t *__restrict__ irp, const int32_t *__r
   }
 }
 
-// top2[u] = the first two in-neighbours of u's degree-ordered in-row (0xffffffff: none)
-__global__ void k_top2(const uint32_t *__restrict__ irp, const int32_t *__restrict__ icol2,
-                       uint32_t n, uint2 *__restrict__ top2) {
-  for (uint32_t u = blockIdx.x * blockDim.x + threadIdx.x; u < n; u += gridDim.x * blockDim.x) {
-    const uint32_t s = irp[u], e = irp[u + 1];
-    top2[u] = make_uint2(e > s ? (uint32_t)icol2[s] : 0xffffffffu,
-                         e > s + 1 ? (uint32_t)icol2[s + 1] : 0xffffffffu);
-  }
-}
-
 // pass 3 (piece-major order): hc[c] = #heavy rows with exactly c pieces; maxc
 __global__ void k_hhist(const uint32_t *__restrict__ rp, uint32_t n, uint32_t *hc, uint32_t *maxc) {
   uint32_t mx = 0;
@@ -349,9 +339,6 @@ struct dawn_graph_s {
   int ms_lanes = 1;               // DAWN_PARAM_MS_LANES (<= L.ms_nlanes)
   uint32_t wdelta = DAWN_WDELTA;   // DAWN_PARAM_WEIGHT_DELTA (0: near/far off)
   double dense_max = 1099511627776.0;  // DAWN_PARAM_DENSE_MAX_ENTRIES (k*n of a dense output)
-  uint32_t hub_cap = 0, hub_w = 0;     // DAWN_PARAM_HUB_WORDS: load-time capacity / current
-  unsigned long long hub_min = 0;      // DAWN_PARAM_HUB_MIN_EDGES (0: automatic)
-  bool top2_on = true;                 // DAWN_PARAM_PULL_TOP2
   // lane streams / fork-join events of dawn_sssp_batch (created at load, host resources only)
   cudaStream_t lane_st[kMaxLanes] = {};
   cudaEvent_t ev_fork = nullptr, ev_join[kMaxLanes] = {};
@@ -443,24 +430,7 @@ dawn_status load_csr(int64_t n, int64_t m, const int64_t *row_ptr, const int32_t
   if ((e = cudaSetDevice(g->device)) != cudaSuccess) { delete g; return cuda_fail(e, "cudaSetDevice"); }
   cudaDeviceGetAttribute(&g->nsm, cudaDevAttrMultiProcessorCount, g->device);
   // small graphs: k_sssp<kNT, 1> (one CTA per SM, 128 registers); big ones k_sssp<kNT, 2>
-  g->sssp_one = (uint64_t)n <= kSsspOneMaxN;
-  if (g->sssp_one) {
-    // bitmap cache capacity: the dynamic shared memory next to k_sssp<kNT, 1>'s static state
-    // (192 KB), never more than the bitmap.  On by default when the whole bitmap fits (ids in any
-    // order: n <= 1,572,864); a prefix of it only helps when low ids are the hubs.  The 2-CTA/SM
-    // variant has none: 2 x 96 KB of shared memory leaves its loads ~36 KB of L1, and a 96 KB
-    // prefix of Kronecker-24 (4.7% of the vertices, or 85% of the arc targets after a hub-first
-    // relabelling, which concentrates the claim atomics on a few words) measured slower either
-    // way.
-    const uint32_t nw4 = (uint32_t)(((n + 31) / 32 + 3) & ~int64_t(3));
-    g->hub_cap = std::min(kHubWordsOne, nw4);
-    if (cudaFuncSetAttribute((const void *)k_sssp<kNT, 1>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)(4 * g->hub_cap)) != cudaSuccess)
-      g->hub_cap = 0;
-    cudaGetLastError();
-    g->hub_w = (g->hub_cap == nw4) ? g->hub_cap : 0u;
-  }
+  g->sssp_one = n <= kSsspOneMaxN;
   g->sssp_grid = g->sssp_one ? std::min<int>(g->nsm, (int)kMaxBlocks)
                              : grid_for((const void *)k_sssp<kNT, 2>, g->nsm);
   {
@@ -599,9 +569,6 @@ dawn_status load_csr(int64_t n, int64_t m, const int64_t *row_ptr, const int32_t
     k_topk_rows<<<g->nsm * 8, 256, 0, st>>>(irp2, sym ? col : in_col, at<uint32_t>(g, L.rp),
                                             (uint32_t)n, at<int32_t>(g, L.icol2));
     g->icol = at<int32_t>(g, L.icol2);
-    if (L.top2)
-      k_top2<<<g->nsm * 8, 256, 0, st>>>(irp2, at<int32_t>(g, L.icol2), (uint32_t)n,
-                                         at<uint2>(g, L.top2));
   }
   if (sym || has_csc) {  // unreached-list seed for the pull sweep
     const uint32_t nblk = (uint32_t)((n + kScanBlock - 1) / kScanBlock);
@@ -682,11 +649,6 @@ dawn_status set_param(dawn_graph g, dawn_param key, double value) {
       if (value < 1) return fail(DAWN_ERR_INVALID_ARGUMENT, "dense limit must be >= 1");
       g->dense_max = std::min(value, 1099511627776.0);
       break;
-    case DAWN_PARAM_HUB_WORDS:
-      g->hub_w = (uint32_t)std::min<double>(value, g->hub_cap) & ~3u;
-      break;
-    case DAWN_PARAM_HUB_MIN_EDGES: g->hub_min = (unsigned long long)std::min(value, 1.8e19); break;
-    case DAWN_PARAM_PULL_TOP2: g->top2_on = value != 0; break;
     case DAWN_PARAM_NARROW_QUEUE_CAP:
       if (value < 32) return fail(DAWN_ERR_INVALID_ARGUMENT, "queue capacity must be >= 32");
       g->narrow_qcap = (uint32_t)std::min<double>(value, g->narrow_qcap_max);
@@ -713,8 +675,6 @@ SsspParams sssp_params(dawn_graph g, uint32_t variant, uint32_t *dist, dawn_sssp
   p.hin_s = at<uint32_t>(g, L.hin.s);
   p.hin_e = at<uint32_t>(g, L.hin.e);
   p.hin_bits = at<uint32_t>(g, L.hin.bits);
-  p.top2 = (L.top2 && g->icol == at<int32_t>(g, L.icol2) && g->top2_on) ? at<uint32_t>(g, L.top2)
-                                                                          : nullptr;
   p.vis = at<uint32_t>(g, Q.vis);
   p.cand = at<uint32_t>(g, Q.cand);
   p.hasin = at<uint32_t>(g, L.hasin);
@@ -746,12 +706,9 @@ SsspParams sssp_params(dawn_graph g, uint32_t variant, uint32_t *dist, dawn_sssp
 dawn_status launch_sssp(dawn_graph g, SsspParams &p, cudaStream_t stream, int lanes = 1) {
   int grid = std::max(1, g->sssp_grid / lanes);
   if (g->m + g->n <= kOneCtaMaxNM) grid = 1;  // tiny graphs: one CTA, barriers are __syncthreads
-  p.hw = g->hub_w;
-  p.hub_min = g->hub_min ? g->hub_min : (unsigned long long)grid * g->hub_w / 8;
   void *args[] = {&p};
   const void *kfn = g->sssp_one ? (const void *)k_sssp<kNT, 1> : (const void *)k_sssp<kNT, 2>;
-  cudaError_t e = cudaLaunchCooperativeKernel(kfn, dim3(grid), dim3(kNT), args,
-                                              4 * (size_t)p.hw, stream);
+  cudaError_t e = cudaLaunchCooperativeKernel(kfn, dim3(grid), dim3(kNT), args, 0, stream);
   if (e != cudaSuccess) return cuda_fail(e, "k_sssp launch");
   return DAWN_OK;
 }
@@ -1803,9 +1760,6 @@ dawn_status dawn_graph_get_param(dawn_graph g, dawn_param key, double *value) {
       case DAWN_PARAM_DENSE_MAX_ENTRIES: *value = g->dense_max; break;
       case DAWN_PARAM_MS_LANES: *value = g->ms_lanes; break;
       case DAWN_PARAM_WEIGHT_DELTA: *value = g->wdelta; break;
-      case DAWN_PARAM_HUB_WORDS: *value = g->hub_w; break;
-      case DAWN_PARAM_HUB_MIN_EDGES: *value = (double)g->hub_min; break;
-      case DAWN_PARAM_PULL_TOP2: *value = (g->top2_on && g->L.top2) ? 1.0 : 0.0; break;
       default: return fail(DAWN_ERR_INVALID_ARGUMENT, "unknown parameter");
     }
     return DAWN_OK;)

@@ -36,7 +36,6 @@ constexpr uint32_t kTopK = 8;  // in-row prefix ordered by in-neighbour out-degr
 constexpr uint32_t kScanBlock = 2048;  // elements per CTA in the load-time piece scan
 constexpr uint32_t kMaxBlocks = 2048;  // cap on persistent grid size (partials buffer)
 constexpr uint32_t kTraceCap = 1 << 16;
-constexpr uint64_t kSsspOneMaxN = 1ull << 22;  // k_sssp<kNT, 1> (1 CTA/SM, 128 regs) up to 2^22
 // k_narrow (narrow_kernel.cuh): one 16-CTA cluster, visited bitmap in distributed shared memory
 constexpr uint32_t kNarrowCluster = 16;            // CTAs per cluster (non-portable size)
 constexpr uint32_t kNarrowVisBytes = 160 * 1024;   // max visited-slice bytes per CTA
@@ -188,7 +187,7 @@ struct Layout {
   MsLaneLayout ms[kMaxLanes];
   int ms_nlanes;
   HeavyList hout, hin;
-  size_t scan_tmp, piece_tmp, hasin, ulist, useg, icol2, top2, arc;
+  size_t scan_tmp, piece_tmp, hasin, ulist, useg, icol2, arc;
   size_t seen, F0, F1, nxt, msctrl, part, srcbuf, total;
   uint64_t srccap, capCf, capHP;
   bool own_irp;
@@ -236,10 +235,6 @@ inline Layout make_layout(int64_t n, int64_t m, uint32_t flags) {
   L.ulist = take(4 * (size_t)n);
   L.useg = take(4 * (size_t)kMaxBlocks * 32);
   L.icol2 = (lean || m == 0) ? 0 : take(4 * (size_t)m);  // in-rows, highest-degree in-neighbours first
-  // the first two entries of every icol2 row as one 8-byte pair per vertex (0xffffffff: none):
-  // a pull probe of them needs no row offset (one dependent round trip less)
-  // (used by the 1-CTA/SM kernel variant only: n <= 2^22)
-  L.top2 = (L.icol2 && (uint64_t)n <= kSsspOneMaxN) ? take(8 * (size_t)n) : 0;
   // k_narrow's augmented arcs (target, target row start, target row end, 0): low-degree graphs
   L.arc = (!lean && m > 0 && (uint64_t)n <= kNarrowMaxN &&
            (uint64_t)m <= (uint64_t)kNarrowMaxAvgDeg * (uint64_t)n)

@@ -34,7 +34,6 @@ struct SsspParams {
   const uint32_t *noin;
   const uint32_t *hin_v, *hin_s, *hin_e, *hin_bits;  // static heavy in-row pieces
   const uint32_t *hasin;  // static ascending list of vertices with an in-edge (n_hasin)
-  const uint32_t *top2;   // [2n]: first two entries of each degree-ordered in-row, or null
   uint32_t *ulist, *useg;  // unreached list (per-warp segments) and segment counts
   uint32_t n_hasin;
   uint32_t *vis, *cand, *fb[3];  // cand: candidate bitmap of bitmap-push levels (zero between uses)
@@ -57,11 +56,6 @@ struct SsspParams {
   // device source list validated before any write (dawn_sssp_batch; vn = 0: host-validated)
   const uint32_t *vsrc;
   uint32_t vn;
-  // hub cache (dynamic shared memory): words [0, hw) of the visited bitmap (push levels) or of
-  // the frontier bitmap (pull levels) are copied into each CTA at the level start; hub_min: push
-  // levels with fewer frontier arcs skip the copy
-  uint32_t hw;
-  unsigned long long hub_min;
 };
 
 // Every CTA checks the whole device source list of a dawn_sssp_batch call before it writes
@@ -85,7 +79,6 @@ struct __align__(16) LevelState {
   uint32_t qe;                  // queue edges of frontier L
   uint32_t big;                 // frontier L (bitmap form) has a row of > kDirectRow arcs
   uint32_t novis;               // candidate push without the visited-word read (see push_item)
-  uint32_t hb;                  // vertices [0, hb) are tested in the CTA's hub cache this level
   unsigned long long mf, explored, push_edges, pad;
   uint32_t *drow;               // this search's distance row
 };
@@ -94,28 +87,6 @@ static_assert(sizeof(LevelState) % 16 == 0, "LevelState is copied as uint4");
 struct WarpStage {
   uint32_t u[64], rs[64], d[64];
 };
-
-// Hub cache: the first hw words of a bitmap in the CTA's dynamic shared memory.  With the
-// graph in hub order (DAWN_GRAPH_HUB_ORDER: the highest-degree vertices take ids 0, 1, ...),
-// those words hold the vertices most arcs point to (Kronecker-24: the first 786K ids are the
-// targets of 85% of the arcs), so most visited tests of a push level and most frontier probes of
-// a pull level are shared-memory reads instead of random L2 sectors.  Push levels cache a
-// level-start snapshot of `vis` (a set bit is final: the arc is skipped; a clear one falls
-// through to the global test, and the CTA sets the bit once it has claimed or marked the
-// vertex); pull levels cache the level-L frontier, which is read-only during the level.
-__device__ __forceinline__ uint32_t *hub_smem() {
-  extern __shared__ __align__(16) uint32_t dawn_hubw[];
-  return dawn_hubw;
-}
-
-// CTA-collective: copy words [0, hw) of src (hw a multiple of 4; the 256-B aligned workspace
-// arrays are readable up to the next multiple of 4 words) into the hub cache
-__device__ __forceinline__ void hub_load(const uint32_t *src, uint32_t hw) {
-  const uint4 *s4 = reinterpret_cast<const uint4 *>(src);
-  uint4 *d4 = reinterpret_cast<uint4 *>(hub_smem());
-  for (uint32_t i = threadIdx.x; i < hw / 4; i += blockDim.x) d4[i] = __ldcg(s4 + i);
-  __syncthreads();
-}
 
 __device__ __forceinline__ unsigned long long globaltimer() {
   unsigned long long t;
@@ -252,7 +223,7 @@ __device__ __forceinline__ void enqueue_frontier(const SsspParams &p, Slot *s, i
 template <int J, bool CAND, bool NOVIS = false>
 __device__ __forceinline__ void push_item(const SsspParams &p, const LevelState &st, Slot *ns,
                                           uint32_t item, uint32_t &n_new,
-                                          uint32_t &m_new, WarpStage &stg,
+                                          unsigned long long &m_new, WarpStage &stg,
                                           uint32_t &cnt) {
   const int q = st.q, qn = q ^ 1;
   const uint32_t lane = lane_id();
@@ -287,15 +258,10 @@ __device__ __forceinline__ void push_item(const SsspParams &p, const LevelState 
   }
   uint32_t cur[J];
   // candidate levels while few vertices are settled (st.novis): most targets are unvisited, so
-  // the visited-word read (one random L2 sector per arc) is skipped; cand_filter drops the rest.
-  // Hub targets (u < st.hb) are tested in the CTA's hub cache instead.
-  const uint32_t hb = st.hb;
-  uint32_t *const hubw = hub_smem();
+  // the visited-word read (one random L2 sector per arc) is skipped; cand_filter drops the rest
 #pragma unroll
   for (int j = 0; j < J; ++j)
-    cur[j] = !act[j] ? ~0u
-                     : (u[j] < hb ? hubw[u[j] >> 5]
-                                  : (NOVIS ? 0u : p.vis[u[j] >> 5]));  // weak: stale 0 = atomic
+    cur[j] = (act[j] && !NOVIS) ? p.vis[u[j] >> 5] : (act[j] ? 0u : ~0u);  // weak: stale 0 = atomic
   if constexpr (CAND) {
     // bitmap push: mark the candidate, settle later in cand_filter (no returning atomic)
 #if DAWN_CAND_FILTER
@@ -309,21 +275,14 @@ __device__ __forceinline__ void push_item(const SsspParams &p, const LevelState 
 #pragma unroll
     for (int j = 0; j < J; ++j) {
       const uint32_t bit = 1u << (u[j] & 31);
-      if (!(cur[j] & bit)) {
-        red_or(p.cand + (u[j] >> 5), bit);
-        if (u[j] < hb) atomicOr(hubw + (u[j] >> 5), bit);  // marked: later arcs of this CTA skip
-      }
+      if (!(cur[j] & bit)) red_or(p.cand + (u[j] >> 5), bit);
     }
   } else {
 #pragma unroll
     for (int j = 0; j < J; ++j) {
       const uint32_t bit = 1u << (u[j] & 31);
       disc[j] = false;
-      if (!(cur[j] & bit)) {
-        const uint32_t old = atomicOr(p.vis + (u[j] >> 5), bit);
-        disc[j] = !(old & bit);
-        if (u[j] < hb) atomicOr(hubw + (u[j] >> 5), old | bit);
-      }
+      if (!(cur[j] & bit)) disc[j] = !(atomicOr(p.vis + (u[j] >> 5), bit) & bit);
     }
 #pragma unroll
     for (int j = 0; j < J; ++j) {
@@ -353,7 +312,7 @@ __device__ __forceinline__ void push_item(const SsspParams &p, const LevelState 
 // intermittently on B200; every cooperative kernel is kept at 0 bytes of stack.
 template <bool NV>
 __device__ void push_level(const SsspParams &p, const LevelState &st, Slot *ns, uint32_t gwarp,
-                           uint32_t nwarps, uint32_t &n_new, uint32_t &m_new,
+                           uint32_t nwarps, uint32_t &n_new, unsigned long long &m_new,
                            WarpStage &stg, long long &t0, unsigned long long *fsm) {
   const uint32_t E = st.qe;
   const uint32_t nchunks = (E + kChunk - 1) / kChunk;
@@ -407,7 +366,7 @@ __device__ void push_level(const SsspParams &p, const LevelState &st, Slot *ns, 
 // frontier vertex of its word and the round's rows are dealt 32 arcs at a time by the owner
 // search of push_item.
 __device__ void push_bitmap(const SsspParams &p, const LevelState &st, Slot *ns, uint32_t gwarp,
-                            uint32_t nwarps, uint32_t &n_new, uint32_t &m_new,
+                            uint32_t nwarps, uint32_t &n_new, unsigned long long &m_new,
                             WarpStage &stg, long long &t0, unsigned long long *fsm) {
   const uint32_t lane = lane_id();
   const uint32_t L1 = st.L + 1;
@@ -445,12 +404,7 @@ __device__ void push_bitmap(const SsspParams &p, const LevelState &st, Slot *ns,
         bool disc = false;
         if (act) {
           const uint32_t bit = 1u << (u & 31);
-          const bool hub = u < st.hb;
-          if (!((hub ? hub_smem()[u >> 5] : p.vis[u >> 5]) & bit)) {
-            const uint32_t old = atomicOr(p.vis + (u >> 5), bit);
-            disc = !(old & bit);
-            if (hub) atomicOr(hub_smem() + (u >> 5), old | bit);
-          }
+          if (!(p.vis[u >> 5] & bit)) disc = !(atomicOr(p.vis + (u >> 5), bit) & bit);
         }
         uint32_t urs = 0, ud = 0;
         if (disc) {
@@ -473,17 +427,11 @@ __device__ __forceinline__ bool fb_test(const uint32_t *fb, uint32_t v) {
   return (fb[v >> 5] >> (v & 31)) & 1u;
 }
 
-// frontier test of a pull probe: hubs (v < hb) from the CTA's copy of the level-L frontier
-__device__ __forceinline__ bool fb_test_hub(const uint32_t *fb, uint32_t v, uint32_t hb) {
-  return ((v < hb ? hub_smem()[v >> 5] : fb[v >> 5]) >> (v & 31)) & 1u;
-}
-
-template <int PR, int J, bool TOP2>  // in-edges probed per lane per round trip (8 when the
-                                     // frontier is sparse); J unreached vertices per lane in
-                                     // flight; TOP2: the pair path (p.top2 set)
+template <int PR, int J>  // in-edges probed per lane per round trip (8 when the frontier is
+                          // sparse); J unreached vertices per lane in flight
 __device__ void pull_level(const SsspParams &p, const LevelState &st, uint32_t gwarp,
-                           uint32_t nwarps, uint32_t &n_new, uint32_t &m_new,
-                           uint32_t &examined, long long &t0, bool &bigf) {
+                           uint32_t nwarps, uint32_t &n_new, unsigned long long &m_new,
+                           unsigned long long &examined, long long &t0, bool &bigf) {
   const uint32_t lane = lane_id();
   const uint32_t L1 = st.L + 1;
   const uint32_t *fcur = p.fb[st.b];
@@ -504,7 +452,6 @@ __device__ void pull_level(const SsspParams &p, const LevelState &st, uint32_t g
   uint32_t wr = 0;
   for (uint32_t ib = 0; ib < cnt; ib += 32 * J) {
     uint32_t u[J], s[J], e[J], j0[J], ef[J];
-    uint2 t2[J];
     bool need[J], found[J], hvy[J];
 #pragma unroll
     for (int j = 0; j < J; ++j) {
@@ -521,43 +468,14 @@ __device__ void pull_level(const SsspParams &p, const LevelState &st, uint32_t g
         const uint32_t bit = 1u << (u[j] & 31);
         need[j] = !(ld_cg(p.vis + (u[j] >> 5)) & bit);   // settled by a push level since
         hvy[j] = ld_nc(p.hin_bits + (u[j] >> 5)) & bit;
-        if constexpr (!TOP2) {
-          s[j] = ld_nc(p.irp + u[j]);                     // speculative, same round trip
-          e[j] = ld_nc(p.irp + u[j] + 1);
-        } else {
-          t2[j] = ld_nc2(p.top2 + 2 * (size_t)u[j]);      // speculative, same round trip
-        }
-      }
-    }
-    // pair path: the first two in-neighbours come from the per-vertex pair, read in parallel
-    // with the visited word (no dependence on the row offset); a hit settles the vertex without
-    // its in-row, and only the others read their row offsets.  The skip counts as the probes it
-    // replaces (1 or 2, for edges_examined).
-    uint32_t skip[J];
-    if constexpr (TOP2) {
-#pragma unroll
-      for (int j = 0; j < J; ++j) {
-        skip[j] = 0;
-        if (need[j] && t2[j].x != ~0u) {
-          const bool h0 = fb_test_hub(fcur, t2[j].x, st.hb);
-          const bool h1 = t2[j].y != ~0u && fb_test_hub(fcur, t2[j].y, st.hb);
-          found[j] = h0 || h1;
-          skip[j] = h0 ? 1u : (t2[j].y != ~0u ? 2u : 1u);
-        }
-      }
-#pragma unroll
-      for (int j = 0; j < J; ++j) {
-        if (need[j]) {  // the settled ones too: their degree feeds m_f
-          s[j] = ld_nc(p.irp + u[j]);
-          e[j] = ld_nc(p.irp + u[j] + 1);
-        }
+        s[j] = ld_nc(p.irp + u[j]);                       // speculative, same round trip
+        e[j] = ld_nc(p.irp + u[j] + 1);
       }
     }
 #pragma unroll
     for (int j = 0; j < J; ++j) {
       if (!need[j]) e[j] = s[j];
       j0[j] = s[j];
-      if constexpr (TOP2) j0[j] += skip[j];
       // heavy rows (in-degree > kHeavy): only the first kHeavyProbe in-edges here; the
       // static pieces finish the rows still unsettled
       ef[j] = hvy[j] ? min(e[j], s[j] + kHeavyProbe) : e[j];
@@ -580,7 +498,7 @@ __device__ void pull_level(const SsspParams &p, const LevelState &st, uint32_t g
         uint32_t hit = PR;
 #pragma unroll
         for (int i = PR - 1; i >= 0; --i)
-          if (v[j][i] != 0xffffffffu && fb_test_hub(fcur, v[j][i], st.hb)) hit = i;
+          if (v[j][i] != 0xffffffffu && fb_test(fcur, v[j][i])) hit = i;
         if (hit < PR) {
           found[j] = true;
           j0[j] += hit + 1;
@@ -655,7 +573,7 @@ __device__ void pull_level(const SsspParams &p, const LevelState &st, uint32_t g
         uint32_t first = 0xffffffffu;  // first round (i) with a hit in this lane
 #pragma unroll
         for (int i = (int)kHW - 1; i >= 0; --i)
-          if (v[i] != 0xffffffffu && fb_test_hub(fcur, v[i], st.hb)) first = (uint32_t)i;
+          if (v[i] != 0xffffffffu && fb_test(fcur, v[i])) first = (uint32_t)i;
         const uint32_t hm = __ballot_sync(DAWN_FULL, first != 0xffffffffu);
         if (hm) {
           const uint32_t fmin = __reduce_min_sync(DAWN_FULL, first);
@@ -687,7 +605,7 @@ __device__ void pull_level(const SsspParams &p, const LevelState &st, uint32_t g
 // write the frontier bitmap fb[b+1] (every word), clear fb[b+2] and cand, set dist = L+1.
 // 32 words per warp iteration (one lane each), then lane-per-vertex for words with news.
 __device__ void cand_filter(const SsspParams &p, const LevelState &st, uint32_t gwarp,
-                            uint32_t nwarps, uint32_t &n_new, uint32_t &m_new,
+                            uint32_t nwarps, uint32_t &n_new, unsigned long long &m_new,
                             bool &bigf) {
   const uint32_t lane = lane_id();
   const uint32_t L1 = st.L + 1;
@@ -811,8 +729,6 @@ __device__ __forceinline__ void level_header(const SsspParams &p, Ctrl *C, Level
     // in-edges per round trip instead of 4
     st.deep = (st.dir == kPull && 6.0 * (double)st.mf < (double)(p.m - st.explored) + (double)st.mf)
                   ? 1u : 0u;
-    // hub cache for this level: every pull level; push levels with enough arcs to repay the copy
-    st.hb = (p.hw && !st.solo && (st.dir == kPull || st.mf >= p.hub_min)) ? p.hw * 32u : 0u;
   }
   if (p.trace && blockIdx.x == 0 && st.L < kTraceCap) {
     TraceRec r;
@@ -892,29 +808,19 @@ __global__ void __launch_bounds__(NT, MINB) k_sssp(SsspParams p) {
   const uint32_t nthreads = nblocks * NT;
   WarpStage &stg = stage[threadIdx.x / 32];
   Ctrl *C = p.ctrl;
-  __shared__ unsigned long long bar_target;  // grid_sync's arrival target (thread 0's)
-  if (threadIdx.x == 0) bar_target = 0;
+  unsigned long long bar_target = 0;
   if (p.vn && sources_invalid<NT>(p.vsrc, p.vn, p.n, &C->bad_src)) return;
-#define NSRC (p.nsrc ? p.nsrc : 1u)
-  // the search index lives in shared memory (re-read where used): the 64-register variant keeps
-  // no per-search value in a register across the level loop
-  __shared__ uint32_t si_sh;
-  if (threadIdx.x == 0) si_sh = 0;
-  __syncthreads();
+  const uint32_t nsrc = p.nsrc ? p.nsrc : 1u;
   // batch mode: the searches run back to back in this launch, a grid barrier apart (no kernel
   // boundary or launch ramp between them)
   bool prefilled = false;  // this CTA's share of row si already holds UNREACHED
-  for (;;) {
-  const uint32_t src = p.nsrc ? ld_nc(p.sources + *(volatile uint32_t *)&si_sh) : p.source;
-  uint32_t *const drow = p.dist + (size_t)(*(volatile uint32_t *)&si_sh) * p.n;
-  // per-search scalars live in shared memory (thread 0 uses them): registers stay free for the
-  // level loops of the 64-register variant
-  __shared__ uint32_t solo_epoch, max_reach;
-  if (threadIdx.x == 0) {
-    solo_epoch = 0;
-    // condition 1 bound: only vertices with an in-edge (plus s itself) can ever be reached
-    max_reach = ld_cg(&C->n_hasin) + ((p.noin[src >> 5] >> (src & 31)) & 1u);
-  }
+  for (uint32_t si = 0; si < nsrc; ++si) {
+  const uint32_t src = p.nsrc ? ld_nc(p.sources + si) : p.source;
+  uint32_t *const drow = p.dist + (size_t)si * p.n;
+  dawn_sssp_stats *const stats_out = p.stats ? p.stats + si : nullptr;
+  uint32_t solo_epoch = 0;
+  // condition 1 bound: only vertices with an in-edge (plus s itself) can ever be reached
+  const uint32_t max_reach = ld_cg(&C->n_hasin) + ((p.noin[src >> 5] >> (src & 31)) & 1u);
 
   if (p.trace && gtid == 0) p.trace[kTraceCap - 1].t_ns = globaltimer();  // kernel timeline
   // ---- k_narrow ran first for this call: finished (nothing to do) or hand-over (resume)
@@ -978,8 +884,7 @@ __global__ void __launch_bounds__(NT, MINB) k_sssp(SsspParams p) {
   grid_sync(&C->bar, nblocks, bar_target);
   if (p.trace && gtid == 0) p.trace[kTraceCap - 1].t_first = globaltimer();
 
-  __shared__ unsigned long long examined;  // this CTA's pull probes of the search
-  if (threadIdx.x == 0) examined = 0;
+  unsigned long long examined = 0;
   bool have_header = false;
   for (;;) {
     if (!have_header) {
@@ -993,8 +898,7 @@ __global__ void __launch_bounds__(NT, MINB) k_sssp(SsspParams p) {
       // ---- solo stretch: narrow push levels on CTA 0 with __syncthreads only
       if (blockIdx.x != 0) {
         __syncthreads();  // every thread has read st.stop / st.solo before thread 0 rewrites st
-        const uint32_t si = *(volatile uint32_t *)&si_sh;
-        if ((MINB == 1 || DAWN_MINB2_EXTRAS) && si + 1 < NSRC && !prefilled) {
+        if ((MINB == 1 || DAWN_MINB2_EXTRAS) && si + 1 < nsrc && !prefilled) {
           // idle while CTA 0 runs the narrow levels: initialise this CTA's share of the next
           // search's distance row (independent memory; its source entry is set at its init)
           uint32_t *nrow = p.dist + (size_t)(si + 1) * p.n;
@@ -1019,7 +923,7 @@ __global__ void __launch_bounds__(NT, MINB) k_sssp(SsspParams p) {
       for (;;) {
         Slot *ns = &C->slot[(st.L + 1) % 3];
         uint32_t n_new = 0;
-        uint32_t m_new = 0;  // per thread and level: <= m < 2^32
+        unsigned long long m_new = 0;
         long long t0 = clock64();
         push_level<MINB == 1>(p, st, ns, lw, NT / 32, n_new, m_new, stg, t0, fsm);
         block_flush(n_new, m_new, &ns->n_new, &ns->m_new, red);
@@ -1093,12 +997,9 @@ __global__ void __launch_bounds__(NT, MINB) k_sssp(SsspParams p) {
       __syncthreads();
     }
 
-    // level-start copy of the hub words: the frontier L bitmap (pull) or the visited bitmap (push)
-    if (st.hb) hub_load(st.dir == kPull ? p.fb[st.b] : p.vis, p.hw);
     Slot *ns = &C->slot[(st.L + 1) % 3];
     uint32_t n_new = 0;
-    uint32_t m_new = 0;   // per thread and level: <= m < 2^32
-    uint32_t exam = 0;    // pull probes of this thread in this level (<= m)
+    unsigned long long m_new = 0;
     bool bigf = false;  // a bitmap frontier being built has a row of > kDirectRow arcs
     phase_add(p, st.L, 3, tconv);
     if (kDirect && direct) {
@@ -1111,26 +1012,16 @@ __global__ void __launch_bounds__(NT, MINB) k_sssp(SsspParams p) {
         phase_add(p, st.L, 1, tconv);
       }
     } else {
-      constexpr int kPrD = MINB == 1 ? DAWN_PULL_DEEP_PR : DAWN_PULL_DEEP_PR2;
-      constexpr int kPr = MINB == 1 ? DAWN_PULL_PR : DAWN_PULL_PR2;
-      constexpr int kJ = MINB == 1 ? DAWN_PULL_J : DAWN_PULL_J2;
-      // pair path: 1-CTA/SM variant only (in 64 registers it fits only with one vertex per lane
-      // in flight, which measured 12% slower on Kronecker-24 than the plain sweep with two)
-      if (MINB == 1 && p.top2) {
-        if (DAWN_PULL_DEEP && st.deep)
-          pull_level<kPrD, kJ, MINB == 1>(p, st, gwarp, nwarps, n_new, m_new, exam, tconv, bigf);
-        else
-          pull_level<kPr, kJ, MINB == 1>(p, st, gwarp, nwarps, n_new, m_new, exam, tconv, bigf);
-      } else {
-        if (DAWN_PULL_DEEP && st.deep)
-          pull_level<kPrD, kJ, false>(p, st, gwarp, nwarps, n_new, m_new, exam, tconv, bigf);
-        else
-          pull_level<kPr, kJ, false>(p, st, gwarp, nwarps, n_new, m_new, exam, tconv, bigf);
-      }
+#if DAWN_PULL_DEEP
+      if (st.deep)
+        pull_level<MINB == 1 ? DAWN_PULL_DEEP_PR : DAWN_PULL_DEEP_PR2, MINB == 1 ? DAWN_PULL_J : DAWN_PULL_J2>(p, st, gwarp, nwarps, n_new, m_new,
+                                                                      examined, tconv, bigf);
+      else
+#endif
+        pull_level<MINB == 1 ? DAWN_PULL_PR : DAWN_PULL_PR2, MINB == 1 ? DAWN_PULL_J : DAWN_PULL_J2>(p, st, gwarp, nwarps, n_new, m_new, examined,
+                                                            tconv, bigf);
     }
     block_flush(n_new, m_new, &ns->n_new, &ns->m_new, red);
-    exam = warp_sum(exam);
-    if (lane_id() == 0 && exam) atomicAdd(&examined, (unsigned long long)exam);
     if constexpr (kDirect) {
       if (__syncthreads_or(bigf) && threadIdx.x == 0) ns->big = 1;  // one store per CTA at most
     }
@@ -1143,11 +1034,8 @@ __global__ void __launch_bounds__(NT, MINB) k_sssp(SsspParams p) {
 
   if (p.trace && gtid == 0) p.trace[kTraceCap - 1].t_last = globaltimer();
   // ---- a7 statistics
-  const uint32_t si = *(volatile uint32_t *)&si_sh;
-  if (p.stats) {
-    dawn_sssp_stats *const stats_out = p.stats + si;
-    __syncthreads();
-    if (threadIdx.x == 0 && examined) atomicAdd(&C->examined, examined);
+  if (stats_out) {
+    block_flush(0u, examined, nullptr, &C->examined, red);
     grid_sync(&C->bar, nblocks, bar_target);
     if (blockIdx.x == 0 && threadIdx.x == 0) {
       dawn_sssp_stats s;
@@ -1160,13 +1048,9 @@ __global__ void __launch_bounds__(NT, MINB) k_sssp(SsspParams p) {
       *stats_out = s;
     }
   }
-  if (si + 1 >= NSRC) break;
-  grid_sync(&C->bar, nblocks, bar_target);  // before the next init (every thread has read si_sh)
-  if (threadIdx.x == 0) si_sh = si + 1;
-  __syncthreads();
+  if (si + 1 < nsrc) grid_sync(&C->bar, nblocks, bar_target);  // before the next init
   }  // sources
   grid_exit(&C->bar, nblocks);
-#undef NSRC
 }
 
 }  // namespace dawn

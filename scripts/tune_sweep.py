@@ -30,8 +30,7 @@ def t():
     return np.median(ts) * 1e3 / len(srcs)
 
 
-base = dict(solo_edges=512, bitmap_push_grow_edges=4096, bitmap_push_edges=1 << 18, alpha=2, beta=96,
-            hub_words=G.get_tuning("hub_words"), hub_min_edges=0, pull_top2=1)
+base = dict(solo_edges=512, bitmap_push_grow_edges=4096, bitmap_push_edges=1 << 18, alpha=2, beta=96)
 print(cfg, "default us/search %.2f" % t(), flush=True)
 SWEEP = {"alpha": (1, 4, 8), "beta": (48, 192), "bitmap_push_edges": (1 << 16, 1 << 20),
          "solo_edges": (128, 2048)}

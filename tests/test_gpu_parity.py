@@ -258,18 +258,6 @@ def test_tunables_never_change_results(knobs):
         check_sssp(g, G, srcs, variants=("auto", "push"))
 
 
-@pytest.mark.parametrize("knobs", [dict(pull_top2=0), dict(hub_words=0), dict(hub_words=4, hub_min_edges=1),
-                                   dict(hub_words=0, pull_top2=0), dict(hub_min_edges=1)])
-def test_cache_and_pair_knobs_never_change_results(knobs):
-    # the bitmap cache (whole bitmap, a 4-word prefix, push levels of any size) and the pull
-    # sweep's in-neighbour pair path, on and off, in every variant (tolerance 0)
-    for g in (graphgen.kron(13, 16), graphgen.er_prob(3000, 0.002, 4), graphgen.grid(200, 150)):
-        G = dev_graph(g)
-        G.set_tuning(**knobs)
-        srcs = [0, g.n - 1] + list(g.sample_sources(3, seed=2))
-        check_sssp(g, G, srcs, variants=("auto", "push", "pull"))
-
-
 def test_narrow_kernel_and_handover():
     # dawn_sssp starts on one 16-CTA cluster (k_narrow); wide frontiers (or full queues) hand
     # over to the grid-wide kernel, which resumes from the frontier bitmap.
