@@ -401,60 +401,88 @@ def run_sssp(args, rank, world, dev, cfg, steps, warmup, e2e=True, with_cpu=Fals
         del ms_dist
     if e2e:
         # end to end through the public API with HOST buffers: the source list H2D (pinned),
-        # dawn_sssp_batch per source, each distance row compacted to 1 byte per vertex on the
-        # device (dawn_dist_u8: exact while eps < 255, checked through its flag) and copied to
-        # pinned host memory on a second stream while the next search runs
+        # dawn_sssp_batch per chunk of sources, each distance row compacted on the device to 4
+        # bits per vertex (dawn_dist_u4: exact while eps < 15, checked through its flag; 1 byte
+        # with dawn_dist_u8 otherwise) and copied to pinned host memory on a second stream while
+        # the next chunk's searches run
         host_src = torch.from_numpy(srcs.astype(np.int32)).pin_memory()
         dev_src = torch.empty_like(host_src, device=dev)
-        host_u8 = torch.empty((k, g.n), dtype=torch.uint8, pin_memory=True)
-        # sources per dawn_sssp_batch call: two searches per batch lane, so a chunk keeps every
-        # lane busy while the previous chunk's rows travel
-        CH = max(1, min(k, 2 * int(G.get_tuning("batch_lanes"))))
-        dev_u8 = torch.empty((2, CH, g.n), dtype=torch.uint8, device=dev)
+        # sources per dawn_sssp_batch call: halving chunks (a multiple of the batch lanes, e.g.
+        # 32, 16, 8, 4, 4 on C4): each chunk's rows travel while the next, half as long, chunk
+        # searches, and only the last small chunk's copy is exposed
+        lanes_b = int(G.get_tuning("batch_lanes"))
+        chunks, c0 = [], 0
+        while c0 < k:
+            c = min(k - c0, max(lanes_b, ((k - c0) // 2) // lanes_b * lanes_b))
+            chunks.append((c0, c0 + c))
+            c0 += c
+        CH = max(c1 - c0 for c0, c1 in chunks)
         flags = torch.zeros(1, dtype=torch.int32, device=dev)
         host_flags = torch.zeros(1, dtype=torch.int32, pin_memory=True)
         copy_stream = torch.cuda.Stream(device=dev)
         slot_free = [torch.cuda.Event(), torch.cuda.Event()]
+        state = {}
+
+        def setup(bits):
+            state.clear()
+            per = g.n // 2 if bits == 4 else g.n  # bytes per row (n even for 4 bits)
+            state["bits"], state["per"] = bits, per
+            state["host"] = torch.empty(k * per, dtype=torch.uint8, pin_memory=True)
+            state["dev"] = torch.empty((2, CH * per), dtype=torch.uint8, device=dev)
+            state["pack"] = dawn.dist_u4 if bits == 4 else dawn.dist_u8
 
         def e2e_step():
+            per, host_b, dev_b, pack = state["per"], state["host"], state["dev"], state["pack"]
             dev_src.copy_(host_src, non_blocking=True)
             flags.zero_()
-            for j, c0 in enumerate(range(0, k, CH)):
-                c1 = min(k, c0 + CH)
+            for j, (c0, c1) in enumerate(chunks):
                 b = j & 1
                 dawn.sssp_batch(G, dev_src[c0:c1], args.variant, out=out[c0:c1])
                 if j >= 2:
-                    stream.wait_event(slot_free[b])  # the copy of chunk j-2 left dev_u8[b]
-                dawn.dist_u8(out[c0:c1], out=dev_u8[b, : c1 - c0], flags=flags)
+                    stream.wait_event(slot_free[b])  # the copy of chunk j-2 left dev_b[b]
+                nbytes = (c1 - c0) * per
+                pack(out[c0:c1], out=dev_b[b, :nbytes], flags=flags)
                 done = torch.cuda.Event()
                 done.record(stream)
                 copy_stream.wait_event(done)
                 with torch.cuda.stream(copy_stream):
-                    host_u8[c0:c1].copy_(dev_u8[b, : c1 - c0], non_blocking=True)
+                    host_b[c0 * per: c0 * per + nbytes].copy_(dev_b[b, :nbytes], non_blocking=True)
                     slot_free[b].record(copy_stream)
             host_flags.copy_(flags, non_blocking=True)
             stream.wait_stream(copy_stream)
 
+        setup(4 if g.n % 2 == 0 else 8)
         e2e_step()
         torch.cuda.synchronize()
+        if int(host_flags[0]):  # a distance >= 15: the 1-byte rows
+            setup(8)
+            e2e_step()
+            torch.cuda.synchronize()
         e_ms = timed(e2e_step, max(1, min(steps, 10)), flush, stream)
         e_tot = sum(e_ms)
         if world > 1:
             t = torch.tensor([e_tot], dtype=torch.float64, device=dev)
             tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
             e_tot = float(t.item())
-        assert int(host_flags[0]) == 0, "a distance >= 255 would need the uint32 row"
+        bits, per, host_b = state["bits"], state["per"], state["host"]
+        assert int(host_flags[0]) == 0, f"a distance did not fit {bits} bits"
         d0 = out[0].cpu().numpy().view(np.uint32)
-        assert np.array_equal(host_u8[0].numpy(), np.where(d0 == 0xFFFFFFFF, 255, d0).astype(np.uint8))
+        if bits == 4:
+            assert np.array_equal(dawn.unpack_u4(host_b[:per].numpy(), g.n), d0)
+        else:
+            assert np.array_equal(host_b[:per].numpy(), np.where(d0 == 0xFFFFFFFF, 255, d0).astype(np.uint8))
+        enc = ("dawn_dist_u4 (4 bits per vertex, exact while eps < 15" if bits == 4 else
+               "dawn_dist_u8 (1 byte per vertex, exact while eps < 255")
         res["e2e"] = {"value": edges_step * len(e_ms) * world / (e_tot * 1e-3) / 1e9,
                       "unit": "GTEPS", "h2d_bytes_per_step": int(host_src.numel() * 4),
-                      "d2h_bytes_per_step": int(host_u8.numel() + 4),
+                      "d2h_bytes_per_step": int(host_b.numel() + 4),
                       "ms_per_step": e_tot / len(e_ms),
-                      "how": f"source list H2D from pinned memory, dawn_sssp_batch per {CH} sources, "
-                             "dawn_dist_u8 (1 byte per vertex, exact while eps < 255; its flag is "
-                             "read back and checked), the rows D2H into pinned memory on a second "
-                             "stream overlapping the next chunk's searches"}
-        del host_u8
+                      "how": f"source list H2D from pinned memory, dawn_sssp_batch per chunk of "
+                             f"{[c1 - c0 for c0, c1 in chunks]} sources, "
+                             f"{enc}; its flag is read back and checked; the first row is "
+                             "compared with the device row), the rows D2H into pinned memory on a "
+                             "second stream overlapping the next chunk's searches"}
+        state.clear()
     if with_cpu:
         cores = len(os.sched_getaffinity(0))
         gte, done, wall = cpu_oracle_sssp(g, srcs, args.cpu_budget, cores)

@@ -345,6 +345,19 @@ dawn_status dawn_dist_u8(const uint32_t *dist, int64_t count, uint8_t *out, uint
                          void *stream);
 
 /*
+ * The same compaction at 4 bits per vertex (two distances per byte): nibble value
+ * min(dist[i], 15), 15 = DAWN_UNREACHED or a finite distance >= 15 (which sets bit 0 of *flags:
+ * the caller then transfers the rows with dawn_dist_u8 or as uint32).  Entry 2j goes to the low
+ * nibble of out[j], entry 2j + 1 to the high nibble; for an odd count the last high nibble is 15.
+ * Kronecker graphs (eps <= 8 on C2/C4) thus move half a byte per vertex to the host.
+ *   dist  DEVICE uint32[count], 16-byte aligned;  out  DEVICE uint8[ceil(count / 2)], 4-byte
+ *   aligned;  flags DEVICE uint32, OR-ed (never cleared by the call).  Enqueue only.
+ * Errors: INVALID_ARGUMENT (NULL with count > 0, misaligned pointers), CUDA.
+ */
+dawn_status dawn_dist_u4(const uint32_t *dist, int64_t count, uint8_t *out, uint32_t *flags,
+                         void *stream);
+
+/*
  * Weighted single-source shortest paths: DAWN's SOVM round over the
  * (min,+) semiring, the extension PAPER.md L596 names as future work (reading Q26 of
  * DESIGN.md): the frontier holds the vertices whose distance dropped in the previous round;

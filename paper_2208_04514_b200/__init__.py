@@ -18,7 +18,7 @@ import numpy as np
 import torch
 
 __all__ = ["build", "Graph", "sssp", "sssp_batch", "msssp", "apsp", "apsp_rows", "apsp_shard",
-           "wsssp", "wsssp_batch", "dist_u8", "part_range", "part_build", "PartGraph", "part_exchange", "part_sssp", "part_sssp_local",
+           "wsssp", "wsssp_batch", "dist_u8", "dist_u4", "unpack_u4", "part_range", "part_build", "PartGraph", "part_exchange", "part_sssp", "part_sssp_local",
            "part_fused_local", "part_sssp_fused", "largest_wcc",
            "check", "DawnError", "UNREACHED", "AUTO", "PUSH", "PULL", "MS_BATCH", "REC_DTYPE",
            "records_to_numpy", "stats_to_dict", "gather_records"]
@@ -128,6 +128,8 @@ def lib():
         L.dawn_wsssp_batch.argtypes = [vp, vp, i64, vp, vp, vp, vp]
         L.dawn_dist_u8.restype = st
         L.dawn_dist_u8.argtypes = [vp, i64, vp, vp, vp]
+        L.dawn_dist_u4.restype = st
+        L.dawn_dist_u4.argtypes = [vp, i64, vp, vp, vp]
         L.dawn_wsssp.restype = st
         L.dawn_wsssp.argtypes = [vp, i64, vp, vp, vp, vp]
         L.dawn_part_range.restype = st
@@ -432,6 +434,32 @@ def dist_u8(dist: torch.Tensor, out: torch.Tensor | None = None,
     flags = flags if flags is not None else torch.zeros(1, dtype=torch.int32, device=dist.device)
     _check(lib().dawn_dist_u8(_dptr(dist), dist.numel(), _dptr(out), _dptr(flags), _stream(stream)))
     return out, flags
+
+
+def dist_u4(dist: torch.Tensor, out: torch.Tensor | None = None,
+            flags: torch.Tensor | None = None, stream=None):
+    """dawn_dist_u4: 4-bit copy of distance rows, two per byte (15 = unreached, or a distance
+    >= 15 that did not fit: then flags[0] bit 0 is set).  Returns (uint8 tensor of
+    ceil(numel / 2) bytes, int32 flags[1])."""
+    assert dist.is_cuda and dist.dtype in (torch.int32, torch.uint32) and dist.is_contiguous()
+    nb = (dist.numel() + 1) // 2
+    out = out if out is not None else torch.empty(nb, dtype=torch.uint8, device=dist.device)
+    assert out.numel() >= nb and out.dtype == torch.uint8
+    flags = flags if flags is not None else torch.zeros(1, dtype=torch.int32, device=dist.device)
+    _check(lib().dawn_dist_u4(_dptr(dist), dist.numel(), _dptr(out), _dptr(flags), _stream(stream)))
+    return out, flags
+
+
+def unpack_u4(packed: np.ndarray, count: int) -> np.ndarray:
+    """Host-side inverse of dawn_dist_u4 (argument marshalling for the caller): uint32 distances
+    with 15 read back as UNREACHED (valid when the call's flag stayed clear)."""
+    b = np.asarray(packed, dtype=np.uint8)
+    d = np.empty(2 * len(b), dtype=np.uint32)
+    d[0::2] = b & 15
+    d[1::2] = b >> 4
+    d = d[:count]
+    d[d == 15] = UNREACHED
+    return d
 
 
 def wsssp(g: Graph, source: int, weights: torch.Tensor, stats: bool = False,

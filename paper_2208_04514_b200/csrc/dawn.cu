@@ -1231,6 +1231,53 @@ __global__ void k_dist_u8(const uint32_t *__restrict__ d, int64_t count, uint8_t
   if (__syncthreads_or(over) && threadIdx.x == 0) atomicOr(flags, 1u);
 }
 
+// 4-bit rows: thread i packs entries 8i .. 8i+7 (two 16-byte loads) into one 32-bit word
+__global__ void k_dist_u4(const uint32_t *__restrict__ d, int64_t count, uint8_t *__restrict__ out,
+                          uint32_t *flags) {
+  const int64_t n8 = count / 8;
+  bool over = false;
+  auto nib = [&](uint32_t v) -> uint32_t {
+    over |= v >= 15u && v != kUnreached;
+    return v < 15u ? v : 15u;
+  };
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n8;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint4 x = __ldcs(reinterpret_cast<const uint4 *>(d) + 2 * i);
+    const uint4 y = __ldcs(reinterpret_cast<const uint4 *>(d) + 2 * i + 1);
+    const uint32_t a[8] = {x.x, x.y, x.z, x.w, y.x, y.y, y.z, y.w};
+    uint32_t packed = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) packed |= nib(a[k]) << (4 * k);
+    reinterpret_cast<uint32_t *>(out)[i] = packed;
+  }
+  // tail (< 8 entries): one thread per output byte
+  const int64_t b0 = 4 * n8, nb = (count + 1) / 2;
+  for (int64_t b = b0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < nb;
+       b += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t lo = nib(d[2 * b]);
+    const uint32_t hi = (2 * b + 1 < count) ? nib(d[2 * b + 1]) : 15u;
+    out[b] = (uint8_t)(lo | (hi << 4));
+  }
+  if (__syncthreads_or(over) && threadIdx.x == 0) atomicOr(flags, 1u);
+}
+
+dawn_status dist_u4(const uint32_t *dist, int64_t count, uint8_t *out, uint32_t *flags,
+                    void *stream) {
+  if (count < 0 || (count > 0 && (!dist || !out || !flags)))
+    return fail(DAWN_ERR_INVALID_ARGUMENT, "bad arguments");
+  if ((reinterpret_cast<uintptr_t>(dist) & 15) || (reinterpret_cast<uintptr_t>(out) & 3))
+    return fail(DAWN_ERR_INVALID_ARGUMENT, "dist must be 16-byte and out 4-byte aligned");
+  if (count == 0) return DAWN_OK;
+  int dev = 0, nsm = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(nsm * 8, (count / 8 + 255) / 256));
+  k_dist_u4<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(dist, count, out, flags);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "k_dist_u4 launch");
+  return DAWN_OK;
+}
+
 dawn_status dist_u8(const uint32_t *dist, int64_t count, uint8_t *out, uint32_t *flags,
                     void *stream) {
   if (count < 0 || (count > 0 && (!dist || !out || !flags)))
@@ -1821,6 +1868,11 @@ dawn_status dawn_graph_ms_counters(dawn_graph g, uint64_t *host_out, void *strea
 dawn_status dawn_dist_u8(const uint32_t *dist, int64_t count, uint8_t *out, uint32_t *flags,
                          void *stream) {
   DAWN_GUARD(return dist_u8(dist, count, out, flags, stream);)
+}
+
+dawn_status dawn_dist_u4(const uint32_t *dist, int64_t count, uint8_t *out, uint32_t *flags,
+                         void *stream) {
+  DAWN_GUARD(return dist_u4(dist, count, out, flags, stream);)
 }
 
 dawn_status dawn_wsssp(dawn_graph g, int64_t source, const uint32_t *weights, uint32_t *dist,

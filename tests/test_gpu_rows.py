@@ -121,3 +121,32 @@ def test_dist_u8_compaction():
     assert u8.cpu().tolist() == [3, 255, 2, 9] and int(fl[0]) == 0
     with pytest.raises(dawn.DawnError):
         dawn.dist_u8(torch.zeros(9, dtype=torch.int32, device="cuda")[1:])  # misaligned
+
+
+def test_dist_u4_compaction():
+    # dawn_dist_u4: 4-bit rows, two per byte (15 = unreached / overflow with the flag); every
+    # tail length 1..17 (the 8-entry vector body plus the per-byte tail, odd counts padded)
+    g = graphgen.kron(11, 16, 11)
+    G = _graph(g)
+    for s in g.sample_sources(3, seed=1):
+        d = dawn.sssp(G, int(s))
+        u4, fl = dawn.dist_u4(d)
+        exp = oracle.bfs_fifo(g.n, g.row_ptr, g.col, int(s))[0]
+        assert int(exp[exp != UNR].max()) < 15 and int(fl[0]) == 0
+        assert np.array_equal(dawn.unpack_u4(u4.cpu().numpy(), g.n), exp)
+    rng = np.random.default_rng(5)
+    for cnt in range(1, 18):
+        v = rng.integers(0, 15, cnt).astype(np.int64)
+        v[rng.random(cnt) < 0.3] = -1
+        x = torch.from_numpy(v.astype(np.int32)).cuda()
+        u4, fl = dawn.dist_u4(x)
+        assert u4.numel() == (cnt + 1) // 2 and int(fl[0]) == 0
+        exp = np.where(v < 0, UNR, v).astype(np.uint32)
+        assert np.array_equal(dawn.unpack_u4(u4.cpu().numpy(), cnt), exp), cnt
+        if cnt % 2:
+            assert int(u4[-1].item()) >> 4 == 15                       # pad nibble
+    u4, fl = dawn.dist_u4(torch.tensor([14, 15, 16, -1, 3], dtype=torch.int32, device="cuda"))
+    assert u4.cpu().tolist() == [14 | (15 << 4), 15 | (15 << 4), 3 | (15 << 4)] and int(fl[0]) == 1
+    with pytest.raises(dawn.DawnError):
+        dawn.dist_u4(torch.zeros(9, dtype=torch.int32, device="cuda")[1:])  # misaligned
+    torch.cuda.synchronize()
