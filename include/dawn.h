@@ -191,6 +191,15 @@ typedef enum {
                                       its own bit-parallel state and stream (independent sources,
                                       PAPER L303-308).  1 .. 3 for n <= 2^22, else 1.  Default
                                       set at load from B200 measurements.      */
+  DAWN_PARAM_BATCH_DYNAMIC = 13,   /* 1: the batch lanes of dawn_sssp_batch take the batch's
+                                      sources one at a time from a shared counter (each lane
+                                      claims its next index while it initialises the current
+                                      search), so the lanes finish together whatever the
+                                      per-source cost; 0: lane l runs the fixed contiguous share
+                                      [k*l/lanes, k*(l+1)/lanes).  Default (set at load): 1 for
+                                      n > 2^22, 0 below (B200: Kronecker-24 +1.2%, Kronecker-20
+                                      -3%).  Which lane runs a source never changes its row or
+                                      statistics.  Speed only.                                 */
   DAWN_PARAM_DENSE_MAX_ENTRIES = 10 /* dense distance outputs (dawn_msssp dist, one piece of
                                       dawn_apsp_rows) are refused with DAWN_ERR_CAPACITY when
                                       rows * n >= this ("dense-matrix mode refused

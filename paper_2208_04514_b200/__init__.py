@@ -240,7 +240,8 @@ class Graph:
 
     _PARAMS = {"alpha": 0, "beta": 1, "ms_alpha": 2, "bitmap_push_edges": 3, "solo_edges": 4,
                "cluster_start": 5, "cluster_handover_edges": 6, "bitmap_push_grow_edges": 7,
-               "narrow_queue_cap": 8, "batch_lanes": 9, "dense_max_entries": 10, "ms_lanes": 11, "weight_delta": 12}
+               "narrow_queue_cap": 8, "batch_lanes": 9, "dense_max_entries": 10, "ms_lanes": 11, "weight_delta": 12,
+               "batch_dynamic": 13}
 
     def get_tuning(self, key: str) -> float:
         """dawn_graph_get_param (e.g. "batch_lanes", "ms_lanes")."""

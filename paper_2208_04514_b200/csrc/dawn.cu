@@ -42,6 +42,9 @@ dawn_status cuda_fail(cudaError_t e, const char *where) {
 void clear_err() { g_err[0] = 0; }
 
 constexpr int kNT = 512;  // threads per CTA of the persistent kernels
+#ifndef DAWN_BATCH_CLAIM
+#define DAWN_BATCH_CLAIM 2  // dynamic batch lanes: 2 = on for the 64-register kernel (n > 2^22)
+#endif
 // Graph-size thresholds of the kernel choice (measured on B200)
 constexpr int64_t kSsspOneMaxN = 1 << 22;  // k_sssp<kNT, 1> (1 CTA/SM, 128 regs) up to 2^22
 constexpr int64_t kOneCtaMaxNM = 1 << 15;  // n + m this small: one CTA, barriers are __syncthreads
@@ -328,6 +331,7 @@ struct dawn_graph_s {
   uint32_t n_hasin = 0;
   bool cluster_start = false;     // DAWN_PARAM_CLUSTER_START (default set at load)
   unsigned long long handover_m = 0;  // DAWN_PARAM_CLUSTER_HANDOVER_EDGES (set at load)
+  bool batch_claim = false;            // DAWN_PARAM_BATCH_DYNAMIC (default set at load)
   bool narrow_owner = false;     // owner-computes queues (ids local: most arcs stay in a CTA)
   bool narrow_ok = false;        // the visited bitmap fits 16 CTAs and the cluster launches
   uint32_t narrow_wpc = 0, narrow_qcap = 0, narrow_grid = 0;
@@ -431,6 +435,9 @@ dawn_status load_csr(int64_t n, int64_t m, const int64_t *row_ptr, const int32_t
   cudaDeviceGetAttribute(&g->nsm, cudaDevAttrMultiProcessorCount, g->device);
   // small graphs: k_sssp<kNT, 1> (one CTA per SM, 128 registers); big ones k_sssp<kNT, 2>
   g->sssp_one = n <= kSsspOneMaxN;
+  // dynamic batch lanes: Kronecker-24 (4 lanes x 16 searches) 1,683 -> 1,702 GTEPS; Kronecker-20
+  // (8 lanes x 8) 1,002 -> 974, so off for the 1-CTA/SM kernel
+  g->batch_claim = DAWN_BATCH_CLAIM == 1 || (DAWN_BATCH_CLAIM == 2 && !g->sssp_one);
   g->sssp_grid = g->sssp_one ? std::min<int>(g->nsm, (int)kMaxBlocks)
                              : grid_for((const void *)k_sssp<kNT, 2>, g->nsm);
   {
@@ -640,6 +647,7 @@ dawn_status set_param(dawn_graph g, dawn_param key, double value) {
       g->lanes = (int)value;
       break;
     case DAWN_PARAM_WEIGHT_DELTA: g->wdelta = (uint32_t)std::min(value, 4294967294.0); break;
+    case DAWN_PARAM_BATCH_DYNAMIC: g->batch_claim = value != 0; break;
     case DAWN_PARAM_MS_LANES:
       if (value < 1 || value > g->L.ms_nlanes || (value > 1 && !g->ev_fork))
         return fail(DAWN_ERR_INVALID_ARGUMENT, "multi-source lanes must be in [1, %d]", g->L.ms_nlanes);
@@ -831,6 +839,13 @@ dawn_status sssp_batch(dawn_graph g, const uint32_t *sources, int64_t k, uint32_
   }
   const int lanes = (g->trace || k < 2) ? 1 : (int)std::min<int64_t>(g->lanes, k);
   if (lanes > 1) {
+    // dynamic lanes: a shared claim counter (lane 0's control block) hands out the batch
+    // indices, one per search, so no lane idles while another finishes a long share
+    uint32_t *claim = g->batch_claim ? &at<Ctrl>(g, g->L.lane[0].ctrl)->claim : nullptr;
+    if (claim) {
+      cudaError_t ec = cudaMemsetAsync(claim, 0, 4, st);
+      if (ec != cudaSuccess) return cuda_fail(ec, "batch claim reset");
+    }
     // independent searches at once: lane l (its own per-search state, its own stream, grid/lanes
     // CTAs) runs the contiguous share [k*l/lanes, k*(l+1)/lanes) of the batch; every lane
     // validates the whole list first, so a bad id still means nothing is written
@@ -838,10 +853,11 @@ dawn_status sssp_batch(dawn_graph g, const uint32_t *sources, int64_t k, uint32_
     for (int l = 1; l < lanes && e == cudaSuccess; ++l) e = cudaStreamWaitEvent(g->lane_st[l], g->ev_fork, 0);
     if (e != cudaSuccess) return cuda_fail(e, "batch fork");
     for (int l = 0; l < lanes; ++l) {
-      const int64_t b = k * l / lanes, c = k * (l + 1) / lanes - b;
+      const int64_t b = claim ? 0 : k * l / lanes, c = claim ? k : k * (l + 1) / lanes - b;
       SsspParams p = sssp_params(g, variant, dist + (size_t)b * g->n, stats ? stats + b : nullptr, l);
       p.sources = sources + b;
       p.nsrc = (uint32_t)c;
+      p.claim = claim;
       p.vsrc = sources;
       p.vn = (uint32_t)k;
       dawn_status sl = launch_sssp(g, p, l ? g->lane_st[l] : st, lanes);
@@ -1807,6 +1823,7 @@ dawn_status dawn_graph_get_param(dawn_graph g, dawn_param key, double *value) {
       case DAWN_PARAM_DENSE_MAX_ENTRIES: *value = g->dense_max; break;
       case DAWN_PARAM_MS_LANES: *value = g->ms_lanes; break;
       case DAWN_PARAM_WEIGHT_DELTA: *value = g->wdelta; break;
+      case DAWN_PARAM_BATCH_DYNAMIC: *value = g->batch_claim ? 1.0 : 0.0; break;
       default: return fail(DAWN_ERR_INVALID_ARGUMENT, "unknown parameter");
     }
     return DAWN_OK;)

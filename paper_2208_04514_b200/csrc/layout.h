@@ -131,7 +131,9 @@ struct Ctrl {
   unsigned long long narrow_fill;  // k_narrow: CTAs done with the init fill (monotonic)
   uint32_t bad_src;             // sticky: a dawn_sssp_batch device source id was >= n
   uint32_t wcc_cnt, wcc_arcs, wcc_root, wcc_k;  // dawn_largest_wcc selection / output size
-  uint32_t pad1[3];
+  uint32_t claim;               // lane 0's: next unclaimed index of a dawn_sssp_batch call
+  uint32_t next_idx;            // the batch index this lane searches next (claimed one ahead)
+  uint32_t pad1;
   alignas(16) unsigned char solo_state[256];  // LevelState snapshot published with solo_epoch
 };
 

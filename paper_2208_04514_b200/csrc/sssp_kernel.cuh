@@ -56,6 +56,10 @@ struct SsspParams {
   // device source list validated before any write (dawn_sssp_batch; vn = 0: host-validated)
   const uint32_t *vsrc;
   uint32_t vn;
+  // dynamic batch lanes: every lane takes the next unclaimed index of the whole batch from this
+  // shared counter (one atomic per search, one ahead) instead of a fixed contiguous share, so
+  // lanes finish together; sources / dist / stats then address the whole batch (nsrc = k)
+  uint32_t *claim;
 };
 
 // Every CTA checks the whole device source list of a dawn_sssp_batch call before it writes
@@ -808,19 +812,36 @@ __global__ void __launch_bounds__(NT, MINB) k_sssp(SsspParams p) {
   const uint32_t nthreads = nblocks * NT;
   WarpStage &stg = stage[threadIdx.x / 32];
   Ctrl *C = p.ctrl;
-  unsigned long long bar_target = 0;
+  __shared__ unsigned long long bar_target;  // grid_sync's arrival target (thread 0's)
+  if (threadIdx.x == 0) bar_target = 0;      // (shared: no register held across the levels)
   if (p.vn && sources_invalid<NT>(p.vsrc, p.vn, p.n, &C->bad_src)) return;
   const uint32_t nsrc = p.nsrc ? p.nsrc : 1u;
   // batch mode: the searches run back to back in this launch, a grid barrier apart (no kernel
-  // boundary or launch ramp between them)
-  bool prefilled = false;  // this CTA's share of row si already holds UNREACHED
-  for (uint32_t si = 0; si < nsrc; ++si) {
-  const uint32_t src = p.nsrc ? ld_nc(p.sources + si) : p.source;
-  uint32_t *const drow = p.dist + (size_t)si * p.n;
-  dawn_sssp_stats *const stats_out = p.stats ? p.stats + si : nullptr;
-  uint32_t solo_epoch = 0;
-  // condition 1 bound: only vertices with an in-edge (plus s itself) can ever be reached
-  const uint32_t max_reach = ld_cg(&C->n_hasin) + ((p.noin[src >> 5] >> (src & 31)) & 1u);
+  // boundary or launch ramp between them).  Dynamic lanes (p.claim): the batch index of the next
+  // search is claimed during the current one's init and read by every CTA after its barrier
+  __shared__ uint32_t next_sh;  // batch index of the next search (kept in shared memory)
+  if (p.claim) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) C->next_idx = atomicAdd(p.claim, 1u);
+    grid_sync(&C->bar, nblocks, bar_target);
+    if (threadIdx.x == 0) next_sh = ld_cg(&C->next_idx);
+  } else if (threadIdx.x == 0) {
+    next_sh = 0;
+  }
+  __syncthreads();
+  bool prefilled = false;  // this CTA's share of the next search's row already holds UNREACHED
+  for (;;) {
+  const uint32_t idx = next_sh;  // batch index of this search
+  if (idx >= nsrc) break;
+  const uint32_t src = p.nsrc ? ld_nc(p.sources + idx) : p.source;
+  uint32_t *const drow = p.dist + (size_t)idx * p.n;
+  dawn_sssp_stats *const stats_out = p.stats ? p.stats + idx : nullptr;
+  // per-search scalars of thread 0 in shared memory (no registers held across the levels)
+  __shared__ uint32_t solo_epoch, max_reach;
+  if (threadIdx.x == 0) {
+    solo_epoch = 0;
+    // condition 1 bound: only vertices with an in-edge (plus s itself) can ever be reached
+    max_reach = ld_cg(&C->n_hasin) + ((p.noin[src >> 5] >> (src & 31)) & 1u);
+  }
 
   if (p.trace && gtid == 0) p.trace[kTraceCap - 1].t_ns = globaltimer();  // kernel timeline
   // ---- k_narrow ran first for this call: finished (nothing to do) or hand-over (resume)
@@ -855,6 +876,7 @@ __global__ void __launch_bounds__(NT, MINB) k_sssp(SsspParams p) {
     for (uint32_t c = gtid; c * kChunk < d0; c += nthreads) p.Cf[0][c] = 0;
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if (p.claim) C->next_idx = atomicAdd(p.claim, 1u);  // published by the barrier below
     for (int i = 0; i < 3; ++i) C->slot[i] = Slot{0, 0, 0, 0, 0};
     C->examined = 0;
     C->solo_epoch = 0;
@@ -882,6 +904,7 @@ __global__ void __launch_bounds__(NT, MINB) k_sssp(SsspParams p) {
   }
   }
   grid_sync(&C->bar, nblocks, bar_target);
+  if (threadIdx.x == 0) next_sh = p.claim ? ld_cg(&C->next_idx) : idx + 1;  // read after a sync
   if (p.trace && gtid == 0) p.trace[kTraceCap - 1].t_first = globaltimer();
 
   unsigned long long examined = 0;
@@ -898,10 +921,11 @@ __global__ void __launch_bounds__(NT, MINB) k_sssp(SsspParams p) {
       // ---- solo stretch: narrow push levels on CTA 0 with __syncthreads only
       if (blockIdx.x != 0) {
         __syncthreads();  // every thread has read st.stop / st.solo before thread 0 rewrites st
-        if ((MINB == 1 || DAWN_MINB2_EXTRAS) && si + 1 < nsrc && !prefilled) {
+        const uint32_t nx = next_sh;  // the next search's batch index
+        if ((MINB == 1 || DAWN_MINB2_EXTRAS) && nx < nsrc && !prefilled) {
           // idle while CTA 0 runs the narrow levels: initialise this CTA's share of the next
           // search's distance row (independent memory; its source entry is set at its init)
-          uint32_t *nrow = p.dist + (size_t)(si + 1) * p.n;
+          uint32_t *nrow = p.dist + (size_t)nx * p.n;
           for (uint32_t i = gtid; i < p.n; i += nthreads) nrow[i] = kUnreached;
           prefilled = true;
         }
@@ -1048,7 +1072,7 @@ __global__ void __launch_bounds__(NT, MINB) k_sssp(SsspParams p) {
       *stats_out = s;
     }
   }
-  if (si + 1 < nsrc) grid_sync(&C->bar, nblocks, bar_target);  // before the next init
+  if (next_sh < nsrc) grid_sync(&C->bar, nblocks, bar_target);  // before the next init
   }  // sources
   grid_exit(&C->bar, nblocks);
 }

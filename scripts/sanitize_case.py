@@ -2,7 +2,7 @@
 (memcheck / racecheck / synccheck).  Each case also checks its result against the oracle so a
 run that the sanitizer perturbs cannot pass silently.
 
-    python scripts/sanitize_case.py [case ...]     cases: sssp1 sssp2 narrow small ms64 wcc
+    python scripts/sanitize_case.py [case ...]     cases: sssp1 sssp2 narrow small ms64 wcc wsssp part pack
 """
 import os
 import sys
@@ -77,6 +77,49 @@ def case_wcc():  # the k_wcc_* helper kernels
     v, e = dawn.largest_wcc(G)
     ov, oe = oracle.largest_wcc(g.n, g.row_ptr, g.col)
     assert np.array_equal(v, ov) and e == oe
+
+
+def case_wsssp():  # k_wsssp: (min,+) rounds, single and batch (device source list)
+    g = graphgen.er(600, 4000, 5)
+    p, i = g.transpose()
+    G = dawn.Graph(g.row_ptr, g.col, False, p, i)
+    w = g.weights(5, 31)
+    wt = torch.from_numpy(w.view(np.int32)).cuda()
+    exp = [oracle.dijkstra(g.n, g.row_ptr, g.col, w, s) for s in (0, 7)]
+    exp = [np.where(e == oracle.UNREACHED64, 0xFFFFFFFF, e).astype(np.uint32) for e in exp]
+    assert np.array_equal(dawn.wsssp(G, 0, wt).cpu().numpy().view(np.uint32), exp[0])
+    D = dawn.wsssp_batch(G, torch.tensor([0, 7], dtype=torch.int32, device="cuda"), wt)
+    assert np.array_equal(D[1].cpu().numpy().view(np.uint32), exp[1])
+
+
+def case_part():  # k_part_begin / k_part_level / k_part_finish (2 partitions, launches per
+    # level) and k_part_fused on one partition (W > 1 fused kernels wait on each other, which a
+    # serialising tool cannot run)
+    g = graphgen.kron(11, 16, 11)
+    exp = oracle.bfs_fifo(g.n, g.row_ptr, g.col, 5)[0]
+    parts = [dawn.PartGraph(dawn.part_build(g.row_ptr, g.col, 2, r), 2, r) for r in range(2)]
+    for v in ("auto", "push", "pull"):
+        d = dawn.part_sssp_local(parts, 5, v)
+        assert np.array_equal(d.cpu().numpy().view(np.uint32), exp), v
+    one = [dawn.PartGraph(dawn.part_build(g.row_ptr, g.col, 1, 0), 1, 0)]
+    assert np.array_equal(dawn.part_fused_local(one, 5).cpu().numpy().view(np.uint32), exp)
+
+
+def case_pack():  # k_dist_u8 / k_dist_u4: vector bodies and ragged tails
+    g = graphgen.kron(10, 16, 10)
+    G = dawn.Graph(g.row_ptr, g.col, True)
+    d = dawn.sssp(G, 3)
+    exp = oracle.bfs_fifo(g.n, g.row_ptr, g.col, 3)[0]
+    u4, fl = dawn.dist_u4(d)
+    assert np.array_equal(dawn.unpack_u4(u4.cpu().numpy(), g.n), exp) and int(fl[0]) == 0
+    u8, fl = dawn.dist_u8(d)
+    assert np.array_equal(u8.cpu().numpy(), np.where(exp == oracle.UNREACHED, 255, exp).astype(np.uint8))
+    for cnt in (1, 7, 9, 13):
+        x = torch.arange(cnt, dtype=torch.int32, device="cuda")
+        u4, _ = dawn.dist_u4(x)
+        assert np.array_equal(dawn.unpack_u4(u4.cpu().numpy(), cnt)[: min(cnt, 15)],
+                              np.arange(min(cnt, 15), dtype=np.uint32))
+        dawn.dist_u8(x)
 
 
 CASES = {k[5:]: f for k, f in globals().items() if k.startswith("case_")}

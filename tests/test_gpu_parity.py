@@ -433,16 +433,27 @@ def test_sssp_batch_lanes():
     srcs = np.concatenate([g.sample_sources(9, seed=11), [0]]).astype(np.int32)
     srcs[3] = srcs[1]                                               # a repeated source
     exp = [oracle.bfs_fifo(g.n, g.row_ptr, g.col, int(s))[0] for s in srcs]
-    for lanes in (1, 2, 4, 8):
-        G.set_tuning(batch_lanes=lanes)
-        for v in VARIANTS:
-            d, st = dawn.sssp_batch(G, torch.from_numpy(srcs).cuda(), v, stats=True, check=True)
-            d = d.cpu().numpy().view(np.uint32)
-            for i, s in enumerate(srcs):
-                assert np.array_equal(d[i], exp[i]), (lanes, v, int(s))
-                rec, er = oracle.record(g.n, g.row_ptr, int(s), exp[i])
-                sd = dawn.stats_to_dict(st[i])
-                assert sd["levels"] == int(rec["ecc"]) and sd["edges_reach"] == er, (lanes, v)
+    # batch_dynamic: lanes claim sources one at a time from a shared counter (1, the default)
+    # or run fixed contiguous shares (0); either way row i / stats i belong to source i
+    for dyn in (1, 0):
+        G.set_tuning(batch_dynamic=dyn)
+        for lanes in (1, 2, 4, 8):
+            G.set_tuning(batch_lanes=lanes)
+            for v in VARIANTS:
+                d, st = dawn.sssp_batch(G, torch.from_numpy(srcs).cuda(), v, stats=True, check=True)
+                d = d.cpu().numpy().view(np.uint32)
+                for i, s in enumerate(srcs):
+                    assert np.array_equal(d[i], exp[i]), (dyn, lanes, v, int(s))
+                    rec, er = oracle.record(g.n, g.row_ptr, int(s), exp[i])
+                    sd = dawn.stats_to_dict(st[i])
+                    assert sd["levels"] == int(rec["ecc"]) and sd["edges_reach"] == er, (dyn, lanes, v)
+    G.set_tuning(batch_dynamic=1)
+    # many more searches than lanes, some far cheaper than others (sources with a tiny reach):
+    # every index is claimed exactly once
+    small = np.concatenate([srcs, np.arange(40, dtype=np.int32)])
+    exps = [oracle.bfs_fifo(g.n, g.row_ptr, g.col, int(s))[0] for s in small]
+    d = dawn.sssp_batch(G, torch.from_numpy(small).cuda()).cpu().numpy().view(np.uint32)
+    assert all(np.array_equal(d[i], exps[i]) for i in range(len(small)))
     with pytest.raises(dawn.DawnError):
         G.set_tuning(batch_lanes=9)
     # the lanes share nothing across calls: a single dawn_sssp between batches still matches
