@@ -18,12 +18,15 @@
 
 namespace dawn {
 
-constexpr uint32_t kPartHdr = 4;  // exchange slice header words: [0] |F_{L+1}| here, [2..3] m_f
+constexpr uint32_t kPartHdr = 4;  // exchange slice header words: [0] |F_{L+1}| here, [1] 1 if
+                                  // one of them has out-degree > kHeavy, [2..3] m_f
 
 struct PartState {
   uint32_t done, dir, prev_nf, ecc;
   uint32_t push_levels, pull_levels, reached, pad;
-  unsigned long long explored, pad2;
+  unsigned long long explored;
+  uint32_t pad2;
+  uint32_t hvy;  // F_L holds a vertex of out-degree > kHeavy: push levels test the heavy pieces
 };
 static_assert(sizeof(PartState) % 16 == 0, "PartState");
 
@@ -78,6 +81,14 @@ __device__ __forceinline__ bool part_ftest(const PartParams &p, const uint32_t *
   return (xld<CG>(rv + (size_t)q * p.S + kPartHdr + (r >> 5)) >> (r & 31)) & 1u;
 }
 
+// per-CTA flag: this level discovered a vertex of out-degree > kHeavy (one shared store per
+// discovery; part_counters ORs it into the slice header once per CTA — a store per discovery
+// straight to the header word serialised millions of same-address stores in L2)
+__device__ __forceinline__ uint32_t *part_hv_smem() {
+  __shared__ uint32_t hv;
+  return &hv;
+}
+
 __device__ __forceinline__ void part_discover(const PartParams &p, uint32_t *sd, uint32_t t,
                                               uint32_t L1, uint32_t &n_new,
                                               unsigned long long &m_new) {
@@ -89,7 +100,9 @@ __device__ __forceinline__ void part_discover(const PartParams &p, uint32_t *sd,
   }
   red_or(sd + kPartHdr + (t >> 5), 1u << (t & 31));
   n_new += 1;
-  m_new += ld_nc(p.deg + t);
+  const uint32_t dg = ld_nc(p.deg + t);
+  m_new += dg;
+  if (dg > kHeavy) *part_hv_smem() = 1u;  // a heavy row: the next push level tests the pieces
 }
 
 // Claim owned vertex t for level L+1 (test-and-set on vis; each vertex is discovered once).
@@ -140,7 +153,9 @@ __device__ __forceinline__ void part_settle(const PartParams &p, uint32_t *sd, u
         p.lev[t] = 255u;
       }
       n_new += 1;
-      m_new += ld_nc(p.deg + t);
+      const uint32_t dg = ld_nc(p.deg + t);
+      m_new += dg;
+      if (dg > kHeavy) *part_hv_smem() = 1u;
     }
   }
 }
@@ -151,13 +166,15 @@ __device__ __forceinline__ void part_header(const PartParams &p, const uint32_t 
                                             PartState &st) {
   if (st.done) return;
   if (L > 0 && st.dir == kPull) st.pad2 = 1;  // a pull level ran: the unreached list is compacted
-  uint32_t nf = 0;
+  uint32_t nf = 0, hv = 0;
   unsigned long long mf = 0;
   for (uint32_t q = 0; q < p.world; ++q) {
     const uint32_t *h = rv + (size_t)q * p.S;
     nf += ld_cg(h);
+    hv |= ld_cg(h + 1);
     mf += ((unsigned long long)ld_cg(h + 3) << 32) | ld_cg(h + 2);
   }
+  st.hvy = hv;
   const uint32_t L1 = L + 1;
   if (nf == 0) {  // condition 2: F_L is empty
     st.done = 1;
@@ -237,7 +254,9 @@ __device__ void part_work(const PartParams &p, const PartState &st, uint32_t L, 
     }
     // (b) heavy out-slice rows: static pieces; warp w takes pieces w + k * nwarps, 32 tested at
     //     once against F_L, then each live piece is expanded 32 arcs per round
-    const uint32_t hend = ld_cg(&p.ctrl->n_hp[0]);
+    //     (only when F_L holds a vertex whose global out-degree exceeds kHeavy: no out-slice row
+    //     of a lighter vertex is heavy on any rank)
+    const uint32_t hend = st.hvy ? ld_cg(&p.ctrl->n_hp[0]) : 0u;
     for (uint32_t pb = gwarp; pb < hend; pb += 32 * nwarps) {
       const uint32_t pcl = pb + lane * nwarps;
       const bool live = pcl < hend && part_ftest<CG>(p, rv, ld_nc(p.hout_v + pcl));
@@ -380,6 +399,10 @@ __device__ __forceinline__ void part_counters(const PartParams &p, uint32_t *sd,
   exam = warp_sum(exam);
   if (threadIdx.x == 0) red[0] = red[1] = red[2] = 0;
   __syncthreads();
+  if (threadIdx.x == 0 && *part_hv_smem()) {
+    sd[1] = 1u;
+    *part_hv_smem() = 0u;
+  }
   if (lane == 0) {
     if (n_new) atomicAdd(&red[0], (unsigned long long)n_new);
     if (m_new) atomicAdd(&red[1], m_new);
@@ -404,6 +427,7 @@ __global__ void k_part_begin(PartParams p) {
       p.send[kPartHdr + (p.src_local >> 5)] = 1u << (p.src_local & 31);
       p.send[0] = 1;
       const unsigned long long d = ld_nc(p.deg + p.src_local);
+      p.send[1] = d > kHeavy ? 1u : 0u;
       p.send[2] = (uint32_t)d;
       p.send[3] = (uint32_t)(d >> 32);
     }
@@ -428,6 +452,7 @@ __global__ void __launch_bounds__(NT, 2) k_part_level(PartParams p, uint32_t L) 
     for (int i = 0; i < (int)(sizeof(PartState) / 16); ++i) d4[i] = __ldcg(s4 + i);
     part_header(p, p.recv, L, st);
     if (blockIdx.x == 0) p.ctrl->st[(L + 1) & 1] = st;
+    *part_hv_smem() = 0u;
   }
   __syncthreads();
   if (st.done) return;
@@ -486,6 +511,7 @@ __global__ void __launch_bounds__(NT, 2) k_part_fused(PartParams p, PartPeers pe
     uint32_t x = 0;
     if (p.src_local != 0xffffffffu) {
       if (i == 0) x = 1;
+      else if (i == 1) x = ld_nc(p.deg + p.src_local) > kHeavy ? 1u : 0u;
       else if (i == 2) x = ld_nc(p.deg + p.src_local);
       else if (i == kPartHdr + (p.src_local >> 5)) x = 1u << (p.src_local & 31);
     }
@@ -495,6 +521,7 @@ __global__ void __launch_bounds__(NT, 2) k_part_fused(PartParams p, PartPeers pe
   if (threadIdx.x == 0) {
     st = PartState{};
     st.dir = (p.variant == DAWN_PULL) ? kPull : kPush;
+    *part_hv_smem() = 0u;
   }
   grid_sync(gb, nblocks, bar);
   if (gtid == 0) {
