@@ -18,15 +18,20 @@
 
 namespace dawn {
 
-constexpr uint32_t kPartHdr = 4;  // exchange slice header words: [0] |F_{L+1}| here, [1] 1 if
-                                  // one of them has out-degree > kHeavy, [2..3] m_f
+constexpr uint32_t kPartHdr = 4;  // exchange slice header words: [0] |F_{L+1}| here, [1] bit 31:
+                                  // one of them has out-degree > kHeavy, bits 0..30 (level-0
+                                  // slices only): this rank's reachable bound (kPartReach),
+                                  // [2..3] m_f
+constexpr uint32_t kPartHeavy = 0x80000000u;
 
 struct PartState {
   uint32_t done, dir, prev_nf, ecc;
   uint32_t push_levels, pull_levels, reached, pad;
   unsigned long long explored;
   uint32_t pad2;
-  uint32_t hvy;  // F_L holds a vertex of out-degree > kHeavy: push levels test the heavy pieces
+  uint32_t hvy;   // F_L holds a vertex of out-degree > kHeavy: push levels test the heavy pieces
+  uint32_t maxr;  // vertices the search can reach: those with an in-edge (+ s if it has none)
+  uint32_t pad3[3];
 };
 static_assert(sizeof(PartState) % 16 == 0, "PartState");
 
@@ -166,15 +171,20 @@ __device__ __forceinline__ void part_header(const PartParams &p, const uint32_t 
                                             PartState &st) {
   if (st.done) return;
   if (L > 0 && st.dir == kPull) st.pad2 = 1;  // a pull level ran: the unreached list is compacted
-  uint32_t nf = 0, hv = 0;
+  uint32_t nf = 0, hv = 0, reach = 0;
   unsigned long long mf = 0;
   for (uint32_t q = 0; q < p.world; ++q) {
     const uint32_t *h = rv + (size_t)q * p.S;
     nf += ld_cg(h);
-    hv |= ld_cg(h + 1);
+    const uint32_t h1 = ld_cg(h + 1);
+    hv |= h1 & kPartHeavy;
+    reach += h1 & ~kPartHeavy;
     mf += ((unsigned long long)ld_cg(h + 3) << 32) | ld_cg(h + 2);
   }
-  st.hvy = hv;
+  st.hvy = hv ? 1u : 0u;
+  // condition 1 bound (k_sssp's max_reach, reading Q9): the ranks' level-0 headers carry their
+  // counts of owned vertices with an in-edge (the source's owner adds s if it has none)
+  if (L == 0) st.maxr = reach;
   const uint32_t L1 = L + 1;
   if (nf == 0) {  // condition 2: F_L is empty
     st.done = 1;
@@ -183,7 +193,7 @@ __device__ __forceinline__ void part_header(const PartParams &p, const uint32_t 
   }
   if (L > 0) st.reached += nf;
   st.explored += mf;
-  if (st.reached + 1 >= p.n || L1 >= p.n) {  // condition 1 (L177) / the n-1 round bound
+  if (st.reached + 1 >= st.maxr || L1 >= p.n) {  // condition 1 (L177) / the n-1 round bound
     st.done = 1;
     st.ecc = L;
     return;
@@ -194,7 +204,7 @@ __device__ __forceinline__ void part_header(const PartParams &p, const uint32_t 
     st.dir = kPull;
   } else {  // the k_sssp rule (level_header), on the global counters
     const double mu = (double)(p.m_total - min(st.explored, p.m_total));
-    const double nu = (double)(p.n - 1 - min(st.reached, p.n - 1));
+    const double nu = (double)(st.maxr - 1 - min(st.reached, st.maxr - 1));
     if (st.dir == kPush) {
       if ((double)mf * (double)mf * p.alpha > nu * mu && nf > st.prev_nf) st.dir = kPull;
     } else {
@@ -277,7 +287,9 @@ __device__ void part_work(const PartParams &p, const PartState &st, uint32_t L, 
     //     vertices with an in-edge at the first pull level, the warp's compacted survivors after;
     //     as k_sssp's pull): two vertices per lane in flight, each scanning its in-row until the
     //     first in-neighbour in F_L (early exit, Eq. 4), 4 independent probes per round trip.
-    //     Vertices with heavy in-rows are left to the pieces but stay in the list while unreached.
+    //     Vertices with heavy in-rows probe their first kHeavyProbe in-edges here (the
+    //     highest-degree sources come first, so most settle) and claim with a returning atomic
+    //     (a piece may find them concurrently); the pieces finish the rest.
     constexpr int PJ = 2;
     const uint32_t cap = (p.n_has + nwarps - 1) / nwarps;
     const uint32_t seg0 = gwarp * cap;
@@ -288,22 +300,26 @@ __device__ void part_work(const PartParams &p, const PartState &st, uint32_t L, 
     uint32_t wr = 0;
     for (uint32_t ib = 0; ib < cnt; ib += 32 * PJ) {
       uint32_t t[PJ], s[PJ], e[PJ], dg[PJ];
-      bool need[PJ], keep[PJ], found[PJ];
+      bool need[PJ], keep[PJ], found[PJ], hv[PJ];
 #pragma unroll
       for (int k = 0; k < PJ; ++k) {
         const uint32_t i2 = ib + k * 32 + lane;
         t[k] = i2 < cnt ? ld_cg(srcl + i2) : 0xffffffffu;
-        need[k] = keep[k] = found[k] = false;
+        need[k] = keep[k] = found[k] = hv[k] = false;
         s[k] = e[k] = dg[k] = 0;
         if (t[k] != 0xffffffffu) {
           const uint32_t bit = 1u << (t[k] & 31);
           keep[k] = !(ld_cg(p.vis + (t[k] >> 5)) & bit);
-          need[k] = keep[k] && !(ld_nc(p.hin_bits + (t[k] >> 5)) & bit);
+          need[k] = keep[k];
+          hv[k] = ld_nc(p.hin_bits + (t[k] >> 5)) & bit;
           s[k] = ld_nc(p.irp + t[k]);  // speculative, same round trip
           e[k] = ld_nc(p.irp + t[k] + 1);
           dg[k] = ld_nc(p.deg + t[k]);
         }
       }
+#pragma unroll
+      for (int k = 0; k < PJ; ++k)
+        if (hv[k]) e[k] = min(e[k], s[k] + kHeavyProbe);  // the pieces scan the rest
       for (;;) {
         bool any = false;
         uint32_t v[PJ][4];
@@ -332,7 +348,15 @@ __device__ void part_work(const PartParams &p, const PartState &st, uint32_t L, 
 #pragma unroll
       for (int k = 0; k < PJ; ++k) {
         if (found[k]) {
-          red_or(p.vis + (t[k] >> 5), 1u << (t[k] & 31));  // light rows: this lane alone settles t
+          const uint32_t w = t[k] >> 5, bit = 1u << (t[k] & 31);
+          if (hv[k]) {
+            if (atomicOr(p.vis + w, bit) & bit) found[k] = false;  // a piece settled t first
+          } else {
+            red_or(p.vis + w, bit);  // light rows: this lane alone settles t
+          }
+        }
+        if (found[k]) {
+          if (dg[k] > kHeavy) *part_hv_smem() = 1u;  // a heavy out-row in F_{L+1}
           if (L1 < 255u) {
             p.lev[t[k]] = (uint8_t)L1;
           } else {
@@ -400,7 +424,7 @@ __device__ __forceinline__ void part_counters(const PartParams &p, uint32_t *sd,
   if (threadIdx.x == 0) red[0] = red[1] = red[2] = 0;
   __syncthreads();
   if (threadIdx.x == 0 && *part_hv_smem()) {
-    sd[1] = 1u;
+    sd[1] = kPartHeavy;  // (the reach bound bits are used in level-0 slices only)
     *part_hv_smem() = 0u;
   }
   if (lane == 0) {
@@ -416,6 +440,14 @@ __device__ __forceinline__ void part_counters(const PartParams &p, uint32_t *sd,
   }
 }
 
+// This rank's share of the reachable bound: its owned vertices with an in-edge, plus the source
+// when this rank owns it and it has none (k_sssp's max_reach split over the ranks).
+__device__ __forceinline__ uint32_t part_reach(const PartParams &p) {
+  const bool s_noin = p.src_local != 0xffffffffu &&
+                      ld_nc(p.irp + p.src_local + 1) == ld_nc(p.irp + p.src_local);
+  return p.n_has + (s_noin ? 1u : 0u);
+}
+
 // dawn_part_begin: vis <- {s} on the owner, level-0 slice (the caller zeroed `send`), state.
 __global__ void k_part_begin(PartParams p) {
   const uint32_t gtid = blockIdx.x * blockDim.x + threadIdx.x, nth = gridDim.x * blockDim.x;
@@ -423,11 +455,12 @@ __global__ void k_part_begin(PartParams p) {
   for (uint32_t w = gtid; w < nwo; w += nth)
     p.vis[w] = (p.src_local != 0xffffffffu && w == (p.src_local >> 5)) ? 1u << (p.src_local & 31) : 0u;
   if (gtid == 0) {
+    p.send[1] = part_reach(p);
     if (p.src_local != 0xffffffffu) {
       p.send[kPartHdr + (p.src_local >> 5)] = 1u << (p.src_local & 31);
       p.send[0] = 1;
       const unsigned long long d = ld_nc(p.deg + p.src_local);
-      p.send[1] = d > kHeavy ? 1u : 0u;
+      if (d > kHeavy) p.send[1] |= kPartHeavy;
       p.send[2] = (uint32_t)d;
       p.send[3] = (uint32_t)(d >> 32);
     }
@@ -508,10 +541,10 @@ __global__ void __launch_bounds__(NT, 2) k_part_fused(PartParams p, PartPeers pe
   for (uint32_t w = gtid; w < nwo; w += nth)
     p.vis[w] = (p.src_local != 0xffffffffu && w == (p.src_local >> 5)) ? 1u << (p.src_local & 31) : 0u;
   for (uint32_t i = gtid; i < p.S; i += nth) {
-    uint32_t x = 0;
+    uint32_t x = (i == 1) ? part_reach(p) : 0u;
     if (p.src_local != 0xffffffffu) {
       if (i == 0) x = 1;
-      else if (i == 1) x = ld_nc(p.deg + p.src_local) > kHeavy ? 1u : 0u;
+      else if (i == 1) x |= ld_nc(p.deg + p.src_local) > kHeavy ? kPartHeavy : 0u;
       else if (i == 2) x = ld_nc(p.deg + p.src_local);
       else if (i == kPartHdr + (p.src_local >> 5)) x = 1u << (p.src_local & 31);
     }

@@ -148,3 +148,34 @@ def test_fused_c2_matches_single_gpu():
         a = dawn.part_fused_local(parts, int(s))
         assert torch.equal(a, dawn.sssp(G, int(s))), s
     torch.cuda.synchronize()
+
+
+def _light_in_heavy_out_graph(seed: int):
+    """0 -> 2,000 A -> 20,000 B (20 arcs per A) -> 100 C (one arc per B), plus H with ONE in-arc
+    (from B[0]) and 1,000 out-arcs to D vertices nothing else reaches.  The growing levels pull,
+    so H (a light in-row) is settled by the light pull pass; the next level (frontier C + H,
+    shrinking, 101 * beta < n) pushes, and only H's heavy out-row reaches D."""
+    rng = np.random.default_rng(seed)
+    A, B, C = np.arange(1, 2001), np.arange(2001, 22001), np.arange(22001, 22101)
+    H, D0 = 22101, 22102
+    e = [[0, int(a)] for a in A]
+    e += [[int(a), int(b)] for a in A for b in rng.choice(B, 20, replace=False)]
+    e += [[int(b), int(rng.choice(C))] for b in B]
+    e += [[int(B[0]), H]] + [[H, D0 + j] for j in range(1000)]
+    e += [[int(c), D0 + 1000 + i] for i, c in enumerate(C)]
+    return graphgen.from_edges(D0 + 1000 + len(C), e)
+
+
+@pytest.mark.parametrize("W", [1, 2, 3])
+def test_push_after_pull_reaches_heavy_out_rows(W):
+    # a vertex settled by the pull pass whose out-row is heavy must make the next push level
+    # test the heavy pieces (slice-header flag); per-level and fused paths, against the oracle
+    g = _light_in_heavy_out_graph(W)
+    parts = _parts(g, W)
+    exp = oracle.bfs_fifo(g.n, g.row_ptr, g.col, 0)[0]
+    assert exp[22102] == 4 and exp[22101] == 3
+    d, sts = dawn.part_sssp_local(parts, 0, "auto", stats=True)
+    assert np.array_equal(d.cpu().numpy().view(np.uint32), exp)
+    x = dawn.stats_to_dict(sts[0])
+    assert x["pull_levels"] >= 1 and x["push_levels"] >= 2, x   # the pull -> push schedule
+    assert np.array_equal(dawn.part_fused_local(parts, 0).cpu().numpy().view(np.uint32), exp)
