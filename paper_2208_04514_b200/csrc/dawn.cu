@@ -1444,7 +1444,8 @@ dawn_status part_build(int64_t n, int64_t m, const int64_t *row_ptr, const int32
 
 struct PartLayout {
   size_t rp, irp, hout_bits, hout_v, hout_s, hout_e, hin_bits, hin_v, hin_s, hin_e;
-  size_t scan_tmp, piece_tmp, vis, cand, lev, send, recv, ctrl, icol2, hasin, ulist, useg, total;
+  size_t scan_tmp, piece_tmp, vis, cand, lev, send, recv, ctrl, icol2, hasin, ulist, useg, hlist;
+  size_t total;
   uint64_t capHP;
 };
 
@@ -1480,6 +1481,7 @@ PartLayout part_layout(int64_t n, int64_t m_r, int32_t world, int64_t R, int64_t
   L.send = take(4 * S);
   L.recv = take(4 * S * (size_t)world);
   L.ctrl = take(sizeof(PartCtrl));
+  L.hlist = take(4 * (size_t)kPartHList);  // heavy frontier vertices of a fused push level
   L.total = o;
   return L;
 }
@@ -1536,6 +1538,7 @@ PartParams part_params(dawn_part p) {
   q.hasin = u32(p->L.hasin);
   q.ulist = u32(p->L.ulist);
   q.useg = u32(p->L.useg);
+  q.hlist = u32(p->L.hlist);
   q.n_has = p->n_has;
   q.lev = reinterpret_cast<uint8_t *>(p->ws + p->L.lev);
   q.dist = p->dist;

@@ -23,6 +23,9 @@ constexpr uint32_t kPartHdr = 4;  // exchange slice header words: [0] |F_{L+1}| 
                                   // slices only): this rank's reachable bound (kPartReach),
                                   // [2..3] m_f
 constexpr uint32_t kPartHeavy = 0x80000000u;
+// Fused push levels list the frontier's heavy out-rows (up to kPartHList vertices) and deal their
+// kHPiece-arc chunks over all warps, instead of testing every static piece against F_L.
+constexpr uint32_t kPartHList = 512;
 
 struct PartState {
   uint32_t done, dir, prev_nf, ecc;
@@ -40,7 +43,7 @@ struct PartCtrl {
   unsigned long long examined;   // adjacency entries read on this rank
   uint32_t n_hp[2];              // static heavy pieces: [0] out-slice rows, [1] in-rows
   unsigned long long xbase;      // fused exchange: this rank's arrival counter at search start
-  uint32_t pad[10];              // [0..3]: the fused kernel's grid barrier
+  uint32_t pad[10];              // [0..3]: the fused kernel's grid barrier, [4]: hlist count
 };
 static_assert(sizeof(GridBarrier) <= 40, "grid barrier in PartCtrl::pad");
 
@@ -60,6 +63,7 @@ struct PartParams {
   uint32_t *cand;                     // candidate bitmap of wide push levels (zero between uses)
   const uint32_t *hasin;              // owned vertices with an in-edge, ascending (n_has)
   uint32_t *ulist, *useg;             // unreached list in per-warp segments, segment counts
+  uint32_t *hlist;                    // fused push: heavy frontier vertices (count: ctrl->pad[4])
   uint32_t n_has;
   uint8_t *lev;                       // deferred distances (as k_sssp: byte L+1, 255 = direct)
   uint32_t *dist;                     // caller's distance slice [R]
@@ -217,7 +221,9 @@ __device__ __forceinline__ void part_header(const PartParams &p, const uint32_t 
 }
 
 // The level's work: F_L in rv (all ranks' slices) -> this rank's slice of F_{L+1} in sd.
-template <int NT, bool CG, int MODE = 0>
+// LIST (fused kernel): push step (a) also lists the frontier's heavy out-rows; the caller runs
+// part_push_heavy after a grid barrier instead of step (b).
+template <int NT, bool CG, int MODE = 0, bool LIST = false>
 __device__ void part_work(const PartParams &p, const PartState &st, uint32_t L, const uint32_t *rv,
                           uint32_t *sd, uint32_t gwarp, uint32_t nwarps, uint32_t &n_new,
                           unsigned long long &m_new, unsigned long long &exam) {
@@ -232,7 +238,15 @@ __device__ void part_work(const PartParams &p, const PartState &st, uint32_t L, 
       uint32_t bits = 0;
       if (gw < p.nwg) {
         const uint32_t q = p.world == 1 ? 0u : gw / wpr;
-        bits = xld<CG>(rv + (size_t)q * p.S + kPartHdr + (gw - q * wpr)) & ~ld_nc(p.hout_bits + gw);
+        const uint32_t fw = xld<CG>(rv + (size_t)q * p.S + kPartHdr + (gw - q * wpr));
+        const uint32_t hw = ld_nc(p.hout_bits + gw);
+        bits = fw & ~hw;
+        if (LIST && st.hvy) {
+          for (uint32_t hb = fw & hw; hb; hb &= hb - 1) {  // rare: heavy frontier vertices
+            const uint32_t i = atomicAdd(&p.ctrl->pad[4], 1u);
+            if (i < kPartHList) p.hlist[i] = gw * 32 + (__ffs(hb) - 1);
+          }
+        }
       }
       while (__ballot_sync(DAWN_FULL, bits != 0)) {
         uint32_t rs = 0, d = 0;
@@ -266,7 +280,7 @@ __device__ void part_work(const PartParams &p, const PartState &st, uint32_t L, 
     //     once against F_L, then each live piece is expanded 32 arcs per round
     //     (only when F_L holds a vertex whose global out-degree exceeds kHeavy: no out-slice row
     //     of a lighter vertex is heavy on any rank)
-    const uint32_t hend = st.hvy ? ld_cg(&p.ctrl->n_hp[0]) : 0u;
+    const uint32_t hend = (st.hvy && !LIST) ? ld_cg(&p.ctrl->n_hp[0]) : 0u;
     for (uint32_t pb = gwarp; pb < hend; pb += 32 * nwarps) {
       const uint32_t pcl = pb + lane * nwarps;
       const bool live = pcl < hend && part_ftest<CG>(p, rv, ld_nc(p.hout_v + pcl));
@@ -410,6 +424,69 @@ __device__ void part_work(const PartParams &p, const PartState &st, uint32_t L, 
         }
       }
     }
+  }
+}
+
+// Fused push levels, after the grid barrier that follows step (a): the listed heavy out-rows are
+// cut into kHPiece-arc chunks numbered across the list (a warp prefix scan per 32 entries) and
+// chunk c goes to warp c mod nwarps; a list that overflowed falls back to testing every static
+// piece against F_L (step (b) of part_work).
+template <bool CG, int MODE>
+__device__ void part_push_heavy(const PartParams &p, const PartState &st, uint32_t L,
+                                const uint32_t *rv, uint32_t *sd, uint32_t gwarp, uint32_t nwarps,
+                                uint32_t &n_new, unsigned long long &m_new,
+                                unsigned long long &exam) {
+  if (!st.hvy) return;
+  const uint32_t lane = lane_id(), L1 = L + 1;
+  const uint32_t cnt = ld_cg(&p.ctrl->pad[4]);
+  if (cnt > kPartHList) {
+    const uint32_t hend = ld_cg(&p.ctrl->n_hp[0]);
+    for (uint32_t pb = gwarp; pb < hend; pb += 32 * nwarps) {
+      const uint32_t pcl = pb + lane * nwarps;
+      const bool live = pcl < hend && part_ftest<CG>(p, rv, ld_nc(p.hout_v + pcl));
+      uint32_t lm = __ballot_sync(DAWN_FULL, live);
+      while (lm) {
+        const uint32_t kk = __ffs(lm) - 1;
+        lm &= lm - 1;
+        const uint32_t pc = pb + kk * nwarps;
+        const uint32_t s = ld_nc(p.hout_s + pc), e = ld_nc(p.hout_e + pc);
+        for (uint32_t j = s + lane; j < e; j += 32) {
+          part_visit<MODE>(p, sd, (uint32_t)ld_nc(p.col + j), L1, n_new, m_new);
+          ++exam;
+        }
+      }
+    }
+    return;
+  }
+  uint32_t base = 0;  // chunks of the entries before this group of 32
+  for (uint32_t i0 = 0; i0 < cnt; i0 += 32) {
+    uint32_t rs = 0, re = 0, nc = 0;
+    if (i0 + lane < cnt) {
+      const uint32_t v = ld_cg(p.hlist + i0 + lane);
+      rs = ld_nc(p.rp + v);
+      re = ld_nc(p.rp + v + 1);
+      nc = (re - rs + kHPiece - 1) / kHPiece;
+    }
+    const uint32_t incl = warp_incl_scan(nc), tot = __shfl_sync(DAWN_FULL, incl, 31);
+    const uint32_t excl = incl - nc;
+    // this warp's chunks c in [base, base + tot) with c mod nwarps == gwarp
+    uint32_t c = base + (gwarp + nwarps - base % nwarps) % nwarps;
+    for (; c < base + tot; c += nwarps) {
+      const uint32_t t = c - base;
+      uint32_t k = 0;  // the entry holding chunk t (last lane with excl <= t)
+#pragma unroll
+      for (uint32_t step = 16; step; step >>= 1) {
+        const uint32_t e = __shfl_sync(DAWN_FULL, excl, k + step);
+        if (k + step < 32 && e <= t) k += step;
+      }
+      const uint32_t s0 = __shfl_sync(DAWN_FULL, rs, k) + (t - __shfl_sync(DAWN_FULL, excl, k)) * kHPiece;
+      const uint32_t e0 = min(__shfl_sync(DAWN_FULL, re, k), s0 + kHPiece);
+      for (uint32_t j = s0 + lane; j < e0; j += 32) {
+        part_visit<MODE>(p, sd, (uint32_t)ld_nc(p.col + j), L1, n_new, m_new);
+        ++exam;
+      }
+    }
+    base += tot;
   }
 }
 
@@ -574,17 +651,27 @@ __global__ void __launch_bounds__(NT, 2) k_part_fused(PartParams p, PartPeers pe
     if (st.done) break;
     const uint32_t *rv = myrecv + (L & 1) * slot_words;
     for (uint32_t i = gtid; i < p.S; i += nth) p.send[i] = 0;
+    if (gtid == 0) C->pad[4] = 0;  // heavy-row list of this level (last read before a barrier)
     grid_sync(gb, nblocks, bar);
     uint32_t n_new = 0;
     unsigned long long m_new = 0, exam = 0;
     if (st.dir == kPush && st.pad) {
       // wide push level: candidates (fire-and-forget marks), settled after a grid barrier
-      if ((unsigned long long)(st.reached + 1) * 32 < p.n)
-        part_work<NT, true, 2>(p, st, L, rv, p.send, gwarp, nwarps, n_new, m_new, exam);
-      else
-        part_work<NT, true, 1>(p, st, L, rv, p.send, gwarp, nwarps, n_new, m_new, exam);
+      if ((unsigned long long)(st.reached + 1) * 32 < p.n) {
+        part_work<NT, true, 2, true>(p, st, L, rv, p.send, gwarp, nwarps, n_new, m_new, exam);
+        if (st.hvy) grid_sync(gb, nblocks, bar);
+        part_push_heavy<true, 2>(p, st, L, rv, p.send, gwarp, nwarps, n_new, m_new, exam);
+      } else {
+        part_work<NT, true, 1, true>(p, st, L, rv, p.send, gwarp, nwarps, n_new, m_new, exam);
+        if (st.hvy) grid_sync(gb, nblocks, bar);
+        part_push_heavy<true, 1>(p, st, L, rv, p.send, gwarp, nwarps, n_new, m_new, exam);
+      }
       grid_sync(gb, nblocks, bar);
       part_settle(p, p.send, L + 1, gtid, nth, n_new, m_new);
+    } else if (st.dir == kPush) {
+      part_work<NT, true, 0, true>(p, st, L, rv, p.send, gwarp, nwarps, n_new, m_new, exam);
+      if (st.hvy) grid_sync(gb, nblocks, bar);
+      part_push_heavy<true, 0>(p, st, L, rv, p.send, gwarp, nwarps, n_new, m_new, exam);
     } else {
       part_work<NT, true>(p, st, L, rv, p.send, gwarp, nwarps, n_new, m_new, exam);
     }
