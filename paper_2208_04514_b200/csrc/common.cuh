@@ -33,6 +33,13 @@ __device__ __forceinline__ uint2 ld_nc2(const uint32_t *p) {  // 8-B aligned pai
   asm volatile("ld.global.nc.v2.u32 {%0, %1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p));
   return r;
 }
+// Weak global load (L1-cacheable): data another CTA or device wrote before an acquire / fence
+// this thread's CTA has passed, and that nobody writes while it is being read.
+__device__ __forceinline__ uint32_t ld_gbl(const uint32_t *p) {
+  uint32_t r;
+  asm volatile("ld.global.u32 %0, [%1];" : "=r"(r) : "l"(p));
+  return r;
+}
 // Mutable data written by other CTAs in an EARLIER phase (after a grid barrier): L2 only.
 __device__ __forceinline__ uint32_t ld_cg(const uint32_t *p) {
   uint32_t r;

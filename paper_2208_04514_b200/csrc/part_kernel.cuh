@@ -76,11 +76,14 @@ struct PartParams {
 };
 
 // Global-memory load of exchange data: the non-coherent path inside one level launch (the
-// buffer is read-only there); L2 in the persistent kernel, whose slots are rewritten by peers
-// between its levels.
+// buffer is read-only there); in the persistent kernel, whose slots are rewritten by peers
+// between its levels, a plain (weak, L1-cacheable) load: the slot read in level L is not written
+// during level L (peers write the other one), and every CTA passes an acquire of the arrival
+// counter and a grid barrier (fence.acq_rel, which invalidates the SM's L1) between the peers'
+// stores into it and its first read — hot frontier words then stay in L1 across the level.
 template <bool CG>
 __device__ __forceinline__ uint32_t xld(const uint32_t *a) {
-  if constexpr (CG) return ld_cg(a); else return ld_nc(a);
+  if constexpr (CG) return ld_gbl(a); else return ld_nc(a);
 }
 
 // Is global vertex v in the frontier held by the gathered slices `rv`?
