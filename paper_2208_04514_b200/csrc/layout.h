@@ -102,6 +102,9 @@ constexpr uint32_t kDirectRow = 256;
 #ifndef DAWN_NOVIS_FRAC
 #define DAWN_NOVIS_FRAC 32  // ... while (reached + 1) * FRAC < reachable vertices (C4 1325 -> 1350 GTEPS; 8: forced push C2 -9%)
 #endif
+#ifndef DAWN_PULL_PREFETCH
+#define DAWN_PULL_PREFETCH 1  // pull sweep: unreached-list entries loaded one iteration ahead
+#endif
 #ifndef DAWN_PULL_J
 #define DAWN_PULL_J 2  // vis words per warp iteration of the pull sweep (independent scans)
 #endif

@@ -454,13 +454,26 @@ __device__ void pull_level(const SsspParams &p, const LevelState &st, uint32_t g
   const uint32_t cnt = st.ul ? ld_cg(p.useg + gwarp)
                              : (seg0 < p.n_hasin ? min(cap, p.n_hasin - seg0) : 0u);
   uint32_t wr = 0;
+#if DAWN_PULL_PREFETCH
+  // the next iteration's list entries are loaded one iteration ahead (the in-place compaction
+  // only writes positions below the current iteration's end, so the read-ahead is never stale)
+  uint32_t un[J];
+#pragma unroll
+  for (int j = 0; j < J; ++j) un[j] = (j * 32 + lane < cnt) ? ld_cg(src + j * 32 + lane) : 0xffffffffu;
+#endif
   for (uint32_t ib = 0; ib < cnt; ib += 32 * J) {
     uint32_t u[J], s[J], e[J], j0[J], ef[J];
     bool need[J], found[J], hvy[J];
 #pragma unroll
     for (int j = 0; j < J; ++j) {
+#if DAWN_PULL_PREFETCH
+      u[j] = un[j];
+      const uint32_t i = ib + 32 * J + j * 32 + lane;
+      un[j] = i < cnt ? ld_cg(src + i) : 0xffffffffu;
+#else
       const uint32_t i = ib + j * 32 + lane;
       u[j] = i < cnt ? ld_cg(src + i) : 0xffffffffu;
+#endif
       found[j] = false;
       need[j] = false;
       hvy[j] = false;
