@@ -178,8 +178,9 @@ typedef enum {
   DAWN_PARAM_BATCH_LANES = 9,      /* dawn_sssp_batch on the grid-wide kernel runs this many
                                       searches at once, each on 1/lanes of the SMs with its own
                                       per-search state and stream (the sources are
-                                      independent).  1 .. 8 (n <= 2^22) or
-                                      1 .. 8 (larger n; 1 with DAWN_GRAPH_LEAN).  Default set at
+                                      independent).  Lanes run the 2-CTA/SM
+                                      kernel.  1 .. 16 (n <= 2^22) or 1 .. 8 (larger n; 1 with
+                                      DAWN_GRAPH_LEAN).  Default set at
                                       load from B200 measurements.              */
   DAWN_PARAM_WEIGHT_DELTA = 12,    /* dawn_wsssp near/far step: a round expands only frontier
                                       vertices with d < T (the others stay in the frontier); T
@@ -193,13 +194,12 @@ typedef enum {
                                       set at load from B200 measurements.      */
   DAWN_PARAM_BATCH_DYNAMIC = 13,   /* 1: the batch lanes of dawn_sssp_batch take the batch's
                                       sources one at a time from a shared counter (each lane
-                                      claims its next index while it initialises the current
-                                      search), so the lanes finish together whatever the
+                                      claims its next index when its current search ends), so
+                                      the lanes finish together whatever the
                                       per-source cost; 0: lane l runs the fixed contiguous share
-                                      [k*l/lanes, k*(l+1)/lanes).  Default (set at load): 1 for
-                                      n > 2^22, 0 below (B200: Kronecker-24 +1.2%, Kronecker-20
-                                      -3%).  Which lane runs a source never changes its row or
-                                      statistics.  Speed only.                                 */
+                                      [k*l/lanes, k*(l+1)/lanes).  Default 1 (B200:
+                                      Kronecker-24 +1.7%, Kronecker-20 +5%).  Which lane runs a
+                                      source never changes its row or statistics.  Speed only. */
   DAWN_PARAM_DENSE_MAX_ENTRIES = 10 /* dense distance outputs (dawn_msssp dist, one piece of
                                       dawn_apsp_rows) are refused with DAWN_ERR_CAPACITY when
                                       rows * n >= this ("dense-matrix mode refused

@@ -46,7 +46,13 @@ constexpr int kNT = 512;  // threads per CTA of the persistent kernels
 #define DAWN_BATCH_CLAIM 2  // dynamic batch lanes: 2 = on for the 64-register kernel (n > 2^22)
 #endif
 // Graph-size thresholds of the kernel choice (measured on B200)
-constexpr int64_t kSsspOneMaxN = 1 << 22;  // k_sssp<kNT, 1> (1 CTA/SM, 128 regs) up to 2^22
+#ifndef DAWN_BATCH_TWO
+#define DAWN_BATCH_TWO 1  // batch lanes use the 2-CTA/SM k_sssp on every graph
+#endif
+#ifndef DAWN_SSSP_ONE_MAX
+#define DAWN_SSSP_ONE_MAX (1 << 22)
+#endif
+constexpr int64_t kSsspOneMaxN = DAWN_SSSP_ONE_MAX;  // k_sssp<kNT, 1> (1 CTA/SM, 128 regs) up to 2^22
 constexpr int64_t kOneCtaMaxNM = 1 << 15;  // n + m this small: one CTA, barriers are __syncthreads
 constexpr int kMsBlocksPerSm = 2;          // k_ms64 CTAs per SM (if they fit)
 constexpr uint32_t kNarrowQcapMax = 1u << 20;
@@ -56,7 +62,7 @@ constexpr int kDefaultMsLanes = DAWN_MS_LANES;  // multi-source lanes (B200 meas
 #define DAWN_WDELTA 8  // near/far step of dawn_wsssp (weights 1..255 on Kronecker-24)
 #endif
 #ifndef DAWN_LANES_SMALL
-#define DAWN_LANES_SMALL 8  // default batch lanes for n <= 2^22 (C2: 2 -> 650, 8 -> 1008 GTEPS)
+#define DAWN_LANES_SMALL 16  // default batch lanes for n <= 2^22 (C2, 2-CTA/SM kernel: 8 -> 1,365, 12 -> 1,443, 16 -> 1,538, 24 -> 1,460, 32 -> 1,502 GTEPS)
 #endif
 #ifndef DAWN_LANES_BIG
 #define DAWN_LANES_BIG 4    // ... and above (C4: 1 -> 1343, 2 -> 1590, 4 -> 1678 GTEPS)
@@ -324,6 +330,7 @@ struct dawn_graph_s {
   bool has_csc;
   float alpha = 2.f, beta = 96.f, ms_alpha = 2.f;
   int sssp_grid, ms_grid, wsssp_grid = 1;
+  int sssp_grid2 = 1;     // grid of the 2-CTA/SM instantiation (batch lanes use it on any graph)
   bool sssp_one = false;  // the 1-CTA-per-SM instantiation of k_sssp (small graphs)
   bool trace;
   size_t small_cap;  // max dynamic smem for k_small (0 = disabled)
@@ -435,11 +442,10 @@ dawn_status load_csr(int64_t n, int64_t m, const int64_t *row_ptr, const int32_t
   cudaDeviceGetAttribute(&g->nsm, cudaDevAttrMultiProcessorCount, g->device);
   // small graphs: k_sssp<kNT, 1> (one CTA per SM, 128 registers); big ones k_sssp<kNT, 2>
   g->sssp_one = n <= kSsspOneMaxN;
-  // dynamic batch lanes: Kronecker-24 (4 lanes x 16 searches) 1,683 -> 1,702 GTEPS; Kronecker-20
-  // (8 lanes x 8) 1,002 -> 974, so off for the 1-CTA/SM kernel
-  g->batch_claim = DAWN_BATCH_CLAIM == 1 || (DAWN_BATCH_CLAIM == 2 && !g->sssp_one);
-  g->sssp_grid = g->sssp_one ? std::min<int>(g->nsm, (int)kMaxBlocks)
-                             : grid_for((const void *)k_sssp<kNT, 2>, g->nsm);
+  // dynamic batch lanes: Kronecker-24 1,690 -> 1,718 GTEPS, Kronecker-20 1,463 -> 1,531
+  g->batch_claim = DAWN_BATCH_CLAIM == 1 || (DAWN_BATCH_CLAIM == 2 && (!g->sssp_one || DAWN_BATCH_TWO));
+  g->sssp_grid2 = grid_for((const void *)k_sssp<kNT, 2>, g->nsm);
+  g->sssp_grid = g->sssp_one ? std::min<int>(g->nsm, (int)kMaxBlocks) : g->sssp_grid2;
   {
     int optin = 0;
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, g->device);
@@ -712,10 +718,14 @@ SsspParams sssp_params(dawn_graph g, uint32_t variant, uint32_t *dist, dawn_sssp
 }
 
 dawn_status launch_sssp(dawn_graph g, SsspParams &p, cudaStream_t stream, int lanes = 1) {
-  int grid = std::max(1, g->sssp_grid / lanes);
+  // batch lanes run the 2-CTA/SM (64-register) instantiation on every graph: twice the warps
+  // per SM hide the latency of several concurrent searches (Kronecker-20 at 8 lanes: 1,030 ->
+  // 1,349 GTEPS); one search on a graph up to 2^22 vertices keeps the 1-CTA/SM one
+  const bool two = !g->sssp_one || (DAWN_BATCH_TWO && lanes > 1);
+  int grid = std::max(1, (two ? g->sssp_grid2 : g->sssp_grid) / lanes);
   if (g->m + g->n <= kOneCtaMaxNM) grid = 1;  // tiny graphs: one CTA, barriers are __syncthreads
   void *args[] = {&p};
-  const void *kfn = g->sssp_one ? (const void *)k_sssp<kNT, 1> : (const void *)k_sssp<kNT, 2>;
+  const void *kfn = two ? (const void *)k_sssp<kNT, 2> : (const void *)k_sssp<kNT, 1>;
   cudaError_t e = cudaLaunchCooperativeKernel(kfn, dim3(grid), dim3(kNT), args, 0, stream);
   if (e != cudaSuccess) return cuda_fail(e, "k_sssp launch");
   return DAWN_OK;

@@ -169,7 +169,7 @@ struct HeavyList {  // static pieces of rows with degree > kHeavy
 // kMaxLanes cooperative launches (one per lane, each on its own share of the SMs and its own
 // stream) run independent searches of one batch at the same time (sources are
 // independent).  Lane 0 is the state every other call uses.
-constexpr int kMaxLanes = 8;
+constexpr int kMaxLanes = 16;   // allocated: 16 up to 2^22 vertices, 8 above (make_layout)
 constexpr int kMsMaxLanes = 4;
 #ifndef DAWN_MS_LANES
 #define DAWN_MS_LANES 4  // default multi-source lanes (C5: 1 -> 707K, 2 -> 815K, 3 -> 829K, 4 -> 847K sources/s)
@@ -270,7 +270,7 @@ inline Layout make_layout(int64_t n, int64_t m, uint32_t flags) {
   }
   // extra lanes (lane 0 = the arrays above): not in lean mode; 4 lanes up to 2^22 vertices
   // (latency-bound searches overlap best), 2 above
-  L.nlanes = lean ? 1 : kMaxLanes;
+  L.nlanes = lean ? 1 : ((uint64_t)n <= (1ull << 22) ? kMaxLanes : 8);
   L.lane[0] = LaneLayout{L.vis, L.cand, {L.fb[0], L.fb[1], L.fb[2]}, {L.Lv[0], L.Lv[1]},
                          {L.Lsd[0], L.Lsd[1]}, {L.Cf[0], L.Cf[1]}, L.ctrl, L.ulist, L.useg};
   for (int l = 1; l < L.nlanes; ++l) {

@@ -831,7 +831,8 @@ __global__ void __launch_bounds__(NT, MINB) k_sssp(SsspParams p) {
   const uint32_t nsrc = p.nsrc ? p.nsrc : 1u;
   // batch mode: the searches run back to back in this launch, a grid barrier apart (no kernel
   // boundary or launch ramp between them).  Dynamic lanes (p.claim): the batch index of the next
-  // search is claimed during the current one's init and read by every CTA after its barrier
+  // search is claimed when the current one ends and read by every CTA after a barrier (claiming
+  // one ahead left lanes idle when a batch has about as many sources as lanes)
   __shared__ uint32_t next_sh;  // batch index of the next search (kept in shared memory)
   if (p.claim) {
     if (blockIdx.x == 0 && threadIdx.x == 0) C->next_idx = atomicAdd(p.claim, 1u);
@@ -889,7 +890,6 @@ __global__ void __launch_bounds__(NT, MINB) k_sssp(SsspParams p) {
     for (uint32_t c = gtid; c * kChunk < d0; c += nthreads) p.Cf[0][c] = 0;
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
-    if (p.claim) C->next_idx = atomicAdd(p.claim, 1u);  // published by the barrier below
     for (int i = 0; i < 3; ++i) C->slot[i] = Slot{0, 0, 0, 0, 0};
     C->examined = 0;
     C->solo_epoch = 0;
@@ -917,7 +917,8 @@ __global__ void __launch_bounds__(NT, MINB) k_sssp(SsspParams p) {
   }
   }
   grid_sync(&C->bar, nblocks, bar_target);
-  if (threadIdx.x == 0) next_sh = p.claim ? ld_cg(&C->next_idx) : idx + 1;  // read after a sync
+  // the next search's index for the solo-stretch prefill: unknown (none) with dynamic lanes
+  if (threadIdx.x == 0) next_sh = p.claim ? nsrc : idx + 1;  // read after a sync
   if (p.trace && gtid == 0) p.trace[kTraceCap - 1].t_first = globaltimer();
 
   unsigned long long examined = 0;
@@ -1085,7 +1086,14 @@ __global__ void __launch_bounds__(NT, MINB) k_sssp(SsspParams p) {
       *stats_out = s;
     }
   }
-  if (next_sh < nsrc) grid_sync(&C->bar, nblocks, bar_target);  // before the next init
+  if (p.claim) {  // dynamic lanes: claim the next index now, publish it by a barrier
+    if (blockIdx.x == 0 && threadIdx.x == 0) C->next_idx = atomicAdd(p.claim, 1u);
+    grid_sync(&C->bar, nblocks, bar_target);
+    if (threadIdx.x == 0) next_sh = ld_cg(&C->next_idx);
+    __syncthreads();
+  } else if (next_sh < nsrc) {
+    grid_sync(&C->bar, nblocks, bar_target);  // before the next init
+  }
   }  // sources
   grid_exit(&C->bar, nblocks);
 }

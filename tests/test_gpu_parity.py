@@ -437,7 +437,7 @@ def test_sssp_batch_lanes():
     # or run fixed contiguous shares (0); either way row i / stats i belong to source i
     for dyn in (1, 0):
         G.set_tuning(batch_dynamic=dyn)
-        for lanes in (1, 2, 4, 8):
+        for lanes in (1, 2, 4, 8, 16):
             G.set_tuning(batch_lanes=lanes)
             for v in VARIANTS:
                 d, st = dawn.sssp_batch(G, torch.from_numpy(srcs).cuda(), v, stats=True, check=True)
@@ -455,7 +455,7 @@ def test_sssp_batch_lanes():
     d = dawn.sssp_batch(G, torch.from_numpy(small).cuda()).cpu().numpy().view(np.uint32)
     assert all(np.array_equal(d[i], exps[i]) for i in range(len(small)))
     with pytest.raises(dawn.DawnError):
-        G.set_tuning(batch_lanes=9)
+        G.set_tuning(batch_lanes=17)
     # the lanes share nothing across calls: a single dawn_sssp between batches still matches
     G.set_tuning(batch_lanes=4)
     dawn.sssp_batch(G, torch.from_numpy(srcs).cuda())
