@@ -236,6 +236,13 @@ __global__ void k_topk_rows(const uint32_t *__restrict__ irp, const int32_t *__r
   }
 }
 
+// top1[u] = the first in-neighbour of u's degree-ordered in-row (0xffffffff: none)
+__global__ void k_top1(const uint32_t *__restrict__ irp, const int32_t *__restrict__ icol2,
+                       uint32_t n, uint32_t *__restrict__ top1) {
+  for (uint32_t u = blockIdx.x * blockDim.x + threadIdx.x; u < n; u += gridDim.x * blockDim.x)
+    top1[u] = irp[u + 1] > irp[u] ? (uint32_t)icol2[irp[u]] : 0xffffffffu;
+}
+
 // pass 3 (piece-major order): hc[c] = #heavy rows with exactly c pieces; maxc
 __global__ void k_hhist(const uint32_t *__restrict__ rp, uint32_t n, uint32_t *hc, uint32_t *maxc) {
   uint32_t mx = 0;
@@ -582,6 +589,8 @@ dawn_status load_csr(int64_t n, int64_t m, const int64_t *row_ptr, const int32_t
     k_topk_rows<<<g->nsm * 8, 256, 0, st>>>(irp2, sym ? col : in_col, at<uint32_t>(g, L.rp),
                                             (uint32_t)n, at<int32_t>(g, L.icol2));
     g->icol = at<int32_t>(g, L.icol2);
+    k_top1<<<g->nsm * 8, 256, 0, st>>>(irp2, at<int32_t>(g, L.icol2), (uint32_t)n,
+                                       at<uint32_t>(g, L.top1));
   }
   if (sym || has_csc) {  // unreached-list seed for the pull sweep
     const uint32_t nblk = (uint32_t)((n + kScanBlock - 1) / kScanBlock);
@@ -689,6 +698,8 @@ SsspParams sssp_params(dawn_graph g, uint32_t variant, uint32_t *dist, dawn_sssp
   p.hin_s = at<uint32_t>(g, L.hin.s);
   p.hin_e = at<uint32_t>(g, L.hin.e);
   p.hin_bits = at<uint32_t>(g, L.hin.bits);
+  p.top1 = (DAWN_PULL_TOP1 && L.top1 && g->icol == at<int32_t>(g, L.icol2)) ? at<uint32_t>(g, L.top1)
+                                                                           : nullptr;
   p.vis = at<uint32_t>(g, Q.vis);
   p.cand = at<uint32_t>(g, Q.cand);
   p.hasin = at<uint32_t>(g, L.hasin);

@@ -102,6 +102,9 @@ constexpr uint32_t kDirectRow = 256;
 #ifndef DAWN_NOVIS_FRAC
 #define DAWN_NOVIS_FRAC 32  // ... while (reached + 1) * FRAC < reachable vertices (C4 1325 -> 1350 GTEPS; 8: forced push C2 -9%)
 #endif
+#ifndef DAWN_PULL_TOP1
+#define DAWN_PULL_TOP1 1  // pull sweep: the first in-neighbour from a per-vertex array
+#endif
 #ifndef DAWN_PULL_PREFETCH
 #define DAWN_PULL_PREFETCH 1  // pull sweep: unreached-list entries loaded one iteration ahead
 #endif
@@ -192,7 +195,7 @@ struct Layout {
   MsLaneLayout ms[kMaxLanes];
   int ms_nlanes;
   HeavyList hout, hin;
-  size_t scan_tmp, piece_tmp, hasin, ulist, useg, icol2, arc;
+  size_t scan_tmp, piece_tmp, hasin, ulist, useg, icol2, top1, arc;
   size_t seen, F0, F1, nxt, msctrl, part, srcbuf, total;
   uint64_t srccap, capCf, capHP;
   bool own_irp;
@@ -287,6 +290,10 @@ inline Layout make_layout(int64_t n, int64_t m, uint32_t flags) {
     q.ulist = take(4 * (size_t)n);
     q.useg = take(4 * (size_t)kMaxBlocks * 32);
   }
+  // the first entry of every degree-ordered in-row (0xffffffff: empty row), read beside the
+  // row offsets so a pull probe of it needs no in-row sector; last, so the other arrays keep
+  // their offsets
+  L.top1 = L.icol2 ? take(4 * (size_t)n) : 0;
   L.total = o;
   return L;
 }

@@ -34,6 +34,7 @@ struct SsspParams {
   const uint32_t *noin;
   const uint32_t *hin_v, *hin_s, *hin_e, *hin_bits;  // static heavy in-row pieces
   const uint32_t *hasin;  // static ascending list of vertices with an in-edge (n_hasin)
+  const uint32_t *top1;   // [n]: first entry of each degree-ordered in-row, or null
   uint32_t *ulist, *useg;  // unreached list (per-warp segments) and segment counts
   uint32_t n_hasin;
   uint32_t *vis, *cand, *fb[3];  // cand: candidate bitmap of bitmap-push levels (zero between uses)
@@ -462,7 +463,7 @@ __device__ void pull_level(const SsspParams &p, const LevelState &st, uint32_t g
   for (int j = 0; j < J; ++j) un[j] = (j * 32 + lane < cnt) ? ld_cg(src + j * 32 + lane) : 0xffffffffu;
 #endif
   for (uint32_t ib = 0; ib < cnt; ib += 32 * J) {
-    uint32_t u[J], s[J], e[J], j0[J], ef[J];
+    uint32_t u[J], s[J], e[J], j0[J], ef[J], t1[J];
     bool need[J], found[J], hvy[J];
 #pragma unroll
     for (int j = 0; j < J; ++j) {
@@ -487,12 +488,19 @@ __device__ void pull_level(const SsspParams &p, const LevelState &st, uint32_t g
         hvy[j] = ld_nc(p.hin_bits + (u[j] >> 5)) & bit;
         s[j] = ld_nc(p.irp + u[j]);                       // speculative, same round trip
         e[j] = ld_nc(p.irp + u[j] + 1);
+        t1[j] = p.top1 ? ld_nc(p.top1 + u[j]) : 0xffffffffu;  // the row's first entry, ditto
       }
     }
 #pragma unroll
     for (int j = 0; j < J; ++j) {
       if (!need[j]) e[j] = s[j];
       j0[j] = s[j];
+      if (p.top1 && e[j] > s[j]) {
+        // the first probe from the per-vertex copy: a hit settles the vertex without a sector
+        // of its in-row (the sweep is then bounded by the row offsets, not the in-rows)
+        found[j] = fb_test(fcur, t1[j]);
+        j0[j] = s[j] + 1;
+      }
       // heavy rows (in-degree > kHeavy): only the first kHeavyProbe in-edges here; the
       // static pieces finish the rows still unsettled
       ef[j] = hvy[j] ? min(e[j], s[j] + kHeavyProbe) : e[j];
