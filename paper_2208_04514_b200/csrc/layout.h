@@ -102,6 +102,9 @@ constexpr uint32_t kDirectRow = 256;
 #ifndef DAWN_NOVIS_FRAC
 #define DAWN_NOVIS_FRAC 32  // ... while (reached + 1) * FRAC < reachable vertices (C4 1325 -> 1350 GTEPS; 8: forced push C2 -9%)
 #endif
+#ifndef DAWN_PULL_SPLIT
+#define DAWN_PULL_SPLIT 1  // pull level = light pass, grid barrier, heavy pieces (C4 +4.5%)
+#endif
 #ifndef DAWN_PULL_TOP1
 #define DAWN_PULL_TOP1 1  // pull sweep: the first in-neighbour from a per-vertex array
 #endif

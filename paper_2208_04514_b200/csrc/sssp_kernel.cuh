@@ -432,8 +432,11 @@ __device__ __forceinline__ bool fb_test(const uint32_t *fb, uint32_t v) {
   return (fb[v >> 5] >> (v & 31)) & 1u;
 }
 
-template <int PR, int J>  // in-edges probed per lane per round trip (8 when the frontier is
-                          // sparse); J unreached vertices per lane in flight
+// PART: 0 the whole level; 1 the light pass only (heavy vertices it settles are claimed with a
+// fire-and-forget reduction: the pieces run after a grid barrier and skip settled vertices);
+// 2 the heavy pieces only
+template <int PR, int J, int PART = 0>  // in-edges probed per lane per round trip (8 when the
+                                        // frontier is sparse); J unreached vertices per lane
 __device__ void pull_level(const SsspParams &p, const LevelState &st, uint32_t gwarp,
                            uint32_t nwarps, uint32_t &n_new, unsigned long long &m_new,
                            unsigned long long &examined, long long &t0, bool &bigf) {
@@ -442,6 +445,7 @@ __device__ void pull_level(const SsspParams &p, const LevelState &st, uint32_t g
   const uint32_t *fcur = p.fb[st.b];
   uint32_t *fnext = p.fb[(st.b + 1) % 3];
   uint32_t *fclr = p.fb[(st.b + 2) % 3];  // held frontier L-1: cleared for level L+1
+  if constexpr (PART != 2) {
   // (0) clear the bitmap of frontier L-1 (becomes the write target of level L+1)
   for (uint32_t w = gwarp * 32 + lane; w < p.nwords; w += nwarps * 32) fclr[w] = 0;
   // (1) unreached vertices, one lane each, from the warp's segment of the unreached list:
@@ -537,7 +541,7 @@ __device__ void pull_level(const SsspParams &p, const LevelState &st, uint32_t g
       if (need[j]) examined += min(j0[j], ef[j]) - s[j];
       if (found[j]) {
         const uint32_t w = u[j] >> 5, bit = 1u << (u[j] & 31);
-        if (hvy[j]) {
+        if (hvy[j] && PART == 0) {
           // a heavy row may be settled concurrently by one of its static pieces: claim with a
           // returning atomic so each vertex is counted exactly once
           if (atomicOr(p.vis + w, bit) & bit) found[j] = false;
@@ -562,6 +566,8 @@ __device__ void pull_level(const SsspParams &p, const LevelState &st, uint32_t g
   }
   if (lane == 0) p.useg[gwarp] = wr;
   phase_add(p, st.L, 0, t0);
+  }  // PART != 2
+  if constexpr (PART == 1) return;
   // (2) heavy rows: static pieces; 32 pieces tested per warp (vis), then a warp scans each
   //     live piece 32 in-edges per round trip
   // every warp gets an equal consecutive share of the piece list (a 32-piece stride left most
@@ -854,9 +860,10 @@ __global__ void __launch_bounds__(NT, MINB) k_sssp(SsspParams p) {
   for (;;) {
   const uint32_t idx = next_sh;  // batch index of this search
   if (idx >= nsrc) break;
+  __shared__ uint32_t cur_sh;  // the same, re-read at the search's end (no register held)
+  if (threadIdx.x == 0) cur_sh = idx;
   const uint32_t src = p.nsrc ? ld_nc(p.sources + idx) : p.source;
   uint32_t *const drow = p.dist + (size_t)idx * p.n;
-  dawn_sssp_stats *const stats_out = p.stats ? p.stats + idx : nullptr;
   // per-search scalars of thread 0 in shared memory (no registers held across the levels)
   __shared__ uint32_t solo_epoch, max_reach;
   if (threadIdx.x == 0) {
@@ -926,7 +933,7 @@ __global__ void __launch_bounds__(NT, MINB) k_sssp(SsspParams p) {
   }
   grid_sync(&C->bar, nblocks, bar_target);
   // the next search's index for the solo-stretch prefill: unknown (none) with dynamic lanes
-  if (threadIdx.x == 0) next_sh = p.claim ? nsrc : idx + 1;  // read after a sync
+  if (threadIdx.x == 0) next_sh = p.claim ? nsrc : cur_sh + 1;  // read after a sync
   if (p.trace && gtid == 0) p.trace[kTraceCap - 1].t_first = globaltimer();
 
   unsigned long long examined = 0;
@@ -1058,14 +1065,23 @@ __global__ void __launch_bounds__(NT, MINB) k_sssp(SsspParams p) {
         phase_add(p, st.L, 1, tconv);
       }
     } else {
-#if DAWN_PULL_DEEP
-      if (st.deep)
-        pull_level<MINB == 1 ? DAWN_PULL_DEEP_PR : DAWN_PULL_DEEP_PR2, MINB == 1 ? DAWN_PULL_J : DAWN_PULL_J2>(p, st, gwarp, nwarps, n_new, m_new,
-                                                                      examined, tconv, bigf);
-      else
-#endif
-        pull_level<MINB == 1 ? DAWN_PULL_PR : DAWN_PULL_PR2, MINB == 1 ? DAWN_PULL_J : DAWN_PULL_J2>(p, st, gwarp, nwarps, n_new, m_new, examined,
-                                                            tconv, bigf);
+      constexpr int kPrD = MINB == 1 ? DAWN_PULL_DEEP_PR : DAWN_PULL_DEEP_PR2;
+      constexpr int kPr = MINB == 1 ? DAWN_PULL_PR : DAWN_PULL_PR2;
+      constexpr int kJ = MINB == 1 ? DAWN_PULL_J : DAWN_PULL_J2;
+      if constexpr (DAWN_PULL_SPLIT) {
+        // light pass, grid barrier, heavy pieces: no returning claim in the light pass
+        if (DAWN_PULL_DEEP && st.deep)
+          pull_level<kPrD, kJ, 1>(p, st, gwarp, nwarps, n_new, m_new, examined, tconv, bigf);
+        else
+          pull_level<kPr, kJ, 1>(p, st, gwarp, nwarps, n_new, m_new, examined, tconv, bigf);
+        grid_sync(&C->bar, nblocks, bar_target);
+        pull_level<kPr, kJ, 2>(p, st, gwarp, nwarps, n_new, m_new, examined, tconv, bigf);
+      } else {
+        if (DAWN_PULL_DEEP && st.deep)
+          pull_level<kPrD, kJ>(p, st, gwarp, nwarps, n_new, m_new, examined, tconv, bigf);
+        else
+          pull_level<kPr, kJ>(p, st, gwarp, nwarps, n_new, m_new, examined, tconv, bigf);
+      }
     }
     block_flush(n_new, m_new, &ns->n_new, &ns->m_new, red);
     if constexpr (kDirect) {
@@ -1080,7 +1096,8 @@ __global__ void __launch_bounds__(NT, MINB) k_sssp(SsspParams p) {
 
   if (p.trace && gtid == 0) p.trace[kTraceCap - 1].t_last = globaltimer();
   // ---- a7 statistics
-  if (stats_out) {
+  if (p.stats) {
+    dawn_sssp_stats *const stats_out = p.stats + *(volatile uint32_t *)&cur_sh;
     block_flush(0u, examined, nullptr, &C->examined, red);
     grid_sync(&C->bar, nblocks, bar_target);
     if (blockIdx.x == 0 && threadIdx.x == 0) {
