@@ -1466,6 +1466,7 @@ dawn_status part_build(int64_t n, int64_t m, const int64_t *row_ptr, const int32
 struct PartLayout {
   size_t rp, irp, hout_bits, hout_v, hout_s, hout_e, hin_bits, hin_v, hin_s, hin_e;
   size_t scan_tmp, piece_tmp, vis, cand, lev, send, recv, ctrl, icol2, hasin, ulist, useg, hlist;
+  size_t top1;
   size_t total;
   uint64_t capHP;
 };
@@ -1503,6 +1504,7 @@ PartLayout part_layout(int64_t n, int64_t m_r, int32_t world, int64_t R, int64_t
   L.recv = take(4 * S * (size_t)world);
   L.ctrl = take(sizeof(PartCtrl));
   L.hlist = take(4 * (size_t)kPartHList);  // heavy frontier vertices of a fused push level
+  L.top1 = take(4 * (size_t)R + 4);  // first entry of every degree-ordered in-row (as k_sssp)
   L.total = o;
   return L;
 }
@@ -1560,6 +1562,7 @@ PartParams part_params(dawn_part p) {
   q.ulist = u32(p->L.ulist);
   q.useg = u32(p->L.useg);
   q.hlist = u32(p->L.hlist);
+  q.top1 = (DAWN_PULL_TOP1 && p->m_r > 0) ? u32(p->L.top1) : nullptr;
   q.n_has = p->n_has;
   q.lev = reinterpret_cast<uint8_t *>(p->ws + p->L.lev);
   q.dist = p->dist;
@@ -1655,9 +1658,12 @@ dawn_status part_load(int64_t n, int64_t m, int32_t world, int32_t rank, int64_t
   // pull probes meet hubs first: each in-row with its 8 sources of largest out-slice degree (a
   // proxy of the global out-degree: labels are random, so a vertex sends ~1/W of its arcs
   // to every range) moved to the front, as k_sssp's degree-ordered in-rows
-  if (m_r > 0 && R > 0)
+  if (m_r > 0 && R > 0) {
     k_topk_rows<<<p->nsm * 8, 256, 0, st>>>(u32(L.irp), in_col, u32(L.rp), (uint32_t)R,
                                             reinterpret_cast<int32_t *>(p->ws + L.icol2));
+    k_top1<<<p->nsm * 8, 256, 0, st>>>(u32(L.irp), reinterpret_cast<int32_t *>(p->ws + L.icol2),
+                                       (uint32_t)R, u32(L.top1));
+  }
   if (R > 0) {  // static ascending list of the owned vertices with an in-edge
     const uint32_t nblk = (uint32_t)((R + kScanBlock - 1) / kScanBlock);
     k_lcount<<<nblk, 256, 0, st>>>(u32(L.irp), (uint32_t)R, u32(L.scan_tmp));

@@ -64,6 +64,7 @@ struct PartParams {
   const uint32_t *hasin;              // owned vertices with an in-edge, ascending (n_has)
   uint32_t *ulist, *useg;             // unreached list in per-warp segments, segment counts
   uint32_t *hlist;                    // fused push: heavy frontier vertices (count: ctrl->pad[4])
+  const uint32_t *top1;               // [R]: first entry of each degree-ordered in-row, or null
   uint32_t n_has;
   uint8_t *lev;                       // deferred distances (as k_sssp: byte L+1, 255 = direct)
   uint32_t *dist;                     // caller's distance slice [R]
@@ -316,7 +317,7 @@ __device__ void part_work(const PartParams &p, const PartState &st, uint32_t L, 
                                  : (seg0 < p.n_has ? min(cap, p.n_has - seg0) : 0u);
     uint32_t wr = 0;
     for (uint32_t ib = 0; ib < cnt; ib += 32 * PJ) {
-      uint32_t t[PJ], s[PJ], e[PJ], dg[PJ];
+      uint32_t t[PJ], s[PJ], e[PJ], dg[PJ], t1[PJ];
       bool need[PJ], keep[PJ], found[PJ], hv[PJ];
 #pragma unroll
       for (int k = 0; k < PJ; ++k) {
@@ -332,11 +333,19 @@ __device__ void part_work(const PartParams &p, const PartState &st, uint32_t L, 
           s[k] = ld_nc(p.irp + t[k]);  // speculative, same round trip
           e[k] = ld_nc(p.irp + t[k] + 1);
           dg[k] = ld_nc(p.deg + t[k]);
+          t1[k] = p.top1 ? ld_nc(p.top1 + t[k]) : 0xffffffffu;  // the in-row's first entry
         }
       }
 #pragma unroll
-      for (int k = 0; k < PJ; ++k)
+      for (int k = 0; k < PJ; ++k) {
         if (hv[k]) e[k] = min(e[k], s[k] + kHeavyProbe);  // the pieces scan the rest
+        if (p.top1 && need[k] && e[k] > s[k]) {
+          // first probe from the per-vertex copy: no in-row sector when it settles the vertex
+          found[k] = part_ftest<CG>(p, rv, t1[k]);
+          exam += 1;
+          s[k] += 1;
+        }
+      }
       for (;;) {
         bool any = false;
         uint32_t v[PJ][4];
