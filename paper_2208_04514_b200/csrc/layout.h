@@ -102,6 +102,9 @@ constexpr uint32_t kDirectRow = 256;
 #ifndef DAWN_NOVIS_FRAC
 #define DAWN_NOVIS_FRAC 32  // ... while (reached + 1) * FRAC < reachable vertices (C4 1325 -> 1350 GTEPS; 8: forced push C2 -9%)
 #endif
+#ifndef DAWN_PULL_HLIST
+#define DAWN_PULL_HLIST 1  // pull pieces phase: only the heavy in-rows the light pass left
+#endif
 #ifndef DAWN_PULL_SPLIT
 #define DAWN_PULL_SPLIT 1  // pull level = light pass, grid barrier, heavy pieces (C4 +4.5%)
 #endif
@@ -141,8 +144,8 @@ struct Ctrl {
   uint32_t bad_src;             // sticky: a dawn_sssp_batch device source id was >= n
   uint32_t wcc_cnt, wcc_arcs, wcc_root, wcc_k;  // dawn_largest_wcc selection / output size
   uint32_t claim;               // lane 0's: next unclaimed index of a dawn_sssp_batch call
-  uint32_t next_idx;            // the batch index this lane searches next (claimed one ahead)
-  uint32_t pad1;
+  uint32_t next_idx;            // the batch index this lane searches next
+  uint32_t hl_cnt[2];           // pull level L: heavy in-rows the light pass left (parity L & 1)
   alignas(16) unsigned char solo_state[256];  // LevelState snapshot published with solo_epoch
 };
 

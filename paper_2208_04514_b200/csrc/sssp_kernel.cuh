@@ -536,6 +536,21 @@ __device__ void pull_level(const SsspParams &p, const LevelState &st, uint32_t g
         }
       }
     }
+    if constexpr (PART == 1 && DAWN_PULL_HLIST) {
+      // heavy rows the first kHeavyProbe probes did not settle: listed for the pieces phase
+      // (the free queue buffer Lv[q^1] holds them: at most one entry per unreached vertex)
+#pragma unroll
+      for (int j = 0; j < J; ++j) {
+        const bool left = hvy[j] && need[j] && !found[j];
+        const uint32_t lm = __ballot_sync(DAWN_FULL, left);
+        if (lm) {
+          uint32_t base = 0;
+          if (lane == 0) base = atomicAdd(&p.ctrl->hl_cnt[st.L & 1], (uint32_t)__popc(lm));
+          base = __shfl_sync(DAWN_FULL, base, 0);
+          if (left) p.Lv[st.q ^ 1][base + __popc(lm & lanemask_lt())] = u[j];
+        }
+      }
+    }
 #pragma unroll
     for (int j = 0; j < J; ++j) {
       if (need[j]) examined += min(j0[j], ef[j]) - s[j];
@@ -568,6 +583,41 @@ __device__ void pull_level(const SsspParams &p, const LevelState &st, uint32_t g
   phase_add(p, st.L, 0, t0);
   }  // PART != 2
   if constexpr (PART == 1) return;
+  if constexpr (PART == 2 && DAWN_PULL_HLIST) {
+    // (2') the heavy rows the light pass left (listed, one warp each, in-edges from the first
+    //      unprobed one, 32 per round trip, early exit); each listed vertex is unique and only
+    //      this phase can settle it now, so the claim needs no returning atomic
+    const uint32_t cnt = ld_cg(&p.ctrl->hl_cnt[st.L & 1]);
+    const uint32_t *hl = p.Lv[st.q ^ 1];
+    for (uint32_t i = gwarp; i < cnt; i += nwarps) {
+      const uint32_t uk = ld_cg(hl + i);
+      if ((ld_cg(p.vis + (uk >> 5)) >> (uk & 31)) & 1u) continue;  // (defensive: settled)
+      const uint32_t sk = ld_nc(p.irp + uk) + kHeavyProbe, ek = ld_nc(p.irp + uk + 1);
+      for (uint32_t j = sk; j < ek; j += 32) {
+        const uint32_t jj = j + lane;
+        const bool hit = jj < ek && fb_test(fcur, (uint32_t)ld_nc(p.icol + jj));
+        const uint32_t hm = __ballot_sync(DAWN_FULL, hit);
+        if (hm) {
+          if (lane == 0) {
+            examined += (j - sk) + __ffs(hm);
+            const uint32_t w = uk >> 5, bit = 1u << (uk & 31);
+            red_or(p.vis + w, bit);
+            red_or(fnext + w, bit);
+            DIST_ST(uk, L1);
+            n_new += 1;
+            const uint32_t dg = p.sym ? (ek - (sk - kHeavyProbe))
+                                      : (ld_nc(p.rp + uk + 1) - ld_nc(p.rp + uk));
+            m_new += dg;
+            bigf |= dg > kDirectRow;
+          }
+          break;
+        }
+        if (j + 32 >= ek && lane == 0) examined += ek - sk;
+      }
+    }
+    phase_add(p, st.L, 1, t0);
+    return;
+  }
   // (2) heavy rows: static pieces; 32 pieces tested per warp (vis), then a warp scans each
   //     live piece 32 in-edges per round trip
   // every warp gets an equal consecutive share of the piece list (a 32-piece stride left most
@@ -717,7 +767,10 @@ __device__ __forceinline__ void level_header(const SsspParams &p, Ctrl *C, Level
   st.qn = (uint32_t)(qp >> 32);
   st.qe = (uint32_t)qp;
   st.big = ld_cg(&cs->big);
-  if (blockIdx.x == 0) C->slot[(st.L + 2) % 3] = Slot{0, 0, 0, 0, 0};
+  if (blockIdx.x == 0) {
+    C->slot[(st.L + 2) % 3] = Slot{0, 0, 0, 0, 0};
+    C->hl_cnt[(st.L + 1) & 1] = 0;  // last used at level L-1, next at level L+1
+  }
   if (st.L > 0) st.reached += st.nf;
   st.explored += st.mf;
   st.stop = 0;
@@ -931,6 +984,7 @@ __global__ void __launch_bounds__(NT, MINB) k_sssp(SsspParams p) {
     st.drow = drow;
   }
   }
+  if (blockIdx.x == 0 && threadIdx.x == 0) C->hl_cnt[0] = C->hl_cnt[1] = 0;  // (also on resume)
   grid_sync(&C->bar, nblocks, bar_target);
   // the next search's index for the solo-stretch prefill: unknown (none) with dynamic lanes
   if (threadIdx.x == 0) next_sh = p.claim ? nsrc : cur_sh + 1;  // read after a sync
