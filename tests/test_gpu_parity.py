@@ -258,6 +258,26 @@ def test_tunables_never_change_results(knobs):
         check_sssp(g, G, srcs, variants=("auto", "push"))
 
 
+def test_unreachable_long_heavy_row():
+    # a hub with a 10,000-entry in-row outside the source's component stays unsettled at every
+    # pull level (listed for the heavy phase each time), and a reachable 9,000-entry hub settles;
+    # all variants, single and batch
+    k = graphgen.kron(14, 16, 14)
+    n0 = k.n
+    e = np.stack([np.repeat(np.arange(k.n), np.diff(k.row_ptr)), k.col.astype(np.int64)], 1).tolist()
+    hub = n0
+    e += [[hub, n0 + 1 + i] for i in range(10000)] + [[n0 + 1 + i, hub] for i in range(10000)]
+    hub2 = n0 + 10001                      # a long hub inside the source's component
+    e += [[hub2, int(v)] for v in range(9000)] + [[int(v), hub2] for v in range(9000)]
+    g = graphgen.from_edges(n0 + 10002, e)
+    G = dev_graph(g)
+    srcs = [0, 5, hub2] + list(k.sample_sources(2, seed=4))
+    check_sssp(g, G, srcs, variants=("auto", "push", "pull"))
+    d = dawn.sssp_batch(G, torch.tensor(srcs, dtype=torch.int32, device="cuda")).cpu().numpy().view(np.uint32)
+    for i, s0 in enumerate(srcs):
+        assert np.array_equal(d[i], oracle.bfs_fifo(g.n, g.row_ptr, g.col, int(s0))[0]), s0
+
+
 def test_narrow_kernel_and_handover():
     # dawn_sssp starts on one 16-CTA cluster (k_narrow); wide frontiers (or full queues) hand
     # over to the grid-wide kernel, which resumes from the frontier bitmap.
