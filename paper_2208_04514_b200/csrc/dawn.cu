@@ -1466,7 +1466,7 @@ dawn_status part_build(int64_t n, int64_t m, const int64_t *row_ptr, const int32
 struct PartLayout {
   size_t rp, irp, hout_bits, hout_v, hout_s, hout_e, hin_bits, hin_v, hin_s, hin_e;
   size_t scan_tmp, piece_tmp, vis, cand, lev, send, recv, ctrl, icol2, hasin, ulist, useg, hlist;
-  size_t top1;
+  size_t top1, hlist2;
   size_t total;
   uint64_t capHP;
 };
@@ -1505,6 +1505,7 @@ PartLayout part_layout(int64_t n, int64_t m_r, int32_t world, int64_t R, int64_t
   L.ctrl = take(sizeof(PartCtrl));
   L.hlist = take(4 * (size_t)kPartHList);  // heavy frontier vertices of a fused push level
   L.top1 = take(4 * (size_t)R + 4);  // first entry of every degree-ordered in-row (as k_sssp)
+  L.hlist2 = take(4 * (size_t)R + 4);  // fused pull: heavy vertices the light pass left
   L.total = o;
   return L;
 }
@@ -1562,6 +1563,7 @@ PartParams part_params(dawn_part p) {
   q.ulist = u32(p->L.ulist);
   q.useg = u32(p->L.useg);
   q.hlist = u32(p->L.hlist);
+  q.hlist2 = u32(p->L.hlist2);
   q.top1 = (DAWN_PULL_TOP1 && p->m_r > 0) ? u32(p->L.top1) : nullptr;
   q.n_has = p->n_has;
   q.lev = reinterpret_cast<uint8_t *>(p->ws + p->L.lev);

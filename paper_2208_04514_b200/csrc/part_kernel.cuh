@@ -64,6 +64,7 @@ struct PartParams {
   const uint32_t *hasin;              // owned vertices with an in-edge, ascending (n_has)
   uint32_t *ulist, *useg;             // unreached list in per-warp segments, segment counts
   uint32_t *hlist;                    // fused push: heavy frontier vertices (count: ctrl->pad[4])
+  uint32_t *hlist2;                   // fused pull: heavy vertices the light pass left (pad[5])
   const uint32_t *top1;               // [R]: first entry of each degree-ordered in-row, or null
   uint32_t n_has;
   uint8_t *lev;                       // deferred distances (as k_sssp: byte L+1, 255 = direct)
@@ -227,7 +228,10 @@ __device__ __forceinline__ void part_header(const PartParams &p, const uint32_t 
 // The level's work: F_L in rv (all ranks' slices) -> this rank's slice of F_{L+1} in sd.
 // LIST (fused kernel): push step (a) also lists the frontier's heavy out-rows; the caller runs
 // part_push_heavy after a grid barrier instead of step (b).
-template <int NT, bool CG, int MODE = 0, bool LIST = false>
+// PPART (pull levels): 0 light pass and heavy pieces; 1 the light pass only (fused kernel):
+// heavy vertices it settles are claimed without a returning atomic and those it leaves are
+// listed for part_pull_heavy, which runs after a grid barrier
+template <int NT, bool CG, int MODE = 0, bool LIST = false, int PPART = 0>
 __device__ void part_work(const PartParams &p, const PartState &st, uint32_t L, const uint32_t *rv,
                           uint32_t *sd, uint32_t gwarp, uint32_t nwarps, uint32_t &n_new,
                           unsigned long long &m_new, unsigned long long &exam) {
@@ -371,11 +375,25 @@ __device__ void part_work(const PartParams &p, const PartState &st, uint32_t L, 
           found[k] = hit < 4;
         }
       }
+      if constexpr (PPART == 1) {
+        // heavy in-rows the first kHeavyProbe probes left unsettled: listed for the heavy phase
+#pragma unroll
+        for (int k = 0; k < PJ; ++k) {
+          const bool left = hv[k] && need[k] && !found[k];
+          const uint32_t lm = __ballot_sync(DAWN_FULL, left);
+          if (lm) {
+            uint32_t base = 0;
+            if (lane == 0) base = atomicAdd(&p.ctrl->pad[5], (uint32_t)__popc(lm));
+            base = __shfl_sync(DAWN_FULL, base, 0);
+            if (left) p.hlist2[base + __popc(lm & lanemask_lt())] = t[k];
+          }
+        }
+      }
 #pragma unroll
       for (int k = 0; k < PJ; ++k) {
         if (found[k]) {
           const uint32_t w = t[k] >> 5, bit = 1u << (t[k] & 31);
-          if (hv[k]) {
+          if (hv[k] && PPART == 0) {
             if (atomicOr(p.vis + w, bit) & bit) found[k] = false;  // a piece settled t first
           } else {
             red_or(p.vis + w, bit);  // light rows: this lane alone settles t
@@ -401,6 +419,7 @@ __device__ void part_work(const PartParams &p, const PartState &st, uint32_t L, 
       }
     }
     if (lane == 0) p.useg[gwarp] = wr;
+    if constexpr (PPART == 1) return;
     // (b) heavy in-rows: static pieces, 32 in-edges per round, stop at the first hit or once
     //     another piece settled the vertex
     const uint32_t hend = ld_cg(&p.ctrl->n_hp[1]);
@@ -499,6 +518,37 @@ __device__ void part_push_heavy(const PartParams &p, const PartState &st, uint32
       }
     }
     base += tot;
+  }
+}
+
+// Fused pull levels, after the grid barrier that follows the light pass: each heavy vertex it
+// left is scanned by one warp from its (kHeavyProbe+1)-th in-edge, 32 per round trip, early
+// exit; the listed vertices are unique and nothing else settles them now (no returning claim).
+template <bool CG>
+__device__ void part_pull_heavy(const PartParams &p, uint32_t L, const uint32_t *rv, uint32_t *sd,
+                                uint32_t gwarp, uint32_t nwarps, uint32_t &n_new,
+                                unsigned long long &m_new, unsigned long long &exam) {
+  const uint32_t lane = lane_id(), L1 = L + 1;
+  const uint32_t cnt = ld_cg(&p.ctrl->pad[5]);
+  for (uint32_t i = gwarp; i < cnt; i += nwarps) {
+    const uint32_t t = ld_cg(p.hlist2 + i);
+    const uint32_t w = t >> 5, bit = 1u << (t & 31);
+    if (ld_cg(p.vis + w) & bit) continue;
+    const uint32_t s = ld_nc(p.irp + t) + kHeavyProbe, e = ld_nc(p.irp + t + 1);
+    for (uint32_t j = s; j < e; j += 32) {
+      const uint32_t jj = j + lane;
+      const bool hit = jj < e && part_ftest<CG>(p, rv, (uint32_t)ld_nc(p.icol + jj));
+      const uint32_t hm = __ballot_sync(DAWN_FULL, hit);
+      if (hm) {
+        if (lane == 0) {
+          exam += (j - s) + __ffs(hm);
+          red_or(p.vis + w, bit);
+          part_discover(p, sd, t, L1, n_new, m_new);
+        }
+        break;
+      }
+      if (j + 32 >= e && lane == 0) exam += e - s;
+    }
   }
 }
 
@@ -663,7 +713,7 @@ __global__ void __launch_bounds__(NT, 2) k_part_fused(PartParams p, PartPeers pe
     if (st.done) break;
     const uint32_t *rv = myrecv + (L & 1) * slot_words;
     for (uint32_t i = gtid; i < p.S; i += nth) p.send[i] = 0;
-    if (gtid == 0) C->pad[4] = 0;  // heavy-row list of this level (last read before a barrier)
+    if (gtid == 0) C->pad[4] = C->pad[5] = 0;  // heavy lists of this level (last read before a barrier)
     grid_sync(gb, nblocks, bar);
     uint32_t n_new = 0;
     unsigned long long m_new = 0, exam = 0;
@@ -685,7 +735,10 @@ __global__ void __launch_bounds__(NT, 2) k_part_fused(PartParams p, PartPeers pe
       if (st.hvy) grid_sync(gb, nblocks, bar);
       part_push_heavy<true, 0>(p, st, L, rv, p.send, gwarp, nwarps, n_new, m_new, exam);
     } else {
-      part_work<NT, true>(p, st, L, rv, p.send, gwarp, nwarps, n_new, m_new, exam);
+      // pull: light pass, grid barrier, the heavy in-rows it left
+      part_work<NT, true, 0, false, 1>(p, st, L, rv, p.send, gwarp, nwarps, n_new, m_new, exam);
+      grid_sync(gb, nblocks, bar);
+      part_pull_heavy<true>(p, L, rv, p.send, gwarp, nwarps, n_new, m_new, exam);
     }
     part_counters(p, p.send, n_new, m_new, exam, red);
     grid_sync(gb, nblocks, bar);
